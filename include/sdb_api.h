@@ -1,0 +1,155 @@
+/*
+ * sdb_api.h — C-ABI of the B200-native SwiftDiffusion add-on hot path.
+ *
+ * The reference (addonsim 0.1.0, /root/reference/pkg) exposes this path only as
+ * plain Python functions; there is no plugin / FFI layer to bind to.  Each entry
+ * point below names the reference interface it replaces (file:line relative to
+ * /root/reference/pkg/src/addonsim/).  The Python host package
+ * (paper_2407_02031_b200) binds these with ctypes and keeps the reference
+ * signatures verbatim on top.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless the parameter name ends in _host.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *     Every launch is stream-ordered and asynchronous; nothing here synchronises
+ *     the host, allocates persistent memory or frees caller memory.
+ *   - Return value: 0 on success, negative SDB_E* code on failure;
+ *     sdb_last_error() returns a thread-local message for the last failure.
+ *   - Layouts: matrices are row-major with an explicit leading dimension
+ *     (elements between consecutive rows); the column stride is always 1.
+ *     Feature maps are NHWC (torch channels_last).
+ */
+#ifndef SDB_API_H_
+#define SDB_API_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ---- error codes ------------------------------------------------------- */
+#define SDB_OK 0
+#define SDB_EINVAL -1   /* bad argument (shape, dtype, alignment)            */
+#define SDB_ECUDA -2    /* a CUDA runtime call failed                         */
+#define SDB_EUNSUP -3   /* combination not supported on this build / device   */
+
+/* ---- dtypes -------------------------------------------------------------- */
+#define SDB_F32 0
+#define SDB_BF16 1
+#define SDB_F16 2
+
+/* Library version / build identification (host only). */
+const char* sdb_version(void);
+/* Thread-local message describing the most recent failure in this thread. */
+const char* sdb_last_error(void);
+/* 1 if a CUDA device of compute capability 10.x is visible, else 0. */
+int sdb_device_ok(int device);
+
+/* ========================================================================
+ * K1 — LoRA patch / unpatch:  W_out = W_in + sign * scale * down @ up
+ *
+ * Replaces the arithmetic core of the reference:
+ *   addonsim/lora.py:84-95   _accumulate(weight, adapter, scale, sign)
+ * which merge_in_place (lora.py:98-104), unmerge_in_place (lora.py:107-114)
+ * and create_and_replace (lora.py:132-144) all route through.  Same factor
+ * convention as the reference: `down` is (h1 x rank), `up` is (rank x h2)
+ * (lora.py:35-36).  Stacked adapters (lora.py:147-160) are passed as one job
+ * whose rank is the sum of ranks, with per-adapter scales folded into `down`.
+ *
+ * Numerics: the rank contraction is accumulated in fp32 (SIMT FFMA, or the
+ * tcgen05 tensor path for bf16 factors at rank >= 32) and added to W with one
+ * rounding per element: W_out = round_w(fma(sign*scale, delta, float(W_in))).
+ * Deterministic: no atomics, no split-K; reruns are bitwise identical.
+ * ======================================================================== */
+typedef struct sdb_lora_job {
+  void* w_in;          /* h1 x h2, row stride ldw (elements), dtype w_dtype          */
+  void* w_out;         /* output, same shape/stride as w_in; == w_in for in-place    */
+  const void* down;    /* h1 x rank, row stride ldd, dtype f_dtype                   */
+  const void* up;      /* rank x h2, row stride ldu, dtype f_dtype                   */
+  int64_t h1, h2;
+  int64_t ldw, ldd, ldu;
+  int32_t rank;
+  float scale;         /* multiplied by `sign` of the launch                        */
+  int64_t tile_begin;  /* filled by sdb_lora_plan(): first tile index of this job   */
+} sdb_lora_job;
+
+/* Fill jobs_host[i].tile_begin for the kernel chosen by (w_dtype, f_dtype,
+ * max rank) and return the total number of tiles through *total_tiles.
+ * path_out (may be NULL) receives 0 = SIMT kernel, 1 = tcgen05 kernel. */
+int sdb_lora_plan(sdb_lora_job* jobs_host, int n_jobs, int w_dtype, int f_dtype,
+                  int64_t* total_tiles, int* path_out);
+
+/* Batched patch over n_jobs matrices whose job table (already planned with
+ * sdb_lora_plan) lives in DEVICE memory at jobs_dev.  One launch covers every
+ * job; `max_ctas` > 0 caps the grid (to leave SMs to a concurrent UNet step
+ * when the patch runs on a side stream), 0 = one CTA per tile. */
+int sdb_lora_patch(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles,
+                   int w_dtype, int f_dtype, int path, float sign, int max_ctas,
+                   void* stream);
+
+/* Single-matrix convenience wrapper (no job table; used by the Python
+ * merge_in_place / unmerge_in_place / create_and_replace shims). */
+int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t ldw,
+                       const void* down, int64_t ldd, const void* up, int64_t ldu,
+                       int32_t rank, float scale, float sign,
+                       int w_dtype, int f_dtype, void* stream);
+
+/* ========================================================================
+ * K2 — GroupNorm (+ optional SiLU), NHWC.
+ *   y = act( (x - mean_g) * rstd_g * gamma_c + beta_c )
+ * The reference models this op only as a latency multiplier
+ * (addonsim/model.py:66-70 unet_opt_submultipliers[2] = 1.072; paper
+ * PAPER.md:572-576).  x, y: [N, HW, C] (channels innermost), dtype `dtype`;
+ * gamma, beta: fp32 [C].  `workspace` must hold sdb_groupnorm_workspace()
+ * bytes.  y may alias x.
+ * ======================================================================== */
+size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
+int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
+                       int64_t n, int64_t hw, int64_t c, int64_t groups, float eps,
+                       int apply_silu, int dtype, void* workspace, void* stream);
+
+/* ========================================================================
+ * K3 — ControlNet residual injection fused with the up-block concat.
+ *   out[p, 0:ch]        = hidden[p, :]                       (hidden may be NULL)
+ *   out[p, ch:ch+cs]    = skip[p, :] + sum_i scales[i] * res_i[p, :]
+ * Replaces the "outputs are added up to the skip connections and middle
+ * block" step (modelled as a zero-cost sum in SPEC.md:234
+ * and charged only comm_ms in addonsim/model.py:151-158).
+ * With hidden == NULL and ch == 0 it is the in-place mid-block add
+ * (out may alias skip).  res_ptrs_host: n_res device pointers (host array).
+ * ======================================================================== */
+int sdb_residual_inject(void* out, const void* hidden, const void* skip,
+                        const void* const* res_ptrs_host, const float* scales_host,
+                        int n_res, int64_t pixels, int64_t ch, int64_t cs,
+                        int dtype, void* stream);
+
+/* ========================================================================
+ * K4 — classifier-free guidance + DDIM (eta = 0) step, fused.
+ *   eps     = eps_u + g * (eps_c - eps_u)           (eps = [eps_u ; eps_c])
+ *   x0      = (x - sqrt(1 - a_t) * eps) / sqrt(a_t)
+ *   x_prev  = sqrt(a_prev) * x0 + sqrt(1 - a_prev) * eps
+ * writes x_prev into x_out (fp32 master latent, may alias x) and, when
+ * unet_in != NULL, into both CFG halves of the next UNet input (dtype
+ * `in_dtype`).  Per-step coefficients are read from the device table
+ * coef[step][4] = {a_t, a_prev, guidance, unused} at index *step_dev, and
+ * *step_dev is incremented by the kernel, so a whole step is graph-capturable.
+ * Not in the reference at all.
+ * ======================================================================== */
+int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out,
+                      void* unet_in, int in_dtype, int64_t latent_elems,
+                      const float* coef, int* step_dev, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDB_API_H_ */

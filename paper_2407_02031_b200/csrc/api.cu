@@ -1,0 +1,150 @@
+// api.cu — the extern "C" boundary declared in include/sdb_api.h.
+// Argument validation + dispatch only; the kernels live in the other units.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace sdb {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+// lora_patch.cu
+int64_t simt_tiles(int64_t h1, int64_t h2);
+int lora_patch_simt(const sdb_lora_job* jobs_dev, const sdb_lora_job& one, int n_jobs,
+                    int64_t total_tiles, int w_dtype, int f_dtype, float sign, int max_ctas,
+                    cudaStream_t st);
+// lora_patch_tc.cu
+int64_t tc_tiles(int64_t h1, int64_t h2);
+bool tc_supported(int w_dtype, int f_dtype, int max_rank);
+int lora_patch_tc(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles, float sign,
+                  int max_ctas, cudaStream_t st);
+// groupnorm_silu.cu
+size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
+int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, int64_t n,
+                   int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype,
+                   void* ws, cudaStream_t st);
+// residual_inject.cu
+int residual_inject(void* out, const void* hidden, const void* skip, const void* const* res,
+                    const float* scales, int n_res, int64_t pixels, int64_t ch, int64_t cs,
+                    int dtype, cudaStream_t st);
+// cfg_step.cu
+int cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,
+                  int in_dtype, int64_t L, const float* coef, int* step_dev, cudaStream_t st);
+
+static int check_job(const sdb_lora_job& j, int idx) {
+  if (j.h1 <= 0 || j.h2 <= 0)
+    return fail(SDB_EINVAL, "lora job " + std::to_string(idx) + ": empty weight");
+  if (j.rank <= 0) return fail(SDB_EINVAL, "lora job " + std::to_string(idx) + ": rank must be >= 1");
+  if (j.ldw < j.h2 || j.ldu < j.h2 || j.ldd < j.rank)
+    return fail(SDB_EINVAL, "lora job " + std::to_string(idx) + ": leading dimension too small");
+  if (!j.w_in || !j.w_out || !j.down || !j.up)
+    return fail(SDB_EINVAL, "lora job " + std::to_string(idx) + ": NULL pointer");
+  return SDB_OK;
+}
+
+}  // namespace sdb
+
+using namespace sdb;
+
+extern "C" {
+
+const char* sdb_version(void) { return "sdb 0.1.0 (sm_100a)"; }
+
+const char* sdb_last_error(void) { return g_last_error.c_str(); }
+
+int sdb_device_ok(int device) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return prop.major == 10 ? 1 : 0;
+}
+
+int sdb_lora_plan(sdb_lora_job* jobs, int n_jobs, int w_dtype, int f_dtype, int64_t* total_tiles,
+                  int* path_out) {
+  if (n_jobs <= 0 || jobs == nullptr || total_tiles == nullptr)
+    return fail(SDB_EINVAL, "sdb_lora_plan: no jobs");
+  int max_rank = 0;
+  for (int i = 0; i < n_jobs; ++i) {
+    if (int rc = check_job(jobs[i], i)) return rc;
+    max_rank = std::max(max_rank, (int)jobs[i].rank);
+  }
+  const int path = tc_supported(w_dtype, f_dtype, max_rank) ? 1 : 0;
+  int64_t t = 0;
+  for (int i = 0; i < n_jobs; ++i) {
+    jobs[i].tile_begin = t;
+    t += path ? tc_tiles(jobs[i].h1, jobs[i].h2) : simt_tiles(jobs[i].h1, jobs[i].h2);
+  }
+  *total_tiles = t;
+  if (path_out) *path_out = path;
+  return SDB_OK;
+}
+
+int sdb_lora_patch(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles, int w_dtype,
+                   int f_dtype, int path, float sign, int max_ctas, void* stream) {
+  if (n_jobs <= 0 || jobs_dev == nullptr) return fail(SDB_EINVAL, "sdb_lora_patch: no jobs");
+  if (total_tiles <= 0) return fail(SDB_EINVAL, "sdb_lora_patch: plan has no tiles");
+  if (path == 1) {
+    if (!(w_dtype == SDB_BF16 && f_dtype == SDB_BF16))
+      return fail(SDB_EUNSUP, "sdb_lora_patch: tcgen05 path needs bf16 weights and factors");
+    return lora_patch_tc(jobs_dev, n_jobs, total_tiles, sign, max_ctas, as_stream(stream));
+  }
+  sdb_lora_job none;
+  std::memset(&none, 0, sizeof(none));
+  return lora_patch_simt(jobs_dev, none, n_jobs, total_tiles, w_dtype, f_dtype, sign, max_ctas,
+                         as_stream(stream));
+}
+
+int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t ldw,
+                       const void* down, int64_t ldd, const void* up, int64_t ldu, int32_t rank,
+                       float scale, float sign, int w_dtype, int f_dtype, void* stream) {
+  sdb_lora_job j;
+  std::memset(&j, 0, sizeof(j));
+  j.w_in = w_in;
+  j.w_out = w_out ? w_out : w_in;
+  j.down = down;
+  j.up = up;
+  j.h1 = h1;
+  j.h2 = h2;
+  j.ldw = ldw;
+  j.ldd = ldd;
+  j.ldu = ldu;
+  j.rank = rank;
+  j.scale = scale;
+  j.tile_begin = 0;
+  if (int rc = check_job(j, 0)) return rc;
+  return lora_patch_simt(nullptr, j, 1, simt_tiles(h1, h2), w_dtype, f_dtype, sign, 0,
+                         as_stream(stream));
+}
+
+size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
+  if (n <= 0 || hw <= 0 || c <= 0 || groups <= 0) return 0;
+  return groupnorm_workspace(n, hw, c, groups);
+}
+
+int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, int64_t n,
+                       int64_t hw, int64_t c, int64_t groups, float eps, int apply_silu, int dtype,
+                       void* workspace, void* stream) {
+  return groupnorm_silu(x, y, gamma, beta, n, hw, c, groups, eps, apply_silu, dtype, workspace,
+                        as_stream(stream));
+}
+
+int sdb_residual_inject(void* out, const void* hidden, const void* skip,
+                        const void* const* res_ptrs_host, const float* scales_host, int n_res,
+                        int64_t pixels, int64_t ch, int64_t cs, int dtype, void* stream) {
+  return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, dtype,
+                         as_stream(stream));
+}
+
+int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,
+                      int in_dtype, int64_t latent_elems, const float* coef, int* step_dev,
+                      void* stream) {
+  return cfg_ddim_step(eps, eps_dtype, x, x_out, unet_in, in_dtype, latent_elems, coef, step_dev,
+                       as_stream(stream));
+}
+
+}  // extern "C"

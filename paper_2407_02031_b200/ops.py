@@ -1,0 +1,253 @@
+"""Torch-facing wrappers over the C-ABI kernels (device tensors in, no copies).
+
+PyTorch supplies device memory and streams; every arithmetic op on this path
+is a hand-written sm_100a kernel in libsdb.so.  Inputs must already be CUDA
+tensors — there is deliberately no CPU branch (a CPU tensor raises).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib
+from .errors import DeviceError, ValidationError
+
+_DTYPES = {torch.float32: _lib.SDB_F32, torch.bfloat16: _lib.SDB_BF16, torch.float16: _lib.SDB_F16}
+_checked_devices: set[int] = set()
+
+
+def sdb_dtype(t: torch.Tensor) -> int:
+    try:
+        return _DTYPES[t.dtype]
+    except KeyError:
+        raise ValidationError(f"unsupported dtype {t.dtype}") from None
+
+
+def require_cuda(*tensors: torch.Tensor) -> None:
+    """Fail loudly unless every tensor lives on an sm_100 CUDA device."""
+    for t in tensors:
+        if t is None:
+            continue
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise DeviceError("paper_2407_02031_b200 kernels need CUDA tensors on a B200 "
+                              "(sm_100); there is no CPU fallback")
+        dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
+        if dev not in _checked_devices:
+            if not _lib.lib().sdb_device_ok(dev):
+                raise DeviceError(f"cuda:{dev} is not an sm_100 (Blackwell B200) device")
+            _checked_devices.add(dev)
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+# --------------------------------------------------------------------------
+# K1 — LoRA patch
+# --------------------------------------------------------------------------
+def _row_stride(t: torch.Tensor, what: str) -> int:
+    if t.dim() != 2:
+        raise ValidationError(f"{what} must be 2-d, got shape {tuple(t.shape)}")
+    if t.stride(1) != 1 and t.shape[1] > 1:
+        raise ValidationError(f"{what} must have unit column stride")
+    return max(t.stride(0), t.shape[1])
+
+
+def lora_patch_one(w_in: torch.Tensor, down: torch.Tensor, up: torch.Tensor, scale: float,
+                   sign: float = 1.0, w_out: Optional[torch.Tensor] = None,
+                   stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """W_out = W_in + sign*scale*down@up on one matrix (in place if w_out is None)."""
+    require_cuda(w_in, down, up, w_out)
+    out = w_in if w_out is None else w_out
+    if out.shape != w_in.shape or out.stride() != w_in.stride() or out.dtype != w_in.dtype:
+        raise ValidationError("w_out must match w_in in shape, stride and dtype")
+    if down.dtype != up.dtype:
+        raise ValidationError("down and up must share a dtype")
+    h1, h2 = w_in.shape
+    if down.shape[0] != h1 or up.shape[1] != h2 or down.shape[1] != up.shape[0]:
+        raise ValidationError(f"factor shapes {tuple(down.shape)} x {tuple(up.shape)} do not match "
+                              f"weight ({h1}, {h2})")
+    _lib.check("sdb_lora_patch_one", _lib.lib().sdb_lora_patch_one(
+        w_in.data_ptr(), out.data_ptr(), h1, h2, _row_stride(w_in, "weight"),
+        down.data_ptr(), _row_stride(down, "down"), up.data_ptr(), _row_stride(up, "up"),
+        int(down.shape[1]), float(scale), float(sign), sdb_dtype(w_in), sdb_dtype(down),
+        _stream_ptr(stream)))
+    return out
+
+
+class LoraPatchPlan:
+    """A planned, device-resident job table for one batched K1 launch.
+
+    entries: sequence of (w_in, w_out or None, down, up, scale).  All weights
+    share one dtype and all factors another.  The table (a packed array of
+    ``sdb_lora_job``) is uploaded once; ``launch`` is then a single kernel
+    launch, capturable in a CUDA graph and cheap enough to run on a side
+    stream at every patch event.
+    """
+
+    def __init__(self, entries: Sequence[tuple], device: Optional[torch.device] = None):
+        if not entries:
+            raise ValidationError("LoraPatchPlan needs at least one job")
+        jobs = (_lib.LoraJob * len(entries))()
+        w_dt = f_dt = None
+        self._keep = []  # keep tensors alive as long as the plan
+        self.alg_bytes = 0
+        self.alg_flops = 0
+        for i, (w_in, w_out, down, up, scale) in enumerate(entries):
+            out = w_in if w_out is None else w_out
+            require_cuda(w_in, out, down, up)
+            if w_dt is None:
+                w_dt, f_dt = sdb_dtype(w_in), sdb_dtype(down)
+            if sdb_dtype(w_in) != w_dt or sdb_dtype(out) != w_dt or sdb_dtype(down) != f_dt \
+                    or sdb_dtype(up) != f_dt:
+                raise ValidationError("all jobs of a plan must share weight and factor dtypes")
+            h1, h2 = w_in.shape
+            r = down.shape[1]
+            if down.shape[0] != h1 or up.shape[1] != h2 or up.shape[0] != r:
+                raise ValidationError(f"job {i}: factor shapes {tuple(down.shape)} x {tuple(up.shape)} "
+                                      f"do not match weight ({h1}, {h2})")
+            if out.stride() != w_in.stride():
+                raise ValidationError(f"job {i}: w_out stride differs from w_in")
+            j = jobs[i]
+            j.w_in, j.w_out = w_in.data_ptr(), out.data_ptr()
+            j.down, j.up = down.data_ptr(), up.data_ptr()
+            j.h1, j.h2 = h1, h2
+            j.ldw = _row_stride(w_in, "weight")
+            j.ldd = _row_stride(down, "down")
+            j.ldu = _row_stride(up, "up")
+            j.rank = r
+            j.scale = float(scale)
+            self._keep += [w_in, out, down, up]
+            ws, fs = w_in.element_size(), down.element_size()
+            self.alg_bytes += 2 * h1 * h2 * ws + (h1 + h2) * r * fs
+            self.alg_flops += 2 * h1 * h2 * r
+        total = ctypes.c_int64(0)
+        path = ctypes.c_int(0)
+        _lib.check("sdb_lora_plan", _lib.lib().sdb_lora_plan(
+            jobs, len(entries), w_dt, f_dt, ctypes.byref(total), ctypes.byref(path)))
+        raw = bytes(jobs)
+        dev = device if device is not None else entries[0][0].device
+        self.table = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+        self.n_jobs = len(entries)
+        self.total_tiles = total.value
+        self.path = path.value
+        self.w_dtype, self.f_dtype = w_dt, f_dt
+
+    def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None,
+               max_ctas: int = 0) -> None:
+        _lib.check("sdb_lora_patch", _lib.lib().sdb_lora_patch(
+            self.table.data_ptr(), self.n_jobs, self.total_tiles, self.w_dtype, self.f_dtype,
+            self.path, float(sign), int(max_ctas), _stream_ptr(stream)))
+
+
+# --------------------------------------------------------------------------
+# K2 — GroupNorm (+SiLU), NHWC
+# --------------------------------------------------------------------------
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def nhwc_view(x: torch.Tensor) -> tuple[int, int, int]:
+    """(N, HW, C) of a 4-d channels_last tensor (or a 3-d [N, L, C] tensor)."""
+    if x.dim() == 4:
+        n, c, h, w = x.shape
+        if not x.is_contiguous(memory_format=torch.channels_last):
+            raise ValidationError("feature maps must be channels_last (NHWC) contiguous")
+        return n, h * w, c
+    if x.dim() == 3:
+        if not x.is_contiguous():
+            raise ValidationError("[N, L, C] tensors must be contiguous")
+        n, l, c = x.shape
+        return n, l, c
+    raise ValidationError(f"expected a 3-d or 4-d tensor, got {x.dim()}-d")
+
+
+def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optional[torch.Tensor],
+                   groups: int = 32, eps: float = 1e-5, silu: bool = True,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    require_cuda(x, gamma, beta, out)
+    n, hw, c = nhwc_view(x)
+    if out is None:
+        out = torch.empty_like(x)
+    if gamma is not None and gamma.dtype != torch.float32:
+        raise ValidationError("gamma/beta must be fp32")
+    ws_bytes = _lib.lib().sdb_groupnorm_workspace(n, hw, c, groups)
+    ws = _workspace(ws_bytes, x.device)
+    _lib.check("sdb_groupnorm_silu", _lib.lib().sdb_groupnorm_silu(
+        x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,
+        beta.data_ptr() if beta is not None else None, n, hw, c, groups, float(eps), int(silu),
+        sdb_dtype(x), ws.data_ptr(), _stream_ptr(None)))
+    return out
+
+
+# --------------------------------------------------------------------------
+# K3 — residual injection fused with the skip concat
+# --------------------------------------------------------------------------
+def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scales: Sequence[float],
+                    hidden: Optional[torch.Tensor] = None,
+                    out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """hidden is None: returns skip + sum s_i r_i (in place into ``out`` or skip).
+    otherwise: returns cat([hidden, skip + sum s_i r_i], dim=C) in channels_last."""
+    require_cuda(skip, hidden, out, *residuals)
+    if len(residuals) != len(scales):
+        raise ValidationError("one scale per residual")
+    n, hw, cs = nhwc_view(skip)
+    for r in residuals:
+        if r.shape != skip.shape or r.dtype != skip.dtype:
+            raise ValidationError(f"residual shape {tuple(r.shape)} != skip {tuple(skip.shape)}")
+        nhwc_view(r)
+    ch = 0
+    if hidden is not None:
+        hn, hhw, ch = nhwc_view(hidden)
+        if (hn, hhw) != (n, hw) or hidden.dtype != skip.dtype:
+            raise ValidationError("hidden and skip must agree on N, H, W and dtype")
+        if out is None:
+            if skip.dim() == 4:
+                out = torch.empty((n, ch + cs, skip.shape[2], skip.shape[3]), dtype=skip.dtype,
+                                  device=skip.device, memory_format=torch.channels_last)
+            else:
+                out = torch.empty((n, hw, ch + cs), dtype=skip.dtype, device=skip.device)
+    elif out is None:
+        out = skip
+    k = len(residuals)
+    ptrs = (ctypes.c_void_p * max(k, 1))(*[r.data_ptr() for r in residuals])
+    sc = (ctypes.c_float * max(k, 1))(*[float(s) for s in scales])
+    _lib.check("sdb_residual_inject", _lib.lib().sdb_residual_inject(
+        out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),
+        ptrs, sc, k, n * hw, ch, cs, sdb_dtype(skip), _stream_ptr(None)))
+    return out
+
+
+# --------------------------------------------------------------------------
+# K4 — CFG combine + DDIM step (+ CFG re-batch of the next UNet input)
+# --------------------------------------------------------------------------
+def cfg_ddim_step(eps: torch.Tensor, x: torch.Tensor, coef: torch.Tensor, step_dev: torch.Tensor,
+                  x_out: Optional[torch.Tensor] = None,
+                  unet_in: Optional[torch.Tensor] = None) -> torch.Tensor:
+    require_cuda(eps, x, coef, step_dev, x_out, unet_in)
+    if x.dtype != torch.float32 or coef.dtype != torch.float32 or step_dev.dtype != torch.int32:
+        raise ValidationError("x / coef must be fp32 and step_dev int32")
+    L = x.numel()
+    if eps.numel() != 2 * L:
+        raise ValidationError("eps must hold the [uncond; cond] batch of 2 latents")
+    if unet_in is not None and unet_in.numel() != 2 * L:
+        raise ValidationError("unet_in must hold 2 latents")
+    out = x if x_out is None else x_out
+    _lib.check("sdb_cfg_ddim_step", _lib.lib().sdb_cfg_ddim_step(
+        eps.data_ptr(), sdb_dtype(eps), x.data_ptr(), out.data_ptr(),
+        unet_in.data_ptr() if unet_in is not None else None,
+        sdb_dtype(unet_in) if unet_in is not None else _lib.SDB_F32, L, coef.data_ptr(),
+        step_dev.data_ptr(), _stream_ptr(None)))
+    return out

@@ -1,0 +1,108 @@
+"""K2 (GroupNorm+SiLU), K3 (residual inject + concat), K4 (CFG + DDIM step)
+against plain PyTorch fp32 references of the same op."""
+
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2407_02031_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def cl(t):
+    return t.contiguous(memory_format=torch.channels_last)
+
+
+# SDXL / SD1.5 GN sites (C, H, W) incl. cpg = 10, 30 (not a multiple of 8)
+GN_SHAPES = [(320, 128, 128), (960, 64, 64), (2560, 32, 32), (640, 32, 32), (1920, 16, 16),
+             (64, 64, 64), (32, 8, 8), (1280, 8, 8)]
+
+
+@pytest.mark.parametrize("c,h,w", GN_SHAPES)
+@pytest.mark.parametrize("silu", [True, False])
+def test_groupnorm_silu_bf16(c, h, w, silu):
+    g = torch.Generator(device="cuda").manual_seed(c + h)
+    x = cl((torch.randn(2, c, h, w, device="cuda", generator=g) * 3 + 1.5).to(torch.bfloat16))
+    gamma = torch.rand(c, device="cuda", generator=g) + 0.5
+    beta = torch.randn(c, device="cuda", generator=g)
+    y = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=silu)
+    ref = F.group_norm(x.float(), 32, gamma, beta, 1e-5)
+    if silu:
+        ref = F.silu(ref)
+    err = (y.float() - ref).abs()
+    # one bf16 rounding of the output: |err| <= 2^-8 |ref| (+ tiny abs term)
+    assert (err <= ref.abs() * 2 ** -8 + 1e-3).all(), float(err.max())
+    assert y.is_contiguous(memory_format=torch.channels_last)
+
+
+def test_groupnorm_fp32_tight_and_in_place():
+    x = cl(torch.randn(2, 640, 32, 32, device="cuda") * 10 + 100)  # large mean: cancellation check
+    gamma = torch.rand(640, device="cuda") + 0.5
+    beta = torch.randn(640, device="cuda")
+    ref = F.silu(F.group_norm(x, 32, gamma, beta, 1e-5))
+    y = ops.groupnorm_silu(x, gamma, beta, silu=True)
+    assert (y - ref).abs().max().item() < 1e-4
+    x2 = x.clone(memory_format=torch.channels_last)
+    ops.groupnorm_silu(x2, gamma, beta, silu=True, out=x2)
+    assert torch.equal(x2, y)
+
+
+@pytest.mark.parametrize("n_res", [0, 1, 2, 3])
+def test_residual_inject_concat(n_res):
+    g = torch.Generator(device="cuda").manual_seed(n_res)
+    hid = cl(torch.randn(2, 640, 32, 32, device="cuda", generator=g).to(torch.bfloat16))
+    skip = cl(torch.randn(2, 320, 32, 32, device="cuda", generator=g).to(torch.bfloat16))
+    res = [cl(torch.randn(2, 320, 32, 32, device="cuda", generator=g).to(torch.bfloat16)) for _ in range(n_res)]
+    scales = [0.8, 0.5, 1.2][:n_res]
+    out = ops.residual_inject(skip, res, scales, hidden=hid)
+    ref_skip = skip.float()
+    for r, s in zip(res, scales):
+        ref_skip = ref_skip + s * r.float()
+    ref = torch.cat([hid.float(), ref_skip], dim=1)
+    assert out.shape == (2, 960, 32, 32) and out.is_contiguous(memory_format=torch.channels_last)
+    err = (out.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 1e-6).all()
+    assert torch.equal(out[:, :640], hid)
+
+
+def test_residual_inject_in_place_mid():
+    mid = cl(torch.randn(2, 1280, 16, 16, device="cuda").to(torch.bfloat16))
+    r = cl(torch.randn(2, 1280, 16, 16, device="cuda").to(torch.bfloat16))
+    exp = (mid.float() + 0.8 * r.float()).to(torch.bfloat16)
+    out = ops.residual_inject(mid, [r], [0.8])
+    assert out.data_ptr() == mid.data_ptr()
+    assert (out.float() - exp.float()).abs().max().item() <= 2 ** -7 * exp.float().abs().max().item()
+
+
+def test_cfg_ddim_step_and_step_counter():
+    L = 4 * 64 * 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    steps = 3
+    coef = torch.tensor([[0.1, 0.3, 7.5, 0.0], [0.3, 0.6, 7.5, 0.0], [0.6, 0.9, 5.0, 0.0]],
+                        device="cuda", dtype=torch.float32)
+    step = torch.zeros(2, device="cuda", dtype=torch.int32)
+    x = torch.randn(L, device="cuda", generator=g)
+    x_ref = x.clone().double()
+    unet_in = torch.empty(2 * L, device="cuda", dtype=torch.bfloat16)
+    for s in range(steps):
+        eps = torch.randn(2 * L, device="cuda", generator=g).to(torch.bfloat16)
+        ops.cfg_ddim_step(eps, x, coef, step, unet_in=unet_in)
+        a_t, a_p, gs = [float(v) for v in coef[s, :3]]
+        e = eps.double()
+        ec = e[:L] + gs * (e[L:] - e[:L])
+        x0 = (x_ref - math.sqrt(1 - a_t) * ec) / math.sqrt(a_t)
+        x_ref = math.sqrt(a_p) * x0 + math.sqrt(1 - a_p) * ec
+        assert (x.double() - x_ref).abs().max().item() < 1e-4 * max(1.0, x_ref.abs().max().item())
+        assert torch.equal(unet_in[:L], unet_in[L:])
+        assert torch.equal(unet_in[:L], x.to(torch.bfloat16))
+        x_ref = x.double()  # re-anchor on the kernel's fp32 state
+    assert step.tolist() == [steps, 0]
+
+
+def test_no_cpu_tensors_accepted():
+    from paper_2407_02031_b200.errors import DeviceError
+    with pytest.raises(DeviceError):
+        ops.groupnorm_silu(torch.randn(1, 32, 4, 4), None, None)

@@ -1,0 +1,275 @@
+"""K1 parity on the B200: the drop-in API and the batched kernel against the
+reference's own outputs (golden fixtures) and the pinned oracle.  Mirrors
+/root/reference/pkg/tests/test_lora.py and test_acceptance.py:341-391."""
+
+import json
+import tracemalloc
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from oracle import lora_ref
+from paper_2407_02031_b200 import lora as L
+from paper_2407_02031_b200 import ops
+from paper_2407_02031_b200.errors import ValidationError
+
+pytestmark = pytest.mark.gpu
+GOLD_NPZ = np.load(Path(__file__).parent / "golden" / "lora_small.npz")
+TOL = 1e-5  # reference gates: test_lora.py:89,101,142; test_acceptance.py:380-385
+
+
+def small_adapter(scale=1.0):
+    return L.LowRankAdapter("tiny", np.array([[1.0], [0.0]]), np.array([[0.0, 2.0]]), scale)
+
+
+def test_merge_small_exact():
+    layer = L.BaseLayer(np.eye(2, dtype=np.float32))
+    L.merge_in_place(layer, small_adapter())
+    assert np.array_equal(layer.weight, np.array([[1.0, 2.0], [0.0, 1.0]], dtype=np.float32))
+    assert layer.patched == [("tiny", 1.0)]
+
+
+def test_merge_scale_override():
+    layer = L.BaseLayer(np.eye(2, dtype=np.float32))
+    L.merge_in_place(layer, small_adapter(), scale=0.5)
+    assert np.array_equal(layer.weight, np.array([[1.0, 1.0], [0.0, 1.0]], dtype=np.float32))
+    assert layer.patched == [("tiny", 0.5)]
+
+
+def test_zero_adapter_is_identity():
+    rng = np.random.default_rng(0)
+    w = rng.uniform(-1, 1, size=(64, 48)).astype(np.float32)
+    layer = L.BaseLayer(w.copy())
+    L.merge_in_place(layer, L.LowRankAdapter("zero", np.zeros((64, 4), np.float32), np.zeros((4, 48), np.float32)))
+    assert np.array_equal(layer.weight, w)
+
+
+def test_double_merge_rejected():
+    layer = L.BaseLayer(np.eye(2, dtype=np.float32))
+    L.merge_in_place(layer, small_adapter())
+    with pytest.raises(ValidationError, match="already merged"):
+        L.merge_in_place(layer, small_adapter())
+
+
+def test_weight_aliasing_preserved():
+    w = np.eye(2, dtype=np.float32)
+    layer = L.BaseLayer(w)
+    assert layer.weight is w
+    L.merge_in_place(layer, small_adapter())
+    assert w[0, 1] == 2.0  # the caller's array was updated in place
+
+
+def test_fortran_order_weight():
+    rng = np.random.default_rng(11)
+    w = np.asfortranarray(rng.standard_normal((70, 50)).astype(np.float32))
+    d = rng.standard_normal((70, 5)).astype(np.float32)
+    u = rng.standard_normal((5, 50)).astype(np.float32)
+    exp = np.ascontiguousarray(w)
+    lora_ref.accumulate(exp, d, u, 0.5, 1.0)
+    layer = L.BaseLayer(w)
+    L.merge_in_place(layer, L.LowRankAdapter("f", d, u, 0.5))
+    assert layer.weight is w and w.flags.f_contiguous  # written back into the caller's F-order array
+    assert np.abs(w - exp).max() <= TOL
+
+
+@pytest.mark.parametrize("name", ["order_first", "order_second", "stack_a", "stack_b"])
+def test_matches_reference_outputs(name):
+    z = GOLD_NPZ
+    w, d, u, s = z[f"{name}__w"], z[f"{name}__down"], z[f"{name}__up"], float(z[f"{name}__scale"])
+    layer = L.BaseLayer(w.copy())
+    L.merge_in_place(layer, L.LowRankAdapter(name, d, u, s))
+    assert np.abs(layer.weight - z[f"{name}__merged"]).max() <= TOL
+
+
+def test_merge_unmerge_round_trip():
+    w, d, u, s = cases.lora_test_cases()["round_trip"]
+    layer = L.BaseLayer(w.copy())
+    ad = L.LowRankAdapter("a", d, u, s)
+    L.merge_in_place(layer, ad)
+    assert not np.array_equal(layer.weight, w)
+    L.unmerge_in_place(layer, ad)
+    assert np.max(np.abs(layer.weight - w)) <= TOL
+    assert layer.patched == []
+
+
+def test_round_trip_any_unmerge_order():
+    tc = cases.lora_test_cases()
+    w, d1, u1, s1 = tc["order_first"]
+    _, d2, u2, s2 = tc["order_second"]
+    first, second = L.LowRankAdapter("first", d1, u1, s1), L.LowRankAdapter("second", d2, u2, s2)
+    layer = L.BaseLayer(w.copy())
+    L.merge_in_place(layer, first)
+    L.merge_in_place(layer, second)
+    L.unmerge_in_place(layer, first)
+    L.unmerge_in_place(layer, second)
+    assert np.max(np.abs(layer.weight - w)) <= TOL
+
+
+def test_create_and_replace_matches_merge_bitwise():
+    w, d, u, s = cases.lora_test_cases()["create_replace"]
+    layer = L.BaseLayer(w.copy())
+    ad = L.LowRankAdapter("a", d, u, s)
+    aug = L.create_and_replace(layer, ad)
+    assert np.array_equal(layer.weight, w) and layer.patched == []
+    L.merge_in_place(layer, ad)
+    assert np.array_equal(aug.effective_weight, layer.weight)
+    assert np.array_equal(aug.base_weight, w)
+    assert aug.nbytes == 2 * layer.nbytes + ad.nbytes
+
+
+def test_stacked_equals_sequential_and_reference():
+    tc = cases.lora_test_cases()
+    w, da, ua, sa = tc["stack_a"]
+    _, db, ub, sb = tc["stack_b"]
+    a, b = L.LowRankAdapter("a", da, ua, sa), L.LowRankAdapter("b", db, ub, sb)
+    seq = L.BaseLayer(w.copy())
+    L.merge_in_place(seq, a, scale=0.7)
+    L.merge_in_place(seq, b, scale=0.3)
+    st = L.stack_adapters("stack", [(a, 0.7), (b, 0.3)])
+    comb = L.BaseLayer(w.copy())
+    L.merge_in_place(comb, st)
+    assert np.abs(seq.weight - comb.weight).max() <= TOL
+    assert np.abs(seq.weight - GOLD_NPZ["stacking__sequential"]).max() <= TOL
+    assert np.abs(comb.weight - GOLD_NPZ["stacking__stacked"]).max() <= TOL
+
+
+def test_merge_does_not_materialize_full_delta():
+    w, d, u, s = cases.lora_test_cases()["no_full_delta"]
+    layer = L.BaseLayer(w.copy())
+    ad = L.LowRankAdapter("a", d, u, s)
+    L.merge_in_place(L.BaseLayer(w.copy()), ad)  # warm up CUDA context / library
+    tracemalloc.start()
+    L.merge_in_place(layer, ad)
+    _, peak = tracemalloc.get_traced_memory()
+    tracemalloc.stop()
+    assert peak < 4 * 1024 * 1024
+    # device-resident: no h1*h2 temporary on the GPU either
+    wt = torch.from_numpy(w.copy()).cuda()
+    dt, ut = torch.from_numpy(d).cuda(), torch.from_numpy(u).cuda()
+    torch.cuda.synchronize()
+    base = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    ops.lora_patch_one(wt, dt, ut, s)
+    torch.cuda.synchronize()
+    assert torch.cuda.max_memory_allocated() - base < w.nbytes // 4
+
+
+def test_bench_merge_shape():
+    result = L.bench_merge(h1=256, h2=256, rank=8, repeats=2, seed=0)
+    assert result["merge_in_place_ms"] > 0 and result["create_and_replace_ms"] > 0
+    assert result["in_place_nbytes"] < result["create_and_replace_nbytes"]
+    assert result["h1"] == 256 and result["rank"] == 8
+    assert result["kernel_ms"] > 0
+
+
+def test_criterion9_on_gpu():
+    """test_acceptance.py:341-391 with the kernel: round trip <= 1e-5, route
+    equivalence <= 1e-6 (bitwise here), linearity <= 1e-5, and every merged
+    weight within 1e-5 of the reference (via the pinned oracle)."""
+    worst = {"round_trip": 0.0, "equivalence": 0.0, "linearity": 0.0, "vs_ref": 0.0}
+    for case in cases.criterion9_layers():
+        i = case["i"]
+        w = case["weight"]
+        d1, u1, s1 = case["first"]
+        d2, u2, s2 = case["second"]
+        a1, a2 = L.LowRankAdapter(f"a{i}", d1, u1, s1), L.LowRankAdapter(f"b{i}", d2, u2, s2)
+        layer = L.BaseLayer(w.copy())
+        L.merge_in_place(layer, a1)
+        merged = layer.weight.copy()
+        ref = w.copy()
+        lora_ref.accumulate(ref, d1, u1, s1, 1.0)
+        worst["vs_ref"] = max(worst["vs_ref"], float(np.abs(merged - ref).max()))
+        L.unmerge_in_place(layer, a1)
+        worst["round_trip"] = max(worst["round_trip"], float(np.abs(layer.weight - w).max()))
+        aug = L.create_and_replace(L.BaseLayer(w.copy()), a1)
+        worst["equivalence"] = max(worst["equivalence"], float(np.abs(aug.effective_weight - merged).max()))
+        seq = L.BaseLayer(w.copy())
+        L.merge_in_place(seq, a1, 0.7)
+        L.merge_in_place(seq, a2, 0.3)
+        comb = L.BaseLayer(w.copy())
+        L.merge_in_place(comb, L.stack_adapters(f"s{i}", [(a1, 0.7), (a2, 0.3)]))
+        worst["linearity"] = max(worst["linearity"], float(np.abs(seq.weight - comb.weight).max()))
+    print("criterion 9 on B200:", worst)
+    assert worst["round_trip"] <= 1e-5
+    assert worst["equivalence"] == 0.0
+    assert worst["linearity"] <= 1e-5
+    assert worst["vs_ref"] <= 1e-5
+
+
+def _bf16(a):
+    return torch.from_numpy(a).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("h1,h2,r", [(320, 36, 8), (1280, 1280, 16), (640, 2048, 64), (4, 2880, 8),
+                                     (10240, 1280, 128), (1280, 11520, 232), (77, 130, 3)])
+def test_bf16_within_one_ulp_of_reference(h1, h2, r):
+    """bf16 weights + bf16 factors: <= 1 bf16 ulp of bf16(ref_fp32(upcast inputs))."""
+    g = torch.Generator().manual_seed(h1 * 7 + h2 + r)
+    w = (torch.randn(h1, h2, generator=g) * 0.02).to(torch.bfloat16)
+    d = (torch.randn(h1, r, generator=g) / r ** 0.5).to(torch.bfloat16)
+    u = torch.randn(r, h2, generator=g).to(torch.bfloat16)
+    scale = 0.8
+    wd = w.cuda()
+    ops.lora_patch_one(wd, d.cuda(), u.cuda(), scale)
+    got = wd.float().cpu().numpy()
+    exp = lora_ref.accumulate_bf16(w.float().numpy(), d.float().numpy(), u.float().numpy(), scale, 1.0)
+    ulp = lora_ref.bf16_ulp(exp)
+    assert (np.abs(got - exp) <= ulp + 1e-30).all()
+
+
+def test_batched_plan_matches_single_and_is_deterministic():
+    """One batched launch over heterogeneous SDXL-like shapes == per-matrix
+    launches, bitwise; reruns bitwise identical; out-of-place leaves w_in."""
+    shapes = [(320, 36), (1280, 1280), (640, 2048), (4, 2880), (1280, 11520), (5120, 640), (1, 8)]
+    r = 24
+    g = torch.Generator().manual_seed(0)
+    ws = [(torch.randn(a, b, generator=g) * 0.02).to(torch.bfloat16).cuda() for a, b in shapes]
+    ds = [(torch.randn(a, r, generator=g) / 5).to(torch.bfloat16).cuda() for a, _ in shapes]
+    us = [torch.randn(r, b, generator=g).to(torch.bfloat16).cuda() for _, b in shapes]
+    outs = [torch.empty_like(w) for w in ws]
+    plan = ops.LoraPatchPlan([(w, o, d, u, 0.9) for w, o, d, u in zip(ws, outs, ds, us)])
+    plan.launch()
+    first = [o.clone() for o in outs]
+    plan.launch()
+    for a, b in zip(first, outs):
+        assert torch.equal(a, b)
+    for w, o, d, u in zip(ws, outs, ds, us):
+        single = w.clone()
+        ops.lora_patch_one(single, d, u, 0.9)
+        assert torch.equal(single, o)
+        assert not torch.equal(w, o) or w.numel() == 0
+
+
+def test_fp32_sdxl_shapes_rel_l2():
+    """fp32 weights on SDXL-shaped layers: rel-L2 <= 1e-5 vs the fp64 oracle."""
+    rng = np.random.default_rng(209)
+    for h1, h2, r in [(1280, 1280, 64), (10240, 1280, 32), (1280, 23040, 8), (640, 5760, 128)]:
+        w = rng.standard_normal((h1, h2)).astype(np.float32)
+        d = (rng.standard_normal((h1, r)) / np.sqrt(r)).astype(np.float32)
+        u = rng.standard_normal((r, h2)).astype(np.float32)
+        layer = L.BaseLayer(w.copy())
+        L.merge_in_place(layer, L.LowRankAdapter("x", d, u, 0.6))
+        ref = w.copy()
+        lora_ref.accumulate(ref, d, u, 0.6, 1.0)
+        rel = np.linalg.norm((layer.weight - ref).ravel()) / np.linalg.norm(ref.ravel())
+        assert rel <= 1e-5, (h1, h2, r, rel)
+        assert np.abs(layer.weight - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max())
+
+
+def test_torch_device_layer_in_place():
+    g = torch.Generator().manual_seed(3)
+    w = torch.randn(300, 200, generator=g).cuda()
+    d = torch.randn(300, 8, generator=g).cuda()
+    u = torch.randn(8, 200, generator=g).cuda()
+    layer = L.BaseLayer(w)
+    ad = L.LowRankAdapter("t", d, u, 0.5)
+    before = w.clone()
+    L.merge_in_place(layer, ad)
+    assert layer.weight.data_ptr() == w.data_ptr()
+    exp = before.double() + 0.5 * (d.double() @ u.double())
+    assert (w.double() - exp).abs().max().item() <= 1e-5
+    L.unmerge_in_place(layer, ad)
+    assert (w - before).abs().max().item() <= 1e-5
