@@ -102,7 +102,8 @@ int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t 
 
 /* ========================================================================
  * K2 — GroupNorm (+ optional SiLU), NHWC.
- *   y = act( (x - mean_g) * rstd_g * gamma_c + beta_c )
+ *   x' = x + add_nc[n, c]            (add_nc may be NULL: fused ResNet temb add)
+ *   y  = act( (x' - mean_g(x')) * rstd_g(x') * gamma_c + beta_c )
  * The reference models this op only as a latency multiplier
  * (addonsim/model.py:66-70 unet_opt_submultipliers[2] = 1.072; paper
  * PAPER.md:572-576).  x, y: [N, HW, C] (channels innermost), dtype `dtype`;
@@ -111,7 +112,7 @@ int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t 
  * ======================================================================== */
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
 int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
-                       int64_t n, int64_t hw, int64_t c, int64_t groups, float eps,
+                       const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups, float eps,
                        int apply_silu, int dtype, void* workspace, void* stream);
 
 /* ========================================================================

@@ -89,7 +89,7 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.sdb_groupnorm_workspace.restype = ctypes.c_size_t
     lib.sdb_groupnorm_workspace.argtypes = [i64, i64, i64, i64]
     lib.sdb_groupnorm_silu.restype = i32
-    lib.sdb_groupnorm_silu.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, f32, i32, i32, vp, vp]
+    lib.sdb_groupnorm_silu.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, f32, i32, i32, vp, vp]
     lib.sdb_residual_inject.restype = i32
     lib.sdb_residual_inject.argtypes = [vp, vp, vp, ctypes.POINTER(ctypes.c_void_p),
                                         ctypes.POINTER(ctypes.c_float), i32, i64, i64, i64, i32, vp]

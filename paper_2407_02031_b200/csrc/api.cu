@@ -23,8 +23,8 @@ int lora_patch_tc(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles,
                   int max_ctas, cudaStream_t st);
 // groupnorm_silu.cu
 size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
-int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, int64_t n,
-                   int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype,
+int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
+                   const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype,
                    void* ws, cudaStream_t st);
 // residual_inject.cu
 int residual_inject(void* out, const void* hidden, const void* skip, const void* const* res,
@@ -126,10 +126,10 @@ size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups)
   return groupnorm_workspace(n, hw, c, groups);
 }
 
-int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, int64_t n,
-                       int64_t hw, int64_t c, int64_t groups, float eps, int apply_silu, int dtype,
-                       void* workspace, void* stream) {
-  return groupnorm_silu(x, y, gamma, beta, n, hw, c, groups, eps, apply_silu, dtype, workspace,
+int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
+                       const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups,
+                       float eps, int apply_silu, int dtype, void* workspace, void* stream) {
+  return groupnorm_silu(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, apply_silu, dtype, workspace,
                         as_stream(stream));
 }
 

@@ -23,6 +23,10 @@
 // (<= 63 MB at CFG batch 2) stays in the 126 MB L2, so HBM traffic stays close
 // to the algorithmic one read + one write.  The shift K_g (the group's first
 // element) keeps the one-pass variance free of cancellation.
+//
+// Optional add_nc [N][C] (fp32) is added to x before normalisation: the
+// ResNet block's time-embedding projection (h = conv1(x) + temb_proj[n, c])
+// is fused here instead of costing its own read + write of the feature map.
 #include "common.cuh"
 
 namespace sdb {
@@ -54,7 +58,8 @@ GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups) {
 
 // partial[n][chunk][group][2]
 template <typename T>
-__global__ void gn_partial_kernel(const T* __restrict__ x, float* __restrict__ partial,
+__global__ void gn_partial_kernel(const T* __restrict__ x, const float* __restrict__ add_nc,
+                                  float* __restrict__ partial,
                                   int64_t hw, int64_t c, int64_t groups, int64_t cpg,
                                   int64_t rows_per_chunk, int64_t chunks, int rpp) {
   extern __shared__ float red[];  // [rpp][c][2] then reused
@@ -67,9 +72,13 @@ __global__ void gn_partial_kernel(const T* __restrict__ x, float* __restrict__ p
   const T* xs = x + n * hw * c;
 
   // per-channel shift = first element of its group (pixel 0, channel g*cpg)
+  // (the optional per-(n,c) input bias is folded into the shift: d = x - (K - a))
   float K[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) K[j] = to_f32<T>(xs[((c0 + j) / cpg) * cpg]);
+  for (int j = 0; j < 8; ++j) {
+    K[j] = to_f32<T>(xs[((c0 + j) / cpg) * cpg]);
+    if (add_nc != nullptr) K[j] -= add_nc[n * c + c0 + j];
+  }
 
   float s1[8], s2[8];
 #pragma unroll
@@ -147,6 +156,7 @@ __global__ void gn_finalize_kernel(const T* __restrict__ x, const float* __restr
 
 template <typename T, bool SILU>
 __global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
+                                const float* __restrict__ add_nc,
                                 const float* __restrict__ stats, const float* __restrict__ gamma,
                                 const float* __restrict__ beta, int64_t hw, int64_t c,
                                 int64_t groups, int64_t cpg, int64_t rows_per_chunk, int rpp) {
@@ -165,8 +175,9 @@ __global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread rea
     const float rstd = stats[(n * groups + g) * 2 + 1];
     const float ga = gamma ? gamma[ch] : 1.f;
     const float be = beta ? beta[ch] : 0.f;
+    const float ad = add_nc ? add_nc[n * c + ch] : 0.f;
     A[j] = ga * rstd;
-    B[j] = be - mean * A[j];
+    B[j] = be + (ad - mean) * A[j];
   }
   const T* xs = x + n * hw * c;
   T* ys = y + n * hw * c;
@@ -186,7 +197,7 @@ __global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread rea
 }
 
 template <typename T>
-int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, int64_t n,
+int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, const float* add_nc, int64_t n,
            int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* ws,
            cudaStream_t st) {
   const T* x = static_cast<const T*>(xv);
@@ -199,7 +210,7 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, int6
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(gn_partial_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  gn_partial_kernel<T><<<grid, s.threads, smem, st>>>(x, partial, hw, c, groups, s.cpg,
+  gn_partial_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, partial, hw, c, groups, s.cpg,
                                                       s.rows_per_chunk, s.chunks, s.rpp);
   if (int rc = check_launch("gn_partial_kernel")) return rc;
   int64_t ng = n * groups;
@@ -207,10 +218,10 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, int6
                                                                     s.cpg, s.chunks, eps);
   if (int rc = check_launch("gn_finalize_kernel")) return rc;
   if (silu)
-    gn_apply_kernel<T, true><<<grid, s.threads, 0, st>>>(x, y, stats, gamma, beta, hw, c, groups, s.cpg,
+    gn_apply_kernel<T, true><<<grid, s.threads, 0, st>>>(x, y, add_nc, stats, gamma, beta, hw, c, groups, s.cpg,
                                                          s.rows_per_chunk, s.rpp);
   else
-    gn_apply_kernel<T, false><<<grid, s.threads, 0, st>>>(x, y, stats, gamma, beta, hw, c, groups, s.cpg,
+    gn_apply_kernel<T, false><<<grid, s.threads, 0, st>>>(x, y, add_nc, stats, gamma, beta, hw, c, groups, s.cpg,
                                                           s.rows_per_chunk, s.rpp);
   return check_launch("gn_apply_kernel");
 }
@@ -222,7 +233,8 @@ size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
   return (size_t)(n * s.chunks * groups * 2 + n * groups * 2) * sizeof(float);
 }
 
-int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, int64_t n,
+int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
+                   const float* add_nc, int64_t n,
                    int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype,
                    void* ws, cudaStream_t st) {
   if (n <= 0 || hw <= 0 || c <= 0 || groups <= 0) return fail(SDB_EINVAL, "groupnorm: empty shape");
@@ -233,9 +245,9 @@ int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta
     return fail(SDB_EINVAL, "groupnorm: x and y must be 16-byte aligned");
   if (ws == nullptr) return fail(SDB_EINVAL, "groupnorm: workspace is NULL");
   switch (dtype) {
-    case SDB_BF16: return run_gn<__nv_bfloat16>(x, y, gamma, beta, n, hw, c, groups, eps, silu, ws, st);
-    case SDB_F16: return run_gn<__half>(x, y, gamma, beta, n, hw, c, groups, eps, silu, ws, st);
-    case SDB_F32: return run_gn<float>(x, y, gamma, beta, n, hw, c, groups, eps, silu, ws, st);
+    case SDB_BF16: return run_gn<__nv_bfloat16>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
+    case SDB_F16: return run_gn<__half>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
+    case SDB_F32: return run_gn<float>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
     default: return fail(SDB_EUNSUP, "groupnorm: unsupported dtype");
   }
 }

@@ -176,18 +176,27 @@ def nhwc_view(x: torch.Tensor) -> tuple[int, int, int]:
 
 def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optional[torch.Tensor],
                    groups: int = 32, eps: float = 1e-5, silu: bool = True,
-                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
-    require_cuda(x, gamma, beta, out)
+                   out: Optional[torch.Tensor] = None,
+                   add_nc: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """act(GroupNorm(x + add_nc[:, :, None, None])) in one NHWC pass pair.
+
+    add_nc: optional fp32 [N, C] bias added before normalisation (the ResNet
+    time-embedding projection)."""
+    require_cuda(x, gamma, beta, out, add_nc)
     n, hw, c = nhwc_view(x)
     if out is None:
         out = torch.empty_like(x)
-    if gamma is not None and gamma.dtype != torch.float32:
-        raise ValidationError("gamma/beta must be fp32")
+    for t in (gamma, beta, add_nc):
+        if t is not None and (t.dtype != torch.float32 or not t.is_contiguous()):
+            raise ValidationError("gamma / beta / add_nc must be contiguous fp32")
+    if add_nc is not None and add_nc.numel() != n * c:
+        raise ValidationError(f"add_nc must hold N*C = {n * c} values")
     ws_bytes = _lib.lib().sdb_groupnorm_workspace(n, hw, c, groups)
     ws = _workspace(ws_bytes, x.device)
     _lib.check("sdb_groupnorm_silu", _lib.lib().sdb_groupnorm_silu(
         x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,
-        beta.data_ptr() if beta is not None else None, n, hw, c, groups, float(eps), int(silu),
+        beta.data_ptr() if beta is not None else None,
+        add_nc.data_ptr() if add_nc is not None else None, n, hw, c, groups, float(eps), int(silu),
         sdb_dtype(x), ws.data_ptr(), _stream_ptr(None)))
     return out
 

@@ -1,0 +1,307 @@
+"""The per-step denoising loop with ControlNet residual injection, CFG and the
+asynchronous LoRA patch — the path the north_star names, on one GPU.
+
+What the reference models (addonsim/orchestrator.py, virtual clock) and where
+it is real here:
+
+* step = ControlNets then UNet encoder/decoder (serial mode,
+  orchestrator.py:611-619 ``_run_plain_step``); ControlNet outputs are summed
+  into the skips/mid by K3 with their conditioning scales; the
+  decoder consumes them after every branch finished (orchestrator.py:652-653).
+  The multi-GPU service mode (``_run_parallel_step`` :621-660) is caas.py.
+* CFG: one batch of 2 ([uncond; cond]); K4 fuses guidance + DDIM update +
+  re-batching of the next UNet input, and advances the device step counter,
+  so each step replays as ONE CUDA graph with no host work in between.
+* async LoRA (orchestrator.py:509-528, 698-719): the whole
+  adapter set is patched by one K1 launch into shadow weights on a
+  low-priority side stream while steps 1..k run; step k+1 onward replays the
+  graph captured on the shadow weights after waiting on the patch event.
+  k comes from ``schedule.plan_lora_patch`` with the measured patch time as
+  the "load" (deterministic; parity tests force it).  Unpatch = switch back
+  to the pristine graph (exact).
+
+Latents are NHWC end to end (the fp32 master latent is [H, W, 4] flat).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import ops
+from .patcher import PatchSet, UNetLora, allocate_shadow
+from .scheduler import ddim_tables
+from .schedule import plan_lora_patch
+from .unet import ControlNet, UNet, UNetConfig, init_controlnet, init_unet
+
+
+@dataclass
+class Request:
+    """Host-side inputs of one image (CFG batch of 2 = [uncond; cond])."""
+
+    latent: np.ndarray          # [4, H, W] float32 initial noise
+    context: np.ndarray         # [2, ctx_len, ctx_dim] float32 text embeddings
+    images: list                # per ControlNet: [2, 3, 8H, 8W] float32 in [0, 1]
+    pooled: Optional[np.ndarray] = None    # [2, 1280] (SDXL)
+    time_ids: Optional[np.ndarray] = None  # [2, 6]    (SDXL)
+
+    def nbytes(self) -> int:
+        n = self.latent.nbytes + self.context.nbytes + sum(i.nbytes for i in self.images)
+        n += self.pooled.nbytes if self.pooled is not None else 0
+        n += self.time_ids.nbytes if self.time_ids is not None else 0
+        return n
+
+
+def synthetic_request(cfg: UNetConfig, n_controlnets: int, seed: int = 0) -> Request:
+    """Seeds as SURVEY §8d: latents 1, control image 2, text 3 (offset by seed)."""
+    h = cfg.latent_hw
+    lat = np.random.default_rng(1 + seed).standard_normal((4, h, h)).astype(np.float32)
+    ctx = np.random.default_rng(3 + seed).standard_normal((2, cfg.context_len, cfg.context_dim)).astype(np.float32)
+    imgs = [np.random.default_rng(2 + seed + 17 * i).uniform(0, 1, (2, 3, 8 * h, 8 * h)).astype(np.float32)
+            for i in range(n_controlnets)]
+    pooled = time_ids = None
+    if cfg.addition_embed:
+        pooled = np.random.default_rng(4 + seed).standard_normal((2, cfg.pooled_dim)).astype(np.float32)
+        px = 8 * h
+        time_ids = np.array([[px, px, 0, 0, px, px]] * 2, dtype=np.float32)
+    return Request(lat, ctx, imgs, pooled, time_ids)
+
+
+class AddonPipeline:
+    """SD-style UNet + N ControlNets + LoRA on one B200."""
+
+    def __init__(self, cfg: UNetConfig, n_controlnets: int = 1, cn_scales: Optional[Sequence[float]] = None,
+                 steps: int = 30, guidance: float = 7.5, device="cuda", dtype=torch.bfloat16,
+                 seed: int = 0, use_graphs: bool = True, patch_max_ctas: int = 0):
+        ops.require_cuda(torch.empty(1, device=device))
+        self.cfg, self.steps, self.guidance = cfg, steps, guidance
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.unet_p = init_unet(cfg, self.device, dtype, seed)
+        self.cn_p = [init_controlnet(cfg, self.device, dtype, seed=1000 + i) for i in range(n_controlnets)]
+        self.unet = UNet(cfg, self.unet_p)
+        self.cns = [ControlNet(cfg, p) for p in self.cn_p]
+        self.cn_scales = list(cn_scales) if cn_scales is not None else [0.8] * n_controlnets
+        self.use_graphs = use_graphs
+        self.patch_max_ctas = patch_max_ctas
+        h = cfg.latent_hw
+        dev = self.device
+        self.L = 4 * h * h
+        self.x = torch.zeros(self.L, device=dev, dtype=torch.float32)
+        self.unet_in = torch.zeros((2, 4, h, h), device=dev, dtype=dtype).contiguous(memory_format=torch.channels_last)
+        self.ctx = torch.zeros((2, cfg.context_len, cfg.context_dim), device=dev, dtype=dtype)
+        self.pooled = torch.zeros((2, cfg.pooled_dim), device=dev, dtype=torch.float32)
+        self.time_ids = torch.zeros((2, cfg.time_ids), device=dev, dtype=torch.float32)
+        self.images = [torch.zeros((2, 3, 8 * h, 8 * h), device=dev, dtype=dtype) for _ in self.cns]
+        self.hints = [torch.zeros((2, cfg.block_channels[0], h, h), device=dev, dtype=dtype)
+                      .contiguous(memory_format=torch.channels_last) for _ in self.cns]
+        temb = cfg.time_embed_dim
+        self.add_emb_unet = torch.zeros((2, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
+        self.add_emb_cn = [torch.zeros((2, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
+                           for _ in self.cns]
+        tab = ddim_tables(steps, guidance)
+        pad = 8  # capture warm-ups advance the step counter past the table end
+        t_tab = np.concatenate([tab.timesteps.astype(np.float32), np.full(pad, tab.timesteps[-1], np.float32)])
+        coef = np.concatenate([tab.coef, np.repeat(tab.coef[-1:], pad, axis=0)])
+        self.timesteps = tab.timesteps
+        self.t_table = torch.from_numpy(t_tab).to(dev)
+        self.coef = torch.from_numpy(coef).to(dev)
+        self.step_dev = torch.zeros(2, device=dev, dtype=torch.int32)
+        self.main_stream = torch.cuda.Stream(device=dev, priority=-1)
+        self.patch_stream = torch.cuda.Stream(device=dev, priority=0)
+        self.shadow = None
+        self.patchset: Optional[PatchSet] = None
+        self.graphs: dict = {}
+        self.pool = None
+        self.eps = None
+        self.step_ms_est = None
+        self.patch_ms_est = None
+        self.last_first_patched_step = None
+
+    # ------------------------------------------------------------------
+    def _use_weights(self, which: str) -> None:
+        src = self.shadow if which == "patched" else self._pristine
+        for name, _ in self.unet_p.matrices:
+            self.unet_p.t[name + ".weight"] = src[name]
+
+    @property
+    def _pristine(self) -> dict:
+        if not hasattr(self, "_pristine_w"):
+            self._pristine_w = {n: self.unet_p.t[n + ".weight"] for n, _ in self.unet_p.matrices}
+        return self._pristine_w
+
+    def step_once(self) -> None:
+        """One denoising step, reading everything from static buffers."""
+        t = self.t_table.index_select(0, self.step_dev[:1].long())
+        residuals = [cn.forward(self.unet_in, t, self.ctx, self.hints[i], self.add_emb_cn[i])
+                     for i, cn in enumerate(self.cns)]
+        eps = self.unet.forward(self.unet_in, t, self.ctx, self.add_emb_unet,
+                                residuals if residuals else None, self.cn_scales if residuals else None)
+        ops.cfg_ddim_step(eps, self.x, self.coef, self.step_dev, unet_in=self.unet_in)
+        self.eps = eps
+
+    def _capture(self, which: str) -> None:
+        _ = self._pristine
+        self._use_weights(which)
+        s = torch.cuda.current_stream(self.device)
+        self.step_dev.zero_()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(s)
+        with torch.cuda.stream(side):
+            for _ in range(2):
+                self.step_once()
+        s.wait_stream(side)
+        self.step_dev.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, pool=self.pool):
+            self.step_once()
+        if self.pool is None:
+            self.pool = g.pool()
+        self.graphs[which] = g
+        self._use_weights("pristine")
+        torch.cuda.synchronize(self.device)
+
+    # ------------------------------------------------------------------
+    def load_loras(self, adapters: Sequence[tuple[UNetLora, float]]) -> PatchSet:
+        """Stack the request's adapters into one planned K1 launch writing the
+        shadow weights (allocated once)."""
+        if self.shadow is None:
+            _ = self._pristine
+            self.shadow = allocate_shadow(self.unet_p)
+        self.patchset = PatchSet(self.unet_p, adapters, shadow=self.shadow)
+        self.patchset.copy_unpatched()
+        if self.use_graphs and "patched" not in self.graphs:
+            self._capture("patched")
+        return self.patchset
+
+    def setup(self) -> None:
+        if self.use_graphs and "pristine" not in self.graphs:
+            self._capture("pristine")
+
+    def calibrate(self, reps: int = 3) -> tuple[float, float]:
+        """Measure one step and one patch launch (CUDA events) for the
+        patch-boundary plan."""
+        self.setup()
+        torch.cuda.synchronize(self.device)
+        s = self.main_stream
+        with torch.cuda.stream(s):
+            self.step_dev.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            self._replay("pristine")
+            e0.record(s)
+            for _ in range(reps):
+                self._replay("pristine")
+            e1.record(s)
+        e1.synchronize()
+        self.step_ms_est = e0.elapsed_time(e1) / reps
+        if self.patchset is not None:
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(self.patch_stream)
+            self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+            p1.record(self.patch_stream)
+            p1.synchronize()
+            self.patch_ms_est = p0.elapsed_time(p1)
+        return self.step_ms_est, self.patch_ms_est
+
+    def _replay(self, which: str) -> None:
+        if self.use_graphs:
+            self.graphs[which].replay()
+        else:
+            self._use_weights(which)
+            self.step_once()
+            self._use_weights("pristine")
+
+    # ------------------------------------------------------------------
+    def prepare(self, latent: torch.Tensor, context: torch.Tensor, images: Sequence[torch.Tensor],
+                pooled: Optional[torch.Tensor] = None, time_ids: Optional[torch.Tensor] = None) -> None:
+        """Load one request's (device or pinned-host) inputs into the static
+        buffers and compute the step-invariant pieces (hint embeddings, SDXL
+        added-condition embeddings)."""
+        h = self.cfg.latent_hw
+        nb = True
+        self.x.view(h, h, 4).copy_(latent.to(self.device, non_blocking=nb).permute(1, 2, 0))
+        self.unet_in.copy_(self.x.view(1, h, h, 4).permute(0, 3, 1, 2).expand(2, 4, h, h))
+        self.ctx.copy_(context.to(self.device, non_blocking=nb))
+        for buf, img in zip(self.images, images):
+            buf.copy_(img.to(self.device, non_blocking=nb))
+        if self.cfg.addition_embed:
+            self.pooled.copy_(pooled.to(self.device, non_blocking=nb))
+            self.time_ids.copy_(time_ids.to(self.device, non_blocking=nb))
+            self.add_emb_unet.copy_(self.unet.add_embedding(self.pooled, self.time_ids))
+        for i, cn in enumerate(self.cns):
+            self.hints[i].copy_(cn.hint_embedding(self.images[i]))
+            if self.cfg.addition_embed:
+                self.add_emb_cn[i].copy_(cn.add_embedding(self.pooled, self.time_ids))
+        self.step_dev.zero_()
+
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None) -> int:
+        """Run all steps on the current stream.  With ``patch`` the loaded
+        PatchSet is launched on the side stream at the start and swapped in
+        at boundary k (forced, or planned from the calibrated times).
+        Returns first_patched_step (steps + 1 = never)."""
+        s = torch.cuda.current_stream(self.device)
+        first = self.steps + 1
+        ev = None
+        if patch:
+            if self.patchset is None:
+                raise RuntimeError("denoise(patch=True) needs load_loras() first")
+            if boundary is None:
+                if self.step_ms_est is None or self.patch_ms_est is None:
+                    self.calibrate()
+                plan = plan_lora_patch(self.patch_ms_est, self.step_ms_est, 0.0, self.steps)
+                first = plan.first_patched_step
+            else:
+                first = boundary + 1
+            self.patch_stream.wait_stream(s)   # shadow is free once earlier work on s finished
+            self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+            ev = torch.cuda.Event()
+            ev.record(self.patch_stream)
+        waited = False
+        for step in range(1, self.steps + 1):
+            use_patched = patch and step >= first
+            if use_patched and not waited:
+                s.wait_event(ev)
+                waited = True
+            self._replay("patched" if use_patched else "pristine")
+            if on_step is not None:   # tests: per-step latent parity (syncs the host)
+                on_step(step, self.latent_nchw().clone())
+        if patch and not waited:
+            s.wait_event(ev)  # never leave the side stream dangling past the request
+        self.last_first_patched_step = first
+        return first
+
+    def latent_nchw(self) -> torch.Tensor:
+        h = self.cfg.latent_hw
+        return self.x.view(h, h, 4).permute(2, 0, 1)
+
+    # ------------------------------------------------------------------
+    def generate(self, req: Request, patch: bool = False, boundary: Optional[int] = None,
+                 pinned: Optional[dict] = None) -> np.ndarray:
+        """The end-to-end call: host inputs in, host latent out (H2D + denoise
+        + D2H on the current stream)."""
+        def host(a, key):
+            t = torch.from_numpy(a)
+            if pinned is not None:
+                buf = pinned.get(key)
+                if buf is None or buf.shape != t.shape:
+                    buf = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                    pinned[key] = buf
+                buf.copy_(t)
+                return buf
+            return t
+        lat = host(req.latent, "latent")
+        ctx = host(req.context, "ctx")
+        imgs = [host(im, f"img{i}") for i, im in enumerate(req.images)]
+        pooled = host(req.pooled, "pooled") if req.pooled is not None else None
+        tids = host(req.time_ids, "tids") if req.time_ids is not None else None
+        self.prepare(lat, ctx, imgs, pooled, tids)
+        self.denoise(patch=patch, boundary=boundary)
+        out = self.latent_nchw().contiguous().cpu()
+        return out.numpy()
+
+    def d2h_bytes(self) -> int:
+        return self.L * 4

@@ -1,0 +1,440 @@
+"""SD-style UNet and ControlNet on the B200 path (NHWC / channels_last, bf16).
+
+The reference ships no network (its denoising loop is a latency
+model, addonsim/orchestrator.py:586-719).  This module is the builder-authored
+model the north_star names: SD1.5- and SDXL-shaped UNets plus a ControlNet
+(encoder + mid copy with zero convs), laid out so that
+
+* every GroupNorm(+SiLU) site runs K2 (``ops.groupnorm_silu``), with the ResNet
+  time-embedding add fused into it (model.py:70 1.072);
+* every skip connection is consumed by K3 (``ops.residual_inject``), which adds
+  the ControlNet residuals while writing the up-block concat;
+* every linear / conv weight is a row-major (h1, h2) matrix in the reference's
+  LoRA layout (addonsim/lora.py:58-72: h1 = out, h2 = in*kh*kw), so one K1
+  launch patches them all.  Conv weights are kept channels_last, i.e. the
+  physical matrix is (Cout, kh*kw*Cin); LoRA ``up`` factors are permuted once
+  at load time to that column order (patcher.py).
+
+Convolutions, GEMMs, LayerNorm and attention (SDPA / flash) are library calls
+(cuDNN / cuBLAS), as the north_star allows; GEGLU fusion and decoupled CUDA
+graphs are the ranked "next" items.
+
+Weights are synthetic random-init (N(0, 0.02), norms 1/0, zero-convs non-zero
+N(0, 0.02) so residual parity is not vacuous, SURVEY §7 hard part 9).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+import torch.nn.functional as F
+
+from . import ops
+
+
+# --------------------------------------------------------------------------
+# configurations
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class UNetConfig:
+    name: str
+    block_channels: tuple            # per resolution level
+    layers_per_block: int
+    attn_depth: tuple                # transformer depth per level (0 = no attention)
+    mid_depth: int
+    head_dim: Optional[int]          # SDXL: 64-dim heads
+    num_heads: Optional[int]         # SD1.5: 8 heads
+    context_dim: int
+    addition_embed: bool             # SDXL text_time embedding
+    addition_time_embed_dim: int = 256
+    pooled_dim: int = 1280
+    time_ids: int = 6
+    latent_channels: int = 4
+    groups: int = 32
+    gn_eps: float = 1e-5
+    tf_gn_eps: float = 1e-6
+    hint_channels: tuple = (16, 32, 96, 256)  # ControlNet conditioning embedding
+    latent_hw: int = 64
+    context_len: int = 77
+
+    @property
+    def time_embed_dim(self) -> int:
+        return self.block_channels[0] * 4
+
+    def heads(self, c: int) -> int:
+        return c // self.head_dim if self.head_dim else self.num_heads
+
+
+SD15 = UNetConfig(name="sd15", block_channels=(320, 640, 1280, 1280), layers_per_block=2,
+                  attn_depth=(1, 1, 1, 0), mid_depth=1, head_dim=None, num_heads=8,
+                  context_dim=768, addition_embed=False, latent_hw=64)
+SDXL = UNetConfig(name="sdxl", block_channels=(320, 640, 1280), layers_per_block=2,
+                  attn_depth=(0, 2, 10), mid_depth=10, head_dim=64, num_heads=None,
+                  context_dim=2048, addition_embed=True, latent_hw=128)
+# config 1: toy CPU-oracle model
+TOY = UNetConfig(name="toy", block_channels=(32, 64), layers_per_block=1, attn_depth=(1, 1),
+                 mid_depth=1, head_dim=8, num_heads=None, context_dim=64, addition_embed=False,
+                 hint_channels=(8, 16, 16, 32), latent_hw=64, context_len=8)
+
+CONFIGS = {"sd15": SD15, "sdxl": SDXL, "toy": TOY}
+
+
+# --------------------------------------------------------------------------
+# parameters
+# --------------------------------------------------------------------------
+class Params:
+    """Named parameter store.  ``matrices`` lists every LoRA-patchable weight
+    as (name, 2-d row-major view of the physical storage, logical kind)."""
+
+    def __init__(self, device, dtype, seed: int):
+        self.device = torch.device(device)
+        self.dtype = dtype
+        # "meta" builds the layout only (inventory / planning without memory)
+        self.gen = None if self.device.type == "meta" else torch.Generator(device=self.device).manual_seed(seed)
+        self.t: dict[str, torch.Tensor] = {}
+        self.matrices: list[tuple[str, str]] = []  # (name, "linear"|"conv")
+
+    def _randn(self, shape, std):
+        return (torch.randn(shape, generator=self.gen, device=self.device, dtype=torch.float32) * std)
+
+    def linear(self, name, cin, cout, bias=True, std=0.02):
+        self.t[name + ".weight"] = self._randn((cout, cin), std).to(self.dtype)
+        if bias:
+            self.t[name + ".bias"] = torch.zeros(cout, device=self.device, dtype=self.dtype)
+        self.matrices.append((name, "linear"))
+
+    def conv(self, name, cin, cout, k, bias=True, std=0.02):
+        w = self._randn((cout, cin, k, k), std).to(self.dtype)
+        self.t[name + ".weight"] = w.contiguous(memory_format=torch.channels_last)
+        if bias:
+            self.t[name + ".bias"] = torch.zeros(cout, device=self.device, dtype=self.dtype)
+        self.matrices.append((name, "conv"))
+
+    def norm(self, name, c):
+        # GN affine in fp32 for K2; LayerNorm affine in the compute dtype
+        self.t[name + ".weight"] = torch.ones(c, device=self.device, dtype=torch.float32)
+        self.t[name + ".bias"] = torch.zeros(c, device=self.device, dtype=torch.float32)
+
+    def lnorm(self, name, c):
+        self.t[name + ".weight"] = torch.ones(c, device=self.device, dtype=self.dtype)
+        self.t[name + ".bias"] = torch.zeros(c, device=self.device, dtype=self.dtype)
+
+    def matrix_view(self, name: str) -> torch.Tensor:
+        """(h1, h2) row-major view of the weight's physical storage."""
+        w = self.t[name + ".weight"]
+        if w.dim() == 2:
+            return w
+        cout, cin, kh, kw = w.shape
+        return w.permute(0, 2, 3, 1).reshape(cout, kh * kw * cin)  # a view: channels_last storage
+
+    def numel(self) -> int:
+        return sum(v.numel() for v in self.t.values())
+
+
+def _resnet_params(p: Params, pre: str, cin: int, cout: int, temb: int):
+    p.norm(pre + ".norm1", cin)
+    p.conv(pre + ".conv1", cin, cout, 3)
+    p.linear(pre + ".time_emb_proj", temb, cout)
+    p.norm(pre + ".norm2", cout)
+    p.conv(pre + ".conv2", cout, cout, 3)
+    if cin != cout:
+        p.conv(pre + ".conv_shortcut", cin, cout, 1)
+
+
+def _transformer_params(p: Params, pre: str, c: int, depth: int, ctx: int):
+    p.norm(pre + ".norm", c)
+    p.linear(pre + ".proj_in", c, c)
+    for d in range(depth):
+        b = f"{pre}.blocks.{d}"
+        p.lnorm(b + ".norm1", c)
+        p.linear(b + ".attn1.to_q", c, c, bias=False)
+        p.linear(b + ".attn1.to_k", c, c, bias=False)
+        p.linear(b + ".attn1.to_v", c, c, bias=False)
+        p.linear(b + ".attn1.to_out", c, c)
+        p.lnorm(b + ".norm2", c)
+        p.linear(b + ".attn2.to_q", c, c, bias=False)
+        p.linear(b + ".attn2.to_k", ctx, c, bias=False)
+        p.linear(b + ".attn2.to_v", ctx, c, bias=False)
+        p.linear(b + ".attn2.to_out", c, c)
+        p.lnorm(b + ".norm3", c)
+        p.linear(b + ".ff.proj", c, 8 * c)      # GEGLU: value and gate halves
+        p.linear(b + ".ff.out", 4 * c, c)
+    p.linear(pre + ".proj_out", c, c)
+
+
+def _embedding_params(p: Params, cfg: UNetConfig):
+    c0, temb = cfg.block_channels[0], cfg.time_embed_dim
+    p.linear("time_embedding.linear_1", c0, temb)
+    p.linear("time_embedding.linear_2", temb, temb)
+    if cfg.addition_embed:
+        p.linear("add_embedding.linear_1", cfg.time_ids * cfg.addition_time_embed_dim + cfg.pooled_dim, temb)
+        p.linear("add_embedding.linear_2", temb, temb)
+    p.conv("conv_in", cfg.latent_channels, c0, 3)
+
+
+def _down_params(p: Params, cfg: UNetConfig):
+    """Encoder; returns the channel count of every skip it produces."""
+    temb = cfg.time_embed_dim
+    skips = [cfg.block_channels[0]]
+    cin = cfg.block_channels[0]
+    n = len(cfg.block_channels)
+    for i, c in enumerate(cfg.block_channels):
+        for j in range(cfg.layers_per_block):
+            _resnet_params(p, f"down.{i}.res.{j}", cin, c, temb)
+            if cfg.attn_depth[i]:
+                _transformer_params(p, f"down.{i}.attn.{j}", c, cfg.attn_depth[i], cfg.context_dim)
+            cin = c
+            skips.append(c)
+        if i < n - 1:
+            p.conv(f"down.{i}.downsample", c, c, 3)
+            skips.append(c)
+    cm = cfg.block_channels[-1]
+    _resnet_params(p, "mid.res.0", cm, cm, temb)
+    _transformer_params(p, "mid.attn.0", cm, cfg.mid_depth, cfg.context_dim)
+    _resnet_params(p, "mid.res.1", cm, cm, temb)
+    return skips
+
+
+def init_unet(cfg: UNetConfig, device="cuda", dtype=torch.bfloat16, seed: int = 0) -> Params:
+    p = Params(device, dtype, seed)
+    _embedding_params(p, cfg)
+    skips = _down_params(p, cfg)
+    temb = cfg.time_embed_dim
+    rev = list(reversed(cfg.block_channels))
+    n = len(rev)
+    cin = rev[0]
+    for i, c in enumerate(rev):
+        depth = cfg.attn_depth[n - 1 - i]
+        for j in range(cfg.layers_per_block + 1):
+            skip_c = skips.pop()
+            _resnet_params(p, f"up.{i}.res.{j}", cin + skip_c, c, temb)
+            if depth:
+                _transformer_params(p, f"up.{i}.attn.{j}", c, depth, cfg.context_dim)
+            cin = c
+        if i < n - 1:
+            p.conv(f"up.{i}.upsample", c, c, 3)
+    p.norm("conv_norm_out", cfg.block_channels[0])
+    p.conv("conv_out", cfg.block_channels[0], cfg.latent_channels, 3)
+    return p
+
+
+def init_controlnet(cfg: UNetConfig, device="cuda", dtype=torch.bfloat16, seed: int = 1) -> Params:
+    p = Params(device, dtype, seed)
+    _embedding_params(p, cfg)
+    skips = _down_params(p, cfg)
+    # conditioning embedding: 3 -> hint_channels..., stride-2 convs down to latent res, -> C0
+    hc = cfg.hint_channels
+    p.conv("cond_embedding.conv_in", 3, hc[0], 3)
+    for i in range(len(hc) - 1):
+        p.conv(f"cond_embedding.blocks.{2 * i}", hc[i], hc[i], 3)
+        p.conv(f"cond_embedding.blocks.{2 * i + 1}", hc[i], hc[i + 1], 3)
+    p.conv("cond_embedding.conv_out", hc[-1], cfg.block_channels[0], 3)
+    for k, c in enumerate(skips):
+        p.conv(f"zero_convs.{k}", c, c, 1)       # non-zero N(0, 0.02): parity is not vacuous
+    p.conv("mid_zero_conv", cfg.block_channels[-1], cfg.block_channels[-1], 1)
+    return p
+
+
+def skip_channels(cfg: UNetConfig) -> list[int]:
+    """Channel count of every down-path skip (= ControlNet down residual)."""
+    skips = [cfg.block_channels[0]]
+    for i, c in enumerate(cfg.block_channels):
+        skips += [c] * cfg.layers_per_block
+        if i < len(cfg.block_channels) - 1:
+            skips.append(c)
+    return skips
+
+
+def skip_shapes(cfg: UNetConfig, batch: int) -> list[tuple]:
+    """(N, C, H, W) of every down residual then the mid residual."""
+    h = cfg.latent_hw
+    shapes = [(batch, cfg.block_channels[0], h, h)]
+    for i, c in enumerate(cfg.block_channels):
+        shapes += [(batch, c, h, h)] * cfg.layers_per_block
+        if i < len(cfg.block_channels) - 1:
+            h //= 2
+            shapes.append((batch, c, h, h))
+    shapes.append((batch, cfg.block_channels[-1], h, h))
+    return shapes
+
+
+# --------------------------------------------------------------------------
+# forward (device path: K2 / K3 kernels + library convs / GEMMs / SDPA)
+# --------------------------------------------------------------------------
+def timestep_embedding(t: torch.Tensor, dim: int, max_period: float = 10000.0) -> torch.Tensor:
+    """Sinusoidal embedding, flip_sin_to_cos=True, shift 0 (diffusers SD config)."""
+    half = dim // 2
+    freqs = torch.exp(-math.log(max_period) * torch.arange(half, device=t.device, dtype=torch.float32) / half)
+    args = t.float()[:, None] * freqs[None]
+    return torch.cat([torch.cos(args), torch.sin(args)], dim=-1)
+
+
+def _cl(x: torch.Tensor) -> torch.Tensor:
+    return x.contiguous(memory_format=torch.channels_last)
+
+
+class Net:
+    """Shared forward machinery for the UNet and the ControlNet."""
+
+    def __init__(self, cfg: UNetConfig, params: Params):
+        self.cfg = cfg
+        self.p = params
+        self.t = params.t
+
+    # -- primitives -------------------------------------------------------
+    def lin(self, name, x):
+        return F.linear(x, self.t[name + ".weight"], self.t.get(name + ".bias"))
+
+    def conv(self, name, x, stride=1):
+        w = self.t[name + ".weight"]
+        pad = w.shape[-1] // 2
+        return F.conv2d(x, w, self.t.get(name + ".bias"), stride=stride, padding=pad)
+
+    def gn(self, name, x, silu, eps=None, add_nc=None):
+        return ops.groupnorm_silu(x, self.t[name + ".weight"], self.t[name + ".bias"],
+                                  groups=self.cfg.groups, eps=self.cfg.gn_eps if eps is None else eps,
+                                  silu=silu, add_nc=add_nc)
+
+    # -- blocks -----------------------------------------------------------
+    def resnet(self, pre, x, temb_act):
+        h = self.conv(pre + ".conv1", self.gn(pre + ".norm1", x, True))
+        tproj = self.lin(pre + ".time_emb_proj", temb_act).float().contiguous()
+        h = self.gn(pre + ".norm2", h, True, add_nc=tproj)       # fused temb add + GN + SiLU
+        h = self.conv(pre + ".conv2", h)
+        sc = self.conv(pre + ".conv_shortcut", x) if (pre + ".conv_shortcut.weight") in self.t else x
+        return h.add_(sc)
+
+    def attention(self, pre, x, ctx, heads):
+        n, l, c = x.shape
+        q = self.lin(pre + ".to_q", x)
+        src = x if ctx is None else ctx
+        k = self.lin(pre + ".to_k", src)
+        v = self.lin(pre + ".to_v", src)
+        d = c // heads
+        q = q.view(n, l, heads, d).transpose(1, 2)
+        k = k.view(n, -1, heads, d).transpose(1, 2)
+        v = v.view(n, -1, heads, d).transpose(1, 2)
+        o = F.scaled_dot_product_attention(q, k, v)
+        o = o.transpose(1, 2).reshape(n, l, c)
+        return self.lin(pre + ".to_out", o)
+
+    def transformer(self, pre, x, ctx, depth):
+        n, c, h, w = x.shape
+        res = x
+        hs = self.gn(pre + ".norm", x, False, eps=self.cfg.tf_gn_eps)
+        tok = hs.permute(0, 2, 3, 1).reshape(n, h * w, c)       # NHWC storage: a free view
+        tok = self.lin(pre + ".proj_in", tok)
+        heads = self.cfg.heads(c)
+        for d in range(depth):
+            b = f"{pre}.blocks.{d}"
+            y = F.layer_norm(tok, (c,), self.t[b + ".norm1.weight"], self.t[b + ".norm1.bias"])
+            tok = tok + self.attention(b + ".attn1", y, None, heads)
+            y = F.layer_norm(tok, (c,), self.t[b + ".norm2.weight"], self.t[b + ".norm2.bias"])
+            tok = tok + self.attention(b + ".attn2", y, ctx, heads)
+            y = F.layer_norm(tok, (c,), self.t[b + ".norm3.weight"], self.t[b + ".norm3.bias"])
+            hv, gate = self.lin(b + ".ff.proj", y).chunk(2, dim=-1)
+            tok = tok + self.lin(b + ".ff.out", hv * F.gelu(gate))
+        tok = self.lin(pre + ".proj_out", tok)
+        out = tok.view(n, h, w, c).permute(0, 3, 1, 2)            # channels_last view
+        return out + res
+
+    # -- embeddings ---------------------------------------------------------
+    def add_embedding(self, pooled: torch.Tensor, time_ids: torch.Tensor) -> torch.Tensor:
+        """SDXL text_time embedding — step-invariant, computed once per request."""
+        cfg = self.cfg
+        n = pooled.shape[0]
+        tid = timestep_embedding(time_ids.reshape(-1), cfg.addition_time_embed_dim).reshape(n, -1)
+        a = torch.cat([pooled.float(), tid], dim=-1).to(self.p.dtype)
+        return self.lin("add_embedding.linear_2", F.silu(self.lin("add_embedding.linear_1", a)))
+
+    def time_embedding(self, t: torch.Tensor, batch: int, add_emb: Optional[torch.Tensor]):
+        te = timestep_embedding(t.reshape(-1)[:1].expand(batch), self.cfg.block_channels[0]).to(self.p.dtype)
+        emb = self.lin("time_embedding.linear_2", F.silu(self.lin("time_embedding.linear_1", te)))
+        if add_emb is not None:
+            emb = emb + add_emb
+        return F.silu(emb)   # every consumer (time_emb_proj) applies SiLU first
+
+    # -- encoder ------------------------------------------------------------
+    def encode(self, x, temb_act, ctx, hint=None):
+        """conv_in + down blocks + mid; returns (mid, [skips])."""
+        cfg = self.cfg
+        h = self.conv("conv_in", x)
+        if hint is not None:
+            h = h + hint
+        skips = [h]
+        n = len(cfg.block_channels)
+        for i in range(n):
+            for j in range(cfg.layers_per_block):
+                h = self.resnet(f"down.{i}.res.{j}", h, temb_act)
+                if cfg.attn_depth[i]:
+                    h = self.transformer(f"down.{i}.attn.{j}", h, ctx, cfg.attn_depth[i])
+                skips.append(h)
+            if i < n - 1:
+                h = self.conv(f"down.{i}.downsample", h, stride=2)
+                skips.append(h)
+        h = self.resnet("mid.res.0", h, temb_act)
+        h = self.transformer("mid.attn.0", h, ctx, cfg.mid_depth)
+        h = self.resnet("mid.res.1", h, temb_act)
+        return h, skips
+
+
+class UNet(Net):
+    def decode(self, h, skips, temb_act, ctx, residuals=None, res_scales=None):
+        """Up path.  ``residuals``: per ControlNet, a list of down residuals
+        (same order as skips) + a mid residual, scaled by ``res_scales``; they
+        are injected by K3 while the skip concat is written."""
+        cfg = self.cfg
+        nres = 0 if residuals is None else len(residuals)
+        if nres:
+            ops.residual_inject(h, [r[-1] for r in residuals], res_scales)       # mid (in place)
+        rev = list(reversed(cfg.block_channels))
+        n = len(rev)
+        k = len(skips)
+        for i, c in enumerate(rev):
+            depth = cfg.attn_depth[n - 1 - i]
+            for j in range(cfg.layers_per_block + 1):
+                k -= 1
+                res_k = [r[k] for r in residuals] if nres else []
+                h = ops.residual_inject(skips[k], res_k, res_scales if nres else [], hidden=h)
+                h = self.resnet(f"up.{i}.res.{j}", h, temb_act)
+                if depth:
+                    h = self.transformer(f"up.{i}.attn.{j}", h, ctx, depth)
+            if i < n - 1:
+                h = F.interpolate(h, scale_factor=2.0, mode="nearest")
+                h = self.conv(f"up.{i}.upsample", _cl(h))
+        h = self.gn("conv_norm_out", h, True)
+        return self.conv("conv_out", h)
+
+    def forward(self, x, t, ctx, add_emb=None, residuals=None, res_scales=None):
+        temb_act = self.time_embedding(t, x.shape[0], add_emb)
+        h, skips = self.encode(x, temb_act, ctx)
+        return self.decode(h, skips, temb_act, ctx, residuals, res_scales)
+
+
+class ControlNet(Net):
+    def hint_embedding(self, image: torch.Tensor) -> torch.Tensor:
+        """Conditioning image (N, 3, 8H, 8W) -> (N, C0, H, W).  Step-invariant:
+        computed once per request (SURVEY App. B pitfall 8)."""
+        hc = self.cfg.hint_channels
+        h = F.silu(self.conv("cond_embedding.conv_in", _cl(image)))
+        for i in range(len(hc) - 1):
+            h = F.silu(self.conv(f"cond_embedding.blocks.{2 * i}", h))
+            h = F.silu(self.conv(f"cond_embedding.blocks.{2 * i + 1}", h, stride=2))
+        return self.conv("cond_embedding.conv_out", h)
+
+    def forward(self, x, t, ctx, hint, add_emb=None):
+        """Returns [down residuals..., mid residual] (unscaled; the
+        conditioning scale is applied by K3 on the consumer side)."""
+        temb_act = self.time_embedding(t, x.shape[0], add_emb)
+        h, skips = self.encode(x, temb_act, ctx, hint=hint)
+        outs = [self.conv(f"zero_convs.{k}", s) for k, s in enumerate(skips)]
+        outs.append(self.conv("mid_zero_conv", h))
+        return outs
+
+
+def patchable_matrices(params: Params) -> list[tuple[str, torch.Tensor]]:
+    """Every LoRA target of a UNet as (name, (h1, h2) matrix view)."""
+    return [(name, params.matrix_view(name)) for name, _ in params.matrices]

@@ -216,8 +216,15 @@ def test_bf16_within_one_ulp_of_reference(h1, h2, r):
     ops.lora_patch_one(wd, d.cuda(), u.cuda(), scale)
     got = wd.float().cpu().numpy()
     exp = lora_ref.accumulate_bf16(w.float().numpy(), d.float().numpy(), u.float().numpy(), scale, 1.0)
+    # 1 bf16 ulp of the exact result, plus the fp32 dot-product error bound
+    # (rank * 2^-24 * sum|terms|) — only visible where the delta cancels to ~0
     ulp = lora_ref.bf16_ulp(exp)
-    assert (np.abs(got - exp) <= ulp + 1e-30).all()
+    terms = np.abs(w.float().numpy()) + scale * (np.abs(d.float().numpy()) @ np.abs(u.float().numpy()))
+    tol = ulp + r * 2.0 ** -24 * terms
+    bad = np.abs(got - exp) > tol
+    assert not bad.any(), (int(bad.sum()), float(np.abs(got - exp)[bad].max()))
+    # and in aggregate: at most 1 ulp everywhere but a vanishing fraction
+    assert (np.abs(got - exp) <= ulp).mean() > 0.999
 
 
 def test_batched_plan_matches_single_and_is_deterministic():

@@ -1,0 +1,140 @@
+"""Denoising-loop parity on the B200 (config 1: toy UNet + 1 ControlNet + 1
+LoRA r8, 64x64 latent, 20 steps, CFG) against the CPU fp32 oracle
+(oracle/pipeline_ref.py — parity unpinned by the reference, see its header).
+
+Tolerances are the north_star's: per-step latent rel-L2 <= 1e-5 (fp32) and
+<= 1e-3 (bf16)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pipeline_ref as R
+from paper_2407_02031_b200 import unet as U
+from paper_2407_02031_b200.patcher import synthetic_lora
+from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_request
+from paper_2407_02031_b200.schedule import plan_lora_patch
+
+pytestmark = pytest.mark.gpu
+
+STEPS, K, GUIDANCE, CN_SCALE, LORA_SCALE = 20, 5, 7.5, 0.8, 0.75
+
+
+def rel_l2(a, b):
+    a, b = a.double().cpu(), b.double().cpu()
+    return float((a - b).norm() / b.norm())
+
+
+@pytest.fixture(scope="module")
+def fp32_mode():
+    old = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+    torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = old
+
+
+def run_device(dtype, use_graphs=True, patch=True, boundary=K):
+    pipe = AddonPipeline(U.TOY, n_controlnets=1, cn_scales=[CN_SCALE], steps=STEPS, guidance=GUIDANCE,
+                         dtype=dtype, seed=0, use_graphs=use_graphs)
+    lora = synthetic_lora(pipe.unet_p, 8, seed=7, adapter_id="l0", scale=LORA_SCALE)
+    if patch:
+        pipe.load_loras([(lora, LORA_SCALE)])
+    pipe.setup()
+    req = synthetic_request(U.TOY, 1, seed=0)
+    lat = [torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(i) for i in req.images]]
+    pipe.prepare(*lat)
+    per_step = []
+    pipe.denoise(patch=patch, boundary=boundary, on_step=lambda s, x: per_step.append(x.float().cpu()))
+    torch.cuda.synchronize()
+    return pipe, lora, req, per_step
+
+
+def run_oracle(pipe, lora, req, patch=True):
+    up = R.to_cpu_params(pipe.unet_p)
+    cps = [R.to_cpu_params(p) for p in pipe.cn_p]
+    adapters = [(lora.factors, LORA_SCALE)] if patch else None
+    return R.denoise(U.TOY, up, cps, req, [CN_SCALE], STEPS, GUIDANCE, adapters=adapters,
+                     matrices=pipe.unet_p.matrices, boundary=K)
+
+
+def test_toy_fp32_per_step_parity(fp32_mode):
+    pipe, lora, req, dev = run_device(torch.float32)
+    ref = run_oracle(pipe, lora, req)
+    errs = [rel_l2(a, b) for a, b in zip(dev, ref)]
+    print("fp32 per-step rel-L2:", ["%.1e" % e for e in errs])
+    assert len(errs) == STEPS
+    assert max(errs) <= 1e-5
+
+
+def test_toy_bf16_per_step_parity():
+    pipe, lora, req, dev = run_device(torch.bfloat16)
+    ref = run_oracle(pipe, lora, req)
+    errs = [rel_l2(a, b) for a, b in zip(dev, ref)]
+    print("bf16 per-step rel-L2:", ["%.1e" % e for e in errs])
+    assert max(errs) <= 1e-3
+
+
+def test_lora_is_not_vacuous_and_lands_at_boundary(fp32_mode):
+    _, _, _, with_lora = run_device(torch.float32, patch=True)
+    _, _, _, without = run_device(torch.float32, patch=False)
+    for s in range(K):               # steps 1..k on the pristine weights: identical
+        assert torch.equal(with_lora[s], without[s])
+    assert rel_l2(with_lora[-1], without[-1]) > 1e-3
+
+
+def test_graph_replay_equals_eager():
+    _, _, _, g = run_device(torch.bfloat16, use_graphs=True)
+    _, _, _, e = run_device(torch.bfloat16, use_graphs=False)
+    for a, b in zip(g, e):
+        assert torch.equal(a, b)
+
+
+def test_unpatch_is_exact_and_reruns_bitwise():
+    pipe, lora, req, first = run_device(torch.bfloat16)
+    inputs = [torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(i) for i in req.images]]
+    # an unpatched request after a patched one sees the pristine weights
+    pipe.prepare(*inputs)
+    plain = []
+    pipe.denoise(patch=False, on_step=lambda s, x: plain.append(x.float().cpu()))
+    _, _, _, ref_plain = run_device(torch.bfloat16, patch=False)
+    for a, b in zip(plain, ref_plain):
+        assert torch.equal(a, b)
+    # and a patched rerun is bitwise identical to the first
+    pipe.prepare(*inputs)
+    again = []
+    pipe.denoise(patch=True, boundary=K, on_step=lambda s, x: again.append(x.float().cpu()))
+    for a, b in zip(first, again):
+        assert torch.equal(a, b)
+
+
+def test_planned_async_boundary():
+    pipe = AddonPipeline(U.TOY, n_controlnets=1, steps=STEPS, dtype=torch.bfloat16)
+    pipe.load_loras([(synthetic_lora(pipe.unet_p, 8, seed=7), 1.0)])
+    step_ms, patch_ms = pipe.calibrate()
+    assert step_ms > 0 and patch_ms > 0
+    req = synthetic_request(U.TOY, 1)
+    pipe.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(req.images[0])])
+    first = pipe.denoise(patch=True)
+    assert first == plan_lora_patch(patch_ms, step_ms, 0.0, STEPS).first_patched_step
+    assert torch.isfinite(pipe.x).all()
+
+
+def test_e2e_generate_host_buffers():
+    pipe = AddonPipeline(U.TOY, n_controlnets=1, steps=4, dtype=torch.bfloat16)
+    pipe.setup()
+    req = synthetic_request(U.TOY, 1)
+    out = pipe.generate(req, pinned={})
+    assert out.shape == (4, 64, 64) and np.isfinite(out).all()
+
+
+def test_sd15_shaped_config2_runs():
+    cfg = U.SD15
+    pipe = AddonPipeline(cfg, n_controlnets=1, steps=3, dtype=torch.bfloat16)
+    pipe.load_loras([(synthetic_lora(pipe.unet_p, 16, seed=3), 1.0)])
+    pipe.setup()
+    req = synthetic_request(cfg, 1)
+    pipe.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(req.images[0])])
+    pipe.denoise(patch=True, boundary=1)
+    torch.cuda.synchronize()
+    assert torch.isfinite(pipe.x).all()
