@@ -1,0 +1,331 @@
+"""bench.py — SDXL + 2 ControlNets + 2 LoRAs (rank 64), 30 DDIM steps, CFG,
+1024x1024 (128x128 latent), on B200 — BASELINE.json's headline metric.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A bench *step* is one image: the full 30-step denoising loop of UNet + 2
+ControlNets at CFG batch 2, with the request's 2 LoRAs patched by one K1
+launch into shadow weights on a low-priority side stream and swapped in at
+the planned boundary (async LoRA, schedule.plan_lora_patch).  Weights are
+synthetic random-init of the SDXL architecture; inputs are synthetic.
+
+value   images/s over the whole job, inputs already resident in HBM
+e2e     the same through the public API (AddonPipeline.generate): pinned host
+        inputs -> H2D -> denoise -> D2H of the final latent, every image
+roofline K1 (the LoRA patch kernel, north_star's >=70%-of-HBM target): algorithmic
+        bytes per launch / its CUDA-event duration on the patch stream inside
+        the timed region (it runs concurrently with the UNet there); the
+        isolated launch is reported beside it
+N > 1   one process per GPU (torchrun, NCCL); each rank serves its own images
+        (replicas — ControlNet-as-a-service sharding is caas.py), so scaling is
+        weak; timing is the max over ranks of CUDA-event time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "p50 s/image & images/s, SDXL+2 ControlNet+2 LoRA, 1/2/4/8 B200 vs CPU ref"
+DENOISE_STEPS = 30
+N_CN = 2
+LORA_RANKS = (64, 64)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v.strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier_sync(world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """The reference CPU path on the host cores (oracle port, see oracle/cpu_bench.py)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.cpu_bench import CpuWorkload
+    from paper_2407_02031_b200 import unet as U
+    wl = CpuWorkload(U.SDXL, N_CN, sum(LORA_RANKS), DENOISE_STEPS)
+    for _ in range(min(args.warmup, 1)):
+        wl.sample()
+    samples = [wl.sample() for _ in range(args.steps)]
+    img_s = [DENOISE_STEPS * s["step_s"] + s["merge_s"] * wl.merge_elems_total / wl.merge_elems_slice
+             for s in samples]
+    med = statistics.median(img_s)
+    value = 1.0 / med
+    cores = torch_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": med * 1000.0,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "p50_s_per_image": med,
+        "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRA r64, 30 DDIM steps, "
+                               "CFG batch 2 — CPU oracle, one bounded sample per step (see sample)",
+                   "model": "sdxl-shaped random init", "global_batch": 1, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": wl.describe()},
+        "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "samples_s": [round(s["sample_s"], 3) for s in samples],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def torch_threads():
+    import torch
+    return torch.get_num_threads()
+
+
+def cpu_baseline_leg():
+    """Bounded CPU sample on rank 0 at N=1 (about one sample, ~10-40 s)."""
+    from oracle.cpu_bench import CpuWorkload
+    from paper_2407_02031_b200 import unet as U
+    wl = CpuWorkload(U.SDXL, N_CN, sum(LORA_RANKS), DENOISE_STEPS)
+    s = wl.sample()
+    img_s = DENOISE_STEPS * s["step_s"] + s["merge_s"] * wl.merge_elems_total / wl.merge_elems_slice
+    return {"value": 1.0 / img_s, "unit": "images/s", "cores": torch_threads(), "kind": "port",
+            "sample": wl.describe(), "sample_s": round(s["sample_s"], 2), "s_per_image_est": round(img_s, 1)}
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    from paper_2407_02031_b200 import ops
+    from paper_2407_02031_b200 import unet as U
+    from paper_2407_02031_b200.patcher import synthetic_lora
+    from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_request
+
+    cfg = U.SDXL
+    pipe = AddonPipeline(cfg, n_controlnets=N_CN, cn_scales=[0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5,
+                         dtype=torch.bfloat16, seed=0, patch_max_ctas=args.patch_ctas)
+    loras = [(synthetic_lora(pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7) for i, r in
+             enumerate(LORA_RANKS)]
+    launches0 = ops.LAUNCHES["count"]
+    pipe.load_loras(loras)
+    pipe.setup()
+    per_step_launches = None
+    step_ms, patch_ms = pipe.calibrate(reps=3)
+    req = synthetic_request(cfg, N_CN, seed=rank)
+    # device-resident copies of the request for the `value` loop
+    dev_in = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
+                  images=[torch.from_numpy(i).cuda() for i in req.images],
+                  pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
+    s = pipe.main_stream
+
+    def image_resident():
+        pipe.prepare(**dev_in)
+        pipe.denoise(patch=True)
+
+    pinned = {}
+
+    def image_e2e():
+        pipe.generate(req, patch=True, pinned=pinned)
+
+    with torch.cuda.stream(s):
+        for _ in range(args.warmup):
+            image_resident()
+        image_e2e()
+    barrier_sync(world)
+
+    # ---- timed: device-resident inputs ------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    pipe.patch_timing = []
+    c0 = ops.LAUNCHES["count"]
+    evs = []
+    barrier_sync(world)
+    with torch.cuda.stream(s):
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all0.record(s)
+        for _ in range(args.steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            image_resident()
+            b.record(s)
+            evs.append((a, b))
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all1.record(s)
+    barrier_sync(world)
+    host_launches = ops.LAUNCHES["count"] - c0
+    total_ms = max_over_ranks(t_all0.elapsed_time(t_all1), world)
+    per_image = [a.elapsed_time(b) / 1000.0 for a, b in evs]
+    patch_ms_live = [p0.elapsed_time(p1) for p0, p1 in pipe.patch_timing]
+    pipe.patch_timing = None
+
+    # ---- timed: end to end through the public API (host buffers) ----------
+    barrier_sync(world)
+    with torch.cuda.stream(s):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(args.steps):
+            image_e2e()
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(s)
+    barrier_sync(world)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    clk = clocks.stop()
+
+    # ---- K1 isolated (for the roofline's context) --------------------------
+    iso = []
+    with torch.cuda.stream(pipe.patch_stream):
+        for _ in range(3):
+            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            p0.record(pipe.patch_stream)
+            pipe.patchset.launch(stream=pipe.patch_stream)
+            p1.record(pipe.patch_stream)
+            p1.synchronize()
+            iso.append(p0.elapsed_time(p1))
+    torch.cuda.synchronize()
+
+    # kernels issued in the timed region: graph replays issue what the capture counted
+    graph_launches_per_step = pipe.launches_per_step
+    gpu_launches = host_launches + graph_launches_per_step * DENOISE_STEPS * args.steps
+
+    hbm, tflops, src = peaks()
+    alg = pipe.patchset.alg_bytes
+    live = statistics.mean(patch_ms_live) if patch_ms_live else None
+    achieved = alg / (live * 1e-3) / 1e9 if live else None
+    images = args.steps * world
+    value = images / (total_ms / 1000.0)
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "p50_s_per_image": statistics.median(per_image),
+        "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
+                               "30 DDIM steps, CFG batch 2, async LoRA patch",
+                   "model": "sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init",
+                   "global_batch": world, "seq_len": None, "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2 (5.1 GB UNet + 5.0 GB ControlNet weights re-read every step)"},
+        "e2e": {"value": images / (e2e_ms / 1000.0), "unit": "images/s",
+                "h2d_bytes_per_step": req.nbytes(), "d2h_bytes_per_step": pipe.d2h_bytes()},
+        "gpu_launches": int(gpu_launches),
+        "roofline": {"kernel": "sdb lora_patch (K1, stacked R=128, all 794 SDXL matrices)",
+                     "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm if achieved else None, "traffic": None,
+                     "alg_bytes_per_launch": alg, "launch_ms_live": live,
+                     "launch_ms_isolated": statistics.median(iso),
+                     "frac_isolated": alg / (statistics.median(iso) * 1e-3) / 1e9 / hbm,
+                     "peak_source": f"{src} MEASURED_PEAKS.json hbm_gbs" if src == "measured" else src},
+        "clocks": clk,
+        "detail": {"step_ms_calibrated": step_ms, "first_patched_step": pipe.last_first_patched_step,
+                   "patch_path": pipe.patchset.plan.path, "per_image_s": [round(x, 4) for x in per_image]},
+    }
+    if world == 1 and rank == 0 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline_leg()
+        except Exception as exc:  # reported, never silently dropped
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--patch-ctas", type=int, default=0, help="cap the K1 grid (0 = one CTA per tile)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

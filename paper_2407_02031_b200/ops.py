@@ -18,6 +18,14 @@ from .errors import DeviceError, ValidationError
 _DTYPES = {torch.float32: _lib.SDB_F32, torch.bfloat16: _lib.SDB_BF16, torch.float16: _lib.SDB_F16}
 _checked_devices: set[int] = set()
 
+#: kernels issued by this process through the C-ABI (a CUDA-graph capture
+#: counts the launches its replays will issue).  bench.py reports it.
+LAUNCHES = {"count": 0}
+
+
+def _count(n: int) -> None:
+    LAUNCHES["count"] += n
+
 
 def sdb_dtype(t: torch.Tensor) -> int:
     try:
@@ -71,6 +79,7 @@ def lora_patch_one(w_in: torch.Tensor, down: torch.Tensor, up: torch.Tensor, sca
     if down.shape[0] != h1 or up.shape[1] != h2 or down.shape[1] != up.shape[0]:
         raise ValidationError(f"factor shapes {tuple(down.shape)} x {tuple(up.shape)} do not match "
                               f"weight ({h1}, {h2})")
+    _count(1)
     _lib.check("sdb_lora_patch_one", _lib.lib().sdb_lora_patch_one(
         w_in.data_ptr(), out.data_ptr(), h1, h2, _row_stride(w_in, "weight"),
         down.data_ptr(), _row_stride(down, "down"), up.data_ptr(), _row_stride(up, "up"),
@@ -139,6 +148,7 @@ class LoraPatchPlan:
 
     def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None,
                max_ctas: int = 0) -> None:
+        _count(1)
         _lib.check("sdb_lora_patch", _lib.lib().sdb_lora_patch(
             self.table.data_ptr(), self.n_jobs, self.total_tiles, self.w_dtype, self.f_dtype,
             self.path, float(sign), int(max_ctas), _stream_ptr(stream)))
@@ -193,6 +203,7 @@ def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optiona
         raise ValidationError(f"add_nc must hold N*C = {n * c} values")
     ws_bytes = _lib.lib().sdb_groupnorm_workspace(n, hw, c, groups)
     ws = _workspace(ws_bytes, x.device)
+    _count(3)
     _lib.check("sdb_groupnorm_silu", _lib.lib().sdb_groupnorm_silu(
         x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,
         beta.data_ptr() if beta is not None else None,
@@ -233,6 +244,7 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
     k = len(residuals)
     ptrs = (ctypes.c_void_p * max(k, 1))(*[r.data_ptr() for r in residuals])
     sc = (ctypes.c_float * max(k, 1))(*[float(s) for s in scales])
+    _count(1)
     _lib.check("sdb_residual_inject", _lib.lib().sdb_residual_inject(
         out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),
         ptrs, sc, k, n * hw, ch, cs, sdb_dtype(skip), _stream_ptr(None)))
@@ -254,6 +266,7 @@ def cfg_ddim_step(eps: torch.Tensor, x: torch.Tensor, coef: torch.Tensor, step_d
     if unet_in is not None and unet_in.numel() != 2 * L:
         raise ValidationError("unet_in must hold 2 latents")
     out = x if x_out is None else x_out
+    _count(1)
     _lib.check("sdb_cfg_ddim_step", _lib.lib().sdb_cfg_ddim_step(
         eps.data_ptr(), sdb_dtype(eps), x.data_ptr(), out.data_ptr(),
         unet_in.data_ptr() if unet_in is not None else None,

@@ -121,6 +121,8 @@ class AddonPipeline:
         self.step_ms_est = None
         self.patch_ms_est = None
         self.last_first_patched_step = None
+        self.patch_timing: Optional[list] = None   # bench: (start, end) events of each patch launch
+        self.launches_per_step = 0
 
     # ------------------------------------------------------------------
     def _use_weights(self, which: str) -> None:
@@ -157,8 +159,10 @@ class AddonPipeline:
         s.wait_stream(side)
         self.step_dev.zero_()
         g = torch.cuda.CUDAGraph()
+        c0 = ops.LAUNCHES["count"]
         with torch.cuda.graph(g, pool=self.pool):
             self.step_once()
+        self.launches_per_step = ops.LAUNCHES["count"] - c0   # our kernels per replay
         if self.pool is None:
             self.pool = g.pool()
         self.graphs[which] = g
@@ -257,9 +261,14 @@ class AddonPipeline:
             else:
                 first = boundary + 1
             self.patch_stream.wait_stream(s)   # shadow is free once earlier work on s finished
+            if self.patch_timing is not None:
+                p0 = torch.cuda.Event(enable_timing=True)
+                p0.record(self.patch_stream)
             self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=self.patch_timing is not None)
             ev.record(self.patch_stream)
+            if self.patch_timing is not None:
+                self.patch_timing.append((p0, ev))
         waited = False
         for step in range(1, self.steps + 1):
             use_patched = patch and step >= first

@@ -406,7 +406,11 @@ class UNet(Net):
                 h = F.interpolate(h, scale_factor=2.0, mode="nearest")
                 h = self.conv(f"up.{i}.upsample", _cl(h))
         h = self.gn("conv_norm_out", h, True)
-        return self.conv("conv_out", h)
+        # eps leaves the UNet in fp32: CFG amplifies (eps_c - eps_u) by the
+        # guidance scale, so a bf16 rounding here would dominate the latent error
+        w = self.t["conv_out.weight"]
+        b = self.t.get("conv_out.bias")
+        return F.conv2d(h.float(), w.float(), None if b is None else b.float(), padding=w.shape[-1] // 2)
 
     def forward(self, x, t, ctx, add_emb=None, residuals=None, res_scales=None):
         temb_act = self.time_embedding(t, x.shape[0], add_emb)
