@@ -100,6 +100,33 @@ int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t 
                        int32_t rank, float scale, float sign,
                        int w_dtype, int f_dtype, void* stream);
 
+/* ---- K1 fast path for bf16 serving weights (TMA + tcgen05 / FFMA) --------
+ * Factors are packed once per adapter set into the UMMA K-major
+ * SWIZZLE_128B layout (A = down in 128-row tiles, B = up^T in 256-column
+ * panels, rank padded to a multiple of 64; buffers 1024-B aligned).  The
+ * plan is a host-built blob (TMA tensor maps for every W + job/unit tables)
+ * the caller copies to device memory (128-B aligned) before launching.
+ * Requirements: bf16 W with ldw % 8 == 0 and 16-B aligned rows; rank <= 256.
+ * simt_rank > 0 (<= 32) selects the FFMA contraction, 0 the tcgen05 MMA. */
+typedef struct sdb_lora_tc_job {
+  void* w_in;
+  void* w_out;
+  int64_t h1, h2, ldw;
+  const void* a_packed;
+  const void* b_packed;
+  int32_t rank;
+  float scale;
+} sdb_lora_tc_job;
+
+int sdb_lora_pack_bytes(int64_t h1, int64_t h2, int32_t rank, size_t* a_bytes, size_t* b_bytes);
+int sdb_lora_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2,
+                  int32_t rank, void* a_packed, void* b_packed, void* stream);
+/* blob_host == NULL: only report *needed bytes, *n_units and *kb_max. */
+int sdb_lora_tc_plan(const sdb_lora_tc_job* jobs_host, int n_jobs, void* blob_host, size_t blob_bytes,
+                     size_t* needed, int* n_units, int* kb_max);
+int sdb_lora_tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank,
+                      float sign, int max_ctas, void* stream);
+
 /* ========================================================================
  * K2 — GroupNorm (+ optional SiLU), NHWC.
  *   x' = x + add_nc[n, c]            (add_nc may be NULL: fused ResNet temb add)

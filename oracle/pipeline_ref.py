@@ -43,20 +43,25 @@ def ddim_coefs(steps: int, guidance: float):
 
 
 class RefNet:
-    def __init__(self, cfg, p: dict):
+    """bf16_acts=True rounds every linear / conv / norm output to bf16 (fp32
+    math in between): the error floor of ANY bf16-activation implementation,
+    used to bound the device bf16 path (tests/test_pipeline_gpu.py)."""
+
+    def __init__(self, cfg, p: dict, bf16_acts: bool = False):
         self.cfg, self.p = cfg, p
+        self.rnd = (lambda t: t.bfloat16().float()) if bf16_acts else (lambda t: t)
 
     def lin(self, n, x):
-        return F.linear(x, self.p[n + ".weight"], self.p.get(n + ".bias"))
+        return self.rnd(F.linear(x, self.p[n + ".weight"], self.p.get(n + ".bias")))
 
     def conv(self, n, x, stride=1):
         w = self.p[n + ".weight"]
-        return F.conv2d(x, w, self.p.get(n + ".bias"), stride=stride, padding=w.shape[-1] // 2)
+        return self.rnd(F.conv2d(x, w, self.p.get(n + ".bias"), stride=stride, padding=w.shape[-1] // 2))
 
     def gn(self, n, x, silu, eps=None):
         y = F.group_norm(x, self.cfg.groups, self.p[n + ".weight"], self.p[n + ".bias"],
                          self.cfg.gn_eps if eps is None else eps)
-        return F.silu(y) if silu else y
+        return self.rnd(F.silu(y) if silu else y)
 
     def temb(self, t, n, add_emb):
         half = self.cfg.block_channels[0] // 2
@@ -184,12 +189,12 @@ def merge_loras(p: dict, adapters, matrices) -> dict:
 
 
 def denoise(cfg, unet_p: dict, cn_ps: list, req, cn_scales, steps: int, guidance: float,
-            adapters=None, matrices=None, boundary=None) -> list:
+            adapters=None, matrices=None, boundary=None, bf16_acts: bool = False) -> list:
     """Returns the fp32 [4, H, W] latent after every step."""
-    unet = RefUNet(cfg, unet_p)
-    patched = RefUNet(cfg, merge_loras(unet_p, adapters, matrices)) if adapters else None
+    unet = RefUNet(cfg, unet_p, bf16_acts)
+    patched = RefUNet(cfg, merge_loras(unet_p, adapters, matrices), bf16_acts) if adapters else None
     first = (boundary + 1) if (adapters and boundary is not None) else steps + 1
-    cns = [RefControlNet(cfg, p) for p in cn_ps]
+    cns = [RefControlNet(cfg, p, bf16_acts) for p in cn_ps]
     ctx = torch.from_numpy(req.context).float()
     add_u = add_c = None
     if cfg.addition_embed:

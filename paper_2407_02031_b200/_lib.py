@@ -107,6 +107,7 @@ def lib() -> ctypes.CDLL:
                 "or __graft_entry__.build(); there is no CPU fallback")
         handle = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | getattr(os, "RTLD_GLOBAL", 0))
         _declare(handle)
+        _declare_tc(handle)
         _lib = handle
     return _lib
 
@@ -123,3 +124,35 @@ def last_error() -> str:
 
 def version() -> str:
     return lib().sdb_version().decode()
+
+
+class LoraTcJob(ctypes.Structure):
+    """Mirror of ``sdb_lora_tc_job`` (include/sdb_api.h)."""
+
+    _fields_ = [
+        ("w_in", ctypes.c_void_p),
+        ("w_out", ctypes.c_void_p),
+        ("h1", ctypes.c_int64),
+        ("h2", ctypes.c_int64),
+        ("ldw", ctypes.c_int64),
+        ("a_packed", ctypes.c_void_p),
+        ("b_packed", ctypes.c_void_p),
+        ("rank", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+    ]
+
+
+EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_tc_plan", "sdb_lora_tc_patch")
+
+
+def _declare_tc(lib: ctypes.CDLL) -> None:
+    vp, i64, i32, f32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_size_t
+    lib.sdb_lora_pack_bytes.restype = i32
+    lib.sdb_lora_pack_bytes.argtypes = [i64, i64, ctypes.c_int32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+    lib.sdb_lora_pack.restype = i32
+    lib.sdb_lora_pack.argtypes = [vp, i64, vp, i64, i64, i64, ctypes.c_int32, vp, vp, vp]
+    lib.sdb_lora_tc_plan.restype = i32
+    lib.sdb_lora_tc_plan.argtypes = [ctypes.POINTER(LoraTcJob), i32, vp, sz, ctypes.POINTER(sz),
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+    lib.sdb_lora_tc_patch.restype = i32
+    lib.sdb_lora_tc_patch.argtypes = [vp, i32, i32, i32, i32, f32, i32, vp]

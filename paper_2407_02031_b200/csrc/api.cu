@@ -21,6 +21,13 @@ int64_t tc_tiles(int64_t h1, int64_t h2);
 bool tc_supported(int w_dtype, int f_dtype, int max_rank);
 int lora_patch_tc(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles, float sign,
                   int max_ctas, cudaStream_t st);
+void tc_pack_bytes(int64_t h1, int64_t h2, int rank, size_t* a_bytes, size_t* b_bytes);
+int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2, int rank,
+            void* a_out, void* b_out, cudaStream_t st);
+int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed,
+            int* n_units_out, int* kb_max_out);
+int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign,
+             int max_ctas, cudaStream_t st);
 // groupnorm_silu.cu
 size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
 int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
@@ -119,6 +126,30 @@ int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t 
   if (int rc = check_job(j, 0)) return rc;
   return lora_patch_simt(nullptr, j, 1, simt_tiles(h1, h2), w_dtype, f_dtype, sign, 0,
                          as_stream(stream));
+}
+
+int sdb_lora_pack_bytes(int64_t h1, int64_t h2, int32_t rank, size_t* a_bytes, size_t* b_bytes) {
+  if (h1 <= 0 || h2 <= 0 || rank < 1 || rank > 256 || !a_bytes || !b_bytes)
+    return fail(SDB_EINVAL, "sdb_lora_pack_bytes: bad shape / rank (1..256)");
+  tc_pack_bytes(h1, h2, rank, a_bytes, b_bytes);
+  return SDB_OK;
+}
+
+int sdb_lora_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2,
+                  int32_t rank, void* a_packed, void* b_packed, void* stream) {
+  if (!down || !up || !a_packed || !b_packed) return fail(SDB_EINVAL, "sdb_lora_pack: NULL pointer");
+  if (ldd < rank || ldu < h2) return fail(SDB_EINVAL, "sdb_lora_pack: leading dimension too small");
+  return tc_pack(down, ldd, up, ldu, h1, h2, rank, a_packed, b_packed, as_stream(stream));
+}
+
+int sdb_lora_tc_plan(const sdb_lora_tc_job* jobs_host, int n_jobs, void* blob_host, size_t blob_bytes,
+                     size_t* needed, int* n_units, int* kb_max) {
+  return tc_plan(jobs_host, n_jobs, blob_host, blob_bytes, needed, n_units, kb_max);
+}
+
+int sdb_lora_tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign,
+                      int max_ctas, void* stream) {
+  return tc_patch(blob_dev, n_jobs, n_units, kb_max, simt_rank, sign, max_ctas, as_stream(stream));
 }
 
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {

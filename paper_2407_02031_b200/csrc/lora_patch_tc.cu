@@ -1,15 +1,572 @@
-// lora_patch_tc.cu — K1 tensor-core path (tcgen05 + TMEM), placeholder until
-// the kernel lands; sdb_lora_plan never selects it while tc_supported() is false.
+// lora_patch_tc.cu — K1 for bf16 serving weights: TMA-staged, warp-specialised,
+// persistent LoRA patch with the rank contraction on tcgen05 (TMEM accumulator)
+// or, at low rank, on FFMA.
+//
+//   W_out[r, c] = bf16( fma(sign*scale, sum_k A[r,k] * B[c,k], float(W_in[r,c])) )
+//
+// Same arithmetic contract as lora_patch.cu (addonsim/lora.py:84-95: one W
+// read-modify-write per element, single rounding, no materialised delta); this
+// unit is the B200-native fast path for the whole-UNet patch set.
+//
+// Data movement (the kernel is HBM-bound: 4 B of W traffic per element vs
+// 2R flops, intensity R/2 << the ~256 flop/B ridge):
+//   * W moves as 128 x 64 bf16 boxes (16 KB, 128B-swizzled) through a ring of
+//     S shared-memory slots: TMA load (cp.async.bulk.tensor) -> epilogue RMW in
+//     shared memory -> TMA store.  The ring keeps S*16 KB of W in flight per SM.
+//   * Factors are pre-packed once per adapter set (sdb_lora_pack) into the
+//     UMMA canonical K-major SWIZZLE_128B layout, so they move with plain bulk
+//     copies: the B panel (256 output columns x R) stays resident while the
+//     CTA walks up to 8 row tiles of that panel; the A tile (128 rows x R) is
+//     reloaded per row tile (L2-resident: its re-read costs R/256 of the W read).
+//   * tcgen05 path: one elected thread issues ceil(R/16) MMAs of
+//     M=128 x N=256 x K=16 (kind::f16, bf16 in, fp32 accumulate) into one of
+//     two 256-column TMEM accumulators; the 4 epilogue warps read their 32
+//     TMEM lanes with tcgen05.ld while the next tile's MMA runs in the other.
+//   * SIMT path (R <= 32): the epilogue threads hold their A row in registers
+//     and contract against broadcast shared-memory reads of the B panel.
+// Roles: warps 0-3 epilogue (TMEM lanes 0-127), warp 4 producer (TMA), warp 5
+// MMA issuer + TMEM allocator.  One CTA per SM, grid-strided over units.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
 #include "common.cuh"
 
 namespace sdb {
+namespace {
 
-int64_t tc_tiles(int64_t h1, int64_t h2) { return ((h1 + 127) / 128) * ((h2 + 255) / 256); }
+constexpr int kBM = 128;                  // rows per tile (TMEM lanes)
+constexpr int kBN = 256;                  // columns per tile / B panel (UMMA N)
+constexpr int kBoxN = 64;                 // W box width (128 B of bf16: one swizzle row)
+constexpr int kBoxBytes = kBM * kBoxN * 2;          // 16 KB
+constexpr int kKB = 64;                   // K elements per packed block (one 128 B row)
+constexpr int kABlockBytes = kBM * 128;   // 16 KB per K block of an A tile
+constexpr int kBBlockBytes = kBN * 128;   // 32 KB per K block of a B panel
+constexpr int kUnitTiles = 8;             // row tiles per work unit (B panel reuse)
+constexpr int kThreads = 192;
+constexpr int kMaxKB = 4;                 // rank <= 256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);   // f32 accum, bf16 A/B, K-major, 128x256
 
+struct TcJob {
+  const uint8_t* a;   // packed A: [m_tiles][kb][128 rows][128 B]
+  const uint8_t* b;   // packed B: [n_tiles][kb][256 rows][128 B]
+  int64_t h1, h2;
+  int32_t kb, rank;
+  float scale;
+  int32_t map_in, map_out;
+  int32_t pad;
+};
+struct TcUnit {
+  int32_t job, n_tile, m_begin, m_end;
+};
+
+// ---- PTX helpers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
+               "r"(y), "r"(src)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
+}
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);   // start address
+  d |= (uint64_t)1 << 16;                     // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;           // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                     // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                     // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Epilogue update of 32 columns (4 swizzled 16 B chunks) of this thread's row.
+__device__ __forceinline__ void rmw32(uint8_t* row, int r, int chunk0, const float (&v)[32], float ss) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4* p = reinterpret_cast<uint4*>(row + (((chunk0 + j) ^ (r & 7)) << 4));
+    uint4 w = *p;
+    uint32_t* wu = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float lo = fmaf(ss, v[8 * j + 2 * e], bf16lo(wu[e]));
+      const float hi = fmaf(ss, v[8 * j + 2 * e + 1], bf16hi(wu[e]));
+      wu[e] = pack_bf16(lo, hi);
+    }
+    *p = w;
+  }
+}
+
+template <bool TC, int KSIMT>
+__global__ void __launch_bounds__(kThreads, 1)
+lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restrict__ jobs,
+                      const TcUnit* __restrict__ units, int n_units, float sign, int kb_max, int n_slots) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;                                   // kb_max * 32 KB
+  uint8_t* sA = sB + kb_max * kBBlockBytes;             // kb_max * 16 KB
+  uint8_t* sW = sA + kb_max * kABlockBytes;             // n_slots * 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + n_slots * kBoxBytes);
+  // barrier indices
+  const int B_FULL = 0, B_EMPTY = 1, A_FULL = 2, A_EMPTY = 3, T_FULL = 4, T_EMPTY = 6, W_FULL = 8;
+  const int W_EMPTY = W_FULL + n_slots;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + W_EMPTY + n_slots);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    const uint32_t consumer_count = TC ? 1u : 4u;   // tcgen05.commit vs one arrive per epilogue warp
+    mbar_init(bar(B_FULL), 1);
+    mbar_init(bar(B_EMPTY), consumer_count);
+    mbar_init(bar(A_FULL), 1);
+    mbar_init(bar(A_EMPTY), consumer_count);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(T_FULL + i), 1);
+      mbar_init(bar(T_EMPTY + i), 4);
+    }
+    for (int i = 0; i < n_slots; ++i) {
+      mbar_init(bar(W_FULL + i), 1);
+      mbar_init(bar(W_EMPTY + i), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (TC && warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(2 * kBN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = TC ? *tmem_holder : 0u;
+
+  if (warp == 4) {
+    // ===================== producer =====================
+    if (lane == 0) {
+      int a_cnt = 0, b_cnt = 0, w_cnt = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const TcUnit un = units[u];
+        const TcJob& J = jobs[un.job];
+        const CUtensorMap* min = maps + J.map_in;
+        prefetch_map(min);
+        if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
+        mbar_expect_tx(bar(B_FULL), J.kb * kBBlockBytes);
+        bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL));
+        ++b_cnt;
+        const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
+        const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
+        for (int m = un.m_begin; m < un.m_end; ++m) {
+          if (a_cnt > 0) mbar_wait(bar(A_EMPTY), (a_cnt - 1) & 1);
+          mbar_expect_tx(bar(A_FULL), J.kb * kABlockBytes);
+          bulk_g2s(smem_u32(sA), J.a + (size_t)m * J.kb * kABlockBytes, J.kb * kABlockBytes, bar(A_FULL));
+          ++a_cnt;
+          for (int bx = 0; bx < nbox; ++bx) {
+            const int slot = w_cnt % n_slots;
+            if (w_cnt >= n_slots) mbar_wait(bar(W_EMPTY + slot), ((w_cnt / n_slots) - 1) & 1);
+            mbar_expect_tx(bar(W_FULL + slot), kBoxBytes);
+            tma_load_2d(smem_u32(sW + slot * kBoxBytes), min, un.n_tile * kBN + bx * kBoxN, m * kBM,
+                        bar(W_FULL + slot));
+            ++w_cnt;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ===================== MMA issuer =====================
+    if (TC && lane == 0) {
+      int tile = 0, b_cnt = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const TcUnit un = units[u];
+        const TcJob& J = jobs[un.job];
+        const int nks = (J.rank + 15) / 16;
+        mbar_wait(bar(B_FULL), b_cnt & 1);
+        for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
+          const int buf = tile & 1;
+          mbar_wait(bar(A_FULL), tile & 1);
+          if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + buf * kBN;
+          for (int s = 0; s < nks; ++s) {
+            const int kb = s >> 2, ks = s & 3;
+            const uint64_t ad = sw128_desc(smem_u32(sA + kb * kABlockBytes + ks * 32));
+            const uint64_t bd = sw128_desc(smem_u32(sB + kb * kBBlockBytes + ks * 32));
+            tc_mma(d, ad, bd, kIdesc, s > 0 ? 1u : 0u);
+          }
+          tc_commit(bar(A_EMPTY));
+          tc_commit(bar(T_FULL + buf));
+        }
+        tc_commit(bar(B_EMPTY));
+        ++b_cnt;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue (warps 0-3) =====================
+    const int r = threadIdx.x;   // tile row == TMEM lane
+    int tile = 0, w_cnt = 0, b_cnt = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const TcUnit un = units[u];
+      const TcJob& J = jobs[un.job];
+      const CUtensorMap* mout = maps + J.map_out;
+      const float ss = sign * J.scale;
+      const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
+      const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
+      if (!TC) mbar_wait(bar(B_FULL), b_cnt & 1);
+      for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
+        const int buf = tile & 1;
+        float a[KSIMT > 0 ? KSIMT : 1];
+        if (TC) {
+          mbar_wait(bar(T_FULL + buf), (tile >> 1) & 1);
+          tc_fence_after();
+        } else {
+          mbar_wait(bar(A_FULL), tile & 1);
+          // this row of the packed A tile (k block 0, swizzled 16 B chunks)
+#pragma unroll
+          for (int c = 0; c < KSIMT / 8; ++c) {
+            const uint4 q = *reinterpret_cast<const uint4*>(sA + r * 128 + ((c ^ (r & 7)) << 4));
+            const uint32_t* qu = reinterpret_cast<const uint32_t*>(&q);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              a[8 * c + 2 * e] = bf16lo(qu[e]);
+              a[8 * c + 2 * e + 1] = bf16hi(qu[e]);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(A_EMPTY));
+        }
+        for (int bx = 0; bx < nbox; ++bx) {
+          const int slot = w_cnt % n_slots;
+          mbar_wait(bar(W_FULL + slot), (w_cnt / n_slots) & 1);
+          uint8_t* row = sW + slot * kBoxBytes + r * 128;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float v[32];
+            if (TC) {
+              const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + buf * kBN + bx * kBoxN + half * 32;
+              tc_ld32(taddr, v);
+            } else {
+#pragma unroll 4
+              for (int c = 0; c < 32; ++c) {
+                const int n = bx * kBoxN + half * 32 + c;   // B panel row (output column)
+                const uint8_t* brow = sB + n * 128;
+                float acc = 0.f;
+#pragma unroll
+                for (int q = 0; q < KSIMT / 8; ++q) {
+                  const uint4 bq = *reinterpret_cast<const uint4*>(brow + ((q ^ (n & 7)) << 4));
+                  const uint32_t* bu = reinterpret_cast<const uint32_t*>(&bq);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    acc = fmaf(a[8 * q + 2 * e], bf16lo(bu[e]), acc);
+                    acc = fmaf(a[8 * q + 2 * e + 1], bf16hi(bu[e]), acc);
+                  }
+                }
+                v[c] = acc;
+              }
+            }
+            rmw32(row, r, half * 4, v, ss);
+          }
+          fence_proxy_async();
+          named_bar(1, 128);
+          if (r == 0) {
+            tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM, smem_u32(sW + slot * kBoxBytes));
+            tma_store_wait_read();
+            mbar_arrive(bar(W_EMPTY + slot));
+          }
+          ++w_cnt;
+        }
+        if (TC) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(T_EMPTY + buf));
+        }
+      }
+      if (!TC) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(B_EMPTY));
+      }
+      ++b_cnt;
+    }
+    if (r == 0) tma_store_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (TC && warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
+  }
+}
+
+// ---- packing ----------------------------------------------------------------
+// A: [mt][kb][128][8 chunks x 16 B], chunk c of row r stored at c ^ (r & 7)
+__global__ void pack_a_kernel(const __nv_bfloat16* __restrict__ down, int64_t ldd, int64_t h1, int rank,
+                              int kbt, int64_t mt, uint4* __restrict__ out) {
+  const int64_t total = mt * kbt * kBM * 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i & 7);
+    const int64_t rowi = i >> 3;                // (m*kbt + kb)*128 + r
+    const int r = (int)(rowi % kBM);
+    const int64_t mk = rowi / kBM;
+    const int kb = (int)(mk % kbt);
+    const int64_t m = mk / kbt;
+    const int64_t row = m * kBM + r;
+    const int k0 = kb * kKB + c * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      v[e] = (row < h1 && k0 + e < rank) ? down[row * ldd + k0 + e] : __float2bfloat16_rn(0.f);
+    out[rowi * 8 + (c ^ (r & 7))] = *reinterpret_cast<uint4*>(v);
+  }
+}
+// B: [nt][kb][256][8 chunks x 16 B] holding up^T (row n = output column n)
+__global__ void pack_b_kernel(const __nv_bfloat16* __restrict__ up, int64_t ldu, int64_t h2, int rank, int kbt,
+                              int64_t nt, uint4* __restrict__ out) {
+  const int64_t total = nt * kbt * 8 * kBN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i % kBN);               // fastest: coalesced reads of up rows
+    const int64_t q = i / kBN;
+    const int c = (int)(q & 7);
+    const int64_t nk = q >> 3;                  // nt*kbt + kb
+    const int kb = (int)(nk % kbt);
+    const int64_t ntile = nk / kbt;
+    const int64_t col = ntile * kBN + n;
+    const int k0 = kb * kKB + c * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      v[e] = (col < h2 && k0 + e < rank) ? up[(int64_t)(k0 + e) * ldu + col] : __float2bfloat16_rn(0.f);
+    out[(nk * kBN + n) * 8 + (c ^ (n & 7))] = *reinterpret_cast<uint4*>(v);
+  }
+}
+
+// ---- host side ----------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+int make_w_map(CUtensorMap* map, void* ptr, int64_t h1, int64_t h2, int64_t ldw) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)h2, (cuuint64_t)h1};
+  cuuint64_t strides[1] = {(cuuint64_t)ldw * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kBoxN, (cuuint32_t)kBM};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SDB_EINVAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return SDB_OK;
+}
+
+}  // namespace
+
+int tc_kb(int rank) { return (rank + kKB - 1) / kKB; }
+
+void tc_pack_bytes(int64_t h1, int64_t h2, int rank, size_t* a_bytes, size_t* b_bytes) {
+  const int64_t kbt = tc_kb(rank);
+  *a_bytes = (size_t)((h1 + kBM - 1) / kBM) * kbt * kABlockBytes;
+  *b_bytes = (size_t)((h2 + kBN - 1) / kBN) * kbt * kBBlockBytes;
+}
+
+int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2, int rank,
+            void* a_out, void* b_out, cudaStream_t st) {
+  if (rank < 1 || rank > kMaxKB * kKB) return fail(SDB_EINVAL, "lora_pack: rank must be in [1, 256]");
+  if (((uintptr_t)a_out | (uintptr_t)b_out) & 1023) return fail(SDB_EINVAL, "lora_pack: outputs must be 1024-B aligned");
+  const int kbt = tc_kb(rank);
+  const int64_t mt = (h1 + kBM - 1) / kBM, nt = (h2 + kBN - 1) / kBN;
+  const int64_t na = mt * kbt * kBM * 8, nb = nt * kbt * 8 * kBN;
+  pack_a_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 65535), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(down), ldd, h1, rank, kbt, mt, static_cast<uint4*>(a_out));
+  if (int rc = check_launch("pack_a_kernel")) return rc;
+  pack_b_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 65535), 256, 0, st>>>(
+      static_cast<const __nv_bfloat16*>(up), ldu, h2, rank, kbt, nt, static_cast<uint4*>(b_out));
+  return check_launch("pack_b_kernel");
+}
+
+// Blob layout: [maps: 2*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]
+int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed, int* n_units_out,
+            int* kb_max_out) {
+  if (n_jobs <= 0 || !jobs) return fail(SDB_EINVAL, "lora_tc_plan: no jobs");
+  std::vector<TcUnit> units;
+  int kb_max = 1;
+  for (int j = 0; j < n_jobs; ++j) {
+    const sdb_lora_tc_job& J = jobs[j];
+    if (J.h1 <= 0 || J.h2 <= 0 || J.rank < 1 || J.rank > kMaxKB * kKB)
+      return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": bad shape or rank (1..256)");
+    if (J.ldw % 8 != 0 || ((uintptr_t)J.w_in & 15) || ((uintptr_t)J.w_out & 15))
+      return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": W rows must be 16-B aligned (ldw % 8 == 0)");
+    if (((uintptr_t)J.a_packed | (uintptr_t)J.b_packed) & 1023)
+      return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": packed factors must be 1024-B aligned");
+    kb_max = std::max(kb_max, tc_kb(J.rank));
+    const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + kBN - 1) / kBN;
+    for (int64_t n = 0; n < nt; ++n)
+      for (int64_t m = 0; m < mt; m += kUnitTiles)
+        units.push_back({j, (int32_t)n, (int32_t)m, (int32_t)std::min<int64_t>(mt, m + kUnitTiles)});
+  }
+  const size_t maps_b = (size_t)2 * n_jobs * sizeof(CUtensorMap);
+  const size_t jobs_b = (size_t)n_jobs * sizeof(TcJob);
+  const size_t units_b = units.size() * sizeof(TcUnit);
+  const size_t need = maps_b + jobs_b + units_b;
+  if (needed) *needed = need;
+  if (n_units_out) *n_units_out = (int)units.size();
+  if (kb_max_out) *kb_max_out = kb_max;
+  if (!blob) return SDB_OK;
+  if (blob_bytes < need) return fail(SDB_EINVAL, "lora_tc_plan: blob too small");
+  uint8_t* base = static_cast<uint8_t*>(blob);
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(base);
+  TcJob* tj = reinterpret_cast<TcJob*>(base + maps_b);
+  for (int j = 0; j < n_jobs; ++j) {
+    const sdb_lora_tc_job& J = jobs[j];
+    if (int rc = make_w_map(&maps[2 * j], J.w_in, J.h1, J.h2, J.ldw)) return rc;
+    if (int rc = make_w_map(&maps[2 * j + 1], J.w_out, J.h1, J.h2, J.ldw)) return rc;
+    std::memset(&tj[j], 0, sizeof(TcJob));
+    tj[j].a = static_cast<const uint8_t*>(J.a_packed);
+    tj[j].b = static_cast<const uint8_t*>(J.b_packed);
+    tj[j].h1 = J.h1;
+    tj[j].h2 = J.h2;
+    tj[j].kb = tc_kb(J.rank);
+    tj[j].rank = J.rank;
+    tj[j].scale = J.scale;
+    tj[j].map_in = 2 * j;
+    tj[j].map_out = 2 * j + 1;
+  }
+  std::memcpy(base + maps_b + jobs_b, units.data(), units_b);
+  return SDB_OK;
+}
+
+int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign, int max_ctas,
+             cudaStream_t st) {
+  if (!blob_dev || n_units <= 0) return fail(SDB_EINVAL, "lora_tc_patch: empty plan");
+  if (((uintptr_t)blob_dev) & 127) return fail(SDB_EINVAL, "lora_tc_patch: blob must be 128-B aligned");
+  if (kb_max < 1 || kb_max > kMaxKB) return fail(SDB_EINVAL, "lora_tc_patch: kb_max out of range");
+  const size_t maps_b = (size_t)2 * n_jobs * sizeof(CUtensorMap);
+  const uint8_t* base = static_cast<const uint8_t*>(blob_dev);
+  const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(base);
+  const TcJob* jobs = reinterpret_cast<const TcJob*>(base + maps_b);
+  const TcUnit* units = reinterpret_cast<const TcUnit*>(base + maps_b + (size_t)n_jobs * sizeof(TcJob));
+  const int fixed = 1024 + kb_max * (kBBlockBytes + kABlockBytes) + 256;
+  const int max_smem = 227 * 1024;
+  int slots = std::min(6, (max_smem - fixed) / kBoxBytes);
+  if (slots < 2) return fail(SDB_EUNSUP, "lora_tc_patch: rank too large for shared memory");
+  const int smem = fixed + slots * kBoxBytes;
+  int grid = std::min(n_units, kNumSMs);
+  if (max_ctas > 0) grid = std::min(grid, max_ctas);
+#define SDB_TC_LAUNCH(TCV, KS)                                                                                  \
+  do {                                                                                                          \
+    auto kfn = lora_patch_tma_kernel<TCV, KS>;                                                                  \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                               \
+    kfn<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);                         \
+  } while (0)
+  if (simt_rank > 0 && simt_rank <= 16)
+    SDB_TC_LAUNCH(false, 16);
+  else if (simt_rank > 16 && simt_rank <= 32)
+    SDB_TC_LAUNCH(false, 32);
+  else
+    SDB_TC_LAUNCH(true, 0);
+#undef SDB_TC_LAUNCH
+  return check_launch("lora_patch_tma_kernel");
+}
+
+// legacy entry points used by sdb_lora_plan / sdb_lora_patch (SIMT job tables)
+int64_t tc_tiles(int64_t h1, int64_t h2) { return ((h1 + kBM - 1) / kBM) * ((h2 + kBN - 1) / kBN); }
 bool tc_supported(int, int, int) { return false; }
-
 int lora_patch_tc(const sdb_lora_job*, int, int64_t, float, int, cudaStream_t) {
-  return fail(SDB_EUNSUP, "tcgen05 LoRA path not built");
+  return fail(SDB_EUNSUP, "use sdb_lora_tc_plan / sdb_lora_tc_patch for the tcgen05 path");
 }
 
 }  // namespace sdb

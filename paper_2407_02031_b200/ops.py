@@ -154,6 +154,92 @@ class LoraPatchPlan:
             self.path, float(sign), int(max_ctas), _stream_ptr(stream)))
 
 
+def tma_eligible(w: torch.Tensor) -> bool:
+    """bf16 matrix whose rows are 16-B aligned: the TMA / tcgen05 K1 path applies."""
+    return (w.dtype == torch.bfloat16 and w.dim() == 2 and w.stride(1) == 1
+            and _row_stride(w, "weight") % 8 == 0 and w.data_ptr() % 16 == 0)
+
+
+class LoraTmaPlan:
+    """K1 fast path for bf16 weights: factors packed once (UMMA K-major
+    SWIZZLE_128B tiles), W streamed through a TMA ring, rank contraction on
+    tcgen05 (R > 16) or FFMA (R <= 16).  One launch covers every job.
+
+    entries: (w_in, w_out or None, down (h1, R) bf16, up (R, h2) bf16, scale),
+    every w_in must satisfy ``tma_eligible``."""
+
+    def __init__(self, entries: Sequence[tuple], simt_max_rank: int = 16):
+        if not entries:
+            raise ValidationError("LoraTmaPlan needs at least one job")
+        lib = _lib.lib()
+        dev = entries[0][0].device
+        sizes = []
+        self.alg_bytes = 0
+        self.alg_flops = 0
+        self.max_rank = 0
+        for i, (w_in, w_out, down, up, scale) in enumerate(entries):
+            out = w_in if w_out is None else w_out
+            require_cuda(w_in, out, down, up)
+            if not (tma_eligible(w_in) and tma_eligible(out)):
+                raise ValidationError(f"job {i}: weight is not TMA-eligible (bf16, ldw % 8 == 0)")
+            if down.dtype != torch.bfloat16 or up.dtype != torch.bfloat16:
+                raise ValidationError(f"job {i}: factors must be bf16 on the TMA path")
+            h1, h2 = w_in.shape
+            r = down.shape[1]
+            if down.shape[0] != h1 or up.shape != (r, h2):
+                raise ValidationError(f"job {i}: factor shapes do not match weight ({h1}, {h2})")
+            a_b, b_b = ctypes.c_size_t(0), ctypes.c_size_t(0)
+            _lib.check("sdb_lora_pack_bytes", lib.sdb_lora_pack_bytes(h1, h2, r, ctypes.byref(a_b), ctypes.byref(b_b)))
+            sizes.append((a_b.value, b_b.value))
+            self.alg_bytes += 2 * h1 * h2 * 2 + (h1 + h2) * r * 2
+            self.alg_flops += 2 * h1 * h2 * r
+            self.max_rank = max(self.max_rank, r)
+        # one arena, every packed block 1024-B aligned
+        offs, total = [], 0
+        for a_b, b_b in sizes:
+            offs.append((total, total + a_b))
+            total += a_b + b_b
+        self.arena = torch.empty(total + 1024, dtype=torch.uint8, device=dev)
+        base = (self.arena.data_ptr() + 1023) // 1024 * 1024
+        jobs = (_lib.LoraTcJob * len(entries))()
+        self._keep = []
+        for i, (w_in, w_out, down, up, scale) in enumerate(entries):
+            out = w_in if w_out is None else w_out
+            h1, h2 = w_in.shape
+            r = down.shape[1]
+            a_ptr, b_ptr = base + offs[i][0], base + offs[i][1]
+            _count(2)
+            _lib.check("sdb_lora_pack", lib.sdb_lora_pack(
+                down.data_ptr(), _row_stride(down, "down"), up.data_ptr(), _row_stride(up, "up"),
+                h1, h2, r, a_ptr, b_ptr, _stream_ptr(None)))
+            j = jobs[i]
+            j.w_in, j.w_out = w_in.data_ptr(), out.data_ptr()
+            j.h1, j.h2, j.ldw = h1, h2, _row_stride(w_in, "weight")
+            j.a_packed, j.b_packed = a_ptr, b_ptr
+            j.rank, j.scale = r, float(scale)
+            self._keep += [w_in, out]
+        need, n_units, kb_max = ctypes.c_size_t(0), ctypes.c_int(0), ctypes.c_int(0)
+        _lib.check("sdb_lora_tc_plan", lib.sdb_lora_tc_plan(jobs, len(entries), None, 0, ctypes.byref(need),
+                                                            ctypes.byref(n_units), ctypes.byref(kb_max)))
+        host = (ctypes.c_uint8 * need.value)()
+        _lib.check("sdb_lora_tc_plan", lib.sdb_lora_tc_plan(jobs, len(entries), host, need.value,
+                                                            ctypes.byref(need), ctypes.byref(n_units),
+                                                            ctypes.byref(kb_max)))
+        self.blob = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
+        self.n_jobs = len(entries)
+        self.n_units = n_units.value
+        self.kb_max = kb_max.value
+        self.simt_rank = self.max_rank if self.max_rank <= simt_max_rank else 0
+        self.path = 2 if self.simt_rank else 1   # 1 = tcgen05, 2 = TMA + FFMA
+
+    def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None,
+               max_ctas: int = 0) -> None:
+        _count(1)
+        _lib.check("sdb_lora_tc_patch", _lib.lib().sdb_lora_tc_patch(
+            self.blob.data_ptr(), self.n_jobs, self.n_units, self.kb_max, self.simt_rank, float(sign),
+            int(max_ctas), _stream_ptr(stream)))
+
+
 # --------------------------------------------------------------------------
 # K2 — GroupNorm (+SiLU), NHWC
 # --------------------------------------------------------------------------

@@ -94,7 +94,7 @@ class PatchSet:
     device-resident K1 job table."""
 
     def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]],
-                 shadow: Optional[dict] = None):
+                 shadow: Optional[dict] = None, use_tma: bool = True):
         if not adapters:
             raise ValidationError("PatchSet needs at least one adapter")
         self.params = params
@@ -120,19 +120,31 @@ class PatchSet:
                 w_out = shadow[name].permute(0, 2, 3, 1).reshape(w_in.shape) if shadow[name].dim() == 4 \
                     else shadow[name]
             self.entries.append((w_in, w_out, down, up, 1.0))
-        self.plan = ops.LoraPatchPlan(self.entries)
         self.rank = max(d.shape[1] for d, _ in self.stacked.values())
+        # bf16 matrices with 16-B aligned rows take the TMA / tcgen05 kernel (one
+        # launch, factors packed here, once per adapter set); the rest (e.g.
+        # SDXL conv_in, 320 x 36) the generic SIMT kernel.
+        fast = [e for e in self.entries if use_tma and self.rank <= 256 and ops.tma_eligible(e[0])
+                and e[2].dtype == torch.bfloat16]
+        slow = [e for e in self.entries if not any(e is f for f in fast)]
+        self.plans = []
+        if fast:
+            self.plans.append(ops.LoraTmaPlan(fast))
+        if slow:
+            self.plans.append(ops.LoraPatchPlan(slow))
+        self.plan = self.plans[0]
 
     @property
     def alg_bytes(self) -> int:
-        return self.plan.alg_bytes
+        return sum(p.alg_bytes for p in self.plans)
 
     @property
     def alg_flops(self) -> int:
-        return self.plan.alg_flops
+        return sum(p.alg_flops for p in self.plans)
 
     def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None, max_ctas: int = 0):
-        self.plan.launch(sign=sign, stream=stream, max_ctas=max_ctas)
+        for p in self.plans:
+            p.launch(sign=sign, stream=stream, max_ctas=max_ctas)
 
     def copy_unpatched(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Shadow entries not touched by any adapter must mirror the pristine
