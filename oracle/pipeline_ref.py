@@ -87,7 +87,7 @@ class RefNet:
         h = h + self.lin(pre + ".time_emb_proj", temb)[:, :, None, None]
         h = self.conv(pre + ".conv2", self.gn(pre + ".norm2", h, True))
         sc = self.conv(pre + ".conv_shortcut", x) if pre + ".conv_shortcut.weight" in self.p else x
-        return h + sc
+        return self.rnd(h + sc)
 
     def attn(self, pre, x, ctx, heads):
         n, l, c = x.shape
@@ -97,7 +97,7 @@ class RefNet:
         q = q.view(n, l, heads, d).transpose(1, 2)
         k = k.view(n, -1, heads, d).transpose(1, 2)
         v = v.view(n, -1, heads, d).transpose(1, 2)
-        o = F.scaled_dot_product_attention(q, k, v)  # CPU: softmax(q k^T / sqrt(d)) v
+        o = self.rnd(F.scaled_dot_product_attention(q, k, v))  # CPU: softmax(q k^T / sqrt(d)) v
         return self.lin(pre + ".to_out", o.transpose(1, 2).reshape(n, l, c))
 
     def transformer(self, pre, x, ctx, depth):
@@ -107,13 +107,13 @@ class RefNet:
         heads = self.cfg.heads(c)
         for d in range(depth):
             b = f"{pre}.blocks.{d}"
-            ln = lambda k, t: F.layer_norm(t, (c,), self.p[f"{b}.{k}.weight"], self.p[f"{b}.{k}.bias"])
-            tok = tok + self.attn(b + ".attn1", ln("norm1", tok), None, heads)
-            tok = tok + self.attn(b + ".attn2", ln("norm2", tok), ctx, heads)
+            ln = lambda k, t: self.rnd(F.layer_norm(t, (c,), self.p[f"{b}.{k}.weight"], self.p[f"{b}.{k}.bias"]))
+            tok = self.rnd(tok + self.attn(b + ".attn1", ln("norm1", tok), None, heads))
+            tok = self.rnd(tok + self.attn(b + ".attn2", ln("norm2", tok), ctx, heads))
             hv, gate = self.lin(b + ".ff.proj", ln("norm3", tok)).chunk(2, -1)
-            tok = tok + self.lin(b + ".ff.out", hv * F.gelu(gate))
+            tok = self.rnd(tok + self.lin(b + ".ff.out", self.rnd(hv * F.gelu(gate))))
         tok = self.lin(pre + ".proj_out", tok)
-        return tok.view(n, h, w, c).permute(0, 3, 1, 2) + x
+        return self.rnd(tok.view(n, h, w, c).permute(0, 3, 1, 2) + x)
 
     def encode(self, x, temb, ctx, hint=None):
         cfg = self.cfg
@@ -143,6 +143,8 @@ class RefUNet(RefNet):
         for r, s in zip(residuals, scales):
             skips = [sk + s * rr for sk, rr in zip(skips, r[:-1])]
             h = h + s * r[-1]
+        skips = [self.rnd(sk) for sk in skips]
+        h = self.rnd(h)
         rev = list(reversed(cfg.block_channels))
         for i, _ in enumerate(rev):
             depth = cfg.attn_depth[len(rev) - 1 - i]

@@ -51,7 +51,7 @@ def lora():
         flush_ms = time_launch(lambda: flush.zero_())
         ms = time_launch(run) - flush_ms
         gbps = ps.alg_bytes / (ms * 1e-3) / 1e9
-        out.append({"ranks": ranks, "R": ps.rank, "path": ps.plan.path, "tiles": ps.plan.total_tiles,
+        out.append({"ranks": ranks, "R": ps.rank, "path": [pl.path for pl in ps.plans],
                     "ms": round(ms, 3), "alg_GB": round(ps.alg_bytes / 1e9, 3), "GBps": round(gbps, 1),
                     "frac": round(gbps / PEAK, 3)})
         print(json.dumps(out[-1]), flush=True)

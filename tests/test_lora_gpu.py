@@ -280,3 +280,51 @@ def test_torch_device_layer_in_place():
     assert (w.double() - exp).abs().max().item() <= 1e-5
     L.unmerge_in_place(layer, ad)
     assert (w - before).abs().max().item() <= 1e-5
+
+
+@pytest.mark.parametrize("ranks", [[8], [16], [24], [64], [64, 64], [8, 32, 64, 128]])
+def test_tma_path_bf16_parity(ranks):
+    """The TMA / tcgen05 K1 path (LoraTmaPlan) on SDXL-like shapes incl. ragged
+    edges: <= 1 bf16 ulp of bf16(fp64 reference) + the fp32 dot-product bound;
+    in place and out of place agree bitwise; reruns are bitwise identical."""
+    r = sum(ranks)
+    shapes = [(1280, 1280), (640, 2048), (10240, 1280), (1280, 11520), (320, 2880), (4, 2880), (77, 136),
+              (200, 72)]
+    g = torch.Generator().manual_seed(r)
+    ws = [(torch.randn(a, b, generator=g) * 0.02).to(torch.bfloat16) for a, b in shapes]
+    ds = [(torch.randn(a, r, generator=g) / r ** 0.5).to(torch.bfloat16) for a, _ in shapes]
+    us = [torch.randn(r, b, generator=g).to(torch.bfloat16) for _, b in shapes]
+    wd = [w.cuda() for w in ws]
+    outs = [torch.empty_like(w) for w in wd]
+    plan = ops.LoraTmaPlan([(w, o, d.cuda(), u.cuda(), 0.7) for w, o, d, u in zip(wd, outs, ds, us)])
+    assert plan.path == (2 if r <= 16 else 1)
+    plan.launch()
+    first = [o.clone() for o in outs]
+    plan.launch()
+    for a, b in zip(first, outs):
+        assert torch.equal(a, b)
+    for w, d, u, o in zip(ws, ds, us, outs):
+        exp = lora_ref.accumulate_bf16(w.float().numpy(), d.float().numpy(), u.float().numpy(), 0.7, 1.0)
+        got = o.float().cpu().numpy()
+        ulp = lora_ref.bf16_ulp(exp)
+        terms = np.abs(w.float().numpy()) + 0.7 * (np.abs(d.float().numpy()) @ np.abs(u.float().numpy()))
+        bad = np.abs(got - exp) > ulp + r * 2.0 ** -24 * terms
+        assert not bad.any(), (w.shape, int(bad.sum()))
+    # in place == out of place; sign -1 undoes within the same bound
+    inplace = [w.clone() for w in wd]
+    plan2 = ops.LoraTmaPlan([(w, None, d.cuda(), u.cuda(), 0.7) for w, d, u in zip(inplace, ds, us)])
+    plan2.launch()
+    for a, b in zip(inplace, outs):
+        assert torch.equal(a, b)
+    assert all(torch.equal(w, w0) for w, w0 in zip(wd, [x.cuda() for x in ws]))  # w_in untouched
+
+
+def test_tma_path_grid_cap_same_result():
+    g = torch.Generator().manual_seed(1)
+    w = (torch.randn(2560, 1280, generator=g) * 0.02).to(torch.bfloat16).cuda()
+    d = (torch.randn(2560, 128, generator=g) / 11).to(torch.bfloat16).cuda()
+    u = torch.randn(128, 1280, generator=g).to(torch.bfloat16).cuda()
+    o1, o2 = torch.empty_like(w), torch.empty_like(w)
+    ops.LoraTmaPlan([(w, o1, d, u, 1.0)]).launch()
+    ops.LoraTmaPlan([(w, o2, d, u, 1.0)]).launch(max_ctas=7)
+    assert torch.equal(o1, o2)
