@@ -135,7 +135,9 @@ int sdb_lora_tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max,
  * (addonsim/model.py:66-70 unet_opt_submultipliers[2] = 1.072; paper
  * PAPER.md:572-576).  x, y: [N, HW, C] (channels innermost), dtype `dtype`;
  * gamma, beta: fp32 [C].  `workspace` must hold sdb_groupnorm_workspace()
- * bytes.  y may alias x.
+ * bytes and be ZERO-initialised once (its first 256 B are per-sample
+ * completion counters that every launch leaves at zero); calls sharing a
+ * workspace must be ordered on one stream.  y may alias x.
  * ======================================================================== */
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
 int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
@@ -156,6 +158,21 @@ int sdb_residual_inject(void* out, const void* hidden, const void* skip,
                         const void* const* res_ptrs_host, const float* scales_host,
                         int n_res, int64_t pixels, int64_t ch, int64_t cs,
                         int dtype, void* stream);
+
+/* ========================================================================
+ * K5 — GEGLU: out[m, 0:f] = proj[m, 0:f] * gelu(proj[m, f:2f]) (exact erf).
+ * The paper's fused GEGLU; in the reference only the
+ * 1.06 sub-multiplier of addonsim/model.py:66-70.  f % 8 == 0.
+ * ======================================================================== */
+int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, void* stream);
+
+/* ========================================================================
+ * K6 — residual add + LayerNorm of the transformer blocks:
+ *   x[m] += d[m] (in place; d may be NULL), y[m] = LN(x[m]) * gamma + beta.
+ * gamma / beta in the same dtype as x; C % 8 == 0, C <= 2560.
+ * ======================================================================== */
+int sdb_add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta,
+                      int64_t rows, int64_t c, float eps, int dtype, void* stream);
 
 /* ========================================================================
  * K4 — classifier-free guidance + DDIM (eta = 0) step, fused.

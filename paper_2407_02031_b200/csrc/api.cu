@@ -37,6 +37,10 @@ int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta
 int residual_inject(void* out, const void* hidden, const void* skip, const void* const* res,
                     const float* scales, int n_res, int64_t pixels, int64_t ch, int64_t cs,
                     int dtype, cudaStream_t st);
+// fused_ops.cu
+int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st);
+int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
+                  float eps, int dtype, cudaStream_t st);
 // cfg_step.cu
 int cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,
                   int in_dtype, int64_t L, const float* coef, int* step_dev, cudaStream_t st);
@@ -169,6 +173,15 @@ int sdb_residual_inject(void* out, const void* hidden, const void* skip,
                         int64_t pixels, int64_t ch, int64_t cs, int dtype, void* stream) {
   return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, dtype,
                          as_stream(stream));
+}
+
+int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, void* stream) {
+  return geglu(proj, out, rows, f, dtype, as_stream(stream));
+}
+
+int sdb_add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows,
+                      int64_t c, float eps, int dtype, void* stream) {
+  return add_layernorm(x, d, y, gamma, beta, rows, c, eps, dtype, as_stream(stream));
 }
 
 int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,

@@ -1,0 +1,163 @@
+// fused_ops.cu — memory-bound fusions around the transformer blocks of the
+// UNet / ControlNet (HBM-bound: one read of each input, one write of each output).
+//
+// K5 geglu:          out[m, :] = h[m, :] * gelu(g[m, :]),  [h | g] = proj[m, 0:2F]
+//                    (the paper's fused GEGLU, PAPER.md:567-570, 70 sites in
+//                    SDXL; the reference keeps only its 1.06 sub-multiplier,
+//                    addonsim/model.py:66-70).  Exact erf GELU as torch's default.
+// K6 add_layernorm:  x[m, :] += d[m, :] (d optional; written back in place), then
+//                    y[m, :] = LayerNorm(x[m, :]) * gamma + beta (eps 1e-5),
+//                    replacing torch's residual add + LayerNorm pair (two extra
+//                    round trips of the residual stream per block).
+// One warp per row (C up to 2560 for LN); fp32 statistics, two-pass over the
+// row held in registers.
+#include "common.cuh"
+
+namespace sdb {
+namespace {
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int64_t rows, int64_t f) {
+  const int64_t vec_per_row = f / 8;
+  const int64_t total = rows * vec_per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / vec_per_row;
+    const int64_t c = (i % vec_per_row) * 8;
+    float h[8], g[8];
+    Vec8<T>::load(proj + m * 2 * f + c, h);
+    Vec8<T>::load(proj + m * 2 * f + f + c, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) h[j] = h[j] * (0.5f * g[j] * (1.f + erff(g[j] * 0.70710678118654752f)));
+    Vec8<T>::store(out + m * f + c, h);
+  }
+}
+
+// NV = vectors of 8 per lane (C = 256 * NV max per warp pass)
+template <typename T, int NV>
+__global__ void __launch_bounds__(256)
+add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* __restrict__ gamma,
+                     const T* __restrict__ beta, int64_t rows, int64_t c, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  T* xr = x + row * c;
+  float v[NV][8];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t col = (int64_t)(k * 32 + lane) * 8;
+    if (col < c) {
+      Vec8<T>::load(xr + col, v[k]);
+      if (d != nullptr) {
+        float dv[8];
+        Vec8<T>::load(d + row * c + col, dv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[k][j] += dv[j];
+        // the residual stream is stored in T: round once, normalise the stored value
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[k][j] = to_f32<T>(from_f32<T>(v[k][j]));
+        Vec8<T>::store(xr + col, v[k]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum += v[k][j];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / (float)c;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t col = (int64_t)(k * 32 + lane) * 8;
+    if (col < c) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float t = v[k][j] - mean;
+        sq = fmaf(t, t, sq);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rstd = rsqrtf(sq / (float)c + eps);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int64_t col = (int64_t)(k * 32 + lane) * 8;
+    if (col < c) {
+      float ga[8], be[8], o[8];
+      Vec8<T>::load(gamma + col, ga);
+      Vec8<T>::load(beta + col, be);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = fmaf((v[k][j] - mean) * rstd, ga[j], be[j]);
+      Vec8<T>::store(y + row * c + col, o);
+    }
+  }
+}
+
+template <typename T>
+int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t st) {
+  const int64_t total = rows * (f / 8);
+  int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+  geglu_kernel<T><<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, st>>>(static_cast<const T*>(proj),
+                                                                         static_cast<T*>(out), rows, f);
+  return check_launch("geglu_kernel");
+}
+
+template <typename T>
+int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
+               float eps, cudaStream_t st) {
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  T* xp = static_cast<T*>(x);
+  const T* dp = static_cast<const T*>(d);
+  T* yp = static_cast<T*>(y);
+  const T* gp = static_cast<const T*>(gamma);
+  const T* bp = static_cast<const T*>(beta);
+  const int nv = (int)((c / 8 + 31) / 32);
+  switch (nv) {
+    case 1: add_layernorm_kernel<T, 1><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 2: add_layernorm_kernel<T, 2><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 3: add_layernorm_kernel<T, 3><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 4: add_layernorm_kernel<T, 4><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 5: add_layernorm_kernel<T, 5><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 6: add_layernorm_kernel<T, 6><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 7: add_layernorm_kernel<T, 7><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 8: add_layernorm_kernel<T, 8><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 9: add_layernorm_kernel<T, 9><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 10: add_layernorm_kernel<T, 10><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    default: return fail(SDB_EINVAL, "add_layernorm: channels must be <= 2560");
+  }
+  return check_launch("add_layernorm_kernel");
+}
+
+}  // namespace
+
+int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st) {
+  if (rows <= 0 || f <= 0 || f % 8 != 0) return fail(SDB_EINVAL, "geglu: width must be a positive multiple of 8");
+  if ((reinterpret_cast<uintptr_t>(proj) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(SDB_EINVAL, "geglu: pointers must be 16-byte aligned");
+  switch (dtype) {
+    case SDB_BF16: return run_geglu<__nv_bfloat16>(proj, out, rows, f, st);
+    case SDB_F16: return run_geglu<__half>(proj, out, rows, f, st);
+    case SDB_F32: return run_geglu<float>(proj, out, rows, f, st);
+    default: return fail(SDB_EUNSUP, "geglu: unsupported dtype");
+  }
+}
+
+int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
+                  float eps, int dtype, cudaStream_t st) {
+  if (rows <= 0 || c <= 0 || c % 8 != 0) return fail(SDB_EINVAL, "add_layernorm: channels must be a multiple of 8");
+  if (!x || !y || !gamma || !beta) return fail(SDB_EINVAL, "add_layernorm: NULL pointer");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(y) |
+       reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(beta)) & 15)
+    return fail(SDB_EINVAL, "add_layernorm: pointers must be 16-byte aligned");
+  switch (dtype) {
+    case SDB_BF16: return run_add_ln<__nv_bfloat16>(x, d, y, gamma, beta, rows, c, eps, st);
+    case SDB_F16: return run_add_ln<__half>(x, d, y, gamma, beta, rows, c, eps, st);
+    case SDB_F32: return run_add_ln<float>(x, d, y, gamma, beta, rows, c, eps, st);
+    default: return fail(SDB_EUNSUP, "add_layernorm: unsupported dtype");
+  }
+}
+
+}  // namespace sdb

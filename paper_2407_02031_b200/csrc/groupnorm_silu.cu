@@ -12,27 +12,33 @@
 // i.e. a strided set.  Thread mapping keeps the 16-byte vector lanes fixed on
 // channels: blockDim = CV * rpp with CV = C/8 vector columns and rpp pixel
 // rows per pass, so each thread always owns the same 8 channels and
-// accumulates them in registers — fully coalesced 16 B loads, no atomics.
+// accumulates them in registers — fully coalesced 16 B loads, no atomics on
+// the data path.
 //
-//   pass 1  gn_partial_kernel : shifted sums  S1 = sum(x-K_g), S2 = sum((x-K_g)^2)
-//                                per (n, chunk, channel-vector) -> reduced per group
-//   pass 2  gn_finalize_kernel: fp64 combine over chunks -> mean, rstd per (n, g)
-//   pass 3  gn_apply_kernel   : y = act(x * a_c + b_c), a_c = gamma_c*rstd_g,
-//                                b_c = beta_c - mean_g*a_c
-// Pass 3 re-reads x right after pass 1 touched it; at SDXL sizes the tensor
-// (<= 63 MB at CFG batch 2) stays in the 126 MB L2, so HBM traffic stays close
-// to the algorithmic one read + one write.  The shift K_g (the group's first
-// element) keeps the one-pass variance free of cancellation.
+//   kernel 1  gn_stats_kernel: per (n, chunk) shifted sums S1 = sum(x'-K_g),
+//             S2 = sum((x'-K_g)^2) reduced per group; the LAST CTA of each
+//             sample (threadfence + counter) combines the chunks in fp64 and
+//             writes mean / rstd — no separate finalize launch and no
+//             co-residency requirement (safe next to a concurrent LoRA patch
+//             or ControlNet on another stream).
+//   kernel 2  gn_apply_kernel: y = act(x * a_c + b_c), a_c = gamma_c*rstd_g,
+//             b_c = beta_c + (add_c - mean_g) * a_c.
+// Kernel 2 re-reads x right after kernel 1 streamed it; at SDXL sizes the
+// tensor (<= 63 MB at CFG batch 2) stays in the 126 MB L2, so HBM traffic
+// stays close to the algorithmic one read + one write.
 //
-// Optional add_nc [N][C] (fp32) is added to x before normalisation: the
-// ResNet block's time-embedding projection (h = conv1(x) + temb_proj[n, c])
-// is fused here instead of costing its own read + write of the feature map.
+// Optional add_nc [N][C] (fp32) is added to x before normalisation (x' = x +
+// add): the ResNet block's time-embedding projection (h = conv1(x) +
+// temb_proj[n, c]) is fused here instead of costing its own read + write of
+// the feature map.  The shift K_g = x[n, pixel 0, g*cpg] is one constant per
+// group, so the variance is shift-invariant and free of cancellation.
 #include "common.cuh"
 
 namespace sdb {
 namespace {
 
 constexpr int kMaxThreads = 512;
+constexpr int kMaxGroups = 64;
 
 struct GnShape {
   int64_t n, hw, c, groups, cv, cpg;
@@ -47,22 +53,24 @@ GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups) {
   s.cpg = c / groups;
   s.rpp = (int)std::max<int64_t>(1, 384 / s.cv);
   s.threads = (int)(s.cv * s.rpp);
-  // ~4 waves of CTAs over 148 SMs across the whole batch
-  int64_t target = (4 * kNumSMs + n - 1) / n;
-  int64_t max_chunks = (hw + s.rpp - 1) / s.rpp;
+  // ~2 waves of CTAs over 148 SMs across the whole batch, >= 4 rows per lane
+  int64_t target = (2 * kNumSMs + n - 1) / n;
+  int64_t max_chunks = std::max<int64_t>(1, hw / (4 * s.rpp));
   s.chunks = std::max<int64_t>(1, std::min<int64_t>(target, max_chunks));
   s.rows_per_chunk = (hw + s.chunks - 1) / s.chunks;
   s.chunks = (hw + s.rows_per_chunk - 1) / s.rows_per_chunk;
   return s;
 }
 
-// partial[n][chunk][group][2]
+// workspace: counters[n] (uint, zero at rest) | stats[n][group][2] | partial[n][chunk][group][2]
 template <typename T>
-__global__ void gn_partial_kernel(const T* __restrict__ x, const float* __restrict__ add_nc,
-                                  float* __restrict__ partial,
-                                  int64_t hw, int64_t c, int64_t groups, int64_t cpg,
-                                  int64_t rows_per_chunk, int64_t chunks, int rpp) {
-  extern __shared__ float red[];  // [rpp][c][2] then reused
+__global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc,
+                                float* __restrict__ partial, float* __restrict__ stats,
+                                unsigned int* __restrict__ counters, int64_t hw, int64_t c,
+                                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int64_t chunks,
+                                int rpp, float eps) {
+  extern __shared__ float red[];  // [rpp][c][2]
+  __shared__ bool is_last;
   const int64_t n = blockIdx.y;
   const int64_t chunk = blockIdx.x;
   const int cv = (int)(c / 8);
@@ -71,15 +79,13 @@ __global__ void gn_partial_kernel(const T* __restrict__ x, const float* __restri
   const int64_t c0 = (int64_t)v * 8;
   const T* xs = x + n * hw * c;
 
-  // per-channel shift = first element of its group (pixel 0, channel g*cpg)
-  // (the optional per-(n,c) input bias is folded into the shift: d = x - (K - a))
+  // d = x' - K_g = x - (K_g - add_c)
   float K[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     K[j] = to_f32<T>(xs[((c0 + j) / cpg) * cpg]);
     if (add_nc != nullptr) K[j] -= add_nc[n * c + c0 + j];
   }
-
   float s1[8], s2[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) { s1[j] = 0.f; s2[j] = 0.f; }
@@ -87,36 +93,35 @@ __global__ void gn_partial_kernel(const T* __restrict__ x, const float* __restri
   const int64_t p0 = chunk * rows_per_chunk;
   const int64_t p1 = min(hw, p0 + rows_per_chunk);
   int64_t p = p0 + r;
-  // 2-deep unroll for memory-level parallelism
-  for (; p + rpp < p1; p += 2 * rpp) {
-    float a[8], b[8];
-    Vec8<T>::load(xs + p * c + c0, a);
-    Vec8<T>::load(xs + (p + rpp) * c + c0, b);
+  for (; p + 3 * rpp < p1; p += 4 * rpp) {   // 4 independent 16 B loads in flight per thread
+    float a[4][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float d = a[j] - K[j];
-      s1[j] += d; s2[j] = fmaf(d, d, s2[j]);
-      float e = b[j] - K[j];
-      s1[j] += e; s2[j] = fmaf(e, e, s2[j]);
-    }
+    for (int u = 0; u < 4; ++u) Vec8<T>::load(xs + (p + u * rpp) * c + c0, a[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = a[u][j] - K[j];
+        s1[j] += d;
+        s2[j] = fmaf(d, d, s2[j]);
+      }
   }
   for (; p < p1; p += rpp) {
     float a[8];
     Vec8<T>::load(xs + p * c + c0, a);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float d = a[j] - K[j];
-      s1[j] += d; s2[j] = fmaf(d, d, s2[j]);
+      const float d = a[j] - K[j];
+      s1[j] += d;
+      s2[j] = fmaf(d, d, s2[j]);
     }
   }
-  // reduce over the rpp row lanes: red[r][ch][2]
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     red[((int64_t)r * c + c0 + j) * 2 + 0] = s1[j];
     red[((int64_t)r * c + c0 + j) * 2 + 1] = s2[j];
   }
   __syncthreads();
-  // one thread per group sums its cpg channels over rpp rows
   for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
     float t1 = 0.f, t2 = 0.f;
     for (int rr = 0; rr < rpp; ++rr)
@@ -128,30 +133,40 @@ __global__ void gn_partial_kernel(const T* __restrict__ x, const float* __restri
     out[0] = t1;
     out[1] = t2;
   }
-}
-
-// stats[n][g] = {mean, rstd}
-template <typename T>
-__global__ void gn_finalize_kernel(const T* __restrict__ x, const float* __restrict__ partial,
-                                   float* __restrict__ stats, int64_t n_total, int64_t hw,
-                                   int64_t c, int64_t groups, int64_t cpg, int64_t chunks,
-                                   float eps) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n_total * groups) return;
-  const int64_t n = idx / groups, g = idx % groups;
-  double t1 = 0.0, t2 = 0.0;
-  for (int64_t ch = 0; ch < chunks; ++ch) {
-    const float* pp = partial + ((n * chunks + ch) * groups + g) * 2;
-    t1 += pp[0];
-    t2 += pp[1];
+  // ---- the last CTA of this sample finalises (no extra launch) ----
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int done = atomicAdd(counters + n, 1u);
+    is_last = (done == (unsigned int)chunks - 1);
   }
-  const double cnt = (double)hw * (double)cpg;
-  const double K = to_f32<T>(x[n * hw * c + g * cpg]);
-  const double dm = t1 / cnt;
-  double var = t2 / cnt - dm * dm;
-  if (var < 0.0) var = 0.0;
-  stats[idx * 2 + 0] = (float)(K + dm);
-  stats[idx * 2 + 1] = (float)(1.0 / sqrt(var + (double)eps));
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int64_t g = warp; g < groups; g += nwarps) {
+    double t1 = 0.0, t2 = 0.0;
+    for (int64_t ch = lane; ch < chunks; ch += 32) {
+      const float* pp = partial + ((n * chunks + ch) * groups + g) * 2;
+      t1 += (double)__ldcg(pp);
+      t2 += (double)__ldcg(pp + 1);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+      t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+    }
+    if (lane == 0) {
+      const double cnt = (double)hw * (double)cpg;
+      const double Kg = (double)to_f32<T>(xs[g * cpg]);
+      const double dm = t1 / cnt;
+      double var = t2 / cnt - dm * dm;
+      if (var < 0.0) var = 0.0;
+      stats[(n * groups + g) * 2 + 0] = (float)(Kg + dm);
+      stats[(n * groups + g) * 2 + 1] = (float)(1.0 / sqrt(var + (double)eps));
+    }
+  }
+  if (threadIdx.x == 0) counters[n] = 0u;  // ready for the next launch / graph replay
 }
 
 template <typename T, bool SILU>
@@ -183,13 +198,32 @@ __global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread rea
   T* ys = y + n * hw * c;
   const int64_t p0 = chunk * rows_per_chunk;
   const int64_t p1 = min(hw, p0 + rows_per_chunk);
-  for (int64_t p = p0 + r; p < p1; p += rpp) {
+  int64_t p = p0 + r;
+  for (; p + rpp < p1; p += 2 * rpp) {
+    float a[8], b[8];
+    Vec8<T>::load(xs + p * c + c0, a);
+    Vec8<T>::load(xs + (p + rpp) * c + c0, b);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float t = fmaf(a[j], A[j], B[j]);
+      float u = fmaf(b[j], A[j], B[j]);
+      if (SILU) {
+        t = t / (1.f + __expf(-t));
+        u = u / (1.f + __expf(-u));
+      }
+      a[j] = t;
+      b[j] = u;
+    }
+    Vec8<T>::store(ys + p * c + c0, a);
+    Vec8<T>::store(ys + (p + rpp) * c + c0, b);
+  }
+  for (; p < p1; p += rpp) {
     float a[8];
     Vec8<T>::load(xs + p * c + c0, a);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float t = fmaf(a[j], A[j], B[j]);
-      if (SILU) t = t / (1.f + expf(-t));
+      if (SILU) t = t / (1.f + __expf(-t));
       a[j] = t;
     }
     Vec8<T>::store(ys + p * c + c0, a);
@@ -198,25 +232,21 @@ __global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread rea
 
 template <typename T>
 int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, const float* add_nc, int64_t n,
-           int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* ws,
-           cudaStream_t st) {
+           int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* ws, cudaStream_t st) {
   const T* x = static_cast<const T*>(xv);
   T* y = static_cast<T*>(yv);
   GnShape s = gn_shape(n, hw, c, groups);
-  float* partial = static_cast<float*>(ws);
-  float* stats = partial + n * s.chunks * groups * 2;
+  unsigned int* counters = static_cast<unsigned int*>(ws);
+  float* stats = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256);
+  float* partial = stats + n * groups * 2;
   dim3 grid((unsigned)s.chunks, (unsigned)n);
   size_t smem = (size_t)s.rpp * c * 2 * sizeof(float);
   if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(gn_partial_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gn_stats_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  gn_partial_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, partial, hw, c, groups, s.cpg,
-                                                      s.rows_per_chunk, s.chunks, s.rpp);
-  if (int rc = check_launch("gn_partial_kernel")) return rc;
-  int64_t ng = n * groups;
-  gn_finalize_kernel<T><<<(unsigned)((ng + 127) / 128), 128, 0, st>>>(x, partial, stats, n, hw, c, groups,
-                                                                    s.cpg, s.chunks, eps);
-  if (int rc = check_launch("gn_finalize_kernel")) return rc;
+  gn_stats_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, partial, stats, counters, hw, c, groups, s.cpg,
+                                                    s.rows_per_chunk, s.chunks, s.rpp, eps);
+  if (int rc = check_launch("gn_stats_kernel")) return rc;
   if (silu)
     gn_apply_kernel<T, true><<<grid, s.threads, 0, st>>>(x, y, add_nc, stats, gamma, beta, hw, c, groups, s.cpg,
                                                          s.rows_per_chunk, s.rpp);
@@ -230,15 +260,16 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, cons
 
 size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
   GnShape s = gn_shape(n, hw, c, groups);
-  return (size_t)(n * s.chunks * groups * 2 + n * groups * 2) * sizeof(float);
+  return 256 + (size_t)(n * groups * 2 + n * s.chunks * groups * 2) * sizeof(float);
 }
 
-int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
-                   const float* add_nc, int64_t n,
-                   int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype,
-                   void* ws, cudaStream_t st) {
+int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc, int64_t n,
+                   int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, void* ws,
+                   cudaStream_t st) {
   if (n <= 0 || hw <= 0 || c <= 0 || groups <= 0) return fail(SDB_EINVAL, "groupnorm: empty shape");
+  if (n > 64) return fail(SDB_EINVAL, "groupnorm: batch > 64 unsupported");
   if (c % groups != 0) return fail(SDB_EINVAL, "groupnorm: channels not divisible by groups");
+  if (groups > kMaxGroups) return fail(SDB_EINVAL, "groupnorm: more than 64 groups");
   if (c % 8 != 0) return fail(SDB_EINVAL, "groupnorm: channels must be a multiple of 8");
   if (c / 8 > kMaxThreads) return fail(SDB_EINVAL, "groupnorm: channels > 4096 unsupported");
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)

@@ -20,12 +20,12 @@
 //     reloaded per row tile (L2-resident: its re-read costs R/256 of the W read).
 //   * tcgen05 path: one elected thread issues ceil(R/16) MMAs of
 //     M=128 x N=256 x K=16 (kind::f16, bf16 in, fp32 accumulate) into one of
-//     two 256-column TMEM accumulators; the 4 epilogue warps read their 32
+//     two 256-column TMEM accumulators; the 8 epilogue warps read their 32
 //     TMEM lanes with tcgen05.ld while the next tile's MMA runs in the other.
 //   * SIMT path (R <= 32): the epilogue threads hold their A row in registers
 //     and contract against broadcast shared-memory reads of the B panel.
-// Roles: warps 0-3 epilogue (TMEM lanes 0-127), warp 4 producer (TMA), warp 5
-// MMA issuer + TMEM allocator.  One CTA per SM, grid-strided over units.
+// Roles: warps 0-7 epilogue (TMEM lane quadrant x column half), warp 8
+// producer (TMA), warp 9 MMA issuer + TMEM allocator.  One CTA per SM, grid-strided over units.
 #include <cuda.h>
 
 #include <algorithm>
@@ -45,7 +45,11 @@ constexpr int kKB = 64;                   // K elements per packed block (one 12
 constexpr int kABlockBytes = kBM * 128;   // 16 KB per K block of an A tile
 constexpr int kBBlockBytes = kBN * 128;   // 32 KB per K block of a B panel
 constexpr int kUnitTiles = 8;             // row tiles per work unit (B panel reuse)
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;              // 2 warps per TMEM lane quadrant (column halves)
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kProducerWarp = kEpiWarps;
+constexpr int kMmaWarp = kEpiWarps + 1;
+constexpr int kThreads = (kEpiWarps + 2) * 32;
 constexpr int kMaxKB = 4;                 // rank <= 256
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
                             ((uint32_t)(kBM >> 4) << 24);   // f32 accum, bf16 A/B, K-major, 128x256
@@ -109,6 +113,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int 
 }
 __device__ __forceinline__ void tma_store_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -196,14 +203,14 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    const uint32_t consumer_count = TC ? 1u : 4u;   // tcgen05.commit vs one arrive per epilogue warp
+    const uint32_t consumer_count = TC ? 1u : (uint32_t)kEpiWarps;   // tcgen05.commit vs one arrive per epilogue warp
     mbar_init(bar(B_FULL), 1);
     mbar_init(bar(B_EMPTY), consumer_count);
     mbar_init(bar(A_FULL), 1);
     mbar_init(bar(A_EMPTY), consumer_count);
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(T_FULL + i), 1);
-      mbar_init(bar(T_EMPTY + i), 4);
+      mbar_init(bar(T_EMPTY + i), kEpiWarps);
     }
     for (int i = 0; i < n_slots; ++i) {
       mbar_init(bar(W_FULL + i), 1);
@@ -211,7 +218,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (TC && warp == 5) {
+  if (TC && warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(2 * kBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -221,7 +228,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   tc_fence_after();
   const uint32_t tmem_base = TC ? *tmem_holder : 0u;
 
-  if (warp == 4) {
+  if (warp == kProducerWarp) {
     // ===================== producer =====================
     if (lane == 0) {
       int a_cnt = 0, b_cnt = 0, w_cnt = 0;
@@ -253,7 +260,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     // ===================== MMA issuer =====================
     if (TC && lane == 0) {
       int tile = 0, b_cnt = 0;
@@ -283,9 +290,13 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     }
     __syncwarp();
   } else {
-    // ===================== epilogue (warps 0-3) =====================
-    const int r = threadIdx.x;   // tile row == TMEM lane
+    // ===================== epilogue (warps 0-7) =====================
+    // warp e reads TMEM lane quadrant (e & 3) (the hardware binds a warp to
+    // lanes 32*(warp % 4)...) and column half (e >> 2) of every 64-column box.
+    const int r = ((warp & 3) << 5) | lane;   // tile row == TMEM lane
+    const int half = warp >> 2;
     int tile = 0, w_cnt = 0, b_cnt = 0;
+    int pending = -1;                          // slot whose TMA store may still be reading smem
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const TcUnit un = units[u];
       const TcJob& J = jobs[un.job];
@@ -320,14 +331,14 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
           const int slot = w_cnt % n_slots;
           mbar_wait(bar(W_FULL + slot), (w_cnt / n_slots) & 1);
           uint8_t* row = sW + slot * kBoxBytes + r * 128;
-#pragma unroll
-          for (int half = 0; half < 2; ++half) {
+          {
             float v[32];
             if (TC) {
-              const uint32_t taddr = tmem_base + ((uint32_t)(warp * 32) << 16) + buf * kBN + bx * kBoxN + half * 32;
+              const uint32_t taddr =
+                  tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + buf * kBN + bx * kBoxN + half * 32;
               tc_ld32(taddr, v);
             } else {
-#pragma unroll 4
+#pragma unroll
               for (int c = 0; c < 32; ++c) {
                 const int n = bx * kBoxN + half * 32 + c;   // B panel row (output column)
                 const uint8_t* brow = sB + n * 128;
@@ -348,11 +359,15 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
             rmw32(row, r, half * 4, v, ss);
           }
           fence_proxy_async();
-          named_bar(1, 128);
-          if (r == 0) {
+          named_bar(1, kEpiThreads);
+          if (threadIdx.x == 0) {
+            // keep one store in flight: release the PREVIOUS slot once its read is done
             tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM, smem_u32(sW + slot * kBoxBytes));
-            tma_store_wait_read();
-            mbar_arrive(bar(W_EMPTY + slot));
+            if (pending >= 0) {
+              tma_store_wait_read1();
+              mbar_arrive(bar(W_EMPTY + pending));
+            }
+            pending = slot;
           }
           ++w_cnt;
         }
@@ -368,11 +383,17 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
       }
       ++b_cnt;
     }
-    if (r == 0) tma_store_wait_all();
+    if (threadIdx.x == 0) {
+      if (pending >= 0) {
+        tma_store_wait_read();
+        mbar_arrive(bar(W_EMPTY + pending));
+      }
+      tma_store_wait_all();
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (TC && warp == 5) {
+  if (TC && warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
   }

@@ -250,7 +250,7 @@ def _workspace(nbytes: int, device: torch.device) -> torch.Tensor:
     key = (device, torch.cuda.current_stream(device).cuda_stream)
     buf = _ws_cache.get(key)
     if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)
+        buf = torch.zeros(max(nbytes, 1 << 16), dtype=torch.uint8, device=device)  # K2 counters start at 0
         _ws_cache[key] = buf
     return buf
 
@@ -335,6 +335,37 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
         out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),
         ptrs, sc, k, n * hw, ch, cs, sdb_dtype(skip), _stream_ptr(None)))
     return out
+
+
+# --------------------------------------------------------------------------
+# K5 / K6 — GEGLU and residual-add + LayerNorm of the transformer blocks
+# --------------------------------------------------------------------------
+def geglu(proj: torch.Tensor) -> torch.Tensor:
+    """proj [..., 2F] contiguous -> [..., F] = proj[..., :F] * gelu(proj[..., F:])."""
+    require_cuda(proj)
+    if not proj.is_contiguous():
+        raise ValidationError("geglu input must be contiguous")
+    f2 = proj.shape[-1]
+    out = torch.empty(proj.shape[:-1] + (f2 // 2,), dtype=proj.dtype, device=proj.device)
+    _count(1)
+    _lib.check("sdb_geglu", _lib.lib().sdb_geglu(proj.data_ptr(), out.data_ptr(), proj.numel() // f2, f2 // 2,
+                                                 sdb_dtype(proj), _stream_ptr(None)))
+    return out
+
+
+def add_layernorm(x: torch.Tensor, d: Optional[torch.Tensor], gamma: torch.Tensor, beta: torch.Tensor,
+                  eps: float = 1e-5) -> torch.Tensor:
+    """x += d (in place, d may be None); returns LayerNorm(x) * gamma + beta."""
+    require_cuda(x, d, gamma, beta)
+    if not x.is_contiguous() or (d is not None and (not d.is_contiguous() or d.shape != x.shape)):
+        raise ValidationError("add_layernorm: x and d must be contiguous and of equal shape")
+    c = x.shape[-1]
+    y = torch.empty_like(x)
+    _count(1)
+    _lib.check("sdb_add_layernorm", _lib.lib().sdb_add_layernorm(
+        x.data_ptr(), d.data_ptr() if d is not None else None, y.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
+        x.numel() // c, c, float(eps), sdb_dtype(x), _stream_ptr(None)))
+    return y
 
 
 # --------------------------------------------------------------------------

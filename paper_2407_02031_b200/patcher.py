@@ -94,7 +94,7 @@ class PatchSet:
     device-resident K1 job table."""
 
     def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]],
-                 shadow: Optional[dict] = None, use_tma: bool = True):
+                 shadow: Optional[dict] = None, use_tma: bool = True, simt_max_rank: int = 16):
         if not adapters:
             raise ValidationError("PatchSet needs at least one adapter")
         self.params = params
@@ -129,7 +129,7 @@ class PatchSet:
         slow = [e for e in self.entries if not any(e is f for f in fast)]
         self.plans = []
         if fast:
-            self.plans.append(ops.LoraTmaPlan(fast))
+            self.plans.append(ops.LoraTmaPlan(fast, simt_max_rank=simt_max_rank))
         if slow:
             self.plans.append(ops.LoraPatchPlan(slow))
         self.plan = self.plans[0]

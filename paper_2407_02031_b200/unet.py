@@ -328,15 +328,15 @@ class Net:
         tok = hs.permute(0, 2, 3, 1).reshape(n, h * w, c)       # NHWC storage: a free view
         tok = self.lin(pre + ".proj_in", tok)
         heads = self.cfg.heads(c)
+        delta = None   # pending residual: fused into the next block's add + LayerNorm (K6)
         for d in range(depth):
             b = f"{pre}.blocks.{d}"
-            y = F.layer_norm(tok, (c,), self.t[b + ".norm1.weight"], self.t[b + ".norm1.bias"])
-            tok = tok + self.attention(b + ".attn1", y, None, heads)
-            y = F.layer_norm(tok, (c,), self.t[b + ".norm2.weight"], self.t[b + ".norm2.bias"])
-            tok = tok + self.attention(b + ".attn2", y, ctx, heads)
-            y = F.layer_norm(tok, (c,), self.t[b + ".norm3.weight"], self.t[b + ".norm3.bias"])
-            hv, gate = self.lin(b + ".ff.proj", y).chunk(2, dim=-1)
-            tok = tok + self.lin(b + ".ff.out", hv * F.gelu(gate))
+            ln = lambda k, dl: ops.add_layernorm(tok, dl, self.t[f"{b}.{k}.weight"], self.t[f"{b}.{k}.bias"])
+            y = ln("norm1", delta)
+            y = ln("norm2", self.attention(b + ".attn1", y, None, heads))
+            y = ln("norm3", self.attention(b + ".attn2", y, ctx, heads))
+            delta = self.lin(b + ".ff.out", ops.geglu(self.lin(b + ".ff.proj", y)))   # K5
+        tok = tok + delta
         tok = self.lin(pre + ".proj_out", tok)
         out = tok.view(n, h, w, c).permute(0, 3, 1, 2)            # channels_last view
         return out + res

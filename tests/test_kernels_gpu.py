@@ -106,3 +106,44 @@ def test_no_cpu_tensors_accepted():
     from paper_2407_02031_b200.errors import DeviceError
     with pytest.raises(DeviceError):
         ops.groupnorm_silu(torch.randn(1, 32, 4, 4), None, None)
+
+
+def test_groupnorm_temb_add_fused():
+    """add_nc (ResNet time-embedding projection) added before normalisation."""
+    x = cl(torch.randn(2, 640, 32, 32, device="cuda").to(torch.bfloat16))
+    add = torch.randn(2, 640, device="cuda") * 3
+    gamma, beta = torch.rand(640, device="cuda") + 0.5, torch.randn(640, device="cuda")
+    y = ops.groupnorm_silu(x, gamma, beta, add_nc=add)
+    ref = F.silu(F.group_norm(x.float() + add[:, :, None, None], 32, gamma, beta, 1e-5))
+    assert ((y.float() - ref).abs() <= ref.abs() * 2 ** -8 + 2e-3).all()
+
+
+def test_groupnorm_repeated_launches_reset_counters():
+    x = cl(torch.randn(2, 320, 64, 64, device="cuda").to(torch.bfloat16))
+    g, b = torch.ones(320, device="cuda"), torch.zeros(320, device="cuda")
+    first = ops.groupnorm_silu(x, g, b)
+    for _ in range(5):
+        assert torch.equal(ops.groupnorm_silu(x, g, b), first)
+
+
+@pytest.mark.parametrize("rows,f", [(2 * 4096, 2560), (2 * 1024, 5120), (77, 256), (3, 8)])
+def test_geglu(rows, f):
+    proj = torch.randn(rows, 2 * f, device="cuda").to(torch.bfloat16)
+    out = ops.geglu(proj)
+    h, g = proj.float().chunk(2, dim=-1)
+    ref = h * F.gelu(g)
+    assert ((out.float() - ref).abs() <= ref.abs() * 2 ** -8 + 1e-5).all()
+
+
+@pytest.mark.parametrize("c", [64, 320, 640, 1280, 2560])
+@pytest.mark.parametrize("with_delta", [True, False])
+def test_add_layernorm(c, with_delta):
+    x = torch.randn(2, 300, c, device="cuda").to(torch.bfloat16)
+    d = torch.randn(2, 300, c, device="cuda").to(torch.bfloat16) if with_delta else None
+    w = (torch.rand(c, device="cuda") + 0.5).to(torch.bfloat16)
+    b = torch.randn(c, device="cuda").to(torch.bfloat16)
+    x_ref = (x.float() + d.float()).to(torch.bfloat16) if with_delta else x.clone()
+    y = ops.add_layernorm(x, d, w, b)
+    assert torch.equal(x, x_ref)  # residual stream updated in place, rounded once
+    ref = F.layer_norm(x_ref.float(), (c,), w.float(), b.float(), 1e-5)
+    assert ((y.float() - ref).abs() <= ref.abs() * 2 ** -7 + 2e-2).all()
