@@ -1,6 +1,5 @@
 // lora_patch_tc.cu — K1 for bf16 serving weights: TMA-staged, warp-specialised,
-// persistent LoRA patch with the rank contraction on tcgen05 (TMEM accumulator)
-// or, at low rank, on FFMA.
+// persistent LoRA patch with the rank contraction on tcgen05 (TMEM accumulator).
 //
 //   W_out[r, c] = bf16( fma(sign*scale, sum_k A[r,k] * B[c,k], float(W_in[r,c])) )
 //
@@ -17,13 +16,12 @@
 //     UMMA canonical K-major SWIZZLE_128B layout, so they move with plain bulk
 //     copies: the B panel (256 output columns x R) stays resident while the
 //     CTA walks up to 8 row tiles of that panel; the A tile (128 rows x R) is
-//     reloaded per row tile (L2-resident: its re-read costs R/256 of the W read).
+//     streamed per row tile in 64-deep K blocks through a 2-stage ring
+//     (L2-resident: its re-read costs R/256 of the W read).
 //   * tcgen05 path: one elected thread issues ceil(R/16) MMAs of
 //     M=128 x N=256 x K=16 (kind::f16, bf16 in, fp32 accumulate) into one of
 //     two 256-column TMEM accumulators; the 8 epilogue warps read their 32
 //     TMEM lanes with tcgen05.ld while the next tile's MMA runs in the other.
-//   * SIMT path (R <= 32): the epilogue threads hold their A row in registers
-//     and contract against broadcast shared-memory reads of the B panel.
 // Roles: warps 0-7 epilogue (TMEM lane quadrant x column half), warp 8
 // producer (TMA), warp 9 MMA issuer + TMEM allocator.  One CTA per SM, grid-strided over units.
 #include <cuda.h>
@@ -51,6 +49,7 @@ constexpr int kProducerWarp = kEpiWarps;
 constexpr int kMmaWarp = kEpiWarps + 1;
 constexpr int kThreads = (kEpiWarps + 2) * 32;
 constexpr int kMaxKB = 4;                 // rank <= 256
+constexpr int kAStages = 2;               // A K-blocks in flight
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
                             ((uint32_t)(kBM >> 4) << 24);   // f32 accum, bf16 A/B, K-major, 128x256
 
@@ -183,18 +182,19 @@ __device__ __forceinline__ void rmw32(uint8_t* row, int r, int chunk0, const flo
   }
 }
 
-template <bool TC, int KSIMT>
+template <int UNUSED>
 __global__ void __launch_bounds__(kThreads, 1)
 lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restrict__ jobs,
                       const TcUnit* __restrict__ units, int n_units, float sign, int kb_max, int n_slots) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = smem;                                   // kb_max * 32 KB
-  uint8_t* sA = sB + kb_max * kBBlockBytes;             // kb_max * 16 KB
-  uint8_t* sW = sA + kb_max * kABlockBytes;             // n_slots * 16 KB
+  uint8_t* sB = smem;                                   // kb_max * 32 KB: resident B panel
+  uint8_t* sA = sB + kb_max * kBBlockBytes;             // kAStages * 16 KB: streamed A K-blocks
+  uint8_t* sW = sA + kAStages * kABlockBytes;           // n_slots * 16 KB: W box ring
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + n_slots * kBoxBytes);
   // barrier indices
-  const int B_FULL = 0, B_EMPTY = 1, A_FULL = 2, A_EMPTY = 3, T_FULL = 4, T_EMPTY = 6, W_FULL = 8;
+  const int B_FULL = 0, B_EMPTY = 1, A_FULL = 2, A_EMPTY = A_FULL + kAStages, T_FULL = A_EMPTY + kAStages;
+  const int T_EMPTY = T_FULL + 2, W_FULL = T_EMPTY + 2;
   const int W_EMPTY = W_FULL + n_slots;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + W_EMPTY + n_slots);
   auto bar = [&](int i) { return smem_u32(bars + i); };
@@ -203,11 +203,12 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    const uint32_t consumer_count = TC ? 1u : (uint32_t)kEpiWarps;   // tcgen05.commit vs one arrive per epilogue warp
     mbar_init(bar(B_FULL), 1);
-    mbar_init(bar(B_EMPTY), consumer_count);
-    mbar_init(bar(A_FULL), 1);
-    mbar_init(bar(A_EMPTY), consumer_count);
+    mbar_init(bar(B_EMPTY), 1);           // tcgen05.commit after the unit's last MMA
+    for (int i = 0; i < kAStages; ++i) {
+      mbar_init(bar(A_FULL + i), 1);
+      mbar_init(bar(A_EMPTY + i), 1);     // tcgen05.commit after the MMAs reading the stage
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(T_FULL + i), 1);
       mbar_init(bar(T_EMPTY + i), kEpiWarps);
@@ -218,7 +219,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (TC && warp == kMmaWarp) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(2 * kBN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -226,10 +227,10 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = TC ? *tmem_holder : 0u;
+  const uint32_t tmem_base = *tmem_holder;
 
   if (warp == kProducerWarp) {
-    // ===================== producer =====================
+    // ===================== producer: B panel, A K-blocks, W boxes =====================
     if (lane == 0) {
       int a_cnt = 0, b_cnt = 0, w_cnt = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
@@ -237,6 +238,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         const TcJob& J = jobs[un.job];
         const CUtensorMap* min = maps + J.map_in;
         prefetch_map(min);
+        const int nkb = (J.rank + kKB - 1) / kKB;
         if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
         mbar_expect_tx(bar(B_FULL), J.kb * kBBlockBytes);
         bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL));
@@ -244,45 +246,51 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
         const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
         for (int m = un.m_begin; m < un.m_end; ++m) {
-          if (a_cnt > 0) mbar_wait(bar(A_EMPTY), (a_cnt - 1) & 1);
-          mbar_expect_tx(bar(A_FULL), J.kb * kABlockBytes);
-          bulk_g2s(smem_u32(sA), J.a + (size_t)m * J.kb * kABlockBytes, J.kb * kABlockBytes, bar(A_FULL));
-          ++a_cnt;
-          for (int bx = 0; bx < nbox; ++bx) {
+          for (int kb = 0; kb < nkb; ++kb, ++a_cnt) {
+            const int st = a_cnt % kAStages;
+            if (a_cnt >= kAStages) mbar_wait(bar(A_EMPTY + st), ((a_cnt / kAStages) - 1) & 1);
+            mbar_expect_tx(bar(A_FULL + st), kABlockBytes);
+            bulk_g2s(smem_u32(sA + st * kABlockBytes), J.a + ((size_t)m * J.kb + kb) * kABlockBytes, kABlockBytes,
+                     bar(A_FULL + st));
+          }
+          for (int bx = 0; bx < nbox; ++bx, ++w_cnt) {
             const int slot = w_cnt % n_slots;
             if (w_cnt >= n_slots) mbar_wait(bar(W_EMPTY + slot), ((w_cnt / n_slots) - 1) & 1);
             mbar_expect_tx(bar(W_FULL + slot), kBoxBytes);
             tma_load_2d(smem_u32(sW + slot * kBoxBytes), min, un.n_tile * kBN + bx * kBoxN, m * kBM,
                         bar(W_FULL + slot));
-            ++w_cnt;
           }
         }
       }
     }
     __syncwarp();
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer =====================
-    if (TC && lane == 0) {
-      int tile = 0, b_cnt = 0;
+    // ===================== MMA issuer (one thread) =====================
+    if (lane == 0) {
+      int tile = 0, b_cnt = 0, a_cnt = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
-        const int nks = (J.rank + 15) / 16;
+        const int nks = (J.rank + 15) / 16;     // K steps of 16 (zero-padded)
+        const int nkb = (J.rank + kKB - 1) / kKB;
         mbar_wait(bar(B_FULL), b_cnt & 1);
         for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
           const int buf = tile & 1;
-          mbar_wait(bar(A_FULL), tile & 1);
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
-          tc_fence_after();
           const uint32_t d = tmem_base + buf * kBN;
-          for (int s = 0; s < nks; ++s) {
-            const int kb = s >> 2, ks = s & 3;
-            const uint64_t ad = sw128_desc(smem_u32(sA + kb * kABlockBytes + ks * 32));
-            const uint64_t bd = sw128_desc(smem_u32(sB + kb * kBBlockBytes + ks * 32));
-            tc_mma(d, ad, bd, kIdesc, s > 0 ? 1u : 0u);
+          for (int kb = 0; kb < nkb; ++kb, ++a_cnt) {
+            const int st = a_cnt % kAStages;
+            mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
+            tc_fence_after();
+            const int ks_end = std::min(4, nks - kb * 4);
+            for (int ks = 0; ks < ks_end; ++ks) {
+              const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
+              const uint64_t bd = sw128_desc(smem_u32(sB + kb * kBBlockBytes + ks * 32));
+              tc_mma(d, ad, bd, kIdesc, (kb | ks) ? 1u : 0u);
+            }
+            tc_commit(bar(A_EMPTY + st));       // stage free once these MMAs completed
           }
-          tc_commit(bar(A_EMPTY));
-          tc_commit(bar(T_FULL + buf));
+          tc_commit(bar(T_FULL + buf));          // accumulator complete
         }
         tc_commit(bar(B_EMPTY));
         ++b_cnt;
@@ -295,7 +303,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     // lanes 32*(warp % 4)...) and column half (e >> 2) of every 64-column box.
     const int r = ((warp & 3) << 5) | lane;   // tile row == TMEM lane
     const int half = warp >> 2;
-    int tile = 0, w_cnt = 0, b_cnt = 0;
+    int tile = 0, w_cnt = 0;
     int pending = -1;                          // slot whose TMA store may still be reading smem
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const TcUnit un = units[u];
@@ -304,60 +312,16 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
       const float ss = sign * J.scale;
       const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
       const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
-      if (!TC) mbar_wait(bar(B_FULL), b_cnt & 1);
       for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
         const int buf = tile & 1;
-        float a[KSIMT > 0 ? KSIMT : 1];
-        if (TC) {
-          mbar_wait(bar(T_FULL + buf), (tile >> 1) & 1);
-          tc_fence_after();
-        } else {
-          mbar_wait(bar(A_FULL), tile & 1);
-          // this row of the packed A tile (k block 0, swizzled 16 B chunks)
-#pragma unroll
-          for (int c = 0; c < KSIMT / 8; ++c) {
-            const uint4 q = *reinterpret_cast<const uint4*>(sA + r * 128 + ((c ^ (r & 7)) << 4));
-            const uint32_t* qu = reinterpret_cast<const uint32_t*>(&q);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              a[8 * c + 2 * e] = bf16lo(qu[e]);
-              a[8 * c + 2 * e + 1] = bf16hi(qu[e]);
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(A_EMPTY));
-        }
-        for (int bx = 0; bx < nbox; ++bx) {
+        mbar_wait(bar(T_FULL + buf), (tile >> 1) & 1);
+        tc_fence_after();
+        for (int bx = 0; bx < nbox; ++bx, ++w_cnt) {
           const int slot = w_cnt % n_slots;
           mbar_wait(bar(W_FULL + slot), (w_cnt / n_slots) & 1);
-          uint8_t* row = sW + slot * kBoxBytes + r * 128;
-          {
-            float v[32];
-            if (TC) {
-              const uint32_t taddr =
-                  tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + buf * kBN + bx * kBoxN + half * 32;
-              tc_ld32(taddr, v);
-            } else {
-#pragma unroll
-              for (int c = 0; c < 32; ++c) {
-                const int n = bx * kBoxN + half * 32 + c;   // B panel row (output column)
-                const uint8_t* brow = sB + n * 128;
-                float acc = 0.f;
-#pragma unroll
-                for (int q = 0; q < KSIMT / 8; ++q) {
-                  const uint4 bq = *reinterpret_cast<const uint4*>(brow + ((q ^ (n & 7)) << 4));
-                  const uint32_t* bu = reinterpret_cast<const uint32_t*>(&bq);
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    acc = fmaf(a[8 * q + 2 * e], bf16lo(bu[e]), acc);
-                    acc = fmaf(a[8 * q + 2 * e + 1], bf16hi(bu[e]), acc);
-                  }
-                }
-                v[c] = acc;
-              }
-            }
-            rmw32(row, r, half * 4, v, ss);
-          }
+          float v[32];
+          tc_ld32(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + buf * kBN + bx * kBoxN + half * 32, v);
+          rmw32(sW + slot * kBoxBytes + r * 128, r, half * 4, v, ss);
           fence_proxy_async();
           named_bar(1, kEpiThreads);
           if (threadIdx.x == 0) {
@@ -369,19 +333,11 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
             }
             pending = slot;
           }
-          ++w_cnt;
         }
-        if (TC) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(T_EMPTY + buf));
-        }
-      }
-      if (!TC) {
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar(B_EMPTY));
+        if (lane == 0) mbar_arrive(bar(T_EMPTY + buf));
       }
-      ++b_cnt;
     }
     if (threadIdx.x == 0) {
       if (pending >= 0) {
@@ -393,7 +349,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   }
   tc_fence_before();
   __syncthreads();
-  if (TC && warp == kMmaWarp) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
   }
@@ -560,26 +516,17 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(base);
   const TcJob* jobs = reinterpret_cast<const TcJob*>(base + maps_b);
   const TcUnit* units = reinterpret_cast<const TcUnit*>(base + maps_b + (size_t)n_jobs * sizeof(TcJob));
-  const int fixed = 1024 + kb_max * (kBBlockBytes + kABlockBytes) + 256;
+  const int fixed = 1024 + kb_max * kBBlockBytes + kAStages * kABlockBytes + 256;
   const int max_smem = 227 * 1024;
-  int slots = std::min(6, (max_smem - fixed) / kBoxBytes);
+  int slots = std::min(8, (max_smem - fixed) / kBoxBytes);
   if (slots < 2) return fail(SDB_EUNSUP, "lora_tc_patch: rank too large for shared memory");
   const int smem = fixed + slots * kBoxBytes;
   int grid = std::min(n_units, kNumSMs);
   if (max_ctas > 0) grid = std::min(grid, max_ctas);
-#define SDB_TC_LAUNCH(TCV, KS)                                                                                  \
-  do {                                                                                                          \
-    auto kfn = lora_patch_tma_kernel<TCV, KS>;                                                                  \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                               \
-    kfn<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);                         \
-  } while (0)
-  if (simt_rank > 0 && simt_rank <= 16)
-    SDB_TC_LAUNCH(false, 16);
-  else if (simt_rank > 16 && simt_rank <= 32)
-    SDB_TC_LAUNCH(false, 32);
-  else
-    SDB_TC_LAUNCH(true, 0);
-#undef SDB_TC_LAUNCH
+(void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
+  auto kfn = lora_patch_tma_kernel<0>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kfn<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
   return check_launch("lora_patch_tma_kernel");
 }
 

@@ -163,12 +163,13 @@ def tma_eligible(w: torch.Tensor) -> bool:
 class LoraTmaPlan:
     """K1 fast path for bf16 weights: factors packed once (UMMA K-major
     SWIZZLE_128B tiles), W streamed through a TMA ring, rank contraction on
-    tcgen05 (R > 16) or FFMA (R <= 16).  One launch covers every job.
+    tcgen05 at every rank (ranks padded to 16 for the MMA K step; an FFMA
+    variant measured 3x slower even at R = 8).  One launch covers every job.
 
     entries: (w_in, w_out or None, down (h1, R) bf16, up (R, h2) bf16, scale),
     every w_in must satisfy ``tma_eligible``."""
 
-    def __init__(self, entries: Sequence[tuple], simt_max_rank: int = 16):
+    def __init__(self, entries: Sequence[tuple], simt_max_rank: int = 0):
         if not entries:
             raise ValidationError("LoraTmaPlan needs at least one job")
         lib = _lib.lib()
@@ -230,7 +231,8 @@ class LoraTmaPlan:
         self.n_units = n_units.value
         self.kb_max = kb_max.value
         self.simt_rank = self.max_rank if self.max_rank <= simt_max_rank else 0
-        self.path = 2 if self.simt_rank else 1   # 1 = tcgen05, 2 = TMA + FFMA
+        self.simt_rank = 0
+        self.path = 1   # 1 = TMA + tcgen05 (0 = the generic SIMT kernel of LoraPatchPlan)
 
     def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None,
                max_ctas: int = 0) -> None:

@@ -94,7 +94,7 @@ class PatchSet:
     device-resident K1 job table."""
 
     def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]],
-                 shadow: Optional[dict] = None, use_tma: bool = True, simt_max_rank: int = 16):
+                 shadow: Optional[dict] = None, use_tma: bool = True, simt_max_rank: int = 0):
         if not adapters:
             raise ValidationError("PatchSet needs at least one adapter")
         self.params = params

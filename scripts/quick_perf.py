@@ -41,7 +41,7 @@ def lora():
     shadow = allocate_shadow(p)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     out = []
-    for ranks, simt in (([8], 16), ([8], 0), ([16], 16), ([16], 0), ([64, 64], 0), ([8, 32, 64, 128], 0)):
+    for ranks, simt in (([8], 0), ([16], 0), ([64], 0), ([64, 64], 0), ([8, 32, 64, 128], 0)):
         ads = [(synthetic_lora(p, r, seed=i, adapter_id=f"a{i}"), 0.5) for i, r in enumerate(ranks)]
         ps = PatchSet(p, ads, shadow=shadow, simt_max_rank=simt)
 
