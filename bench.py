@@ -175,10 +175,137 @@ def cpu_baseline_leg():
 
 
 # ---------------------------------------------------------------------------
+def run_caas(args, world, rank, local):
+    """N > 1: ControlNet-as-a-service groups (caas.py) — base GPU + one GPU per
+    ControlNet; leftover ranks serve whole images alone."""
+    import torch
+    from paper_2407_02031_b200 import ops
+    from paper_2407_02031_b200 import unet as U
+    from paper_2407_02031_b200.caas import CaaSNode, caas_layout
+    from paper_2407_02031_b200.patcher import synthetic_lora
+    from paper_2407_02031_b200.pipeline import synthetic_request
+
+    cfg = U.SDXL
+    layout = caas_layout(world, N_CN)
+    node = CaaSNode(cfg, layout, rank, [0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16, seed=0)
+    role = node.role
+    if role in ("base", "solo"):
+        node.load_loras([(synthetic_lora(node.pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7)
+                         for i, r in enumerate(LORA_RANKS)])
+    node.setup()
+    req = synthetic_request(cfg, N_CN, seed=rank)
+    dev_in = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
+                  images=[torch.from_numpy(i).cuda() for i in req.images],
+                  pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
+    pinned = {k: (v.cpu().pin_memory() if not isinstance(v, list) else [x.cpu().pin_memory() for x in v])
+              for k, v in dev_in.items()}
+    producer = role in ("base", "solo")
+    p = node.pipe if producer else None
+
+    def image(inputs, patch=True):
+        if producer:
+            node.prepare(**inputs)
+        else:
+            node.prepare()
+        node.denoise(patch=patch) if producer else node.denoise()
+
+    s = torch.cuda.current_stream()
+    # calibrate the patch plan on the base: one unpatched image, one isolated patch
+    if producer:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+    image(dev_in, patch=False)
+    if producer:
+        b.record()
+        b.synchronize()
+        p.step_ms_est = a.elapsed_time(b) / DENOISE_STEPS
+        c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c.record(p.patch_stream)
+        p.patchset.launch(stream=p.patch_stream)
+        d.record(p.patch_stream)
+        d.synchronize()
+        p.patch_ms_est = c.elapsed_time(d)
+    for _ in range(args.warmup):
+        image(dev_in)
+    barrier_sync(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    c0 = ops.LAUNCHES["count"]
+    evs = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t0.record(s)
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        image(dev_in)
+        b.record(s)
+        evs.append((a, b))
+    t1 = torch.cuda.Event(enable_timing=True)
+    t1.record(s)
+    barrier_sync(world)
+    host_launches = ops.LAUNCHES["count"] - c0
+    total_ms = max_over_ranks(t0.elapsed_time(t1), world)
+    per_image = [a.elapsed_time(b) / 1000.0 for a, b in evs] if producer else []
+    # e2e: pinned host inputs -> H2D -> denoise -> D2H of the latent, every image
+    barrier_sync(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        image(pinned)
+        if producer:
+            node.latent_nchw().contiguous().cpu()
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record(s)
+    barrier_sync(world)
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    clk = clocks.stop()
+    producers = sum(1 for g in layout.groups)
+    images = args.steps * producers
+    # per-image latency of group bases (not solos) for p50, gathered to rank 0
+    import torch.distributed as dist
+    lat = torch.tensor([statistics.median(per_image) if (role == "base" or (role == "solo" and
+                        all(not g.services for g in layout.groups))) else 0.0], device="cuda", dtype=torch.float64)
+    dist.all_reduce(lat, op=dist.ReduceOp.MAX)
+    graph_launches = 0
+    if role == "base":
+        graph_launches = node.pipe.launches_per_step
+    hbm, _, src = peaks()
+    line = None
+    if rank == 0:
+        alg = p.patchset.alg_bytes
+        line = {
+            "metric": METRIC, "value": images / (total_ms / 1000.0), "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "p50_s_per_image": float(lat.item()),
+            "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
+                                   "30 DDIM steps, CFG batch 2, async LoRA patch",
+                       "model": "sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init",
+                       "global_batch": producers, "seq_len": None,
+                       "parallelism": "ControlNet-as-a-service groups " +
+                                      "; ".join(str(g.ranks) for g in layout.groups),
+                       "l2": "inputs larger than L2 (weights re-read every step)"},
+            "e2e": {"value": images / (e2e_ms / 1000.0), "unit": "images/s",
+                    "h2d_bytes_per_step": req.nbytes(), "d2h_bytes_per_step": 4 * node.L},
+            "gpu_launches": int(host_launches * world + graph_launches * DENOISE_STEPS * args.steps * world),
+            "roofline": {"kernel": "sdb lora_patch (K1, stacked R=128, all 794 SDXL matrices)", "bound": "hbm",
+                         "achieved": alg / (p.patch_ms_est * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": alg / (p.patch_ms_est * 1e-3) / 1e9 / hbm, "traffic": None,
+                         "launch_ms_isolated": p.patch_ms_est, "peak_source": src},
+            "clocks": clk,
+            "detail": {"layout": [list(g.ranks) for g in layout.groups],
+                       "first_patched_step": p.last_first_patched_step, "step_ms_est": p.step_ms_est},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_setup(args.gpus)
     torch.cuda.set_device(local)
+    if world > 1:
+        return run_caas(args, world, rank, local)
     from paper_2407_02031_b200 import ops
     from paper_2407_02031_b200 import unet as U
     from paper_2407_02031_b200.patcher import synthetic_lora

@@ -1,0 +1,446 @@
+"""ControlNet-as-a-service across GPUs — the multi-GPU form of the denoising loop.
+
+Reference semantics (addonsim/orchestrator.py:181-188 ``parallel_step_latency``,
+:621-660 ``_run_parallel_step``): each ControlNet runs on its
+own service GPU concurrently with the base UNet's encoder; its outputs are
+shipped to the base GPU and the decoder starts once the encoder AND every
+branch are done (orchestrator.py:652-653).  Here that is a real exchange:
+
+* one process per GPU (torch.distributed, NCCL over NVLink/NVSwitch);
+  ``caas_layout`` splits the ranks into groups of 1 base + up to n_cn service
+  GPUs; leftover ranks serve whole images alone (``solo``, the serial
+  orchestrator.py:611-619 step).
+* per request: the base broadcasts the conditioning inputs (text embeddings,
+  control images, SDXL added conditions) to its services once; hint and
+  added-condition embeddings are then computed locally (step-invariant).
+* per step: the base broadcasts the 4xHxW fp32 latent + timestep (256 KiB for
+  SDXL, the paper's "send latent" C0); every service runs its ControlNet(s)
+  and writes the conditioning-scaled sum of its residuals into one flat
+  buffer (the scales are folded into the zero convolutions at load); one
+  NCCL reduce(SUM) onto the base (the paper's 108 MiB "feature map" transfer,
+  C1) overlaps the base's encoder; the base's decoder consumes the reduced
+  residuals through K3.  The only data-path collectives are that broadcast
+  and that reduce — there is no other exchange.
+
+The transport (``CaaSProtocol``) is separated from the compute so the same
+protocol code runs under gloo on CPU in the tests with a stand-in compute.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class Group:
+    base: int
+    services: tuple          # ranks
+    cn_of_service: tuple     # per service rank: tuple of ControlNet indices it runs
+
+    @property
+    def ranks(self) -> tuple:
+        return (self.base,) + self.services
+
+
+@dataclass(frozen=True)
+class CaaSLayout:
+    world: int
+    n_cn: int
+    groups: tuple            # Group, including size-1 "solo" groups
+
+    def group_of(self, rank: int) -> Group:
+        for g in self.groups:
+            if rank in g.ranks:
+                return g
+        raise ValueError(f"rank {rank} not in layout")
+
+    def role(self, rank: int) -> str:
+        g = self.group_of(rank)
+        if not g.services:
+            return "solo"
+        return "base" if rank == g.base else "service"
+
+
+def caas_layout(world: int, n_cn: int) -> CaaSLayout:
+    """Groups of min(world, 1 + n_cn) ranks (base first); ControlNet i runs on
+    service i % n_services; leftover ranks are solo replicas."""
+    if world < 1 or n_cn < 0:
+        raise ValueError("world must be >= 1 and n_cn >= 0")
+    gs = max(1, min(world, 1 + n_cn))
+    groups = []
+    n_groups = world // gs
+    for k in range(n_groups):
+        base = k * gs
+        services = tuple(range(base + 1, base + gs))
+        cn_of = tuple(tuple(i for i in range(n_cn) if services and i % len(services) == j)
+                      for j in range(len(services)))
+        groups.append(Group(base, services, cn_of))
+    for r in range(n_groups * gs, world):
+        groups.append(Group(r, (), ()))
+    return CaaSLayout(world, n_cn, tuple(groups))
+
+
+def make_groups(layout: CaaSLayout, rank: int):
+    """Create every multi-rank group's communicator — collectively: EVERY rank
+    (solo ones included) must call this, in the same order.  Returns this
+    rank's group (None for a solo rank)."""
+    mine = None
+    for g in layout.groups:
+        if g.services:
+            pg = dist.new_group(list(g.ranks))
+            if rank in g.ranks:
+                mine = pg
+    return mine
+
+
+class CaaSProtocol:
+    """The per-request / per-step exchange of one group (NCCL on GPU, gloo on CPU).
+
+    msg    float32 [L + 1]: the fp32 latent (NHWC order) and the timestep.
+    flats  residual buffers: on a service, its own one (the conditioning-scaled
+           sum of its ControlNets' down + mid residuals, NHWC, concatenated);
+           on the base, one receive buffer per service (K3 sums them while it
+           writes the skip concat, so the base never zeroes or reduces).
+
+    Ordering: the broadcast and the point-to-point transfers of a group share
+    one communicator (one NCCL stream), so a service's next-step receive
+    completes only after its previous send — the service may then overwrite
+    its buffer without an extra fence."""
+
+    def __init__(self, layout: CaaSLayout, rank: int, msg: torch.Tensor, flats: Sequence[torch.Tensor], pg=None):
+        self.layout = layout
+        self.rank = rank
+        self.group = layout.group_of(rank)
+        self.role = layout.role(rank)
+        self.msg = msg
+        self.flats = list(flats)
+        self.pg = pg if pg is not None else make_groups(layout, rank)
+
+    # -- per request --------------------------------------------------------
+    def share_request(self, tensors: Sequence[torch.Tensor]) -> None:
+        """Broadcast the request's conditioning tensors from the base (in place)."""
+        for t in tensors:
+            dist.broadcast(t, src=self.group.base, group=self.pg)
+
+    # -- per step -------------------------------------------------------------
+    def base_step_begin(self) -> list:
+        """Base: ship (latent, t) and post one receive per service; returns the
+        handles to wait on before the decoder.  Everything is stream-ordered
+        after the work already queued (the previous step's K4)."""
+        dist.broadcast(self.msg, src=self.group.base, group=self.pg, async_op=True)
+        ops = [dist.P2POp(dist.irecv, f, peer=s, group=self.pg) for f, s in zip(self.flats, self.group.services)]
+        return dist.batch_isend_irecv(ops)
+
+    def service_receive(self) -> None:
+        work = dist.broadcast(self.msg, src=self.group.base, group=self.pg, async_op=True)
+        work.wait()
+
+    def service_send(self):
+        return dist.batch_isend_irecv([dist.P2POp(dist.isend, self.flats[0], peer=self.group.base, group=self.pg)])
+
+
+def residual_layout(shapes: Sequence[tuple]) -> tuple[list, int]:
+    """Offsets of each (N, C, H, W) residual inside the flat buffer."""
+    offs, total = [], 0
+    for s in shapes:
+        offs.append(total)
+        total += int(np.prod(s))
+    return offs, total
+
+
+def flat_views(flat: torch.Tensor, shapes: Sequence[tuple]) -> list:
+    """channels_last 4-d views of the flat residual buffer (NHWC memory)."""
+    offs, _ = residual_layout(shapes)
+    out = []
+    for o, (n, c, h, w) in zip(offs, shapes):
+        out.append(flat[o:o + n * c * h * w].view(n, h, w, c).permute(0, 3, 1, 2))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the real node: graph-captured compute on B200 around the protocol
+# ---------------------------------------------------------------------------
+class CaaSNode:
+    """One rank of the ControlNet-as-a-service deployment.
+
+    base:    UNet + K4; encoder graph || (service ControlNets + reduce); decoder graph
+    service: the ControlNets assigned to this rank; one graph per step
+    solo:    the single-GPU AddonPipeline (ControlNets inline)
+    """
+
+    def __init__(self, cfg, layout: CaaSLayout, rank: int, cn_scales: Sequence[float], steps: int = 30,
+                 guidance: float = 7.5, dtype=torch.bfloat16, seed: int = 0, device=None):
+        from . import ops
+        from .pipeline import AddonPipeline
+        from .unet import ControlNet, init_controlnet, skip_shapes
+        self.cfg, self.layout, self.rank = cfg, layout, rank
+        self.role = layout.role(rank)
+        self.group = layout.group_of(rank)
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.steps = steps
+        n_cn = layout.n_cn
+        self.ops = ops
+        h = cfg.latent_hw
+        self.L = 4 * h * h
+        # communicators are created collectively by every rank, solo ones included
+        self.pg = make_groups(layout, rank) if dist.is_initialized() else None
+        if self.role == "solo":
+            self.pipe = AddonPipeline(cfg, n_controlnets=n_cn, cn_scales=cn_scales, steps=steps, guidance=guidance,
+                                      device=self.device, dtype=dtype, seed=seed)
+            return
+        self.shapes = skip_shapes(cfg, 2)
+        _, total = residual_layout(self.shapes)
+        self.msg = torch.zeros(self.L + 1, device=self.device, dtype=torch.float32)
+        n_flat = len(self.group.services) if self.role == "base" else 1
+        self.flats = [torch.zeros(total, device=self.device, dtype=dtype) for _ in range(n_flat)]
+        self.views = [flat_views(f, self.shapes) for f in self.flats]
+        if self.role == "base":
+            # UNet only (no ControlNet weights on the base GPU)
+            self.pipe = AddonPipeline(cfg, n_controlnets=0, steps=steps, guidance=guidance, device=self.device,
+                                      dtype=dtype, seed=seed, use_graphs=False)   # the node captures its own
+            self.pipe.x = self.msg[: self.L]            # K4 writes the latent straight into the message
+        else:
+            mine = self.group.cn_of_service[self.group.services.index(rank)]
+            self.cn_idx = mine
+            self.cn_p = [init_controlnet(cfg, self.device, dtype, seed=1000 + i) for i in mine]
+            for p, i in zip(self.cn_p, mine):       # fold the conditioning scale into the zero convs
+                for k in list(p.t):
+                    if k.startswith("zero_convs.") or k.startswith("mid_zero_conv."):
+                        p.t[k] = (p.t[k].float() * float(cn_scales[i])).to(p.t[k].dtype)
+            self.cns = [ControlNet(cfg, p) for p in self.cn_p]
+            temb = cfg.time_embed_dim
+            self.unet_in = torch.zeros((2, 4, h, h), device=self.device, dtype=dtype).contiguous(
+                memory_format=torch.channels_last)
+            self.ctx = torch.zeros((2, cfg.context_len, cfg.context_dim), device=self.device, dtype=dtype)
+            self.hints = [torch.zeros((2, cfg.block_channels[0], h, h), device=self.device, dtype=dtype)
+                          .contiguous(memory_format=torch.channels_last) for _ in mine]
+            self.add_emb = [torch.zeros((2, temb), device=self.device, dtype=dtype) if cfg.addition_embed else None
+                            for _ in mine]
+        # loopback (all roles in one process, see LoopbackGroup) runs without a communicator
+        self.proto = CaaSProtocol(layout, rank, self.msg, self.flats, pg=self.pg) if dist.is_initialized() else None
+        self.graphs = {}
+
+    # -- capture --------------------------------------------------------------
+    def _service_step(self):
+        h = self.cfg.latent_hw
+        lat = self.msg[: self.L].view(1, h, h, 4).permute(0, 3, 1, 2)
+        self.unet_in.copy_(lat.expand(2, 4, h, h))
+        t = self.msg[self.L:self.L + 1]
+        outs = [cn.forward(self.unet_in, t, self.ctx, self.hints[i], self.add_emb[i]) for i, cn in enumerate(self.cns)]
+        for j, v in enumerate(self.views[0]):
+            if len(outs) > 1:   # several ControlNets on this GPU: sum them into the send buffer (K3)
+                self.ops.residual_inject(outs[0][j], [o[j] for o in outs[1:]], [1.0] * (len(outs) - 1), out=v)
+            else:
+                v.copy_(outs[0][j])
+
+    def _base_encode(self):
+        p = self.pipe
+        t = p.t_table.index_select(0, p.step_dev[:1].long())
+        temb = p.unet.time_embedding(t, 2, p.add_emb_unet)
+        h, skips = p.unet.encode(p.unet_in, temb, p.ctx)
+        self._enc = (temb, h, skips)
+
+    def _base_decode(self):
+        p = self.pipe
+        temb, h, skips = self._enc
+        eps = p.unet.decode(h, skips, temb, p.ctx, self.views, [1.0] * len(self.views))
+        self.ops.cfg_ddim_step(eps, p.x, p.coef, p.step_dev, unet_in=p.unet_in)
+        # timestep of the NEXT step rides in the message
+        self.msg[self.L:self.L + 1].copy_(p.t_table.index_select(0, p.step_dev[:1].long()))
+
+    def _capture(self, name, fn, pool=None):
+        s = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(s)
+        with torch.cuda.stream(side):
+            fn()
+        s.wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, pool=pool):
+            fn()
+        self.graphs[name] = g
+        return g
+
+    def load_loras(self, adapters) -> None:
+        """LoRA lives on the base UNet only (ControlNets are not patched)."""
+        if self.role in ("base", "solo"):
+            self.pipe.load_loras(adapters)
+
+    def setup(self) -> None:
+        if self.role == "solo":
+            self.pipe.setup()
+            return
+        if self.role == "base":
+            p = self.pipe
+            _ = p._pristine
+            variants = ["pristine"] + (["patched"] if p.patchset is not None else [])
+            pool = None
+            for which in variants:
+                p._use_weights(which)
+                p.step_dev.zero_()
+                g = self._capture("enc_" + which, self._base_encode, pool=pool)
+                pool = g.pool()
+                self._capture("dec_" + which, self._base_decode, pool=pool)
+                p._use_weights("pristine")
+            p.step_dev.zero_()
+        else:
+            self._capture("svc", self._service_step)
+        torch.cuda.synchronize(self.device)
+
+    # -- per request -------------------------------------------------------------
+    def request_tensors(self, context=None, images=None, pooled=None, time_ids=None) -> list:
+        """The conditioning tensors shipped base -> services once per request
+        (filled on the base, receive buffers elsewhere)."""
+        cfg, dev, h = self.cfg, self.device, self.cfg.latent_hw
+        ctx = torch.empty((2, cfg.context_len, cfg.context_dim), device=dev, dtype=torch.float32)
+        imgs = [torch.empty((2, 3, 8 * h, 8 * h), device=dev, dtype=torch.float32) for _ in range(self.layout.n_cn)]
+        extra = [torch.empty((2, cfg.pooled_dim), device=dev), torch.empty((2, cfg.time_ids), device=dev)] \
+            if cfg.addition_embed else []
+        if self.role == "base":
+            ctx.copy_(context.to(dev, non_blocking=True))
+            for b, im in zip(imgs, images):
+                b.copy_(im.to(dev, non_blocking=True))
+            if cfg.addition_embed:
+                extra[0].copy_(pooled.to(dev, non_blocking=True))
+                extra[1].copy_(time_ids.to(dev, non_blocking=True))
+        return [ctx] + imgs + extra
+
+    def finish_prepare(self, shared: list, latent=None) -> None:
+        """Step-invariant per-request work once the conditioning is local."""
+        cfg = self.cfg
+        ctx, imgs = shared[0], shared[1:1 + self.layout.n_cn]
+        extra = shared[1 + self.layout.n_cn:]
+        if self.role == "base":
+            self.pipe.prepare(latent, ctx, [], extra[0] if extra else None, extra[1] if extra else None)
+            self.msg[self.L:self.L + 1].copy_(self.pipe.t_table[:1])
+            return
+        self.ctx.copy_(ctx)
+        for k, (i, cn) in enumerate(zip(self.cn_idx, self.cns)):
+            self.hints[k].copy_(cn.hint_embedding(imgs[i].to(self.ctx.dtype)))
+            if cfg.addition_embed:
+                self.add_emb[k].copy_(cn.add_embedding(extra[0], extra[1]))
+
+    def prepare(self, latent=None, context=None, images=None, pooled=None, time_ids=None) -> None:
+        """Base passes the request; services receive it (their args are ignored)."""
+        if self.role == "solo":
+            self.pipe.prepare(latent, context, images, pooled, time_ids)
+            return
+        shared = self.request_tensors(context, images, pooled, time_ids)
+        self.proto.share_request(shared)
+        self.finish_prepare(shared, latent)
+
+    def base_encode(self, which: str = "pristine") -> None:
+        self.graphs["enc_" + which].replay()
+
+    def base_decode(self, which: str = "pristine") -> None:
+        self.graphs["dec_" + which].replay()
+
+    def service_step(self) -> None:
+        self.graphs["svc"].replay()
+
+    def start_patch(self, boundary: Optional[int] = None):
+        """Base: launch the request's LoRA patch (shadow weights, low-priority
+        side stream) and return (first_patched_step, event) — same semantics as
+        AddonPipeline.denoise (schedule.plan_lora_patch)."""
+        from .schedule import plan_lora_patch
+        p = self.pipe
+        if boundary is None:
+            if p.step_ms_est is None or p.patch_ms_est is None:
+                raise RuntimeError("calibrate the base (step_ms_est / patch_ms_est) or pass a boundary")
+            first = plan_lora_patch(p.patch_ms_est, p.step_ms_est, 0.0, self.steps).first_patched_step
+        else:
+            first = boundary + 1
+        p.patch_stream.wait_stream(torch.cuda.current_stream(self.device))
+        p.patchset.launch(stream=p.patch_stream, max_ctas=p.patch_max_ctas)
+        ev = torch.cuda.Event()
+        ev.record(p.patch_stream)
+        p.last_first_patched_step = first
+        return first, ev
+
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None) -> None:
+        if self.role == "solo":
+            self.pipe.denoise(patch=patch, boundary=boundary)
+            return
+        first, ev = (self.steps + 1, None)
+        if self.role == "base" and patch:
+            first, ev = self.start_patch(boundary)
+        s = torch.cuda.current_stream(self.device)
+        for step in range(1, self.steps + 1):
+            if self.role == "base":
+                which = "patched" if step >= first else "pristine"
+                if step == first:
+                    s.wait_event(ev)
+                works = self.proto.base_step_begin()
+                self.base_encode(which)               # overlaps the services' ControlNets
+                for w in works:
+                    w.wait()                          # decoder after the encoder AND every branch
+                self.base_decode(which)
+            else:
+                self.proto.service_receive()
+                self.service_step()
+                self.proto.service_send()
+        if ev is not None and first > self.steps:
+            s.wait_event(ev)
+
+    def latent_nchw(self) -> Optional[torch.Tensor]:
+        if self.role == "service":
+            return None
+        return self.pipe.latent_nchw()
+
+
+class LoopbackGroup:
+    """One CaaS group with every role in ONE process on ONE GPU: the transfers
+    become device copies (services run before the base's encoder, serially).
+    Exercises exactly the split compute of the multi-GPU path — encoder and
+    decoder graphs, scale-folded service ControlNets, per-service residual
+    buffers summed by K3 — so its parity with the single-GPU pipeline is
+    testable on the one B200 the test box has."""
+
+    def __init__(self, cfg, n_cn: int, cn_scales: Sequence[float], steps: int = 30, guidance: float = 7.5,
+                 dtype=torch.bfloat16, seed: int = 0, n_services: Optional[int] = None):
+        world = 1 + (n_cn if n_services is None else n_services)
+        self.layout = caas_layout(world, n_cn)
+        self.nodes = [CaaSNode(cfg, self.layout, r, cn_scales, steps, guidance, dtype, seed) for r in range(world)]
+        self.base, self.services = self.nodes[0], self.nodes[1:]
+        self.steps = steps
+
+    def setup(self) -> None:
+        for n in self.nodes:
+            n.setup()
+
+    def prepare(self, latent, context, images, pooled=None, time_ids=None) -> None:
+        shared = self.base.request_tensors(context, images, pooled, time_ids)
+        self.base.finish_prepare(shared, latent)
+        for s in self.services:
+            s.finish_prepare([t.clone() for t in shared])
+
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None) -> None:
+        first, ev = (self.steps + 1, None)
+        if patch:
+            first, ev = self.base.start_patch(boundary)
+        s = torch.cuda.current_stream()
+        for step in range(1, self.steps + 1):
+            which = "patched" if step >= first else "pristine"
+            if step == first:
+                s.wait_event(ev)
+            for k, svc in enumerate(self.services):
+                svc.msg.copy_(self.base.msg)
+                svc.service_step()
+                self.base.flats[k].copy_(svc.flats[0])
+            self.base.base_encode(which)
+            self.base.base_decode(which)
+            if on_step is not None:
+                on_step(step, self.latent_nchw().clone())
+        if ev is not None and first > self.steps:
+            s.wait_event(ev)
+
+    def load_loras(self, adapters) -> None:
+        self.base.load_loras(adapters)
+
+    def latent_nchw(self) -> torch.Tensor:
+        return self.base.latent_nchw()

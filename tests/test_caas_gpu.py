@@ -1,0 +1,76 @@
+"""The multi-GPU ControlNet-as-a-service compute split, exercised on ONE B200
+through the loopback group (caas.LoopbackGroup): encoder / decoder graphs on
+the base, scale-folded ControlNets on the services, per-service residual
+buffers summed by K3.  It must reproduce the single-GPU pipeline (which runs
+the ControlNets inline, addonsim/orchestrator.py:611-619) — the reference's
+claim that CaaS changes latency, not results."""
+
+import pytest
+import torch
+
+from paper_2407_02031_b200 import unet as U
+from paper_2407_02031_b200.caas import LoopbackGroup
+from paper_2407_02031_b200.patcher import synthetic_lora
+from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_request
+
+pytestmark = pytest.mark.gpu
+STEPS = 6
+SCALES = [0.8, 0.6]
+
+
+def rel(a, b):
+    return float((a.double() - b.double()).norm() / b.double().norm())
+
+
+@pytest.fixture(scope="module")
+def fp32_mode():
+    old = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+    torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = old
+
+
+def inputs(req):
+    return [torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(i) for i in req.images]]
+
+
+def single_gpu(dtype, patch):
+    pipe = AddonPipeline(U.TOY, n_controlnets=2, cn_scales=SCALES, steps=STEPS, dtype=dtype, seed=0)
+    if patch:
+        pipe.load_loras([(synthetic_lora(pipe.unet_p, 8, seed=7), 0.75)])
+    pipe.setup()
+    req = synthetic_request(U.TOY, 2)
+    pipe.prepare(*inputs(req))
+    lat = []
+    pipe.denoise(patch=patch, boundary=2, on_step=lambda s, x: lat.append(x.float().cpu()))
+    return lat
+
+
+def loopback(dtype, patch, n_services):
+    grp = LoopbackGroup(U.TOY, 2, SCALES, steps=STEPS, dtype=dtype, seed=0, n_services=n_services)
+    if patch:
+        grp.load_loras([(synthetic_lora(grp.base.pipe.unet_p, 8, seed=7), 0.75)])
+    grp.setup()
+    req = synthetic_request(U.TOY, 2)
+    grp.prepare(*inputs(req))
+    lat = []
+    grp.denoise(patch=patch, boundary=2, on_step=lambda s, x: lat.append(x.float().cpu()))
+    return lat
+
+
+@pytest.mark.parametrize("n_services", [1, 2])
+def test_caas_split_matches_single_gpu_fp32(fp32_mode, n_services):
+    ref = single_gpu(torch.float32, patch=True)
+    got = loopback(torch.float32, patch=True, n_services=n_services)
+    errs = [rel(a, b) for a, b in zip(got, ref)]
+    print("caas vs single (fp32):", ["%.1e" % e for e in errs])
+    assert max(errs) <= 1e-5
+
+
+def test_caas_split_matches_single_gpu_bf16():
+    ref = single_gpu(torch.bfloat16, patch=True)
+    got = loopback(torch.bfloat16, patch=True, n_services=2)
+    errs = [rel(a, b) for a, b in zip(got, ref)]
+    print("caas vs single (bf16):", ["%.1e" % e for e in errs])
+    assert max(errs) <= 1e-2
