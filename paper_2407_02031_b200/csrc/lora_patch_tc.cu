@@ -92,21 +92,37 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
+// L2 policies: W is streamed exactly once (evict-first); the packed factors are
+// re-read by every column panel / row tile (evict-last keeps them resident).
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           dst),
-      "l"(map), "r"(x), "r"(y), "r"(bar)
+      "l"(src), "r"(bytes), "r"(bar), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, uint32_t src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
-               "r"(y), "r"(src)
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, uint32_t src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                   map),
+               "r"(x), "r"(y), "r"(src), "l"(pol)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -232,7 +248,10 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   if (warp == kProducerWarp) {
     // ===================== producer: B panel, A K-blocks, W boxes =====================
     if (lane == 0) {
-      int a_cnt = 0, b_cnt = 0, w_cnt = 0;
+      const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+      int b_cnt = 0;
+      int a_st = 0, a_round = 0;   // A ring position
+      int w_slot = 0, w_round = 0; // W ring position
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
@@ -241,24 +260,25 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         const int nkb = (J.rank + kKB - 1) / kKB;
         if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
         mbar_expect_tx(bar(B_FULL), J.kb * kBBlockBytes);
-        bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL));
+        bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL),
+                 keep);
         ++b_cnt;
         const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
         const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
         for (int m = un.m_begin; m < un.m_end; ++m) {
-          for (int kb = 0; kb < nkb; ++kb, ++a_cnt) {
-            const int st = a_cnt % kAStages;
-            if (a_cnt >= kAStages) mbar_wait(bar(A_EMPTY + st), ((a_cnt / kAStages) - 1) & 1);
-            mbar_expect_tx(bar(A_FULL + st), kABlockBytes);
-            bulk_g2s(smem_u32(sA + st * kABlockBytes), J.a + ((size_t)m * J.kb + kb) * kABlockBytes, kABlockBytes,
-                     bar(A_FULL + st));
+          for (int kb = 0; kb < nkb; ++kb) {
+            if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
+            mbar_expect_tx(bar(A_FULL + a_st), kABlockBytes);
+            bulk_g2s(smem_u32(sA + a_st * kABlockBytes), J.a + ((size_t)m * J.kb + kb) * kABlockBytes, kABlockBytes,
+                     bar(A_FULL + a_st), keep);
+            if (++a_st == kAStages) { a_st = 0; ++a_round; }
           }
-          for (int bx = 0; bx < nbox; ++bx, ++w_cnt) {
-            const int slot = w_cnt % n_slots;
-            if (w_cnt >= n_slots) mbar_wait(bar(W_EMPTY + slot), ((w_cnt / n_slots) - 1) & 1);
-            mbar_expect_tx(bar(W_FULL + slot), kBoxBytes);
-            tma_load_2d(smem_u32(sW + slot * kBoxBytes), min, un.n_tile * kBN + bx * kBoxN, m * kBM,
-                        bar(W_FULL + slot));
+          for (int bx = 0; bx < nbox; ++bx) {
+            if (w_round > 0) mbar_wait(bar(W_EMPTY + w_slot), (w_round - 1) & 1);
+            mbar_expect_tx(bar(W_FULL + w_slot), kBoxBytes);
+            tma_load_2d(smem_u32(sW + w_slot * kBoxBytes), min, un.n_tile * kBN + bx * kBoxN, m * kBM,
+                        bar(W_FULL + w_slot), stream);
+            if (++w_slot == n_slots) { w_slot = 0; ++w_round; }
           }
         }
       }
@@ -279,7 +299,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           const uint32_t d = tmem_base + buf * kBN;
           for (int kb = 0; kb < nkb; ++kb, ++a_cnt) {
-            const int st = a_cnt % kAStages;
+            const int st = a_cnt & (kAStages - 1);
             mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
             tc_fence_after();
             const int ks_end = std::min(4, nks - kb * 4);
@@ -303,8 +323,9 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     // lanes 32*(warp % 4)...) and column half (e >> 2) of every 64-column box.
     const int r = ((warp & 3) << 5) | lane;   // tile row == TMEM lane
     const int half = warp >> 2;
-    int tile = 0, w_cnt = 0;
+    int tile = 0, w_slot = 0, w_round = 0;
     int pending = -1;                          // slot whose TMA store may still be reading smem
+    const uint64_t stream = policy_evict_first();
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const TcUnit un = units[u];
       const TcJob& J = jobs[un.job];
@@ -316,9 +337,10 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         const int buf = tile & 1;
         mbar_wait(bar(T_FULL + buf), (tile >> 1) & 1);
         tc_fence_after();
-        for (int bx = 0; bx < nbox; ++bx, ++w_cnt) {
-          const int slot = w_cnt % n_slots;
-          mbar_wait(bar(W_FULL + slot), (w_cnt / n_slots) & 1);
+        for (int bx = 0; bx < nbox; ++bx) {
+          const int slot = w_slot;
+          mbar_wait(bar(W_FULL + slot), w_round & 1);
+          if (++w_slot == n_slots) { w_slot = 0; ++w_round; }
           float v[32];
           tc_ld32(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + buf * kBN + bx * kBoxN + half * 32, v);
           rmw32(sW + slot * kBoxBytes + r * 128, r, half * 4, v, ss);
@@ -326,7 +348,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
           named_bar(1, kEpiThreads);
           if (threadIdx.x == 0) {
             // keep one store in flight: release the PREVIOUS slot once its read is done
-            tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM, smem_u32(sW + slot * kBoxBytes));
+            tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM, smem_u32(sW + slot * kBoxBytes), stream);
             if (pending >= 0) {
               tma_store_wait_read1();
               mbar_arrive(bar(W_EMPTY + pending));
