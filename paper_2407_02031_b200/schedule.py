@@ -78,7 +78,21 @@ class LatencyProfile:
 PROFILES = {"paper-h800-sdxl": LatencyProfile()}
 
 
+def _register_measured() -> None:
+    """Add the measured B200 profile (profiles/b200_sdxl_profile.json, written
+    by ``python -m paper_2407_02031_b200.profile`` on a B200) when present."""
+    try:
+        from .profile import load
+        prof = load()
+    except Exception:   # a malformed file must not break the planner
+        prof = None
+    if prof is not None:
+        PROFILES["b200-sdxl"] = prof
+
+
 def get_profile(name: str) -> LatencyProfile:
+    if name == "b200-sdxl" and name not in PROFILES:
+        _register_measured()
     if name not in PROFILES:
         raise ValidationError(f"unknown profile {name!r}; available: {sorted(PROFILES)}")
     return PROFILES[name]
