@@ -85,8 +85,21 @@ def physical_up(params: Params, name: str, up: torch.Tensor) -> torch.Tensor:
 
 
 def allocate_shadow(params: Params) -> dict:
-    """Patched copies of every matrix weight (same shape / memory format)."""
-    return {name: torch.empty_like(params.t[name + ".weight"]) for name, _ in params.matrices}
+    """Patched copies of every matrix weight (same shape / memory format).
+    Fused storages (e.g. attention q|k|v) get one shadow storage whose row
+    blocks are the members' shadows, so the patched forward keeps its single
+    GEMM; keys are matrix names plus the fused parents."""
+    shadow = {}
+    for parent, members in params.fused.items():
+        ps = torch.empty_like(params.t[parent + ".weight"])
+        shadow[parent] = ps
+        rows = params.t[members[0] + ".weight"].shape[0]
+        for i, m in enumerate(members):
+            shadow[m] = ps[i * rows:(i + 1) * rows]
+    for name, _ in params.matrices:
+        if name not in shadow:
+            shadow[name] = torch.empty_like(params.t[name + ".weight"])
+    return shadow
 
 
 class PatchSet:

@@ -125,15 +125,18 @@ class AddonPipeline:
         self.launches_per_step = 0
 
     # ------------------------------------------------------------------
+    def _weight_names(self) -> list:
+        return [n for n, _ in self.unet_p.matrices] + list(self.unet_p.fused)
+
     def _use_weights(self, which: str) -> None:
         src = self.shadow if which == "patched" else self._pristine
-        for name, _ in self.unet_p.matrices:
+        for name in self._weight_names():
             self.unet_p.t[name + ".weight"] = src[name]
 
     @property
     def _pristine(self) -> dict:
         if not hasattr(self, "_pristine_w"):
-            self._pristine_w = {n: self.unet_p.t[n + ".weight"] for n, _ in self.unet_p.matrices}
+            self._pristine_w = {n: self.unet_p.t[n + ".weight"] for n in self._weight_names()}
         return self._pristine_w
 
     def step_once(self) -> None:

@@ -96,6 +96,7 @@ class Params:
         self.gen = None if self.device.type == "meta" else torch.Generator(device=self.device).manual_seed(seed)
         self.t: dict[str, torch.Tensor] = {}
         self.matrices: list[tuple[str, str]] = []  # (name, "linear"|"conv")
+        self.fused: dict[str, list] = {}           # parent -> member matrices (views of it)
 
     def _randn(self, shape, std):
         return (torch.randn(shape, generator=self.gen, device=self.device, dtype=torch.float32) * std)
@@ -121,6 +122,17 @@ class Params:
     def lnorm(self, name, c):
         self.t[name + ".weight"] = torch.ones(c, device=self.device, dtype=self.dtype)
         self.t[name + ".bias"] = torch.zeros(c, device=self.device, dtype=self.dtype)
+
+    def fused_linear(self, parent: str, members: list, cin: int, cout: int, std=0.02):
+        """Bias-free linears sharing one (len(members)*cout, cin) storage: the
+        forward runs ONE GEMM on ``parent``; LoRA targets each member (a row
+        block, i.e. a contiguous row-major (cout, cin) view)."""
+        w = self._randn((len(members) * cout, cin), std).to(self.dtype)
+        self.t[parent + ".weight"] = w
+        for i, m in enumerate(members):
+            self.t[m + ".weight"] = w[i * cout:(i + 1) * cout]
+            self.matrices.append((m, "linear"))
+        self.fused[parent] = list(members)
 
     def matrix_view(self, name: str) -> torch.Tensor:
         """(h1, h2) row-major view of the weight's physical storage."""
@@ -150,14 +162,11 @@ def _transformer_params(p: Params, pre: str, c: int, depth: int, ctx: int):
     for d in range(depth):
         b = f"{pre}.blocks.{d}"
         p.lnorm(b + ".norm1", c)
-        p.linear(b + ".attn1.to_q", c, c, bias=False)
-        p.linear(b + ".attn1.to_k", c, c, bias=False)
-        p.linear(b + ".attn1.to_v", c, c, bias=False)
+        p.fused_linear(b + ".attn1.to_qkv", [b + ".attn1.to_q", b + ".attn1.to_k", b + ".attn1.to_v"], c, c)
         p.linear(b + ".attn1.to_out", c, c)
         p.lnorm(b + ".norm2", c)
         p.linear(b + ".attn2.to_q", c, c, bias=False)
-        p.linear(b + ".attn2.to_k", ctx, c, bias=False)
-        p.linear(b + ".attn2.to_v", ctx, c, bias=False)
+        p.fused_linear(b + ".attn2.to_kv", [b + ".attn2.to_k", b + ".attn2.to_v"], ctx, c)
         p.linear(b + ".attn2.to_out", c, c)
         p.lnorm(b + ".norm3", c)
         p.linear(b + ".ff.proj", c, 8 * c)      # GEGLU: value and gate halves
@@ -309,10 +318,11 @@ class Net:
 
     def attention(self, pre, x, ctx, heads):
         n, l, c = x.shape
-        q = self.lin(pre + ".to_q", x)
-        src = x if ctx is None else ctx
-        k = self.lin(pre + ".to_k", src)
-        v = self.lin(pre + ".to_v", src)
+        if ctx is None:   # self-attention: one GEMM for q, k, v (fused weight storage)
+            q, k, v = F.linear(x, self.t[pre + ".to_qkv.weight"]).split(c, dim=-1)
+        else:             # cross-attention: q from x, one GEMM for k, v from the context
+            q = self.lin(pre + ".to_q", x)
+            k, v = F.linear(ctx, self.t[pre + ".to_kv.weight"]).split(c, dim=-1)
         d = c // heads
         q = q.view(n, l, heads, d).transpose(1, 2)
         k = k.view(n, -1, heads, d).transpose(1, 2)

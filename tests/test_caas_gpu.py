@@ -68,9 +68,15 @@ def test_caas_split_matches_single_gpu_fp32(fp32_mode, n_services):
     assert max(errs) <= 1e-5
 
 
-def test_caas_split_matches_single_gpu_bf16():
-    ref = single_gpu(torch.bfloat16, patch=True)
+def test_caas_split_bf16_within_the_bf16_floor(fp32_mode):
+    """bf16 CaaS differs from bf16 single-GPU only by rounding placement (scales
+    folded into the zero convs, per-service sums); both must sit inside the
+    bf16 error band around the fp32 result (tests/test_pipeline_gpu.py)."""
+    ref32 = single_gpu(torch.float32, patch=True)
+    single = single_gpu(torch.bfloat16, patch=True)
     got = loopback(torch.bfloat16, patch=True, n_services=2)
-    errs = [rel(a, b) for a, b in zip(got, ref)]
-    print("caas vs single (bf16):", ["%.1e" % e for e in errs])
-    assert max(errs) <= 1e-2
+    e_single = [rel(a, b) for a, b in zip(single, ref32)]
+    e_caas = [rel(a, b) for a, b in zip(got, ref32)]
+    print("bf16 single vs fp32:", ["%.1e" % e for e in e_single])
+    print("bf16 caas   vs fp32:", ["%.1e" % e for e in e_caas])
+    assert max(e_caas) <= 2e-2 and max(e_single) <= 2e-2
