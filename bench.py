@@ -312,30 +312,59 @@ def run_ours(args):
     from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_request
 
     cfg = U.SDXL
-    pipe = AddonPipeline(cfg, n_controlnets=N_CN, cn_scales=[0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5,
-                         dtype=torch.bfloat16, seed=0, patch_max_ctas=args.patch_ctas)
-    loras = [(synthetic_lora(pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7) for i, r in
-             enumerate(LORA_RANKS)]
-    launches0 = ops.LAUNCHES["count"]
-    pipe.load_loras(loras)
-    pipe.setup()
-    per_step_launches = None
-    step_ms, patch_ms = pipe.calibrate(reps=3)
     req = synthetic_request(cfg, N_CN, seed=rank)
     # device-resident copies of the request for the `value` loop
     dev_in = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
                   images=[torch.from_numpy(i).cuda() for i in req.images],
                   pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
-    s = pipe.main_stream
+    if args.mode == "serial":
+        # ControlNets inline (orchestrator.py:611-619), one CUDA graph per step
+        eng = AddonPipeline(cfg, n_controlnets=N_CN, cn_scales=[0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5,
+                            dtype=torch.bfloat16, seed=0, patch_max_ctas=args.patch_ctas)
+        pipe = eng
+    else:
+        # ControlNet branches on their own streams beside the UNet encoder (CaaS split on one GPU)
+        from paper_2407_02031_b200.caas import LoopbackGroup
+        eng = LoopbackGroup(cfg, N_CN, [0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16,
+                            seed=0, concurrent=True)
+        pipe = eng.base.pipe
+        pipe.patch_max_ctas = args.patch_ctas
+    loras = [(synthetic_lora(pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7) for i, r in
+             enumerate(LORA_RANKS)]
+    eng.load_loras(loras)
+    eng.setup()
+    if args.mode == "serial":
+        step_ms, patch_ms = pipe.calibrate(reps=3)
+        s = pipe.main_stream
+    else:
+        s = eng.main_stream
+        with torch.cuda.stream(s):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            eng.prepare(**dev_in)
+            a.record(s)
+            eng.denoise(patch=False)
+            b.record(s)
+            b.synchronize()
+            pipe.step_ms_est = step_ms = a.elapsed_time(b) / DENOISE_STEPS
+            c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.record(pipe.patch_stream)
+            pipe.patchset.launch(stream=pipe.patch_stream)
+            d.record(pipe.patch_stream)
+            d.synchronize()
+            pipe.patch_ms_est = patch_ms = c.elapsed_time(d)
 
     def image_resident():
-        pipe.prepare(**dev_in)
-        pipe.denoise(patch=True)
+        eng.prepare(**dev_in)
+        eng.denoise(patch=True)
 
-    pinned = {}
+    pinned = {k: (v.cpu().pin_memory() if not isinstance(v, list) else [x.cpu().pin_memory() for x in v])
+              for k, v in dev_in.items()}
 
     def image_e2e():
-        pipe.generate(req, patch=True, pinned=pinned)
+        # the public call: pinned host inputs -> H2D -> denoise -> D2H of the final latent
+        eng.prepare(**pinned)
+        eng.denoise(patch=True)
+        eng.latent_nchw().contiguous().cpu()
 
     with torch.cuda.stream(s):
         for _ in range(args.warmup):
@@ -394,7 +423,8 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # kernels issued in the timed region: graph replays issue what the capture counted
-    graph_launches_per_step = pipe.launches_per_step
+    graph_launches_per_step = pipe.launches_per_step if args.mode == "serial" else \
+        sum(n.launches_per_step for n in eng.nodes)
     gpu_launches = host_launches + graph_launches_per_step * DENOISE_STEPS * args.steps
 
     hbm, tflops, src = peaks()
@@ -411,7 +441,9 @@ def run_ours(args):
         "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
                                "30 DDIM steps, CFG batch 2, async LoRA patch",
                    "model": "sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init",
-                   "global_batch": world, "seq_len": None, "parallelism": f"replicas x{world}",
+                   "global_batch": world, "seq_len": None,
+                   "parallelism": ("1 GPU, ControlNet branches on side streams concurrent with the UNet encoder"
+                                   if args.mode == "branch" else "1 GPU, ControlNets inline"),
                    "l2": "inputs larger than L2 (5.1 GB UNet + 5.0 GB ControlNet weights re-read every step)"},
         "e2e": {"value": images / (e2e_ms / 1000.0), "unit": "images/s",
                 "h2d_bytes_per_step": req.nbytes(), "d2h_bytes_per_step": pipe.d2h_bytes()},
@@ -447,6 +479,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--patch-ctas", type=int, default=0, help="cap the K1 grid (0 = one CTA per tile)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--mode", choices=["branch", "serial"], default="branch",
+                    help="1 GPU: ControlNet branches concurrent with the encoder (branch) or inline (serial)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

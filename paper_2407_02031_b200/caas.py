@@ -224,6 +224,7 @@ class CaaSNode:
         # loopback (all roles in one process, see LoopbackGroup) runs without a communicator
         self.proto = CaaSProtocol(layout, rank, self.msg, self.flats, pg=self.pg) if dist.is_initialized() else None
         self.graphs = {}
+        self.graph_launches = {}
 
     # -- capture --------------------------------------------------------------
     def _service_step(self):
@@ -261,10 +262,22 @@ class CaaSNode:
             fn()
         s.wait_stream(side)
         g = torch.cuda.CUDAGraph()
+        c0 = self.ops.LAUNCHES["count"]
         with torch.cuda.graph(g, pool=pool):
             fn()
+        self.graph_launches[name] = self.ops.LAUNCHES["count"] - c0   # our kernels per replay
         self.graphs[name] = g
         return g
+
+    @property
+    def launches_per_step(self) -> int:
+        """This repo's kernels issued per denoising step by this node's graphs."""
+        g = self.graph_launches
+        if self.role == "base":
+            return g.get("enc_pristine", 0) + g.get("dec_pristine", 0)
+        if self.role == "service":
+            return g.get("svc", 0)
+        return self.pipe.launches_per_step
 
     def load_loras(self, adapters) -> None:
         """LoRA lives on the base UNet only (ControlNets are not patched)."""
@@ -356,9 +369,15 @@ class CaaSNode:
         else:
             first = boundary + 1
         p.patch_stream.wait_stream(torch.cuda.current_stream(self.device))
+        timing = p.patch_timing is not None
+        if timing:
+            p0 = torch.cuda.Event(enable_timing=True)
+            p0.record(p.patch_stream)
         p.patchset.launch(stream=p.patch_stream, max_ctas=p.patch_max_ctas)
-        ev = torch.cuda.Event()
+        ev = torch.cuda.Event(enable_timing=timing)
         ev.record(p.patch_stream)
+        if timing:
+            p.patch_timing.append((p0, ev))
         p.last_first_patched_step = first
         return first, ev
 
@@ -394,20 +413,35 @@ class CaaSNode:
 
 
 class LoopbackGroup:
-    """One CaaS group with every role in ONE process on ONE GPU: the transfers
-    become device copies (services run before the base's encoder, serially).
-    Exercises exactly the split compute of the multi-GPU path — encoder and
-    decoder graphs, scale-folded service ControlNets, per-service residual
-    buffers summed by K3 — so its parity with the single-GPU pipeline is
-    testable on the one B200 the test box has."""
+    """One CaaS group with every role in ONE process on ONE GPU.
+
+    The services read the base's message buffer and write straight into the
+    base's per-service residual buffers (aliased, no transfer).  Exercises
+    exactly the split compute of the multi-GPU path — encoder and decoder
+    graphs, scale-folded service ControlNets, per-service residual buffers
+    summed by K3 — so its parity with the single-GPU pipeline is testable on
+    one B200.  With ``concurrent=True`` each service's ControlNet graph runs on
+    its own stream alongside the base's encoder graph (the paper's branch
+    parallelism inside one GPU: the 32x32-level GEMMs of SDXL at CFG batch 2
+    fill barely half of the 148 SMs, the branches fill the rest); the decoder
+    waits for every branch (orchestrator.py:652-653)."""
 
     def __init__(self, cfg, n_cn: int, cn_scales: Sequence[float], steps: int = 30, guidance: float = 7.5,
-                 dtype=torch.bfloat16, seed: int = 0, n_services: Optional[int] = None):
+                 dtype=torch.bfloat16, seed: int = 0, n_services: Optional[int] = None,
+                 concurrent: bool = False):
         world = 1 + (n_cn if n_services is None else n_services)
         self.layout = caas_layout(world, n_cn)
         self.nodes = [CaaSNode(cfg, self.layout, r, cn_scales, steps, guidance, dtype, seed) for r in range(world)]
         self.base, self.services = self.nodes[0], self.nodes[1:]
+        for k, svc in enumerate(self.services):   # alias before any graph is captured
+            svc.msg = self.base.msg
+            svc.flats = [self.base.flats[k]]
+            svc.views = [self.base.views[k]]
         self.steps = steps
+        self.concurrent = concurrent
+        dev = self.base.device
+        self.streams = [torch.cuda.Stream(device=dev) for _ in self.services] if concurrent else []
+        self.main_stream = torch.cuda.Stream(device=dev, priority=-1)
 
     def setup(self) -> None:
         for n in self.nodes:
@@ -428,11 +462,22 @@ class LoopbackGroup:
             which = "patched" if step >= first else "pristine"
             if step == first:
                 s.wait_event(ev)
-            for k, svc in enumerate(self.services):
-                svc.msg.copy_(self.base.msg)
-                svc.service_step()
-                self.base.flats[k].copy_(svc.flats[0])
-            self.base.base_encode(which)
+            if self.concurrent:
+                done = []
+                for svc, st in zip(self.services, self.streams):
+                    st.wait_stream(s)              # message of this step is written
+                    with torch.cuda.stream(st):
+                        svc.service_step()
+                    e = torch.cuda.Event()
+                    e.record(st)
+                    done.append(e)
+                self.base.base_encode(which)
+                for e in done:
+                    s.wait_event(e)
+            else:
+                for svc in self.services:
+                    svc.service_step()
+                self.base.base_encode(which)
             self.base.base_decode(which)
             if on_step is not None:
                 on_step(step, self.latent_nchw().clone())

@@ -272,14 +272,26 @@ def nhwc_view(x: torch.Tensor) -> tuple[int, int, int]:
     raise ValidationError(f"expected a 3-d or 4-d tensor, got {x.dim()}-d")
 
 
+def groupnorm_workspace(x: torch.Tensor, groups: int = 32) -> torch.Tensor:
+    """A zeroed K2 workspace sized for x (its counters must start at zero;
+    every launch leaves them at zero)."""
+    n, hw, c = nhwc_view(x)
+    return torch.zeros(max(_lib.lib().sdb_groupnorm_workspace(n, hw, c, groups), 256), dtype=torch.uint8,
+                       device=x.device)
+
+
 def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optional[torch.Tensor],
                    groups: int = 32, eps: float = 1e-5, silu: bool = True,
                    out: Optional[torch.Tensor] = None,
-                   add_nc: Optional[torch.Tensor] = None) -> torch.Tensor:
+                   add_nc: Optional[torch.Tensor] = None,
+                   workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """act(GroupNorm(x + add_nc[:, :, None, None])) in one NHWC pass pair.
 
     add_nc: optional fp32 [N, C] bias added before normalisation (the ResNet
-    time-embedding projection)."""
+    time-embedding projection).  workspace: a buffer from
+    ``groupnorm_workspace`` owned by the call site (required when calls may run
+    concurrently on different streams, e.g. inside concurrently replayed CUDA
+    graphs); default: one shared per stream."""
     require_cuda(x, gamma, beta, out, add_nc)
     n, hw, c = nhwc_view(x)
     if out is None:
@@ -290,7 +302,12 @@ def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optiona
     if add_nc is not None and add_nc.numel() != n * c:
         raise ValidationError(f"add_nc must hold N*C = {n * c} values")
     ws_bytes = _lib.lib().sdb_groupnorm_workspace(n, hw, c, groups)
-    ws = _workspace(ws_bytes, x.device)
+    if workspace is not None:
+        if workspace.numel() < ws_bytes:
+            raise ValidationError("groupnorm workspace too small for this input")
+        ws = workspace
+    else:
+        ws = _workspace(ws_bytes, x.device)
     _count(3)
     _lib.check("sdb_groupnorm_silu", _lib.lib().sdb_groupnorm_silu(
         x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,

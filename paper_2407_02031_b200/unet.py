@@ -292,6 +292,7 @@ class Net:
         self.cfg = cfg
         self.p = params
         self.t = params.t
+        self._gn_ws: dict = {}
 
     # -- primitives -------------------------------------------------------
     def lin(self, name, x):
@@ -303,9 +304,15 @@ class Net:
         return F.conv2d(x, w, self.t.get(name + ".bias"), stride=stride, padding=pad)
 
     def gn(self, name, x, silu, eps=None, add_nc=None):
+        # one K2 workspace per (site, shape) of THIS network: graphs of different
+        # networks (UNet, ControlNets) may replay concurrently on other streams
+        key = (name, tuple(x.shape))
+        ws = self._gn_ws.get(key)
+        if ws is None:
+            ws = self._gn_ws[key] = ops.groupnorm_workspace(x, self.cfg.groups)
         return ops.groupnorm_silu(x, self.t[name + ".weight"], self.t[name + ".bias"],
                                   groups=self.cfg.groups, eps=self.cfg.gn_eps if eps is None else eps,
-                                  silu=silu, add_nc=add_nc)
+                                  silu=silu, add_nc=add_nc, workspace=ws)
 
     # -- blocks -----------------------------------------------------------
     def resnet(self, pre, x, temb_act):

@@ -47,8 +47,9 @@ def single_gpu(dtype, patch):
     return lat
 
 
-def loopback(dtype, patch, n_services):
-    grp = LoopbackGroup(U.TOY, 2, SCALES, steps=STEPS, dtype=dtype, seed=0, n_services=n_services)
+def loopback(dtype, patch, n_services, concurrent=False):
+    grp = LoopbackGroup(U.TOY, 2, SCALES, steps=STEPS, dtype=dtype, seed=0, n_services=n_services,
+                        concurrent=concurrent)
     if patch:
         grp.load_loras([(synthetic_lora(grp.base.pipe.unet_p, 8, seed=7), 0.75)])
     grp.setup()
@@ -66,6 +67,15 @@ def test_caas_split_matches_single_gpu_fp32(fp32_mode, n_services):
     errs = [rel(a, b) for a, b in zip(got, ref)]
     print("caas vs single (fp32):", ["%.1e" % e for e in errs])
     assert max(errs) <= 1e-5
+
+
+def test_concurrent_branches_are_bitwise_serial():
+    """ControlNet graphs on their own streams beside the encoder graph: same
+    kernels, same inputs -> bitwise the serial loopback (no shared workspace)."""
+    a = loopback(torch.bfloat16, patch=True, n_services=2, concurrent=True)
+    b = loopback(torch.bfloat16, patch=True, n_services=2, concurrent=False)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
 
 
 def test_caas_split_bf16_within_the_bf16_floor(fp32_mode):
