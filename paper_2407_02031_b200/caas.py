@@ -120,28 +120,71 @@ class CaaSProtocol:
         self.msg = msg
         self.flats = list(flats)
         self.pg = pg if pg is not None else make_groups(layout, rank)
+        # gloo carries host tensors only: device buffers are staged through host
+        # copies (used to run the multi-process path on ONE GPU in the tests)
+        self.staged = msg.is_cuda and dist.get_backend(self.pg) == "gloo"
+        if self.staged:
+            self._msg_h = torch.empty(msg.shape, dtype=msg.dtype)
+            self._flats_h = [torch.empty(f.shape, dtype=f.dtype) for f in self.flats]
+        self._pending = []
 
     # -- per request --------------------------------------------------------
     def share_request(self, tensors: Sequence[torch.Tensor]) -> None:
         """Broadcast the request's conditioning tensors from the base (in place)."""
         for t in tensors:
-            dist.broadcast(t, src=self.group.base, group=self.pg)
+            if self.staged:
+                h = t.cpu()
+                dist.broadcast(h, src=self.group.base, group=self.pg)
+                t.copy_(h)
+            else:
+                dist.broadcast(t, src=self.group.base, group=self.pg)
 
     # -- per step -------------------------------------------------------------
     def base_step_begin(self) -> list:
         """Base: ship (latent, t) and post one receive per service; returns the
         handles to wait on before the decoder.  Everything is stream-ordered
         after the work already queued (the previous step's K4)."""
+        if self.staged:
+            self._msg_h.copy_(self.msg)
+            dist.broadcast(self._msg_h, src=self.group.base, group=self.pg)
+            ops = [dist.P2POp(dist.irecv, h, peer=s, group=self.pg)
+                   for h, s in zip(self._flats_h, self.group.services)]
+            return [_StagedWork(dist.batch_isend_irecv(ops), list(zip(self._flats_h, self.flats)))]
         dist.broadcast(self.msg, src=self.group.base, group=self.pg, async_op=True)
         ops = [dist.P2POp(dist.irecv, f, peer=s, group=self.pg) for f, s in zip(self.flats, self.group.services)]
         return dist.batch_isend_irecv(ops)
 
     def service_receive(self) -> None:
+        if self.staged:
+            for w in self._pending:     # previous send done before the buffer is reused
+                w.wait()
+            self._pending = []
+            dist.broadcast(self._msg_h, src=self.group.base, group=self.pg)
+            self.msg.copy_(self._msg_h)
+            return
         work = dist.broadcast(self.msg, src=self.group.base, group=self.pg, async_op=True)
         work.wait()
 
     def service_send(self):
+        if self.staged:
+            self._flats_h[0].copy_(self.flats[0])
+            self._pending = dist.batch_isend_irecv([dist.P2POp(dist.isend, self._flats_h[0], peer=self.group.base,
+                                                               group=self.pg)])
+            return self._pending
         return dist.batch_isend_irecv([dist.P2POp(dist.isend, self.flats[0], peer=self.group.base, group=self.pg)])
+
+
+class _StagedWork:
+    """gloo receive into host buffers, then the device copy the decoder reads."""
+
+    def __init__(self, works, pairs):
+        self.works, self.pairs = works, pairs
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        for h, d in self.pairs:
+            d.copy_(h, non_blocking=False)
 
 
 def residual_layout(shapes: Sequence[tuple]) -> tuple[list, int]:
