@@ -231,7 +231,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     }
     for (int i = 0; i < n_slots; ++i) {
       mbar_init(bar(W_FULL + i), 1);
-      mbar_init(bar(W_EMPTY + i), 1);
+      mbar_init(bar(W_EMPTY + i), 4);   // the 4 warps (quadrants) of the owning group
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -319,10 +319,12 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
     __syncwarp();
   } else {
     // ===================== epilogue (warps 0-7) =====================
-    // warp e reads TMEM lane quadrant (e & 3) (the hardware binds a warp to
-    // lanes 32*(warp % 4)...) and column half (e >> 2) of every 64-column box.
-    const int r = ((warp & 3) << 5) | lane;   // tile row == TMEM lane
-    const int half = warp >> 2;
+    // warp e owns TMEM lane quadrant q = e & 3 (rows 32q..32q+31) and, with
+    // the other 3 warps of its group g = e >> 2, every other W box: no
+    // cross-warp barrier — each warp TMA-stores its own 32-row sub-box.
+    const int q = warp & 3, grp = warp >> 2;
+    const int r = (q << 5) | lane;             // tile row == TMEM lane
+    int box = 0;                               // running box counter (group ownership)
     int tile = 0, w_slot = 0, w_round = 0;
     int pending = -1;                          // slot whose TMA store may still be reading smem
     const uint64_t stream = policy_evict_first();
@@ -338,17 +340,25 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         mbar_wait(bar(T_FULL + buf), (tile >> 1) & 1);
         tc_fence_after();
         for (int bx = 0; bx < nbox; ++bx) {
-          const int slot = w_slot;
-          mbar_wait(bar(W_FULL + slot), w_round & 1);
+          const int slot = w_slot, round = w_round;
           if (++w_slot == n_slots) { w_slot = 0; ++w_round; }
-          float v[32];
-          tc_ld32(tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + buf * kBN + bx * kBoxN + half * 32, v);
-          rmw32(sW + slot * kBoxBytes + r * 128, r, half * 4, v, ss);
+          const bool mine = ((box++ & 1) == grp);   // warp-uniform
+          if (!mine) continue;
+          mbar_wait(bar(W_FULL + slot), round & 1);
+          uint8_t* row = sW + slot * kBoxBytes + r * 128;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            float v[32];
+            tc_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * kBN + bx * kBoxN + hf * 32, v);
+            rmw32(row, r, hf * 4, v, ss);
+          }
           fence_proxy_async();
-          named_bar(1, kEpiThreads);
-          if (threadIdx.x == 0) {
-            // keep one store in flight: release the PREVIOUS slot once its read is done
-            tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM, smem_u32(sW + slot * kBoxBytes), stream);
+          __syncwarp();
+          if (lane == 0) {
+            // this warp's 32 rows of the box; keep one store in flight and
+            // release the PREVIOUS slot once its smem read is done
+            tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM + q * 32,
+                         smem_u32(sW + slot * kBoxBytes + q * 32 * 128), stream);
             if (pending >= 0) {
               tma_store_wait_read1();
               mbar_arrive(bar(W_EMPTY + pending));
@@ -361,7 +371,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         if (lane == 0) mbar_arrive(bar(T_EMPTY + buf));
       }
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       if (pending >= 0) {
         tma_store_wait_read();
         mbar_arrive(bar(W_EMPTY + pending));
@@ -438,12 +448,12 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int make_w_map(CUtensorMap* map, void* ptr, int64_t h1, int64_t h2, int64_t ldw) {
+int make_w_map(CUtensorMap* map, void* ptr, int64_t h1, int64_t h2, int64_t ldw, int box_rows) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)h2, (cuuint64_t)h1};
   cuuint64_t strides[1] = {(cuuint64_t)ldw * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBoxN, (cuuint32_t)kBM};
+  cuuint32_t box[2] = {(cuuint32_t)kBoxN, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -511,8 +521,9 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
   TcJob* tj = reinterpret_cast<TcJob*>(base + maps_b);
   for (int j = 0; j < n_jobs; ++j) {
     const sdb_lora_tc_job& J = jobs[j];
-    if (int rc = make_w_map(&maps[2 * j], J.w_in, J.h1, J.h2, J.ldw)) return rc;
-    if (int rc = make_w_map(&maps[2 * j + 1], J.w_out, J.h1, J.h2, J.ldw)) return rc;
+    // loads move whole 128-row boxes; each epilogue warp stores its own 32 rows
+    if (int rc = make_w_map(&maps[2 * j], J.w_in, J.h1, J.h2, J.ldw, kBM)) return rc;
+    if (int rc = make_w_map(&maps[2 * j + 1], J.w_out, J.h1, J.h2, J.ldw, 32)) return rc;
     std::memset(&tj[j], 0, sizeof(TcJob));
     tj[j].a = static_cast<const uint8_t*>(J.a_packed);
     tj[j].b = static_cast<const uint8_t*>(J.b_packed);
