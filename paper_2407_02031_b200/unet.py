@@ -31,6 +31,7 @@ from typing import Optional, Sequence
 
 import torch
 import torch.nn.functional as F
+from torch.nn.attention import SDPBackend, sdpa_kernel
 
 from . import ops
 
@@ -334,7 +335,13 @@ class Net:
         q = q.view(n, l, heads, d).transpose(1, 2)
         k = k.view(n, -1, heads, d).transpose(1, 2)
         v = v.view(n, -1, heads, d).transpose(1, 2)
-        o = F.scaled_dot_product_attention(q, k, v)
+        if ctx is not None and q.is_cuda and q.dtype != torch.float32:
+            # 77-token cross-attention: the flash kernel beats cuDNN's pick
+            # (scripts/attn_probe.py on B200: 15.6 vs 18.7 us at 32x32)
+            with sdpa_kernel([SDPBackend.FLASH_ATTENTION, SDPBackend.CUDNN_ATTENTION]):
+                o = F.scaled_dot_product_attention(q, k, v)
+        else:
+            o = F.scaled_dot_product_attention(q, k, v)
         o = o.transpose(1, 2).reshape(n, l, c)
         return self.lin(pre + ".to_out", o)
 
