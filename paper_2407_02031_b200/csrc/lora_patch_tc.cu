@@ -198,14 +198,17 @@ __device__ __forceinline__ void rmw32(uint8_t* row, int r, int chunk0, const flo
   }
 }
 
-template <int UNUSED>
+template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
 lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restrict__ jobs,
                       const TcUnit* __restrict__ units, int n_units, float sign, int kb_max, int n_slots) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sB = smem;                                   // kb_max * 32 KB: resident B panel
-  uint8_t* sA = sB + kb_max * kBBlockBytes;             // kAStages * 16 KB: streamed A K-blocks
+  constexpr int kPanelBlock = BN * 128;                 // bytes of one K block of the B panel
+  constexpr uint32_t kIdescBN = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                ((uint32_t)(kBM >> 4) << 24);   // f32 accum, bf16 A/B, K-major, 128 x BN
+  uint8_t* sB = smem;                                   // kb_max * BN * 128 B: resident B panel
+  uint8_t* sA = sB + kb_max * kPanelBlock;              // kAStages * 16 KB: streamed A K-blocks
   uint8_t* sW = sA + kAStages * kABlockBytes;           // n_slots * 16 KB: W box ring
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + n_slots * kBoxBytes);
   // barrier indices
@@ -237,7 +240,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   }
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(2 * kBN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -259,11 +262,19 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         prefetch_map(min);
         const int nkb = (J.rank + kKB - 1) / kKB;
         if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
-        mbar_expect_tx(bar(B_FULL), J.kb * kBBlockBytes);
-        bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL),
-                 keep);
+        mbar_expect_tx(bar(B_FULL), J.kb * kPanelBlock);
+        if (BN == kBN) {
+          bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL),
+                   keep);
+        } else {  // a BN-wide half of a packed 256-wide panel: one copy per K block
+          const int p256 = un.n_tile / (kBN / BN), hh = un.n_tile % (kBN / BN);
+          for (int kb = 0; kb < J.kb; ++kb)
+            bulk_g2s(smem_u32(sB + kb * kPanelBlock),
+                     J.b + (((size_t)p256 * J.kb + kb) * kBN + (size_t)hh * BN) * 128, kPanelBlock, bar(B_FULL),
+                     keep);
+        }
         ++b_cnt;
-        const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
+        const int64_t ncols = std::min<int64_t>(BN, J.h2 - (int64_t)un.n_tile * BN);
         const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
         for (int m = un.m_begin; m < un.m_end; ++m) {
           for (int kb = 0; kb < nkb; ++kb) {
@@ -276,7 +287,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
           for (int bx = 0; bx < nbox; ++bx) {
             if (w_round > 0) mbar_wait(bar(W_EMPTY + w_slot), (w_round - 1) & 1);
             mbar_expect_tx(bar(W_FULL + w_slot), kBoxBytes);
-            tma_load_2d(smem_u32(sW + w_slot * kBoxBytes), min, un.n_tile * kBN + bx * kBoxN, m * kBM,
+            tma_load_2d(smem_u32(sW + w_slot * kBoxBytes), min, un.n_tile * BN + bx * kBoxN, m * kBM,
                         bar(W_FULL + w_slot), stream);
             if (++w_slot == n_slots) { w_slot = 0; ++w_round; }
           }
@@ -297,7 +308,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
           const int buf = tile & 1;
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
-          const uint32_t d = tmem_base + buf * kBN;
+          const uint32_t d = tmem_base + buf * BN;
           for (int kb = 0; kb < nkb; ++kb, ++a_cnt) {
             const int st = a_cnt & (kAStages - 1);
             mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
@@ -305,8 +316,8 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
             const int ks_end = std::min(4, nks - kb * 4);
             for (int ks = 0; ks < ks_end; ++ks) {
               const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
-              const uint64_t bd = sw128_desc(smem_u32(sB + kb * kBBlockBytes + ks * 32));
-              tc_mma(d, ad, bd, kIdesc, (kb | ks) ? 1u : 0u);
+              const uint64_t bd = sw128_desc(smem_u32(sB + kb * kPanelBlock + ks * 32));
+              tc_mma(d, ad, bd, kIdescBN, (kb | ks) ? 1u : 0u);
             }
             tc_commit(bar(A_EMPTY + st));       // stage free once these MMAs completed
           }
@@ -333,7 +344,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
       const TcJob& J = jobs[un.job];
       const CUtensorMap* mout = maps + J.map_out;
       const float ss = sign * J.scale;
-      const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
+      const int64_t ncols = std::min<int64_t>(BN, J.h2 - (int64_t)un.n_tile * BN);
       const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
       for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
         const int buf = tile & 1;
@@ -349,7 +360,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
             float v[32];
-            tc_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * kBN + bx * kBoxN + hf * 32, v);
+            tc_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * BN + bx * kBoxN + hf * 32, v);
             rmw32(row, r, hf * 4, v, ss);
           }
           fence_proxy_async();
@@ -357,7 +368,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
           if (lane == 0) {
             // this warp's 32 rows of the box; keep one store in flight and
             // release the PREVIOUS slot once its smem read is done
-            tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM + q * 32,
+            tma_store_2d(mout, un.n_tile * BN + bx * kBoxN, m * kBM + q * 32,
                          smem_u32(sW + slot * kBoxBytes + q * 32 * 128), stream);
             if (pending >= 0) {
               tma_store_wait_read1();
@@ -383,7 +394,7 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
   }
 }
 
@@ -487,6 +498,13 @@ int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t 
   return check_launch("pack_b_kernel");
 }
 
+// Tile width: the B panel (BN x Rpad bf16) stays resident in shared memory.
+// Up to rank 128 a 256-wide panel (64 KB) leaves room for an 8-slot W ring;
+// above it a 256-wide panel (128 KB) would squeeze the ring to 4 slots, so the
+// panel narrows to 128 columns (the A tile is then re-read twice as often, from
+// L2 under the evict-last policy) and the ring keeps 8 slots.
+static int tile_n_for(int kb_max) { return kb_max > 2 ? 128 : kBN; }
+
 // Blob layout: [maps: 2*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]
 int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed, int* n_units_out,
             int* kb_max_out) {
@@ -502,7 +520,11 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
     if (((uintptr_t)J.a_packed | (uintptr_t)J.b_packed) & 1023)
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": packed factors must be 1024-B aligned");
     kb_max = std::max(kb_max, tc_kb(J.rank));
-    const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + kBN - 1) / kBN;
+  }
+  const int bn = tile_n_for(kb_max);
+  for (int j = 0; j < n_jobs; ++j) {
+    const sdb_lora_tc_job& J = jobs[j];
+    const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + bn - 1) / bn;
     for (int64_t n = 0; n < nt; ++n)
       for (int64_t m = 0; m < mt; m += kUnitTiles)
         units.push_back({j, (int32_t)n, (int32_t)m, (int32_t)std::min<int64_t>(mt, m + kUnitTiles)});
@@ -549,15 +571,16 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(base);
   const TcJob* jobs = reinterpret_cast<const TcJob*>(base + maps_b);
   const TcUnit* units = reinterpret_cast<const TcUnit*>(base + maps_b + (size_t)n_jobs * sizeof(TcJob));
-  const int fixed = 1024 + kb_max * kBBlockBytes + kAStages * kABlockBytes + 256;
+  const int bn = tile_n_for(kb_max);
+  const int fixed = 1024 + kb_max * bn * 128 + kAStages * kABlockBytes + 256;
   const int max_smem = 227 * 1024;
   int slots = std::min(8, (max_smem - fixed) / kBoxBytes);
   if (slots < 2) return fail(SDB_EUNSUP, "lora_tc_patch: rank too large for shared memory");
   const int smem = fixed + slots * kBoxBytes;
   int grid = std::min(n_units, kNumSMs);
   if (max_ctas > 0) grid = std::min(grid, max_ctas);
-(void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
-  auto kfn = lora_patch_tma_kernel<0>;
+  (void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
+  auto kfn = bn == kBN ? lora_patch_tma_kernel<kBN> : lora_patch_tma_kernel<128>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   kfn<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
   return check_launch("lora_patch_tma_kernel");
