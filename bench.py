@@ -300,6 +300,67 @@ def run_caas(args, world, rank, local):
     dist.destroy_process_group()
 
 
+def k1_traffic():
+    """DRAM bytes (read + write) of one K1 launch of this workload, from the
+    committed `ncu --set full` capture (profiles/k1_traffic.json)."""
+    p = ROOT / "profiles" / "k1_traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    return d["dram_bytes_read"] + d["dram_bytes_write"]
+
+
+def other_kernels_roofline(hbm: float) -> list:
+    """The step's HBM-bound kernels at their largest SDXL shapes (CFG batch 2),
+    timed with CUDA events one launch at a time, L2 flushed in between (a
+    >126 MB write).  Algorithmic bytes: one read of every input + one write of
+    every output (K2's second read of x, served from L2, is not counted)."""
+    import torch
+    from paper_2407_02031_b200 import ops
+    dev = "cuda"
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    cl = torch.channels_last
+
+    def timed(fn, reps=10):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    out = []
+    x = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+    g, bta = torch.ones(320, device=dev), torch.zeros(320, device=dev)
+    add = torch.zeros(2, 320, device=dev)
+    ws = ops.groupnorm_workspace(x)
+    y = torch.empty_like(x)
+    ms = timed(lambda: ops.groupnorm_silu(x, g, bta, out=y, add_nc=add, workspace=ws))
+    out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16", 2 * x.numel() * 2, ms))
+    tok = torch.randn(2, 4096, 640, device=dev).to(torch.bfloat16)
+    d = torch.randn_like(tok)
+    lw, lb = torch.ones(640, device=dev, dtype=torch.bfloat16), torch.zeros(640, device=dev, dtype=torch.bfloat16)
+    ms = timed(lambda: ops.add_layernorm(tok, d, lw, lb))
+    out.append(("K6 add+layernorm [2,4096,640] bf16", 4 * tok.numel() * 2, ms))
+    proj = torch.randn(2, 4096, 5120, device=dev).to(torch.bfloat16)
+    ms = timed(lambda: ops.geglu(proj))
+    out.append(("K5 geglu [2,4096,5120]->[...,2560] bf16", proj.numel() * 2 * 3 // 2, ms))
+    hid = torch.randn(2, 640, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+    skip = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+    res = [torch.randn_like(skip) for _ in range(2)]
+    ms = timed(lambda: ops.residual_inject(skip, res, [0.8, 0.6], hidden=hid))
+    out.append(("K3 inject 2 residuals + concat [2,640|320,128,128] bf16",
+                (hid.numel() + 3 * skip.numel() + hid.numel() + skip.numel()) * 2, ms))
+    del flush
+    return [{"kernel": k, "achieved": b / (m * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+             "frac": b / (m * 1e-3) / 1e9 / hbm, "alg_bytes": b, "launch_ms": m} for k, b, m in out]
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_setup(args.gpus)
@@ -450,7 +511,7 @@ def run_ours(args):
         "gpu_launches": int(gpu_launches),
         "roofline": {"kernel": "sdb lora_patch (K1, stacked R=128, all 794 SDXL matrices)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm if achieved else None, "traffic": None,
+                     "frac": achieved / hbm if achieved else None, "traffic": k1_traffic(),
                      "alg_bytes_per_launch": alg, "launch_ms_live": live,
                      "launch_ms_isolated": statistics.median(iso),
                      "frac_isolated": alg / (statistics.median(iso) * 1e-3) / 1e9 / hbm,
@@ -459,6 +520,7 @@ def run_ours(args):
         "detail": {"step_ms_calibrated": step_ms, "first_patched_step": pipe.last_first_patched_step,
                    "patch_path": pipe.patchset.plan.path, "per_image_s": [round(x, 4) for x in per_image]},
     }
+    line["roofline_other_kernels"] = other_kernels_roofline(hbm)
     if world == 1 and rank == 0 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline_leg()

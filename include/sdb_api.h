@@ -119,6 +119,17 @@ typedef struct sdb_lora_tc_job {
 } sdb_lora_tc_job;
 
 int sdb_lora_pack_bytes(int64_t h1, int64_t h2, int32_t rank, size_t* a_bytes, size_t* b_bytes);
+/* Stack-and-pack from up to 8 adapters' own bf16 factor buffers (the stacked
+ * set of lora.py:147-160, scales folded in fp32 into A, one rounding):
+ * packed rank = sum of the sources' ranks. */
+typedef struct sdb_lora_src {
+  const void* down; int64_t ldd;   /* h1 x rank   */
+  const void* up;   int64_t ldu;   /* rank x h2   */
+  int32_t rank;
+  float scale;
+} sdb_lora_src;
+int sdb_lora_pack_multi(const sdb_lora_src* srcs_host, int n_src, int64_t h1, int64_t h2,
+                        void* a_packed, void* b_packed, void* stream);
 int sdb_lora_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2,
                   int32_t rank, void* a_packed, void* b_packed, void* stream);
 /* blob_host == NULL: only report *needed bytes, *n_units and *kb_max. */

@@ -142,8 +142,21 @@ class LoraTcJob(ctypes.Structure):
     ]
 
 
-EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_tc_plan", "sdb_lora_tc_patch",
-                       "sdb_geglu", "sdb_add_layernorm")
+class LoraSrc(ctypes.Structure):
+    """Mirror of ``sdb_lora_src`` (include/sdb_api.h)."""
+
+    _fields_ = [
+        ("down", ctypes.c_void_p),
+        ("ldd", ctypes.c_int64),
+        ("up", ctypes.c_void_p),
+        ("ldu", ctypes.c_int64),
+        ("rank", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+    ]
+
+
+EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_tc_plan",
+                       "sdb_lora_tc_patch", "sdb_geglu", "sdb_add_layernorm")
 
 
 def _declare_tc(lib: ctypes.CDLL) -> None:
@@ -152,6 +165,8 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
     lib.sdb_lora_pack_bytes.argtypes = [i64, i64, ctypes.c_int32, ctypes.POINTER(sz), ctypes.POINTER(sz)]
     lib.sdb_lora_pack.restype = i32
     lib.sdb_lora_pack.argtypes = [vp, i64, vp, i64, i64, i64, ctypes.c_int32, vp, vp, vp]
+    lib.sdb_lora_pack_multi.restype = i32
+    lib.sdb_lora_pack_multi.argtypes = [ctypes.POINTER(LoraSrc), i32, i64, i64, vp, vp, vp]
     lib.sdb_lora_tc_plan.restype = i32
     lib.sdb_lora_tc_plan.argtypes = [ctypes.POINTER(LoraTcJob), i32, vp, sz, ctypes.POINTER(sz),
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]

@@ -322,10 +322,10 @@ class CaaSNode:
             return g.get("svc", 0)
         return self.pipe.launches_per_step
 
-    def load_loras(self, adapters) -> None:
+    def load_loras(self, adapters, host_resident: bool = False) -> None:
         """LoRA lives on the base UNet only (ControlNets are not patched)."""
         if self.role in ("base", "solo"):
-            self.pipe.load_loras(adapters)
+            self.pipe.load_loras(adapters, host_resident=host_resident)
 
     def setup(self) -> None:
         if self.role == "solo":
@@ -411,14 +411,8 @@ class CaaSNode:
             first = plan_lora_patch(p.patch_ms_est, p.step_ms_est, 0.0, self.steps).first_patched_step
         else:
             first = boundary + 1
-        p.patch_stream.wait_stream(torch.cuda.current_stream(self.device))
         timing = p.patch_timing is not None
-        if timing:
-            p0 = torch.cuda.Event(enable_timing=True)
-            p0.record(p.patch_stream)
-        p.patchset.launch(stream=p.patch_stream, max_ctas=p.patch_max_ctas)
-        ev = torch.cuda.Event(enable_timing=timing)
-        ev.record(p.patch_stream)
+        p0, ev = p.launch_patch(timing=timing)
         if timing:
             p.patch_timing.append((p0, ev))
         p.last_first_patched_step = first
@@ -527,8 +521,8 @@ class LoopbackGroup:
         if ev is not None and first > self.steps:
             s.wait_event(ev)
 
-    def load_loras(self, adapters) -> None:
-        self.base.load_loras(adapters)
+    def load_loras(self, adapters, host_resident: bool = False) -> None:
+        self.base.load_loras(adapters, host_resident=host_resident)
 
     def latent_nchw(self) -> torch.Tensor:
         return self.base.latent_nchw()

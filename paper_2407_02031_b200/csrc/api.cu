@@ -24,6 +24,8 @@ int lora_patch_tc(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles,
 void tc_pack_bytes(int64_t h1, int64_t h2, int rank, size_t* a_bytes, size_t* b_bytes);
 int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2, int rank,
             void* a_out, void* b_out, cudaStream_t st);
+int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, void* a_out, void* b_out,
+                  cudaStream_t st);
 int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed,
             int* n_units_out, int* kb_max_out);
 int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign,
@@ -144,6 +146,11 @@ int sdb_lora_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, in
   if (!down || !up || !a_packed || !b_packed) return fail(SDB_EINVAL, "sdb_lora_pack: NULL pointer");
   if (ldd < rank || ldu < h2) return fail(SDB_EINVAL, "sdb_lora_pack: leading dimension too small");
   return tc_pack(down, ldd, up, ldu, h1, h2, rank, a_packed, b_packed, as_stream(stream));
+}
+
+int sdb_lora_pack_multi(const sdb_lora_src* srcs_host, int n_src, int64_t h1, int64_t h2, void* a_packed,
+                        void* b_packed, void* stream) {
+  return tc_pack_multi(srcs_host, n_src, h1, h2, a_packed, b_packed, as_stream(stream));
 }
 
 int sdb_lora_tc_plan(const sdb_lora_tc_job* jobs_host, int n_jobs, void* blob_host, size_t blob_bytes,

@@ -399,6 +399,80 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
 }
 
 // ---- packing ----------------------------------------------------------------
+// Multi-source packing: the stacked adapter set (lora.py:147-160: down' =
+// [d_1*f32(s_1) | d_2*f32(s_2) ...], up' = [u_1; u_2 ...]) is assembled while
+// packing, straight from each adapter's own factor buffers — no stacked copy.
+constexpr int kMaxSrc = 8;
+struct PackSrcs {
+  const __nv_bfloat16* down[kMaxSrc];
+  const __nv_bfloat16* up[kMaxSrc];
+  int64_t ldd[kMaxSrc], ldu[kMaxSrc];
+  int koff[kMaxSrc + 1];   // prefix sums of the ranks
+  float scale[kMaxSrc];
+  int n;
+};
+
+__device__ __forceinline__ int src_of(const PackSrcs& s, int k) {
+  int i = 0;
+  while (i + 1 < s.n && k >= s.koff[i + 1]) ++i;
+  return i;
+}
+
+__global__ void pack_a_multi_kernel(PackSrcs s, int64_t h1, int kbt, int64_t mt, uint4* __restrict__ out) {
+  const int rank = s.koff[s.n];
+  const int64_t total = mt * kbt * kBM * 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i & 7);
+    const int64_t rowi = i >> 3;                // (m*kbt + kb)*128 + r
+    const int r = (int)(rowi % kBM);
+    const int64_t mk = rowi / kBM;
+    const int kb = (int)(mk % kbt);
+    const int64_t m = mk / kbt;
+    const int64_t row = m * kBM + r;
+    const int k0 = kb * kKB + c * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = k0 + e;
+      float x = 0.f;
+      if (row < h1 && k < rank) {
+        const int si = src_of(s, k);
+        // f32(d) * f32(s), rounded once to bf16 (the reference folds in fp32)
+        x = __bfloat162float(s.down[si][row * s.ldd[si] + (k - s.koff[si])]) * s.scale[si];
+      }
+      v[e] = __float2bfloat16_rn(x);
+    }
+    out[rowi * 8 + (c ^ (r & 7))] = *reinterpret_cast<uint4*>(v);
+  }
+}
+
+__global__ void pack_b_multi_kernel(PackSrcs s, int64_t h2, int kbt, int64_t nt, uint4* __restrict__ out) {
+  const int rank = s.koff[s.n];
+  const int64_t total = nt * kbt * 8 * kBN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i % kBN);               // fastest: coalesced reads of up rows
+    const int64_t q = i / kBN;
+    const int c = (int)(q & 7);
+    const int64_t nk = q >> 3;                  // nt*kbt + kb
+    const int kb = (int)(nk % kbt);
+    const int64_t ntile = nk / kbt;
+    const int64_t col = ntile * kBN + n;
+    const int k0 = kb * kKB + c * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = k0 + e;
+      __nv_bfloat16 x = __float2bfloat16_rn(0.f);
+      if (col < h2 && k < rank) {
+        const int si = src_of(s, k);
+        x = s.up[si][(int64_t)(k - s.koff[si]) * s.ldu[si] + col];
+      }
+      v[e] = x;
+    }
+    out[(nk * kBN + n) * 8 + (c ^ (n & 7))] = *reinterpret_cast<uint4*>(v);
+  }
+}
+
 // A: [mt][kb][128][8 chunks x 16 B], chunk c of row r stored at c ^ (r & 7)
 __global__ void pack_a_kernel(const __nv_bfloat16* __restrict__ down, int64_t ldd, int64_t h1, int rank,
                               int kbt, int64_t mt, uint4* __restrict__ out) {
@@ -496,6 +570,38 @@ int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t 
   pack_b_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 65535), 256, 0, st>>>(
       static_cast<const __nv_bfloat16*>(up), ldu, h2, rank, kbt, nt, static_cast<uint4*>(b_out));
   return check_launch("pack_b_kernel");
+}
+
+int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, void* a_out, void* b_out,
+                  cudaStream_t st) {
+  if (n_src < 1 || n_src > kMaxSrc || !srcs) return fail(SDB_EINVAL, "lora_pack_multi: 1..8 sources");
+  if (((uintptr_t)a_out | (uintptr_t)b_out) & 1023)
+    return fail(SDB_EINVAL, "lora_pack_multi: outputs must be 1024-B aligned");
+  PackSrcs s;
+  std::memset(&s, 0, sizeof(s));
+  s.n = n_src;
+  s.koff[0] = 0;
+  for (int i = 0; i < n_src; ++i) {
+    if (!srcs[i].down || !srcs[i].up || srcs[i].rank < 1 || srcs[i].ldd < srcs[i].rank || srcs[i].ldu < h2)
+      return fail(SDB_EINVAL, "lora_pack_multi: source " + std::to_string(i) + ": bad pointer / rank / stride");
+    s.down[i] = static_cast<const __nv_bfloat16*>(srcs[i].down);
+    s.up[i] = static_cast<const __nv_bfloat16*>(srcs[i].up);
+    s.ldd[i] = srcs[i].ldd;
+    s.ldu[i] = srcs[i].ldu;
+    s.scale[i] = srcs[i].scale;
+    s.koff[i + 1] = s.koff[i] + srcs[i].rank;
+  }
+  const int rank = s.koff[n_src];
+  if (rank > kMaxKB * kKB) return fail(SDB_EINVAL, "lora_pack_multi: stacked rank must be <= 256");
+  const int kbt = tc_kb(rank);
+  const int64_t mt = (h1 + kBM - 1) / kBM, nt = (h2 + kBN - 1) / kBN;
+  const int64_t na = mt * kbt * kBM * 8, nb = nt * kbt * 8 * kBN;
+  pack_a_multi_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 65535), 256, 0, st>>>(
+      s, h1, kbt, mt, static_cast<uint4*>(a_out));
+  if (int rc = check_launch("pack_a_multi_kernel")) return rc;
+  pack_b_multi_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 65535), 256, 0, st>>>(
+      s, h2, kbt, nt, static_cast<uint4*>(b_out));
+  return check_launch("pack_b_multi_kernel");
 }
 
 // Tile width: the B panel (BN x Rpad bf16) stays resident in shared memory.

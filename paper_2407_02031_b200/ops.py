@@ -166,10 +166,15 @@ class LoraTmaPlan:
     tcgen05 at every rank (ranks padded to 16 for the MMA K step; an FFMA
     variant measured 3x slower even at R = 8).  One launch covers every job.
 
-    entries: (w_in, w_out or None, down (h1, R) bf16, up (R, h2) bf16, scale),
-    every w_in must satisfy ``tma_eligible``."""
+    entries: (w_in, w_out or None, down (h1, R) bf16, up (R, h2) bf16, scale)
+    or (w_in, w_out or None, [(down_i, up_i, s_i), ...], None, scale) — the
+    adapters of a stack given separately: they are stacked (scales folded,
+    lora.py:147-160) while packing, straight from their own buffers.  Every
+    w_in must satisfy ``tma_eligible``.  ``repack(stream)`` re-runs the
+    packing from the same factor buffers (after they were refreshed, e.g. by
+    an async host-to-device fetch)."""
 
-    def __init__(self, entries: Sequence[tuple], simt_max_rank: int = 0):
+    def __init__(self, entries: Sequence[tuple], simt_max_rank: int = 0, stream=None):
         if not entries:
             raise ValidationError("LoraTmaPlan needs at least one job")
         lib = _lib.lib()
@@ -178,23 +183,29 @@ class LoraTmaPlan:
         self.alg_bytes = 0
         self.alg_flops = 0
         self.max_rank = 0
+        self._srcs = []      # per job: (ctypes sdb_lora_src array, n, h1, h2)
+        norm = []
         for i, (w_in, w_out, down, up, scale) in enumerate(entries):
             out = w_in if w_out is None else w_out
-            require_cuda(w_in, out, down, up)
+            srcs = list(down) if isinstance(down, (list, tuple)) else [(down, up, 1.0)]
             if not (tma_eligible(w_in) and tma_eligible(out)):
                 raise ValidationError(f"job {i}: weight is not TMA-eligible (bf16, ldw % 8 == 0)")
-            if down.dtype != torch.bfloat16 or up.dtype != torch.bfloat16:
-                raise ValidationError(f"job {i}: factors must be bf16 on the TMA path")
             h1, h2 = w_in.shape
-            r = down.shape[1]
-            if down.shape[0] != h1 or up.shape != (r, h2):
-                raise ValidationError(f"job {i}: factor shapes do not match weight ({h1}, {h2})")
+            r = 0
+            for d, u, _ in srcs:
+                require_cuda(w_in, out, d, u)
+                if d.dtype != torch.bfloat16 or u.dtype != torch.bfloat16:
+                    raise ValidationError(f"job {i}: factors must be bf16 on the TMA path")
+                if d.shape[0] != h1 or u.shape != (d.shape[1], h2):
+                    raise ValidationError(f"job {i}: factor shapes do not match weight ({h1}, {h2})")
+                r += d.shape[1]
             a_b, b_b = ctypes.c_size_t(0), ctypes.c_size_t(0)
             _lib.check("sdb_lora_pack_bytes", lib.sdb_lora_pack_bytes(h1, h2, r, ctypes.byref(a_b), ctypes.byref(b_b)))
             sizes.append((a_b.value, b_b.value))
             self.alg_bytes += 2 * h1 * h2 * 2 + (h1 + h2) * r * 2
             self.alg_flops += 2 * h1 * h2 * r
             self.max_rank = max(self.max_rank, r)
+            norm.append((w_in, out, srcs, r, scale))
         # one arena, every packed block 1024-B aligned
         offs, total = [], 0
         for a_b, b_b in sizes:
@@ -204,21 +215,23 @@ class LoraTmaPlan:
         base = (self.arena.data_ptr() + 1023) // 1024 * 1024
         jobs = (_lib.LoraTcJob * len(entries))()
         self._keep = []
-        for i, (w_in, w_out, down, up, scale) in enumerate(entries):
-            out = w_in if w_out is None else w_out
+        for i, (w_in, out, srcs, r, scale) in enumerate(norm):
             h1, h2 = w_in.shape
-            r = down.shape[1]
             a_ptr, b_ptr = base + offs[i][0], base + offs[i][1]
-            _count(2)
-            _lib.check("sdb_lora_pack", lib.sdb_lora_pack(
-                down.data_ptr(), _row_stride(down, "down"), up.data_ptr(), _row_stride(up, "up"),
-                h1, h2, r, a_ptr, b_ptr, _stream_ptr(None)))
+            arr = (_lib.LoraSrc * len(srcs))()
+            for k, (d, u, s) in enumerate(srcs):
+                arr[k].down, arr[k].ldd = d.data_ptr(), _row_stride(d, "down")
+                arr[k].up, arr[k].ldu = u.data_ptr(), _row_stride(u, "up")
+                arr[k].rank, arr[k].scale = d.shape[1], float(s)
+                self._keep += [d, u]
+            self._srcs.append((arr, len(srcs), h1, h2, a_ptr, b_ptr))
             j = jobs[i]
             j.w_in, j.w_out = w_in.data_ptr(), out.data_ptr()
             j.h1, j.h2, j.ldw = h1, h2, _row_stride(w_in, "weight")
             j.a_packed, j.b_packed = a_ptr, b_ptr
             j.rank, j.scale = r, float(scale)
             self._keep += [w_in, out]
+        self.repack(stream)
         need, n_units, kb_max = ctypes.c_size_t(0), ctypes.c_int(0), ctypes.c_int(0)
         _lib.check("sdb_lora_tc_plan", lib.sdb_lora_tc_plan(jobs, len(entries), None, 0, ctypes.byref(need),
                                                             ctypes.byref(n_units), ctypes.byref(kb_max)))
@@ -233,6 +246,13 @@ class LoraTmaPlan:
         self.simt_rank = self.max_rank if self.max_rank <= simt_max_rank else 0
         self.simt_rank = 0
         self.path = 1   # 1 = TMA + tcgen05 (0 = the generic SIMT kernel of LoraPatchPlan)
+
+    def repack(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """(Re-)stack and pack every job's factors into the arena (2 kernels per job)."""
+        lib, sp = _lib.lib(), _stream_ptr(stream)
+        for arr, n, h1, h2, a_ptr, b_ptr in self._srcs:
+            _count(2)
+            _lib.check("sdb_lora_pack_multi", lib.sdb_lora_pack_multi(arr, n, h1, h2, a_ptr, b_ptr, sp))
 
     def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None,
                max_ctas: int = 0) -> None:

@@ -38,6 +38,7 @@ class UNetLora:
     adapter_id: str
     factors: dict            # name -> (down, up)
     scale: float = 1.0
+    up_physical: bool = False   # True: up columns already in the stored weight's order
 
     @property
     def rank(self) -> int:
@@ -112,40 +113,61 @@ class PatchSet:
             raise ValidationError("PatchSet needs at least one adapter")
         self.params = params
         self.shadow = shadow
+        self.adapters = list(adapters)
         names = [n for n, _ in params.matrices if any(n in a.factors for a, _ in adapters)]
-        self.entries = []
-        self.stacked = {}
+        self.touched = set(names)
+        ranks = {n: sum(a.factors[n][0].shape[1] for a, _ in adapters if n in a.factors) for n in names}
+        self.rank = max(ranks.values())
+        fast, slow = [], []
+        self.stacked = {}    # name -> (down, up) for the generic-kernel matrices
         for name in names:
-            downs, ups = [], []
-            for a, s in adapters:
-                if name not in a.factors:
-                    continue
-                d, u = a.factors[name]
-                # lora.py:153 folds f32(s) into down; done in fp32, one rounding to the factor dtype
-                downs.append((d.float() * np.float32(s)).to(d.dtype))
-                ups.append(physical_up(params, name, u))
-            down = torch.cat(downs, dim=1).contiguous()
-            up = torch.cat(ups, dim=0).contiguous()
-            self.stacked[name] = (down, up)
+            present = [(a, s) for a, s in adapters if name in a.factors]
             w_in = params.matrix_view(name)
             w_out = None
             if shadow is not None:
                 w_out = shadow[name].permute(0, 2, 3, 1).reshape(w_in.shape) if shadow[name].dim() == 4 \
                     else shadow[name]
-            self.entries.append((w_in, w_out, down, up, 1.0))
-        self.rank = max(d.shape[1] for d, _ in self.stacked.values())
-        # bf16 matrices with 16-B aligned rows take the TMA / tcgen05 kernel (one
-        # launch, factors packed here, once per adapter set); the rest (e.g.
-        # SDXL conv_in, 320 x 36) the generic SIMT kernel.
-        fast = [e for e in self.entries if use_tma and self.rank <= 256 and ops.tma_eligible(e[0])
-                and e[2].dtype == torch.bfloat16]
-        slow = [e for e in self.entries if not any(e is f for f in fast)]
+            ups = [a.factors[name][1] if a.up_physical else physical_up(params, name, a.factors[name][1])
+                   for a, _ in present]
+            if (use_tma and self.rank <= 256 and ops.tma_eligible(w_in)
+                    and all(a.factors[name][0].dtype == torch.bfloat16 for a, _ in present)):
+                # bf16, 16-B rows: the TMA / tcgen05 kernel; adapters stacked while packing
+                srcs = [(a.factors[name][0], u, float(np.float32(s))) for (a, s), u in zip(present, ups)]
+                fast.append((w_in, w_out, srcs, None, 1.0))
+            else:
+                # everything else (e.g. SDXL conv_in, 320 x 36): the generic kernel on a
+                # stacked copy — lora.py:153 folds f32(s) into down in fp32, one rounding
+                self.stacked[name] = self._stack(name, present, ups)
+                down, up = self.stacked[name]
+                slow.append((w_in, w_out, down, up, 1.0))
+        self._slow_src = {n: [(a, s) for a, s in adapters if n in a.factors] for n in self.stacked}
         self.plans = []
         if fast:
             self.plans.append(ops.LoraTmaPlan(fast, simt_max_rank=simt_max_rank))
         if slow:
             self.plans.append(ops.LoraPatchPlan(slow))
         self.plan = self.plans[0]
+
+    def _stack(self, name, present, ups=None, out=None):
+        if ups is None:
+            ups = [a.factors[name][1] if a.up_physical else physical_up(self.params, name, a.factors[name][1])
+                   for a, _ in present]
+        downs = [(a.factors[name][0].float() * np.float32(s)).to(a.factors[name][0].dtype) for a, s in present]
+        if out is None:
+            return torch.cat(downs, dim=1).contiguous(), torch.cat(ups, dim=0).contiguous()
+        torch.cat(downs, dim=1, out=out[0])
+        torch.cat(ups, dim=0, out=out[1])
+        return out
+
+    def refresh(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Re-stack / re-pack from the adapters' (refreshed) factor buffers,
+        stream-ordered: the step between an async fetch and the patch."""
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            for p in self.plans:
+                if isinstance(p, ops.LoraTmaPlan):
+                    p.repack(stream)
+            for name, present in self._slow_src.items():
+                self._stack(name, present, out=self.stacked[name])
 
     @property
     def alg_bytes(self) -> int:
@@ -164,11 +186,50 @@ class PatchSet:
         weight (only needed when adapters cover a subset of matrices)."""
         if self.shadow is None:
             return
-        touched = set(self.stacked)
+        touched = self.touched
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
             for name, _ in self.params.matrices:
                 if name not in touched:
                     self.shadow[name].copy_(self.params.t[name + ".weight"])
+
+
+class AdapterBank:
+    """Adapters resident in pinned HOST memory — the LoRA cache tier the paper
+    fetches from (the reference's tiered fetch,
+    addons.py:22-28) — each with a device staging twin.  ``fetch(stream)`` is
+    one asynchronous H2D copy per adapter (copy engine, overlaps compute); the
+    device views it fills are what a PatchSet packs from, so fetch -> repack ->
+    patch is a stream-ordered chain that needs no host round trip."""
+
+    def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]], device=None):
+        device = torch.device(device) if device is not None else params.device
+        self.host, self.dev, self.adapters = [], [], []
+        self.nbytes = 0
+        for a, s in adapters:
+            dtype = next(iter(a.factors.values()))[0].dtype
+            items = []
+            for name, (d, u) in a.factors.items():
+                up = u if a.up_physical else physical_up(params, name, u.to(params.device))
+                items.append((name, d, up))
+            total = sum(d.numel() + up.numel() for _, d, up in items)
+            host = torch.empty(total, dtype=dtype).pin_memory()
+            dev = torch.empty(total, dtype=dtype, device=device)
+            views, off = {}, 0
+            for name, d, up in items:
+                nd, nu = d.numel(), up.numel()
+                host[off:off + nd].copy_(d.reshape(-1).cpu())
+                host[off + nd:off + nd + nu].copy_(up.reshape(-1).cpu())
+                views[name] = (dev[off:off + nd].view(d.shape), dev[off + nd:off + nd + nu].view(up.shape))
+                off += nd + nu
+            self.host.append(host)
+            self.dev.append(dev)
+            self.nbytes += total * host.element_size()
+            self.adapters.append((UNetLora(a.adapter_id, views, a.scale, up_physical=True), s))
+
+    def fetch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            for h, d in zip(self.host, self.dev):
+                d.copy_(h, non_blocking=True)
 
 
 class _nullctx:

@@ -33,7 +33,7 @@ import numpy as np
 import torch
 
 from . import ops
-from .patcher import PatchSet, UNetLora, allocate_shadow
+from .patcher import AdapterBank, PatchSet, UNetLora, allocate_shadow
 from .scheduler import ddim_tables
 from .schedule import plan_lora_patch
 from .unet import ControlNet, UNet, UNetConfig, init_controlnet, init_unet
@@ -113,6 +113,9 @@ class AddonPipeline:
         self.step_dev = torch.zeros(2, device=dev, dtype=torch.int32)
         self.main_stream = torch.cuda.Stream(device=dev, priority=-1)
         self.patch_stream = torch.cuda.Stream(device=dev, priority=0)
+        self.copy_stream = torch.cuda.Stream(device=dev, priority=0)
+        self.bank = None
+        self.patch_graph = None
         self.shadow = None
         self.patchset: Optional[PatchSet] = None
         self.graphs: dict = {}
@@ -173,17 +176,62 @@ class AddonPipeline:
         torch.cuda.synchronize(self.device)
 
     # ------------------------------------------------------------------
-    def load_loras(self, adapters: Sequence[tuple[UNetLora, float]]) -> PatchSet:
+    def load_loras(self, adapters: Sequence[tuple[UNetLora, float]], host_resident: bool = False) -> PatchSet:
         """Stack the request's adapters into one planned K1 launch writing the
-        shadow weights (allocated once)."""
+        shadow weights (allocated once).
+
+        host_resident: the adapters live in pinned host memory (AdapterBank)
+        and every patched request re-fetches them — the async LoRA fetch path
+        (orchestrator.py:509-528): H2D on a copy stream,
+        then ONE CUDA graph on the patch stream re-stacks/re-packs them and
+        runs K1, all overlapped with the first denoising steps; the plan's
+        "load" time is fetch + pack + patch."""
         if self.shadow is None:
             _ = self._pristine
             self.shadow = allocate_shadow(self.unet_p)
+        self.bank = AdapterBank(self.unet_p, adapters, self.device) if host_resident else None
+        if self.bank is not None:
+            adapters = self.bank.adapters
+            self.bank.fetch()
         self.patchset = PatchSet(self.unet_p, adapters, shadow=self.shadow)
         self.patchset.copy_unpatched()
+        self.patch_graph = None
+        if self.bank is not None:
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            self.patch_stream.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.graph(g, stream=self.patch_stream):
+                self.patchset.refresh(self.patch_stream)
+                self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+            self.patch_graph = g
         if self.use_graphs and "patched" not in self.graphs:
             self._capture("patched")
         return self.patchset
+
+    def launch_patch(self, timing: bool = False):
+        """Enqueue the request's patch on the side streams; returns (start, done)
+        events (start is None unless timing).  Host-resident adapters: fetch on
+        the copy stream, then the captured refresh+patch graph."""
+        s = torch.cuda.current_stream(self.device)
+        p0 = torch.cuda.Event(enable_timing=True) if timing else None
+        if self.bank is not None:
+            self.copy_stream.wait_stream(s)
+            self.copy_stream.wait_stream(self.patch_stream)   # previous pack finished reading staging
+            if timing:
+                p0.record(self.copy_stream)
+            self.bank.fetch(self.copy_stream)
+            self.patch_stream.wait_stream(self.copy_stream)
+            self.patch_stream.wait_stream(s)                  # shadow free once earlier steps finished
+            with torch.cuda.stream(self.patch_stream):
+                self.patch_graph.replay()
+        else:
+            self.patch_stream.wait_stream(s)
+            if timing:
+                p0.record(self.patch_stream)
+            self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+        ev = torch.cuda.Event(enable_timing=timing)
+        ev.record(self.patch_stream)
+        return p0, ev
 
     def setup(self) -> None:
         if self.use_graphs and "pristine" not in self.graphs:
@@ -206,12 +254,9 @@ class AddonPipeline:
         e1.synchronize()
         self.step_ms_est = e0.elapsed_time(e1) / reps
         if self.patchset is not None:
-            p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            p0.record(self.patch_stream)
-            self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
-            p1.record(self.patch_stream)
+            p0, p1 = self.launch_patch(timing=True)
             p1.synchronize()
-            self.patch_ms_est = p0.elapsed_time(p1)
+            self.patch_ms_est = p0.elapsed_time(p1)   # the plan's "load": fetch + pack + patch
         return self.step_ms_est, self.patch_ms_est
 
     def _replay(self, which: str) -> None:
@@ -263,13 +308,7 @@ class AddonPipeline:
                 first = plan.first_patched_step
             else:
                 first = boundary + 1
-            self.patch_stream.wait_stream(s)   # shadow is free once earlier work on s finished
-            if self.patch_timing is not None:
-                p0 = torch.cuda.Event(enable_timing=True)
-                p0.record(self.patch_stream)
-            self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
-            ev = torch.cuda.Event(enable_timing=self.patch_timing is not None)
-            ev.record(self.patch_stream)
+            p0, ev = self.launch_patch(timing=self.patch_timing is not None)
             if self.patch_timing is not None:
                 self.patch_timing.append((p0, ev))
         waited = False

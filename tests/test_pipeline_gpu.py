@@ -133,6 +133,32 @@ def test_planned_async_boundary():
     assert torch.isfinite(pipe.x).all()
 
 
+def test_host_resident_lora_fetch_path_is_bitwise_device_path():
+    """Adapters in pinned host memory, fetched per request on the copy stream,
+    re-packed + patched by the captured patch graph: bitwise the same latents
+    as device-resident adapters (same kernels, same packed operands)."""
+    def run(host):
+        pipe = AddonPipeline(U.TOY, n_controlnets=1, steps=6, dtype=torch.bfloat16, seed=0)
+        los = [(synthetic_lora(pipe.unet_p, r, seed=7 + r, adapter_id=f"l{r}"), 0.6) for r in (8, 16)]
+        pipe.load_loras(los, host_resident=host)
+        pipe.setup()
+        req = synthetic_request(U.TOY, 1)
+        out = []
+        for _ in range(2):   # the second request re-fetches
+            pipe.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context),
+                         [torch.from_numpy(req.images[0])])
+            pipe.denoise(patch=True, boundary=2)
+            out.append(pipe.latent_nchw().clone())
+        return out, pipe
+    dev, _ = run(False)
+    host, pipe = run(True)
+    for a, b in zip(dev, host):
+        assert torch.equal(a, b)
+    assert pipe.bank is not None and pipe.bank.nbytes > 0
+    step_ms, load_ms = pipe.calibrate()
+    assert load_ms > 0
+
+
 def test_e2e_generate_host_buffers():
     pipe = AddonPipeline(U.TOY, n_controlnets=1, steps=4, dtype=torch.bfloat16)
     pipe.setup()
