@@ -399,7 +399,7 @@ class CaaSNode:
     def service_step(self) -> None:
         self.graphs["svc"].replay()
 
-    def start_patch(self, boundary: Optional[int] = None):
+    def start_patch(self, boundary: Optional[int] = None, fetch: bool = True):
         """Base: launch the request's LoRA patch (shadow weights, low-priority
         side stream) and return (first_patched_step, event) — same semantics as
         AddonPipeline.denoise (schedule.plan_lora_patch)."""
@@ -412,19 +412,19 @@ class CaaSNode:
         else:
             first = boundary + 1
         timing = p.patch_timing is not None
-        p0, ev = p.launch_patch(timing=timing)
+        p0, ev = p.launch_patch(timing=timing, fetch=fetch)
         if timing:
             p.patch_timing.append((p0, ev))
         p.last_first_patched_step = first
         return first, ev
 
-    def denoise(self, patch: bool = False, boundary: Optional[int] = None) -> None:
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None, fetch: bool = True) -> None:
         if self.role == "solo":
-            self.pipe.denoise(patch=patch, boundary=boundary)
+            self.pipe.denoise(patch=patch, boundary=boundary, fetch=fetch)
             return
         first, ev = (self.steps + 1, None)
         if self.role == "base" and patch:
-            first, ev = self.start_patch(boundary)
+            first, ev = self.start_patch(boundary, fetch=fetch)
         s = torch.cuda.current_stream(self.device)
         for step in range(1, self.steps + 1):
             if self.role == "base":
@@ -490,10 +490,11 @@ class LoopbackGroup:
         for s in self.services:
             s.finish_prepare([t.clone() for t in shared])
 
-    def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None) -> None:
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None,
+                fetch: bool = True) -> None:
         first, ev = (self.steps + 1, None)
         if patch:
-            first, ev = self.base.start_patch(boundary)
+            first, ev = self.base.start_patch(boundary, fetch=fetch)
         s = torch.cuda.current_stream()
         for step in range(1, self.steps + 1):
             which = "patched" if step >= first else "pristine"

@@ -606,10 +606,11 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
 
 // Tile width: the B panel (BN x Rpad bf16) stays resident in shared memory.
 // Up to rank 128 a 256-wide panel (64 KB) leaves room for an 8-slot W ring;
-// above it a 256-wide panel (128 KB) would squeeze the ring to 4 slots, so the
-// panel narrows to 128 columns (the A tile is then re-read twice as often, from
-// L2 under the evict-last policy) and the ring keeps 8 slots.
-static int tile_n_for(int kb_max) { return kb_max > 2 ? 128 : kBN; }
+// above it the 256-wide panel (128 KB) squeezes the ring to 4 slots.  A
+// 128-wide panel (8 slots, but the A tile re-read twice as often) measured
+// slower at R = 232 (3.94 vs 3.36-3.67 ms, round 1), so 256 is kept at every
+// rank; the BN=128 instantiation stays for experiments.
+static int tile_n_for(int /*kb_max*/) { return kBN; }
 
 // Blob layout: [maps: 2*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]
 int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed, int* n_units_out,

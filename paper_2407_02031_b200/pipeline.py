@@ -208,13 +208,14 @@ class AddonPipeline:
             self._capture("patched")
         return self.patchset
 
-    def launch_patch(self, timing: bool = False):
+    def launch_patch(self, timing: bool = False, fetch: bool = True):
         """Enqueue the request's patch on the side streams; returns (start, done)
         events (start is None unless timing).  Host-resident adapters: fetch on
-        the copy stream, then the captured refresh+patch graph."""
+        the copy stream (skipped with fetch=False: the staging already holds
+        them), then the captured refresh+patch graph."""
         s = torch.cuda.current_stream(self.device)
         p0 = torch.cuda.Event(enable_timing=True) if timing else None
-        if self.bank is not None:
+        if self.bank is not None and fetch:
             self.copy_stream.wait_stream(s)
             self.copy_stream.wait_stream(self.patch_stream)   # previous pack finished reading staging
             if timing:
@@ -223,7 +224,7 @@ class AddonPipeline:
             self.patch_stream.wait_stream(self.copy_stream)
             self.patch_stream.wait_stream(s)                  # shadow free once earlier steps finished
             with torch.cuda.stream(self.patch_stream):
-                self.patch_graph.replay()
+                self.patch_graph.replay()                     # re-stack/re-pack + K1
         else:
             self.patch_stream.wait_stream(s)
             if timing:
@@ -290,7 +291,8 @@ class AddonPipeline:
                 self.add_emb_cn[i].copy_(cn.add_embedding(self.pooled, self.time_ids))
         self.step_dev.zero_()
 
-    def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None) -> int:
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None,
+                fetch: bool = True) -> int:
         """Run all steps on the current stream.  With ``patch`` the loaded
         PatchSet is launched on the side stream at the start and swapped in
         at boundary k (forced, or planned from the calibrated times).
@@ -308,7 +310,7 @@ class AddonPipeline:
                 first = plan.first_patched_step
             else:
                 first = boundary + 1
-            p0, ev = self.launch_patch(timing=self.patch_timing is not None)
+            p0, ev = self.launch_patch(timing=self.patch_timing is not None, fetch=fetch)
             if self.patch_timing is not None:
                 self.patch_timing.append((p0, ev))
         waited = False
