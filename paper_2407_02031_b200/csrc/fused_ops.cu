@@ -35,8 +35,19 @@ geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int64_t rows, int6
 }
 
 // NV = vectors of 8 per lane (C = 256 * NV max per warp pass)
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
+  if constexpr (sizeof(T) == 2) {
+    const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = to_f32<T>(h[i]);
+  }
+}
+
+// 16-bit T: every load of the row (x, d, gamma, beta) is issued before any is
+// consumed — one memory round trip per row instead of three dependent ones.
 template <typename T, int NV>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(128)
 add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* __restrict__ gamma,
                      const T* __restrict__ beta, int64_t rows, int64_t c, float eps) {
   const int lane = threadIdx.x & 31;
@@ -45,14 +56,28 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
   T* xr = x + row * c;
   float v[NV][8];
   float sum = 0.f;
+  uint4 xq[NV], dq[NV], gq[NV], bq[NV];
+  constexpr bool kHalf = sizeof(T) == 2;
+  if constexpr (kHalf) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int64_t col = (int64_t)(k * 32 + lane) * 8;
+      if (col < c) {
+        xq[k] = *reinterpret_cast<const uint4*>(xr + col);
+        if (d != nullptr) dq[k] = *reinterpret_cast<const uint4*>(d + row * c + col);
+        gq[k] = __ldg(reinterpret_cast<const uint4*>(gamma + col));
+        bq[k] = __ldg(reinterpret_cast<const uint4*>(beta + col));
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const int64_t col = (int64_t)(k * 32 + lane) * 8;
     if (col < c) {
-      Vec8<T>::load(xr + col, v[k]);
+      if constexpr (kHalf) unpack8<T>(xq[k], v[k]); else Vec8<T>::load(xr + col, v[k]);
       if (d != nullptr) {
         float dv[8];
-        Vec8<T>::load(d + row * c + col, dv);
+        if constexpr (kHalf) unpack8<T>(dq[k], dv); else Vec8<T>::load(d + row * c + col, dv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[k][j] += dv[j];
         // the residual stream is stored in T: round once, normalise the stored value
@@ -87,8 +112,13 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
     const int64_t col = (int64_t)(k * 32 + lane) * 8;
     if (col < c) {
       float ga[8], be[8], o[8];
-      Vec8<T>::load(gamma + col, ga);
-      Vec8<T>::load(beta + col, be);
+      if constexpr (kHalf) {
+        unpack8<T>(gq[k], ga);
+        unpack8<T>(bq[k], be);
+      } else {
+        Vec8<T>::load(gamma + col, ga);
+        Vec8<T>::load(beta + col, be);
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) o[j] = fmaf((v[k][j] - mean) * rstd, ga[j], be[j]);
       Vec8<T>::store(y + row * c + col, o);
@@ -108,7 +138,7 @@ int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t
 template <typename T>
 int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                float eps, cudaStream_t st) {
-  const unsigned grid = (unsigned)((rows + 7) / 8);
+  const unsigned grid = (unsigned)((rows + 3) / 4);   // 4 rows (warps) per 128-thread CTA
   T* xp = static_cast<T*>(x);
   const T* dp = static_cast<const T*>(d);
   T* yp = static_cast<T*>(y);
@@ -116,16 +146,16 @@ int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* b
   const T* bp = static_cast<const T*>(beta);
   const int nv = (int)((c / 8 + 31) / 32);
   switch (nv) {
-    case 1: add_layernorm_kernel<T, 1><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 2: add_layernorm_kernel<T, 2><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 3: add_layernorm_kernel<T, 3><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 4: add_layernorm_kernel<T, 4><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 5: add_layernorm_kernel<T, 5><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 6: add_layernorm_kernel<T, 6><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 7: add_layernorm_kernel<T, 7><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 8: add_layernorm_kernel<T, 8><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 9: add_layernorm_kernel<T, 9><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 10: add_layernorm_kernel<T, 10><<<grid, 256, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 1: add_layernorm_kernel<T, 1><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 2: add_layernorm_kernel<T, 2><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 3: add_layernorm_kernel<T, 3><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 4: add_layernorm_kernel<T, 4><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 5: add_layernorm_kernel<T, 5><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 6: add_layernorm_kernel<T, 6><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 7: add_layernorm_kernel<T, 7><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 8: add_layernorm_kernel<T, 8><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 9: add_layernorm_kernel<T, 9><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 10: add_layernorm_kernel<T, 10><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
     default: return fail(SDB_EINVAL, "add_layernorm: channels must be <= 2560");
   }
   return check_launch("add_layernorm_kernel");

@@ -93,12 +93,12 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
   const int64_t p0 = chunk * rows_per_chunk;
   const int64_t p1 = min(hw, p0 + rows_per_chunk);
   int64_t p = p0 + r;
-  for (; p + 3 * rpp < p1; p += 4 * rpp) {   // 4 independent 16 B loads in flight per thread
-    float a[4][8];
+  for (; p + 7 * rpp < p1; p += 8 * rpp) {   // 8 independent 16 B loads in flight per thread
+    float a[8][8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) Vec8<T>::load(xs + (p + u * rpp) * c + c0, a[u]);
+    for (int u = 0; u < 8; ++u) Vec8<T>::load(xs + (p + u * rpp) * c + c0, a[u]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float d = a[u][j] - K[j];
@@ -143,7 +143,10 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
   __syncthreads();
   if (!is_last) return;
   __threadfence();
+  // full warps only (blockDim = CV * rpp need not be a multiple of 32): the
+  // shuffles below need all 32 lanes
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (warp >= nwarps) return;
   for (int64_t g = warp; g < groups; g += nwarps) {
     double t1 = 0.0, t2 = 0.0;
     for (int64_t ch = lane; ch < chunks; ch += 32) {
