@@ -335,13 +335,13 @@ class CaaSNode:
             p = self.pipe
             _ = p._pristine
             variants = ["pristine"] + (["patched"] if p.patchset is not None else [])
-            pool = None
             for which in variants:
+                # one memory pool per (encoder, decoder) pair: the pair hands its
+                # activations over inside the pool, pairs never share one
                 p._use_weights(which)
                 p.step_dev.zero_()
-                g = self._capture("enc_" + which, self._base_encode, pool=pool)
-                pool = g.pool()
-                self._capture("dec_" + which, self._base_decode, pool=pool)
+                g = self._capture("enc_" + which, self._base_encode)
+                self._capture("dec_" + which, self._base_decode, pool=g.pool())
                 p._use_weights("pristine")
             p.step_dev.zero_()
         else:
