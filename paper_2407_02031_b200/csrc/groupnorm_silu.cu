@@ -13,14 +13,17 @@
 // channels: blockDim = CV * rpp with CV = C/8 vector columns and rpp pixel
 // rows per pass, so each thread always owns the same 8 channels and
 // accumulates them in registers — fully coalesced 16 B loads, no atomics on
-// the data path.
+// the data path.  Every thread handles exactly kRowsPerThread pixel rows per
+// chunk and issues all of their loads before consuming any (the kernel is a
+// streaming pass: memory-level parallelism is the whole game).
 //
 //   kernel 1  gn_stats_kernel: per (n, chunk) shifted sums S1 = sum(x'-K_g),
-//             S2 = sum((x'-K_g)^2) reduced per group; the LAST CTA of each
-//             sample (threadfence + counter) combines the chunks in fp64 and
-//             writes mean / rstd — no separate finalize launch and no
-//             co-residency requirement (safe next to a concurrent LoRA patch
-//             or ControlNet on another stream).
+//             S2 = sum((x'-K_g)^2) reduced per group in shared memory and
+//             added to per-(n, g) fp64 accumulators; the LAST CTA of each
+//             sample (threadfence + counter) turns them into mean / rstd and
+//             re-zeroes them — no separate finalize launch, no serial tail,
+//             no co-residency requirement (safe next to a concurrent LoRA
+//             patch or ControlNet on another stream).
 //   kernel 2  gn_apply_kernel: y = act(x * a_c + b_c), a_c = gamma_c*rstd_g,
 //             b_c = beta_c + (add_c - mean_g) * a_c.
 // Kernel 2 re-reads x right after kernel 1 streamed it; at SDXL sizes the
@@ -39,6 +42,36 @@ namespace {
 
 constexpr int kMaxThreads = 512;
 constexpr int kMaxGroups = 64;
+constexpr int kRowsPerThread = 8;
+
+// 8 consecutive elements of T held as raw registers until they are consumed
+template <typename T> struct Raw8 { uint4 u; };
+template <> struct Raw8<float> { float4 a, b; };
+
+template <typename T>
+__device__ __forceinline__ Raw8<T> load_raw(const T* p) {
+  Raw8<T> r;
+  r.u = *reinterpret_cast<const uint4*>(p);
+  return r;
+}
+template <>
+__device__ __forceinline__ Raw8<float> load_raw<float>(const float* p) {
+  Raw8<float> r;
+  r.a = *reinterpret_cast<const float4*>(p);
+  r.b = *reinterpret_cast<const float4*>(p + 4);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void unpack(const Raw8<T>& r, float (&v)[8]) {
+  const T* h = reinterpret_cast<const T*>(&r.u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = to_f32<T>(h[i]);
+}
+template <>
+__device__ __forceinline__ void unpack<float>(const Raw8<float>& r, float (&v)[8]) {
+  v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w;
+  v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
+}
 
 struct GnShape {
   int64_t n, hw, c, groups, cv, cpg;
@@ -51,24 +84,20 @@ GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups) {
   s.n = n; s.hw = hw; s.c = c; s.groups = groups;
   s.cv = c / 8;
   s.cpg = c / groups;
-  s.rpp = (int)std::max<int64_t>(1, 384 / s.cv);
+  s.rpp = (int)std::max<int64_t>(1, 256 / s.cv);
   s.threads = (int)(s.cv * s.rpp);
-  // ~2 waves of CTAs over 148 SMs across the whole batch, >= 4 rows per lane
-  int64_t target = (2 * kNumSMs + n - 1) / n;
-  int64_t max_chunks = std::max<int64_t>(1, hw / (4 * s.rpp));
-  s.chunks = std::max<int64_t>(1, std::min<int64_t>(target, max_chunks));
-  s.rows_per_chunk = (hw + s.chunks - 1) / s.chunks;
+  s.rows_per_chunk = (int64_t)s.rpp * kRowsPerThread;
   s.chunks = (hw + s.rows_per_chunk - 1) / s.rows_per_chunk;
   return s;
 }
 
-// workspace: counters[n] (uint, zero at rest) | stats[n][group][2] | partial[n][chunk][group][2]
+// workspace: counters[n] (uint) | acc[n][group][2] (double) — both zero at rest —
+// | stats[n][group][2] (float)
 template <typename T>
-__global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc,
-                                float* __restrict__ partial, float* __restrict__ stats,
-                                unsigned int* __restrict__ counters, int64_t hw, int64_t c,
-                                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int64_t chunks,
-                                int rpp, float eps) {
+__global__ void __launch_bounds__(kMaxThreads)
+gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, double* __restrict__ acc,
+                float* __restrict__ stats, unsigned int* __restrict__ counters, int64_t hw, int64_t c,
+                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int64_t chunks, int rpp, float eps) {
   extern __shared__ float red[];  // [rpp][c][2]
   __shared__ bool is_last;
   const int64_t n = blockIdx.y;
@@ -78,7 +107,16 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
   const int r = threadIdx.x / cv;
   const int64_t c0 = (int64_t)v * 8;
   const T* xs = x + n * hw * c;
+  const int64_t p0 = chunk * rows_per_chunk + r;
+  const int64_t p1 = min(hw, chunk * rows_per_chunk + rows_per_chunk);
 
+  // issue every load of this thread first
+  Raw8<T> buf[kRowsPerThread];
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const int64_t p = p0 + (int64_t)u * rpp;
+    if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
+  }
   // d = x' - K_g = x - (K_g - add_c)
   float K[8];
 #pragma unroll
@@ -89,31 +127,17 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
   float s1[8], s2[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) { s1[j] = 0.f; s2[j] = 0.f; }
-
-  const int64_t p0 = chunk * rows_per_chunk;
-  const int64_t p1 = min(hw, p0 + rows_per_chunk);
-  int64_t p = p0 + r;
-  for (; p + 7 * rpp < p1; p += 8 * rpp) {   // 8 independent 16 B loads in flight per thread
-    float a[8][8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) Vec8<T>::load(xs + (p + u * rpp) * c + c0, a[u]);
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    if (p0 + (int64_t)u * rpp < p1) {
+      float a[8];
+      unpack<T>(buf[u], a);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float d = a[u][j] - K[j];
+        const float d = a[j] - K[j];
         s1[j] += d;
         s2[j] = fmaf(d, d, s2[j]);
       }
-  }
-  for (; p < p1; p += rpp) {
-    float a[8];
-    Vec8<T>::load(xs + p * c + c0, a);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float d = a[j] - K[j];
-      s1[j] += d;
-      s2[j] = fmaf(d, d, s2[j]);
     }
   }
 #pragma unroll
@@ -122,6 +146,9 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
     red[((int64_t)r * c + c0 + j) * 2 + 1] = s2[j];
   }
   __syncthreads();
+  // per-group partials of this chunk go straight into fp64 accumulators: the
+  // partials are fp32 sums of similar magnitude, so their fp64 sum is exact in
+  // practice and the mean / rstd rounded to fp32 do not depend on arrival order
   for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
     float t1 = 0.f, t2 = 0.f;
     for (int rr = 0; rr < rpp; ++rr)
@@ -129,9 +156,8 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
         t1 += red[((int64_t)rr * c + ch) * 2 + 0];
         t2 += red[((int64_t)rr * c + ch) * 2 + 1];
       }
-    float* out = partial + ((n * chunks + chunk) * groups + g) * 2;
-    out[0] = t1;
-    out[1] = t2;
+    atomicAdd(acc + (n * groups + g) * 2 + 0, (double)t1);
+    atomicAdd(acc + (n * groups + g) * 2 + 1, (double)t2);
   }
   // ---- the last CTA of this sample finalises (no extra launch) ----
   __threadfence();
@@ -143,47 +169,44 @@ __global__ void gn_stats_kernel(const T* __restrict__ x, const float* __restrict
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  // full warps only (blockDim = CV * rpp need not be a multiple of 32): the
-  // shuffles below need all 32 lanes
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  if (warp >= nwarps) return;
-  for (int64_t g = warp; g < groups; g += nwarps) {
-    double t1 = 0.0, t2 = 0.0;
-    for (int64_t ch = lane; ch < chunks; ch += 32) {
-      const float* pp = partial + ((n * chunks + ch) * groups + g) * 2;
-      t1 += (double)__ldcg(pp);
-      t2 += (double)__ldcg(pp + 1);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-      t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-    }
-    if (lane == 0) {
-      const double cnt = (double)hw * (double)cpg;
-      const double Kg = (double)to_f32<T>(xs[g * cpg]);
-      const double dm = t1 / cnt;
-      double var = t2 / cnt - dm * dm;
-      if (var < 0.0) var = 0.0;
-      stats[(n * groups + g) * 2 + 0] = (float)(Kg + dm);
-      stats[(n * groups + g) * 2 + 1] = (float)(1.0 / sqrt(var + (double)eps));
-    }
+  for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
+    double* a = acc + (n * groups + g) * 2;
+    const double t1 = __ldcg(a), t2 = __ldcg(a + 1);
+    const double cnt = (double)hw * (double)cpg;
+    const double Kg = (double)to_f32<T>(xs[g * cpg]);
+    const double dm = t1 / cnt;
+    double var = t2 / cnt - dm * dm;
+    if (var < 0.0) var = 0.0;
+    stats[(n * groups + g) * 2 + 0] = (float)(Kg + dm);
+    stats[(n * groups + g) * 2 + 1] = (float)(1.0 / sqrt(var + (double)eps));
+    a[0] = 0.0;   // accumulators and counter are back at zero for the next launch / graph replay
+    a[1] = 0.0;
   }
-  if (threadIdx.x == 0) counters[n] = 0u;  // ready for the next launch / graph replay
+  if (threadIdx.x == 0) counters[n] = 0u;
 }
 
 template <typename T, bool SILU>
-__global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
-                                const float* __restrict__ add_nc,
-                                const float* __restrict__ stats, const float* __restrict__ gamma,
-                                const float* __restrict__ beta, int64_t hw, int64_t c,
-                                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int rpp) {
+__global__ void __launch_bounds__(kMaxThreads)
+gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
+                const float* __restrict__ add_nc, const float* __restrict__ stats,
+                const float* __restrict__ gamma, const float* __restrict__ beta, int64_t hw, int64_t c,
+                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int rpp) {
   const int64_t n = blockIdx.y;
   const int64_t chunk = blockIdx.x;
   const int cv = (int)(c / 8);
   const int v = threadIdx.x % cv;
   const int r = threadIdx.x / cv;
   const int64_t c0 = (int64_t)v * 8;
+  const T* xs = x + n * hw * c;
+  T* ys = y + n * hw * c;
+  const int64_t p0 = chunk * rows_per_chunk + r;
+  const int64_t p1 = min(hw, chunk * rows_per_chunk + rows_per_chunk);
+  Raw8<T> buf[kRowsPerThread];
+#pragma unroll
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const int64_t p = p0 + (int64_t)u * rpp;
+    if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
+  }
   float A[8], B[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -197,39 +220,20 @@ __global__ void gn_apply_kernel(const T* x, T* y,  // may alias: same-thread rea
     A[j] = ga * rstd;
     B[j] = be + (ad - mean) * A[j];
   }
-  const T* xs = x + n * hw * c;
-  T* ys = y + n * hw * c;
-  const int64_t p0 = chunk * rows_per_chunk;
-  const int64_t p1 = min(hw, p0 + rows_per_chunk);
-  int64_t p = p0 + r;
-  for (; p + rpp < p1; p += 2 * rpp) {
-    float a[8], b[8];
-    Vec8<T>::load(xs + p * c + c0, a);
-    Vec8<T>::load(xs + (p + rpp) * c + c0, b);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float t = fmaf(a[j], A[j], B[j]);
-      float u = fmaf(b[j], A[j], B[j]);
-      if (SILU) {
-        t = t / (1.f + __expf(-t));
-        u = u / (1.f + __expf(-u));
+  for (int u = 0; u < kRowsPerThread; ++u) {
+    const int64_t p = p0 + (int64_t)u * rpp;
+    if (p < p1) {
+      float a[8];
+      unpack<T>(buf[u], a);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float t = fmaf(a[j], A[j], B[j]);
+        if (SILU) t = t / (1.f + __expf(-t));
+        a[j] = t;
       }
-      a[j] = t;
-      b[j] = u;
+      Vec8<T>::store(ys + p * c + c0, a);
     }
-    Vec8<T>::store(ys + p * c + c0, a);
-    Vec8<T>::store(ys + (p + rpp) * c + c0, b);
-  }
-  for (; p < p1; p += rpp) {
-    float a[8];
-    Vec8<T>::load(xs + p * c + c0, a);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float t = fmaf(a[j], A[j], B[j]);
-      if (SILU) t = t / (1.f + __expf(-t));
-      a[j] = t;
-    }
-    Vec8<T>::store(ys + p * c + c0, a);
   }
 }
 
@@ -240,14 +244,14 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, cons
   T* y = static_cast<T*>(yv);
   GnShape s = gn_shape(n, hw, c, groups);
   unsigned int* counters = static_cast<unsigned int*>(ws);
-  float* stats = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + 256);
-  float* partial = stats + n * groups * 2;
+  double* acc = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + 256);
+  float* stats = reinterpret_cast<float*>(acc + n * groups * 2);
   dim3 grid((unsigned)s.chunks, (unsigned)n);
   size_t smem = (size_t)s.rpp * c * 2 * sizeof(float);
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(gn_stats_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
-  gn_stats_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, partial, stats, counters, hw, c, groups, s.cpg,
+  gn_stats_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, acc, stats, counters, hw, c, groups, s.cpg,
                                                     s.rows_per_chunk, s.chunks, s.rpp, eps);
   if (int rc = check_launch("gn_stats_kernel")) return rc;
   if (silu)
@@ -262,8 +266,9 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, cons
 }  // namespace
 
 size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
-  GnShape s = gn_shape(n, hw, c, groups);
-  return 256 + (size_t)(n * groups * 2 + n * s.chunks * groups * 2) * sizeof(float);
+  (void)hw;
+  (void)c;
+  return 256 + (size_t)(n * groups * 2) * (sizeof(double) + sizeof(float));
 }
 
 int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc, int64_t n,
