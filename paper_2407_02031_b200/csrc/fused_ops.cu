@@ -16,21 +16,38 @@
 namespace sdb {
 namespace {
 
+// Each thread owns kGegluVec 8-element vectors spaced one grid apart and issues
+// all of their loads (value and gate halves) before computing any.
+constexpr int kGegluVec = 4;
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int64_t rows, int64_t f) {
   const int64_t vec_per_row = f / 8;
   const int64_t total = rows * vec_per_row;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / vec_per_row;
-    const int64_t c = (i % vec_per_row) * 8;
-    float h[8], g[8];
-    Vec8<T>::load(proj + m * 2 * f + c, h);
-    Vec8<T>::load(proj + m * 2 * f + f + c, g);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += stride * kGegluVec) {
+    float h[kGegluVec][8], g[kGegluVec][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = h[j] * (0.5f * g[j] * (1.f + erff(g[j] * 0.70710678118654752f)));
-    Vec8<T>::store(out + m * f + c, h);
+    for (int u = 0; u < kGegluVec; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        const int64_t m = i / vec_per_row, c = (i % vec_per_row) * 8;
+        Vec8<T>::load(proj + m * 2 * f + c, h[u]);
+        Vec8<T>::load(proj + m * 2 * f + f + c, g[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kGegluVec; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < total) {
+        const int64_t m = i / vec_per_row, c = (i % vec_per_row) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          h[u][j] = h[u][j] * (0.5f * g[u][j] * (1.f + erff(g[u][j] * 0.70710678118654752f)));
+        Vec8<T>::store(out + m * f + c, h[u]);
+      }
+    }
   }
 }
 
@@ -129,7 +146,7 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
 template <typename T>
 int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t st) {
   const int64_t total = rows * (f / 8);
-  int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 16);
+  int64_t grid = std::min<int64_t>((total + 256 * kGegluVec - 1) / (256 * kGegluVec), (int64_t)kNumSMs * 8);
   geglu_kernel<T><<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, st>>>(static_cast<const T*>(proj),
                                                                          static_cast<T*>(out), rows, f);
   return check_launch("geglu_kernel");
