@@ -86,7 +86,13 @@ GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups) {
   s.cpg = c / groups;
   s.rpp = (int)std::max<int64_t>(1, 256 / s.cv);
   s.threads = (int)(s.cv * s.rpp);
-  s.rows_per_chunk = (int64_t)s.rpp * kRowsPerThread;
+  // ~2 CTAs per SM over the whole batch; each thread walks its chunk in
+  // batches of kRowsPerThread rows (all loads of a batch in flight), so the
+  // per-CTA fixed costs (shift, reduction, accumulator atomics) amortise
+  const int64_t batch = (int64_t)s.rpp * kRowsPerThread;
+  const int64_t want = std::max<int64_t>(1, (2 * kNumSMs + n - 1) / n);
+  s.chunks = std::max<int64_t>(1, std::min<int64_t>(want, (hw + batch - 1) / batch));
+  s.rows_per_chunk = (hw + s.chunks - 1) / s.chunks;
   s.chunks = (hw + s.rows_per_chunk - 1) / s.rows_per_chunk;
   return s;
 }
@@ -110,13 +116,6 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, doubl
   const int64_t p0 = chunk * rows_per_chunk + r;
   const int64_t p1 = min(hw, chunk * rows_per_chunk + rows_per_chunk);
 
-  // issue every load of this thread first
-  Raw8<T> buf[kRowsPerThread];
-#pragma unroll
-  for (int u = 0; u < kRowsPerThread; ++u) {
-    const int64_t p = p0 + (int64_t)u * rpp;
-    if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
-  }
   // d = x' - K_g = x - (K_g - add_c)
   float K[8];
 #pragma unroll
@@ -127,16 +126,25 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, doubl
   float s1[8], s2[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) { s1[j] = 0.f; s2[j] = 0.f; }
+  for (int64_t pb = p0; pb < p1; pb += (int64_t)rpp * kRowsPerThread) {
+    // every load of the batch first
+    Raw8<T> buf[kRowsPerThread];
 #pragma unroll
-  for (int u = 0; u < kRowsPerThread; ++u) {
-    if (p0 + (int64_t)u * rpp < p1) {
-      float a[8];
-      unpack<T>(buf[u], a);
+    for (int u = 0; u < kRowsPerThread; ++u) {
+      const int64_t p = pb + (int64_t)u * rpp;
+      if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
+    }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float d = a[j] - K[j];
-        s1[j] += d;
-        s2[j] = fmaf(d, d, s2[j]);
+    for (int u = 0; u < kRowsPerThread; ++u) {
+      if (pb + (int64_t)u * rpp < p1) {
+        float a[8];
+        unpack<T>(buf[u], a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = a[j] - K[j];
+          s1[j] += d;
+          s2[j] = fmaf(d, d, s2[j]);
+        }
       }
     }
   }
@@ -201,12 +209,6 @@ gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
   T* ys = y + n * hw * c;
   const int64_t p0 = chunk * rows_per_chunk + r;
   const int64_t p1 = min(hw, chunk * rows_per_chunk + rows_per_chunk);
-  Raw8<T> buf[kRowsPerThread];
-#pragma unroll
-  for (int u = 0; u < kRowsPerThread; ++u) {
-    const int64_t p = p0 + (int64_t)u * rpp;
-    if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
-  }
   float A[8], B[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -220,19 +222,27 @@ gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
     A[j] = ga * rstd;
     B[j] = be + (ad - mean) * A[j];
   }
+  for (int64_t pb = p0; pb < p1; pb += (int64_t)rpp * kRowsPerThread) {
+    Raw8<T> buf[kRowsPerThread];
 #pragma unroll
-  for (int u = 0; u < kRowsPerThread; ++u) {
-    const int64_t p = p0 + (int64_t)u * rpp;
-    if (p < p1) {
-      float a[8];
-      unpack<T>(buf[u], a);
+    for (int u = 0; u < kRowsPerThread; ++u) {
+      const int64_t p = pb + (int64_t)u * rpp;
+      if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
+    }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float t = fmaf(a[j], A[j], B[j]);
-        if (SILU) t = t / (1.f + __expf(-t));
-        a[j] = t;
+    for (int u = 0; u < kRowsPerThread; ++u) {
+      const int64_t p = pb + (int64_t)u * rpp;
+      if (p < p1) {
+        float a[8];
+        unpack<T>(buf[u], a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float t = fmaf(a[j], A[j], B[j]);
+          if (SILU) t = t / (1.f + __expf(-t));
+          a[j] = t;
+        }
+        Vec8<T>::store(ys + p * c + c0, a);
       }
-      Vec8<T>::store(ys + p * c + c0, a);
     }
   }
 }

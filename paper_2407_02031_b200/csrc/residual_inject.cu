@@ -28,15 +28,16 @@ struct ResArgs {
   float scale[kMaxRes];
 };
 
+// 32-bit index math (callers guarantee pixels * (ch + cs) / 8 < 2^31): the
+// emulated 64-bit division per vector cost more than the memory traffic.
 template <typename T, int NR>
 __global__ void __launch_bounds__(256)
 residual_inject_kernel(T* out, const T* __restrict__ hidden,
                        const T* skip, ResArgs<T> ra, int n_res,
                        int64_t pixels, int64_t ch, int64_t cs) {
-  const int64_t vh = ch / 8, vs = cs / 8, vrow = vh + vs;
-  const int64_t total = pixels * vrow;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const uint32_t vh = (uint32_t)(ch / 8), vs = (uint32_t)(cs / 8), vrow = vh + vs;
+  const uint32_t total = (uint32_t)(pixels * vrow);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int64_t p = i / vrow;
     const int64_t v = i % vrow;
     float a[8];
@@ -70,6 +71,8 @@ int run_inject(void* out, const void* hidden, const void* skip, const void* cons
     ra.scale[i] = i < n_res ? scales[i] : 0.f;
   }
   const int64_t total = pixels * ((ch + cs) / 8);
+  if (total + (int64_t)kNumSMs * 8 * 256 >= (int64_t)INT32_MAX)
+    return fail(SDB_EINVAL, "residual_inject: tensor too large (>= 2^31 vectors)");
   int64_t grid = (total + 255) / 256;
   const int64_t cap = (int64_t)kNumSMs * 8;
   if (grid > cap) grid = cap;
