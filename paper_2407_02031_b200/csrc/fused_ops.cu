@@ -70,13 +70,26 @@ __global__ void __launch_bounds__(128)
 add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* __restrict__ gamma,
                      const T* __restrict__ beta, int64_t rows, int64_t c, float eps) {
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  constexpr bool kHalf = sizeof(T) == 2;
+  // gamma / beta are the same for every row: loaded once per warp
+  uint4 gq[NV], bq[NV];
+  if constexpr (kHalf) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int64_t col = (int64_t)(k * 32 + lane) * 8;
+      if (col < c) {
+        gq[k] = __ldg(reinterpret_cast<const uint4*>(gamma + col));
+        bq[k] = __ldg(reinterpret_cast<const uint4*>(beta + col));
+      }
+    }
+  }
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps_total) {
   T* xr = x + row * c;
   float v[NV][8];
   float sum = 0.f;
-  uint4 xq[NV], dq[NV], gq[NV], bq[NV];
-  constexpr bool kHalf = sizeof(T) == 2;
+  uint4 xq[NV], dq[NV];
   if constexpr (kHalf) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -84,8 +97,6 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
       if (col < c) {
         xq[k] = *reinterpret_cast<const uint4*>(xr + col);
         if (d != nullptr) dq[k] = *reinterpret_cast<const uint4*>(d + row * c + col);
-        gq[k] = __ldg(reinterpret_cast<const uint4*>(gamma + col));
-        bq[k] = __ldg(reinterpret_cast<const uint4*>(beta + col));
       }
     }
   }
@@ -143,6 +154,7 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
       Vec8<T>::store(y + row * c + col, o);
     }
   }
+  }  // rows of this warp
 }
 
 template <typename T>
@@ -161,7 +173,9 @@ int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t
 template <typename T>
 int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                float eps, cudaStream_t st) {
-  const unsigned grid = (unsigned)((rows + 3) / 4);   // 4 rows (warps) per 128-thread CTA
+  // 4 warps per 128-thread CTA, each warp walks rows grid-stride (gamma / beta
+  // loaded once); ~8 CTAs per SM
+  const unsigned grid = (unsigned)std::min<int64_t>((rows + 3) / 4, (int64_t)kNumSMs * 8);
   T* xp = static_cast<T*>(x);
   const T* dp = static_cast<const T*>(d);
   T* yp = static_cast<T*>(y);
