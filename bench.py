@@ -101,8 +101,16 @@ def dist_setup(n_gpus):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("SDB_SHARE_ONE_GPU") == "1":
+            # test harness only: every rank on cuda:0 over gloo (device buffers
+            # staged through host memory by caas.CaaSProtocol) — exercises the
+            # multi-GPU control path on a 1-GPU box; numbers are meaningless
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -119,9 +127,14 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch.distributed as dist
     if world == 1:
         return x
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_red_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def _red_device() -> str:
+    import torch.distributed as dist
+    return "cpu" if dist.get_backend() == "gloo" else "cuda"
 
 
 # ---------------------------------------------------------------------------
@@ -264,7 +277,8 @@ def run_caas(args, world, rank, local):
     # per-image latency of group bases (not solos) for p50, gathered to rank 0
     import torch.distributed as dist
     lat = torch.tensor([statistics.median(per_image) if (role == "base" or (role == "solo" and
-                        all(not g.services for g in layout.groups))) else 0.0], device="cuda", dtype=torch.float64)
+                        all(not g.services for g in layout.groups))) else 0.0], device=_red_device(),
+                       dtype=torch.float64)
     dist.all_reduce(lat, op=dist.ReduceOp.MAX)
     graph_launches = 0
     if role == "base":

@@ -20,30 +20,29 @@ namespace {
 // all of their loads (value and gate halves) before computing any.
 constexpr int kGegluVec = 4;
 
-// IDX: 32-bit index math when the launch has < 2^31 vectors (64-bit integer
-// division is emulated and dominated this kernel), 64-bit otherwise.
-template <typename T, typename IDX>
-__global__ void __launch_bounds__(256)
+// 2-d mapping, no integer division: blockIdx.x picks a 8*blockDim-wide column
+// slice of the row, each thread walks rows grid-stride (kGegluVec rows per
+// round, all loads issued first).
+template <typename T>
+__global__ void __launch_bounds__(128)
 geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int64_t rows, int64_t f) {
-  const IDX vec_per_row = (IDX)(f / 8);
-  const IDX total = (IDX)(rows * (f / 8));
-  const IDX stride = (IDX)gridDim.x * blockDim.x;
-  for (IDX i0 = (IDX)blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += stride * kGegluVec) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c >= f) return;
+  const int64_t rstride = gridDim.y;
+  for (int64_t m0 = blockIdx.y; m0 < rows; m0 += rstride * kGegluVec) {
     float h[kGegluVec][8], g[kGegluVec][8];
 #pragma unroll
     for (int u = 0; u < kGegluVec; ++u) {
-      const IDX i = i0 + u * stride;
-      if (i < total) {
-        const int64_t m = i / vec_per_row, c = (int64_t)(i % vec_per_row) * 8;
+      const int64_t m = m0 + u * rstride;
+      if (m < rows) {
         Vec8<T>::load(proj + m * 2 * f + c, h[u]);
         Vec8<T>::load(proj + m * 2 * f + f + c, g[u]);
       }
     }
 #pragma unroll
     for (int u = 0; u < kGegluVec; ++u) {
-      const IDX i = i0 + u * stride;
-      if (i < total) {
-        const int64_t m = i / vec_per_row, c = (int64_t)(i % vec_per_row) * 8;
+      const int64_t m = m0 + u * rstride;
+      if (m < rows) {
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           h[u][j] = h[u][j] * (0.5f * g[u][j] * (1.f + erff(g[u][j] * 0.70710678118654752f)));
@@ -159,14 +158,12 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
 
 template <typename T>
 int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t st) {
-  const int64_t total = rows * (f / 8);
-  int64_t grid = std::min<int64_t>((total + 256 * kGegluVec - 1) / (256 * kGegluVec), (int64_t)kNumSMs * 8);
-  if (total + (int64_t)256 * kNumSMs * 8 * kGegluVec < (int64_t)INT32_MAX)
-    geglu_kernel<T, uint32_t><<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, st>>>(
-        static_cast<const T*>(proj), static_cast<T*>(out), rows, f);
-  else
-    geglu_kernel<T, int64_t><<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, st>>>(
-        static_cast<const T*>(proj), static_cast<T*>(out), rows, f);
+  const unsigned gx = (unsigned)((f / 8 + 127) / 128);
+  // ~16 CTAs of 128 threads per SM in flight overall
+  const int64_t want_y = std::max<int64_t>(1, (int64_t)kNumSMs * 16 / gx);
+  const unsigned gy = (unsigned)std::min<int64_t>(std::min<int64_t>(want_y, (rows + kGegluVec - 1) / kGegluVec), 65535);
+  geglu_kernel<T><<<dim3(gx, std::max(gy, 1u)), 128, 0, st>>>(static_cast<const T*>(proj), static_cast<T*>(out),
+                                                               rows, f);
   return check_launch("geglu_kernel");
 }
 

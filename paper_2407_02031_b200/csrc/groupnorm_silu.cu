@@ -157,15 +157,30 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, doubl
   // per-group partials of this chunk go straight into fp64 accumulators: the
   // partials are fp32 sums of similar magnitude, so their fp64 sum is exact in
   // practice and the mean / rstd rounded to fp32 do not depend on arrival order
-  for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
-    float t1 = 0.f, t2 = 0.f;
-    for (int rr = 0; rr < rpp; ++rr)
-      for (int64_t ch = g * cpg; ch < (g + 1) * cpg; ++ch) {
-        t1 += red[((int64_t)rr * c + ch) * 2 + 0];
-        t2 += red[((int64_t)rr * c + ch) * 2 + 1];
+  // one warp per group: lanes sum the group's (rpp x cpg) partials, shuffle-reduce
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int per_group = rpp * (int)cpg;
+    if (warp < nwarps) {
+      for (int64_t g = warp; g < groups; g += nwarps) {
+        float t1 = 0.f, t2 = 0.f;
+        for (int e = lane; e < per_group; e += 32) {
+          const int rr = e / (int)cpg;
+          const int64_t ch = g * cpg + e % (int)cpg;
+          t1 += red[((int64_t)rr * c + ch) * 2 + 0];
+          t2 += red[((int64_t)rr * c + ch) * 2 + 1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          t1 += __shfl_xor_sync(0xffffffffu, t1, o);
+          t2 += __shfl_xor_sync(0xffffffffu, t2, o);
+        }
+        if (lane == 0) {
+          atomicAdd(acc + (n * groups + g) * 2 + 0, (double)t1);
+          atomicAdd(acc + (n * groups + g) * 2 + 1, (double)t2);
+        }
       }
-    atomicAdd(acc + (n * groups + g) * 2 + 0, (double)t1);
-    atomicAdd(acc + (n * groups + g) * 2 + 1, (double)t2);
+    }
   }
   // ---- the last CTA of this sample finalises (no extra launch) ----
   __threadfence();
@@ -238,7 +253,7 @@ gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           float t = fmaf(a[j], A[j], B[j]);
-          if (SILU) t = t / (1.f + __expf(-t));
+          if (SILU) t = __fdividef(t, 1.f + __expf(-t));   // -> 0 as t -> -inf
           a[j] = t;
         }
         Vec8<T>::store(ys + p * c + c0, a);
