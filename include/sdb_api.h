@@ -146,8 +146,10 @@ int sdb_lora_tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max,
  * (addonsim/model.py:66-70 unet_opt_submultipliers[2] = 1.072; paper
  * PAPER.md:572-576).  x, y: [N, HW, C] (channels innermost), dtype `dtype`;
  * gamma, beta: fp32 [C].  `workspace` must hold sdb_groupnorm_workspace()
- * bytes and be ZERO-initialised once (per-sample completion counters and
- * fp64 group accumulators that every launch leaves at zero); calls sharing a
+ * bytes (a constant, ~130 KB) and be ZERO-initialised once: it holds an epoch
+ * word and two fp64 accumulator banks that the launches themselves recycle
+ * (each launch zeroes the bank the previous one used), so it stays valid
+ * across launches and CUDA-graph replays with any shape; calls sharing a
  * workspace must be ordered on one stream.  y may alias x.
  * ======================================================================== */
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);

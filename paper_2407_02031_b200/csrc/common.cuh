@@ -85,6 +85,94 @@ template <> struct Vec8<__half> {
   static __device__ __forceinline__ void store(__half* p, const float (&v)[8]) { Vec8Half<int>::store(p, v); }
 };
 
+// ---- 8 elements held as raw registers until consumed ----------------------
+// (loads issued early without unpacking: 4 registers per 16-bit vector)
+template <typename T> struct Raw8 { uint4 u; };
+template <> struct Raw8<float> { float4 a, b; };
+
+template <typename T>
+__device__ __forceinline__ Raw8<T> load_raw(const T* p) {
+  Raw8<T> r;
+  r.u = *reinterpret_cast<const uint4*>(p);
+  return r;
+}
+template <>
+__device__ __forceinline__ Raw8<float> load_raw<float>(const float* p) {
+  Raw8<float> r;
+  r.a = *reinterpret_cast<const float4*>(p);
+  r.b = *reinterpret_cast<const float4*>(p + 4);
+  return r;
+}
+template <typename T>
+__device__ __forceinline__ void store_raw(T* p, const Raw8<T>& r) {
+  *reinterpret_cast<uint4*>(p) = r.u;
+}
+template <>
+__device__ __forceinline__ void store_raw<float>(float* p, const Raw8<float>& r) {
+  *reinterpret_cast<float4*>(p) = r.a;
+  *reinterpret_cast<float4*>(p + 4) = r.b;
+}
+template <typename T>
+__device__ __forceinline__ void unpack(const Raw8<T>& r, float (&v)[8]) {
+  const T* h = reinterpret_cast<const T*>(&r.u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = to_f32<T>(h[i]);
+}
+template <>
+__device__ __forceinline__ void unpack<float>(const Raw8<float>& r, float (&v)[8]) {
+  v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w;
+  v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
+}
+
+// element pair i (0..3) of a raw vector as float2, and back (round to nearest)
+template <typename T> __device__ __forceinline__ float2 get_pair(const Raw8<T>& r, int i);
+template <> __device__ __forceinline__ float2 get_pair<__nv_bfloat16>(const Raw8<__nv_bfloat16>& r, int i) {
+  const uint32_t u = (&r.u.x)[i];
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+template <> __device__ __forceinline__ float2 get_pair<__half>(const Raw8<__half>& r, int i) {
+  const uint32_t u = (&r.u.x)[i];
+  return __half22float2(*reinterpret_cast<const __half2*>(&u));
+}
+template <> __device__ __forceinline__ float2 get_pair<float>(const Raw8<float>& r, int i) {
+  const float4& q = i < 2 ? r.a : r.b;
+  return (i & 1) ? make_float2(q.z, q.w) : make_float2(q.x, q.y);
+}
+template <typename T> __device__ __forceinline__ void set_pair(Raw8<T>& r, int i, float2 v);
+template <> __device__ __forceinline__ void set_pair<__nv_bfloat16>(Raw8<__nv_bfloat16>& r, int i, float2 v) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(v.x, v.y);
+  (&r.u.x)[i] = *reinterpret_cast<uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ void set_pair<__half>(Raw8<__half>& r, int i, float2 v) {
+  __half2 h = __floats2half2_rn(v.x, v.y);
+  (&r.u.x)[i] = *reinterpret_cast<uint32_t*>(&h);
+}
+template <> __device__ __forceinline__ void set_pair<float>(Raw8<float>& r, int i, float2 v) {
+  float4& q = i < 2 ? r.a : r.b;
+  if (i & 1) { q.z = v.x; q.w = v.y; } else { q.x = v.x; q.y = v.y; }
+}
+
+// ---- packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2 / FADD2: two lanes of
+// work per issue slot; each lane rounds exactly like the scalar op) ----------
+__device__ __forceinline__ uint64_t f2_bits(float2 a) { return *reinterpret_cast<uint64_t*>(&a); }
+__device__ __forceinline__ float2 f2_from(uint64_t b) { return *reinterpret_cast<float2*>(&b); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+  return f2_from(d);
+}
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+  return f2_from(d);
+}
+__device__ __forceinline__ float2 f2s(float s) { return make_float2(s, s); }
+
 inline int dtype_size(int dt) {
   switch (dt) {
     case SDB_F32: return 4;

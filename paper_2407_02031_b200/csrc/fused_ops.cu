@@ -20,158 +20,172 @@ namespace {
 // all of their loads (value and gate halves) before computing any.
 constexpr int kGegluVec = 4;
 
+// GELU(g) = g * Phi(g) on a pair of values with packed fp32x2 arithmetic.
+// Phi comes from erf by Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7 in erf,
+// i.e. at fp32 rounding level and far below the bf16 output ulp), rearranged so
+// that no branch is needed and the negative tail has no cancellation:
+//   GELU(g) = 0.5 (g + |g|) - 0.5 |g| P(t) exp(-g^2 / 2),  t = 1 / (1 + p |g| / sqrt 2)
+// Two MUFU ops (rcp, ex2) and ~11 packed instructions per pair instead of the
+// libdevice erff's ~25 scalar instructions and two divergent paths per value.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float2 gelu2(float2 g) {
+  constexpr float kP = 0.3275911f * 0.70710678118654752f;     // p / sqrt(2)
+  // A&S coefficients a1..a5 scaled by -0.5
+  constexpr float b1 = -0.5f * 0.254829592f, b2 = -0.5f * -0.284496736f, b3 = -0.5f * 1.421413741f,
+                  b4 = -0.5f * -1.453152027f, b5 = -0.5f * 1.061405429f;
+  constexpr float kE = -0.72134752044448170f;                 // -log2(e) / 2
+  float2 a = make_float2(fabsf(g.x), fabsf(g.y));
+  // the tail term is 0 beyond |g| ~ 13; the clamp keeps inf * 0 out of it
+  const float2 ac = make_float2(fminf(a.x, 64.f), fminf(a.y, 64.f));
+  const float2 den = f2fma(ac, f2s(kP), f2s(1.f));
+  const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+  float2 q = f2fma(t, f2s(b5), f2s(b4));
+  q = f2fma(t, q, f2s(b3));
+  q = f2fma(t, q, f2s(b2));
+  q = f2fma(t, q, f2s(b1));
+  q = f2mul(t, q);                                            // -0.5 P(t)
+  const float2 w = f2mul(f2mul(ac, ac), f2s(kE));
+  const float2 e = make_float2(ex2_approx(w.x), ex2_approx(w.y));
+  const float2 m = f2mul(f2mul(ac, e), q);                    // -0.5 |g| P(t) e^{-g^2/2}
+  return f2fma(f2add(g, a), f2s(0.5f), m);
+}
+
 // 2-d mapping, no integer division: blockIdx.x picks a 8*blockDim-wide column
 // slice of the row, each thread walks rows grid-stride (kGegluVec rows per
-// round, all loads issued first).
+// round, all loads issued first, kept as raw registers until consumed).
+// 32-bit offsets: the host checks rows * 2f < 2^31.
 template <typename T>
 __global__ void __launch_bounds__(128)
-geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int64_t rows, int64_t f) {
-  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int rows, int f) {
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c >= f) return;
-  const int64_t rstride = gridDim.y;
-  for (int64_t m0 = blockIdx.y; m0 < rows; m0 += rstride * kGegluVec) {
-    float h[kGegluVec][8], g[kGegluVec][8];
+  const T* src = proj + c;
+  T* dst = out + c;
+  const int rstride = gridDim.y;
+  for (int m0 = blockIdx.y; m0 < rows; m0 += rstride * kGegluVec) {
+    Raw8<T> h[kGegluVec], g[kGegluVec];
 #pragma unroll
     for (int u = 0; u < kGegluVec; ++u) {
-      const int64_t m = m0 + u * rstride;
+      const int m = m0 + u * rstride;
       if (m < rows) {
-        Vec8<T>::load(proj + m * 2 * f + c, h[u]);
-        Vec8<T>::load(proj + m * 2 * f + f + c, g[u]);
+        h[u] = load_raw<T>(src + (unsigned)m * (unsigned)(2 * f));
+        g[u] = load_raw<T>(src + (unsigned)m * (unsigned)(2 * f) + f);
       }
     }
 #pragma unroll
     for (int u = 0; u < kGegluVec; ++u) {
-      const int64_t m = m0 + u * rstride;
+      const int m = m0 + u * rstride;
       if (m < rows) {
+        Raw8<T> o;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          h[u][j] = h[u][j] * (0.5f * g[u][j] * (1.f + erff(g[u][j] * 0.70710678118654752f)));
-        Vec8<T>::store(out + m * f + c, h[u]);
+        for (int i = 0; i < 4; ++i) set_pair<T>(o, i, f2mul(get_pair<T>(h[u], i), gelu2(get_pair<T>(g[u], i))));
+        store_raw<T>(dst + (unsigned)m * (unsigned)f, o);
       }
     }
   }
 }
 
-// NV = vectors of 8 per lane (C = 256 * NV max per warp pass)
-template <typename T>
-__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
-  if constexpr (sizeof(T) == 2) {
-    const T* h = reinterpret_cast<const T*>(&u);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = to_f32<T>(h[i]);
-  }
-}
-
-// 16-bit T: every load of the row (x, d, gamma, beta) is issued before any is
-// consumed — one memory round trip per row instead of three dependent ones.
+// One warp per row, NV = vectors of 8 per lane (C <= 256 * NV).  Every load of
+// the row (x, d) is issued before any is consumed; the rounded residual x + d
+// is kept as raw T registers (it is stored in T, so nothing is lost) and both
+// reductions and the output read it back — half the registers of an fp32 copy,
+// so more rows are in flight per SM.  gamma / beta are re-read per row from L1.
 template <typename T, int NV>
 __global__ void __launch_bounds__(128)
 add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* __restrict__ gamma,
-                     const T* __restrict__ beta, int64_t rows, int64_t c, float eps) {
+                     const T* __restrict__ beta, int rows, int c, float eps) {
   const int lane = threadIdx.x & 31;
-  constexpr bool kHalf = sizeof(T) == 2;
-  // gamma / beta are the same for every row: loaded once per warp
-  uint4 gq[NV], bq[NV];
-  if constexpr (kHalf) {
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += warps_total) {
+    const size_t base = (size_t)row * c;
+    Raw8<T> vq[NV], dq[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const int64_t col = (int64_t)(k * 32 + lane) * 8;
+      const int col = (k * 32 + lane) * 8;
       if (col < c) {
-        gq[k] = __ldg(reinterpret_cast<const uint4*>(gamma + col));
-        bq[k] = __ldg(reinterpret_cast<const uint4*>(beta + col));
+        vq[k] = load_raw<T>(x + base + col);
+        if (d != nullptr) dq[k] = load_raw<T>(d + base + col);
       }
     }
-  }
-  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
-       row += warps_total) {
-  T* xr = x + row * c;
-  float v[NV][8];
-  float sum = 0.f;
-  uint4 xq[NV], dq[NV];
-  if constexpr (kHalf) {
+    float2 s = f2s(0.f);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      const int64_t col = (int64_t)(k * 32 + lane) * 8;
+      const int col = (k * 32 + lane) * 8;
       if (col < c) {
-        xq[k] = *reinterpret_cast<const uint4*>(xr + col);
-        if (d != nullptr) dq[k] = *reinterpret_cast<const uint4*>(d + row * c + col);
+        if (d != nullptr) {
+          // the residual stream is stored in T: round once, normalise the stored value
+#pragma unroll
+          for (int i = 0; i < 4; ++i) set_pair<T>(vq[k], i, f2add(get_pair<T>(vq[k], i), get_pair<T>(dq[k], i)));
+          store_raw<T>(x + base + col, vq[k]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s = f2add(s, get_pair<T>(vq[k], i));
+      }
+    }
+    float sum = s.x + s.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum / (float)c;
+    const float2 nm = f2s(-mean);
+    float2 q = f2s(0.f);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < c) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 t = f2add(get_pair<T>(vq[k], i), nm);
+          q = f2fma(t, t, q);
+        }
+      }
+    }
+    float sq = q.x + q.y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    const float2 rstd = f2s(rsqrtf(sq / (float)c + eps));
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int col = (k * 32 + lane) * 8;
+      if (col < c) {
+        const Raw8<T> gq = load_raw<T>(gamma + col), bq = load_raw<T>(beta + col);
+        Raw8<T> o;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 t = f2mul(f2add(get_pair<T>(vq[k], i), nm), rstd);
+          set_pair<T>(o, i, f2fma(t, get_pair<T>(gq, i), get_pair<T>(bq, i)));
+        }
+        store_raw<T>(y + base + col, o);
       }
     }
   }
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int64_t col = (int64_t)(k * 32 + lane) * 8;
-    if (col < c) {
-      if constexpr (kHalf) unpack8<T>(xq[k], v[k]); else Vec8<T>::load(xr + col, v[k]);
-      if (d != nullptr) {
-        float dv[8];
-        if constexpr (kHalf) unpack8<T>(dq[k], dv); else Vec8<T>::load(d + row * c + col, dv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[k][j] += dv[j];
-        // the residual stream is stored in T: round once, normalise the stored value
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[k][j] = to_f32<T>(from_f32<T>(v[k][j]));
-        Vec8<T>::store(xr + col, v[k]);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) sum += v[k][j];
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-  const float mean = sum / (float)c;
-  float sq = 0.f;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int64_t col = (int64_t)(k * 32 + lane) * 8;
-    if (col < c) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float t = v[k][j] - mean;
-        sq = fmaf(t, t, sq);
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-  const float rstd = rsqrtf(sq / (float)c + eps);
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int64_t col = (int64_t)(k * 32 + lane) * 8;
-    if (col < c) {
-      float ga[8], be[8], o[8];
-      if constexpr (kHalf) {
-        unpack8<T>(gq[k], ga);
-        unpack8<T>(bq[k], be);
-      } else {
-        Vec8<T>::load(gamma + col, ga);
-        Vec8<T>::load(beta + col, be);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = fmaf((v[k][j] - mean) * rstd, ga[j], be[j]);
-      Vec8<T>::store(y + row * c + col, o);
-    }
-  }
-  }  // rows of this warp
 }
 
 template <typename T>
 int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t st) {
+  if (rows * 2 * f >= (int64_t)INT32_MAX) return fail(SDB_EINVAL, "geglu: input must hold < 2^31 elements");
   const unsigned gx = (unsigned)((f / 8 + 127) / 128);
   // ~16 CTAs of 128 threads per SM in flight overall
   const int64_t want_y = std::max<int64_t>(1, (int64_t)kNumSMs * 16 / gx);
   const unsigned gy = (unsigned)std::min<int64_t>(std::min<int64_t>(want_y, (rows + kGegluVec - 1) / kGegluVec), 65535);
   geglu_kernel<T><<<dim3(gx, std::max(gy, 1u)), 128, 0, st>>>(static_cast<const T*>(proj), static_cast<T*>(out),
-                                                               rows, f);
+                                                               (int)rows, (int)f);
   return check_launch("geglu_kernel");
 }
 
 template <typename T>
 int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                float eps, cudaStream_t st) {
-  // 4 warps per 128-thread CTA, each warp walks rows grid-stride (gamma / beta
-  // loaded once); ~8 CTAs per SM
+  if (rows >= (int64_t)INT32_MAX) return fail(SDB_EINVAL, "add_layernorm: too many rows");
+  // 4 warps per 128-thread CTA, each warp walks rows grid-stride; ~8 CTAs per SM
   const unsigned grid = (unsigned)std::min<int64_t>((rows + 3) / 4, (int64_t)kNumSMs * 8);
   T* xp = static_cast<T*>(x);
   const T* dp = static_cast<const T*>(d);

@@ -9,305 +9,353 @@
 //
 // Layout: NHWC (torch channels_last) because the convolutions around every
 // GN site run channels_last on cuDNN; a group is C/G channels of every pixel,
-// i.e. a strided set.  Thread mapping keeps the 16-byte vector lanes fixed on
-// channels: blockDim = CV * rpp with CV = C/8 vector columns and rpp pixel
-// rows per pass, so each thread always owns the same 8 channels and
-// accumulates them in registers — fully coalesced 16 B loads, no atomics on
-// the data path.  Every thread handles exactly kRowsPerThread pixel rows per
-// chunk and issues all of their loads before consuming any (the kernel is a
-// streaming pass: memory-level parallelism is the whole game).
+// i.e. a strided set — but a run of whole pixels is one contiguous span.  So
+// each CTA owns a chunk of consecutive pixels of one sample and moves it with
+// ONE bulk copy (cp.async.bulk, completion on an mbarrier) into shared memory:
+// one memory round trip per CTA instead of a chain of register batches.  The
+// SDXL feature maps are 5-63 MB, i.e. a few microseconds of HBM time, so the
+// number of dependent round trips per CTA — not bandwidth — was the limit.
 //
-//   kernel 1  gn_stats_kernel: per (n, chunk) shifted sums S1 = sum(x'-K_g),
-//             S2 = sum((x'-K_g)^2) reduced per group in shared memory and
-//             added to per-(n, g) fp64 accumulators; the LAST CTA of each
-//             sample (threadfence + counter) turns them into mean / rstd and
-//             re-zeroes them — no separate finalize launch, no serial tail,
-//             no co-residency requirement (safe next to a concurrent LoRA
-//             patch or ControlNet on another stream).
-//   kernel 2  gn_apply_kernel: y = act(x * a_c + b_c), a_c = gamma_c*rstd_g,
-//             b_c = beta_c + (add_c - mean_g) * a_c.
-// Kernel 2 re-reads x right after kernel 1 streamed it; at SDXL sizes the
-// tensor (<= 63 MB at CFG batch 2) stays in the 126 MB L2, so HBM traffic
-// stays close to the algorithmic one read + one write.
+//   kernel 1  gn_stats_kernel: chunk -> smem; per-thread shifted sums over
+//             its 8 channels (shift K = the chunk's first pixel, per group:
+//             no cancellation); per-group fold in shared memory; lane 0 turns
+//             the chunk's (S1, S2) into raw moments (sum x', sum x'^2) in fp64
+//             and adds them with fire-and-forget fp64 atomics.  No counters,
+//             no fences, no last-CTA tail, no co-residency requirement (safe
+//             next to a concurrent LoRA patch or ControlNet on another stream).
+//   kernel 2  gn_apply_kernel: chunk -> smem (L2 hit: kernel 1 read it with
+//             an evict-last hint) while the first `groups` threads turn the
+//             fp64 moments into mean / rstd (fp64: var = E[x'^2] - mean^2 keeps
+//             ~1e-8 relative precision even at |mean| / std = 1e4); then
+//             y = act(x * a_c + b_c), a_c = gamma_c*rstd_g,
+//             b_c = beta_c + (add_c - mean_g) * a_c, stored straight to HBM.
+//
+// Accumulator reset without a memset launch: the workspace holds two fp64
+// accumulator banks and an epoch word.  Launch L accumulates into bank
+// (epoch & 1) and zeroes the other bank (last used by launch L-1, whose apply
+// kernel has finished); the apply kernel reads the bank recorded in `cur` and
+// its CTA (0, 0) advances the epoch.  Every launch therefore starts on a zero
+// bank, including CUDA-graph replays; launches sharing a workspace must be
+// ordered on one stream (the C-ABI contract).
 //
 // Optional add_nc [N][C] (fp32) is added to x before normalisation (x' = x +
 // add): the ResNet block's time-embedding projection (h = conv1(x) +
 // temb_proj[n, c]) is fused here instead of costing its own read + write of
-// the feature map.  The shift K_g = x[n, pixel 0, g*cpg] is one constant per
-// group, so the variance is shift-invariant and free of cancellation.
+// the feature map.
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace sdb {
 namespace {
 
 constexpr int kMaxThreads = 512;
+constexpr int kMaxN = 64;
 constexpr int kMaxGroups = 64;
-constexpr int kRowsPerThread = 8;
+constexpr int kTileMax = 80 * 1024;          // chunk bytes per CTA (2 CTAs / SM)
+constexpr int kBankDoubles = kMaxN * kMaxGroups * 2;
+constexpr size_t kWsHeader = 256;            // epoch (u32) | cur (u32) | pad
+constexpr size_t kWsBytes = kWsHeader + 2 * kBankDoubles * sizeof(double);
 
-// 8 consecutive elements of T held as raw registers until they are consumed
-template <typename T> struct Raw8 { uint4 u; };
-template <> struct Raw8<float> { float4 a, b; };
-
-template <typename T>
-__device__ __forceinline__ Raw8<T> load_raw(const T* p) {
-  Raw8<T> r;
-  r.u = *reinterpret_cast<const uint4*>(p);
-  return r;
-}
-template <>
-__device__ __forceinline__ Raw8<float> load_raw<float>(const float* p) {
-  Raw8<float> r;
-  r.a = *reinterpret_cast<const float4*>(p);
-  r.b = *reinterpret_cast<const float4*>(p + 4);
-  return r;
-}
-template <typename T>
-__device__ __forceinline__ void unpack(const Raw8<T>& r, float (&v)[8]) {
-  const T* h = reinterpret_cast<const T*>(&r.u);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = to_f32<T>(h[i]);
-}
-template <>
-__device__ __forceinline__ void unpack<float>(const Raw8<float>& r, float (&v)[8]) {
-  v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w;
-  v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
-}
-
-struct GnShape {
-  int64_t n, hw, c, groups, cv, cpg;
-  int rpp, threads;
-  int64_t chunks, rows_per_chunk;
+struct WsHeader {
+  unsigned int epoch;
+  unsigned int cur;
 };
 
-GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups) {
+struct GnShape {
+  int64_t n, hw, c, groups, cv, cpg, es;
+  int rpp, threads;
+  int64_t chunks, rows_per_chunk;
+  size_t tile_bytes;
+};
+
+GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups, int64_t es) {
   GnShape s;
-  s.n = n; s.hw = hw; s.c = c; s.groups = groups;
+  s.n = n; s.hw = hw; s.c = c; s.groups = groups; s.es = es;
   s.cv = c / 8;
   s.cpg = c / groups;
   s.rpp = (int)std::max<int64_t>(1, 256 / s.cv);
   s.threads = (int)(s.cv * s.rpp);
-  // ~2 CTAs per SM over the whole batch; each thread walks its chunk in
-  // batches of kRowsPerThread rows (all loads of a batch in flight), so the
-  // per-CTA fixed costs (shift, reduction, accumulator atomics) amortise
-  const int64_t batch = (int64_t)s.rpp * kRowsPerThread;
+  // ~2 CTAs per SM over the whole batch, each chunk <= kTileMax bytes
   const int64_t want = std::max<int64_t>(1, (2 * kNumSMs + n - 1) / n);
-  s.chunks = std::max<int64_t>(1, std::min<int64_t>(want, (hw + batch - 1) / batch));
-  s.rows_per_chunk = (hw + s.chunks - 1) / s.chunks;
+  int64_t rpc = (hw + want - 1) / want;
+  rpc = std::min<int64_t>(rpc, std::max<int64_t>(1, kTileMax / (c * es)));
+  s.rows_per_chunk = std::max<int64_t>(1, rpc);
   s.chunks = (hw + s.rows_per_chunk - 1) / s.rows_per_chunk;
+  s.tile_bytes = (size_t)(s.rows_per_chunk * c * es);
   return s;
 }
 
-// workspace: counters[n] (uint) | acc[n][group][2] (double) — both zero at rest —
-// | stats[n][group][2] (float)
+// Group of each of a thread's 8 channels without a division per channel: one
+// 32-bit division for the first, then a running remainder (cpg may be < 8).
+__device__ __forceinline__ void channel_groups(int c0, int cpg, int (&g)[8]) {
+  int gg = c0 / cpg, rem = c0 - gg * cpg;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    g[j] = gg;
+    if (++rem == cpg) { rem = 0; ++gg; }
+  }
+}
+
+// Thread 0: bulk-copy rows [pbeg, pbeg + m) of one sample into the tile.
+template <typename T>
+__device__ __forceinline__ void load_chunk(uint8_t* tile, const T* xs, int pbeg, int m, int c, uint64_t* bar,
+                                           uint64_t pol) {
+  if (threadIdx.x == 0) {
+    const uint32_t b = smem_u32(bar);
+    mbar_init(b, 1);
+    mbar_fence_init();
+    const uint32_t bytes = (uint32_t)m * (uint32_t)c * (uint32_t)sizeof(T);
+    mbar_expect_tx(b, bytes);
+    bulk_g2s(smem_u32(tile), xs + (size_t)pbeg * c, bytes, b, pol);
+  }
+}
+
+// All index math is 32-bit within one sample (host checks hw * c < 2^31).
 template <typename T>
 __global__ void __launch_bounds__(kMaxThreads)
-gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, double* __restrict__ acc,
-                float* __restrict__ stats, unsigned int* __restrict__ counters, int64_t hw, int64_t c,
-                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int64_t chunks, int rpp, float eps) {
-  extern __shared__ float red[];  // [rpp][c][2]
-  __shared__ bool is_last;
-  const int64_t n = blockIdx.y;
-  const int64_t chunk = blockIdx.x;
-  const int cv = (int)(c / 8);
+gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8_t* __restrict__ ws, int hw, int c,
+                int groups, int cpg, int rows_per_chunk, int rpp, size_t tile_bytes) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  uint8_t* tile = smem;
+  float* red1 = reinterpret_cast<float*>(smem + tile_bytes);   // [rpp][c]
+  float* red2 = red1 + rpp * c;                                 // [rpp][c]
+  const int n = blockIdx.y;
+  const int cv = c >> 3;
   const int v = threadIdx.x % cv;
   const int r = threadIdx.x / cv;
-  const int64_t c0 = (int64_t)v * 8;
-  const T* xs = x + n * hw * c;
-  const int64_t p0 = chunk * rows_per_chunk + r;
-  const int64_t p1 = min(hw, chunk * rows_per_chunk + rows_per_chunk);
+  const int c0 = v * 8;
+  const T* xs = x + (size_t)n * hw * c;
+  const int pbeg = blockIdx.x * rows_per_chunk;
+  const int m = min(hw, pbeg + rows_per_chunk) - pbeg;
+  // kernel 2 re-reads the chunk right away: keep it in L2
+  load_chunk<T>(tile, xs, pbeg, m, c, &bar, policy_evict_last());
 
-  // d = x' - K_g = x - (K_g - add_c)
-  float K[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    K[j] = to_f32<T>(xs[((c0 + j) / cpg) * cpg]);
-    if (add_nc != nullptr) K[j] -= add_nc[n * c + c0 + j];
-  }
-  float s1[8], s2[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) { s1[j] = 0.f; s2[j] = 0.f; }
-  for (int64_t pb = p0; pb < p1; pb += (int64_t)rpp * kRowsPerThread) {
-    // every load of the batch first
-    Raw8<T> buf[kRowsPerThread];
-#pragma unroll
-    for (int u = 0; u < kRowsPerThread; ++u) {
-      const int64_t p = pb + (int64_t)u * rpp;
-      if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
-    }
-#pragma unroll
-    for (int u = 0; u < kRowsPerThread; ++u) {
-      if (pb + (int64_t)u * rpp < p1) {
-        float a[8];
-        unpack<T>(buf[u], a);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float d = a[j] - K[j];
-          s1[j] += d;
-          s2[j] = fmaf(d, d, s2[j]);
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    red[((int64_t)r * c + c0 + j) * 2 + 0] = s1[j];
-    red[((int64_t)r * c + c0 + j) * 2 + 1] = s2[j];
-  }
-  __syncthreads();
-  // per-group partials of this chunk go straight into fp64 accumulators: the
-  // partials are fp32 sums of similar magnitude, so their fp64 sum is exact in
-  // practice and the mean / rstd rounded to fp32 do not depend on arrival order
-  // one warp per group: lanes sum the group's (rpp x cpg) partials, shuffle-reduce
+  // accumulator bank of this launch; zero the other one (a grid-strided slice per CTA)
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+  const unsigned int epoch = *reinterpret_cast<volatile unsigned int*>(&hdr->epoch);
+  double* bank = reinterpret_cast<double*>(ws + kWsHeader) + (size_t)(epoch & 1u) * kBankDoubles;
+  double* other = reinterpret_cast<double*>(ws + kWsHeader) + (size_t)((epoch + 1u) & 1u) * kBankDoubles;
   {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const int per_group = rpp * (int)cpg;
-    if (warp < nwarps) {
-      for (int64_t g = warp; g < groups; g += nwarps) {
-        float t1 = 0.f, t2 = 0.f;
-        for (int e = lane; e < per_group; e += 32) {
-          const int rr = e / (int)cpg;
-          const int64_t ch = g * cpg + e % (int)cpg;
-          t1 += red[((int64_t)rr * c + ch) * 2 + 0];
-          t2 += red[((int64_t)rr * c + ch) * 2 + 1];
-        }
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    const int ctas = gridDim.x * gridDim.y;
+    for (int i = cta * blockDim.x + threadIdx.x; i < kBankDoubles; i += ctas * blockDim.x) other[i] = 0.0;
+    if (cta == 0 && threadIdx.x == 0) hdr->cur = epoch & 1u;
+  }
+  int g8[8];
+  channel_groups(c0, cpg, g8);
+  __syncthreads();            // barrier init visible before anyone waits on it
+  mbar_wait(smem_u32(&bar), 0);
+
+  const T* t = reinterpret_cast<const T*>(tile);
+  // shift: the chunk's first pixel, first channel of each group
+  float2 nK[4];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-          t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-        }
-        if (lane == 0) {
-          atomicAdd(acc + (n * groups + g) * 2 + 0, (double)t1);
-          atomicAdd(acc + (n * groups + g) * 2 + 1, (double)t2);
-        }
-      }
+  for (int i = 0; i < 4; ++i)
+    nK[i] = make_float2(-to_f32<T>(t[g8[2 * i] * cpg]), -to_f32<T>(t[g8[2 * i + 1] * cpg]));
+  float2 s1[4], s2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { s1[i] = f2s(0.f); s2[i] = f2s(0.f); }
+#pragma unroll 4
+  for (int row = r; row < m; row += rpp) {
+    const Raw8<T> q = load_raw<T>(t + row * c + c0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 d = f2add(get_pair<T>(q, i), nK[i]);
+      s1[i] = f2add(s1[i], d);
+      s2[i] = f2fma(d, d, s2[i]);
     }
   }
-  // ---- the last CTA of this sample finalises (no extra launch) ----
-  __threadfence();
+  *reinterpret_cast<float4*>(red1 + r * c + c0) = make_float4(s1[0].x, s1[0].y, s1[1].x, s1[1].y);
+  *reinterpret_cast<float4*>(red1 + r * c + c0 + 4) = make_float4(s1[2].x, s1[2].y, s1[3].x, s1[3].y);
+  *reinterpret_cast<float4*>(red2 + r * c + c0) = make_float4(s2[0].x, s2[0].y, s2[1].x, s2[1].y);
+  *reinterpret_cast<float4*>(red2 + r * c + c0 + 4) = make_float4(s2[2].x, s2[2].y, s2[3].x, s2[3].y);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int done = atomicAdd(counters + n, 1u);
-    is_last = (done == (unsigned int)chunks - 1);
+  // fold the rpp pixel rows into row 0 (one thread per channel column)
+  if (rpp > 1) {
+    for (int ch = threadIdx.x; ch < c; ch += blockDim.x) {
+      float a1 = red1[ch], a2 = red2[ch];
+      for (int rr = 1; rr < rpp; ++rr) {
+        a1 += red1[rr * c + ch];
+        a2 += red2[rr * c + ch];
+      }
+      red1[ch] = a1;
+      red2[ch] = a2;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int64_t g = threadIdx.x; g < groups; g += blockDim.x) {
-    double* a = acc + (n * groups + g) * 2;
-    const double t1 = __ldcg(a), t2 = __ldcg(a + 1);
-    const double cnt = (double)hw * (double)cpg;
-    const double Kg = (double)to_f32<T>(xs[g * cpg]);
-    const double dm = t1 / cnt;
-    double var = t2 / cnt - dm * dm;
-    if (var < 0.0) var = 0.0;
-    stats[(n * groups + g) * 2 + 0] = (float)(Kg + dm);
-    stats[(n * groups + g) * 2 + 1] = (float)(1.0 / sqrt(var + (double)eps));
-    a[0] = 0.0;   // accumulators and counter are back at zero for the next launch / graph replay
-    a[1] = 0.0;
+  // one full warp per group: lanes over the group's channels, shuffle-reduce,
+  // lane 0 converts the chunk's shifted sums to raw moments of x' = x + add
+  // in fp64 (add is per channel, so per channel) and adds them to the bank
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int g = warp; warp < nwarps && g < groups; g += nwarps) {
+    const double K = (double)to_f32<T>(t[g * cpg]);
+    double m1 = 0.0, m2 = 0.0;
+    for (int k = lane; k < cpg; k += 32) {
+      const int ch = g * cpg + k;
+      const double a = add_nc != nullptr ? (double)add_nc[n * c + ch] : 0.0;
+      const double sh = K + a;                       // x' - sh = x - K = d
+      const double S1 = (double)red1[ch], S2 = (double)red2[ch];
+      m1 += S1 + (double)m * sh;                     // sum x'
+      m2 += S2 + sh * (2.0 * S1 + (double)m * sh);   // sum x'^2
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    }
+    if (lane == 0) {
+      atomicAdd(bank + (n * kMaxGroups + g) * 2 + 0, m1);
+      atomicAdd(bank + (n * kMaxGroups + g) * 2 + 1, m2);
+    }
   }
-  if (threadIdx.x == 0) counters[n] = 0u;
 }
 
 template <typename T, bool SILU>
 __global__ void __launch_bounds__(kMaxThreads)
-gn_apply_kernel(const T* x, T* y,  // may alias: same-thread read-then-write
-                const float* __restrict__ add_nc, const float* __restrict__ stats,
-                const float* __restrict__ gamma, const float* __restrict__ beta, int64_t hw, int64_t c,
-                int64_t groups, int64_t cpg, int64_t rows_per_chunk, int rpp) {
-  const int64_t n = blockIdx.y;
-  const int64_t chunk = blockIdx.x;
-  const int cv = (int)(c / 8);
+gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into smem before writing it
+                const float* __restrict__ add_nc, uint8_t* __restrict__ ws, const float* __restrict__ gamma,
+                const float* __restrict__ beta, int hw, int c, int groups, int cpg, int rows_per_chunk, int rpp,
+                float eps) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ float2 gstat[kMaxGroups];   // (mean, rstd)
+  const int n = blockIdx.y;
+  const int cv = c >> 3;
   const int v = threadIdx.x % cv;
   const int r = threadIdx.x / cv;
-  const int64_t c0 = (int64_t)v * 8;
-  const T* xs = x + n * hw * c;
-  T* ys = y + n * hw * c;
-  const int64_t p0 = chunk * rows_per_chunk + r;
-  const int64_t p1 = min(hw, chunk * rows_per_chunk + rows_per_chunk);
-  float A[8], B[8];
+  const int c0 = v * 8;
+  const size_t base = (size_t)n * hw * c;
+  const int pbeg = blockIdx.x * rows_per_chunk;
+  const int m = min(hw, pbeg + rows_per_chunk) - pbeg;
+  load_chunk<T>(smem, x + base, pbeg, m, c, &bar, policy_evict_first());
+
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+  if (threadIdx.x < groups) {
+    const unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&hdr->cur);
+    const double* bank = reinterpret_cast<const double*>(ws + kWsHeader) + (size_t)cur * kBankDoubles;
+    const double m1 = __ldcg(bank + (n * kMaxGroups + threadIdx.x) * 2 + 0);
+    const double m2 = __ldcg(bank + (n * kMaxGroups + threadIdx.x) * 2 + 1);
+    const double cnt = (double)hw * (double)cpg;
+    const double mean = m1 / cnt;
+    double var = m2 / cnt - mean * mean;
+    if (var < 0.0) var = 0.0;
+    gstat[threadIdx.x] = make_float2((float)mean, (float)(1.0 / sqrt(var + (double)eps)));
+  }
+  // every apply CTA has its bank index already (cur): advancing the epoch
+  // here only affects the next launch's stats kernel
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&hdr->epoch, 1u);
+  int g8[8];
+  channel_groups(c0, cpg, g8);
+  float ga[8], be[8], ad[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    const int64_t ch = c0 + j;
-    const int64_t g = ch / cpg;
-    const float mean = stats[(n * groups + g) * 2 + 0];
-    const float rstd = stats[(n * groups + g) * 2 + 1];
-    const float ga = gamma ? gamma[ch] : 1.f;
-    const float be = beta ? beta[ch] : 0.f;
-    const float ad = add_nc ? add_nc[n * c + ch] : 0.f;
-    A[j] = ga * rstd;
-    B[j] = be + (ad - mean) * A[j];
+    ga[j] = gamma ? gamma[c0 + j] : 1.f;
+    be[j] = beta ? beta[c0 + j] : 0.f;
+    ad[j] = add_nc ? add_nc[n * c + c0 + j] : 0.f;
   }
-  for (int64_t pb = p0; pb < p1; pb += (int64_t)rpp * kRowsPerThread) {
-    Raw8<T> buf[kRowsPerThread];
+  __syncthreads();
+  float2 A[4], B[4];
+  {
+    float a[8], b[8];
 #pragma unroll
-    for (int u = 0; u < kRowsPerThread; ++u) {
-      const int64_t p = pb + (int64_t)u * rpp;
-      if (p < p1) buf[u] = load_raw<T>(xs + p * c + c0);
+    for (int j = 0; j < 8; ++j) {
+      const float2 st = gstat[g8[j]];
+      a[j] = ga[j] * st.y;
+      b[j] = be[j] + (ad[j] - st.x) * a[j];
     }
 #pragma unroll
-    for (int u = 0; u < kRowsPerThread; ++u) {
-      const int64_t p = pb + (int64_t)u * rpp;
-      if (p < p1) {
-        float a[8];
-        unpack<T>(buf[u], a);
+    for (int i = 0; i < 4; ++i) {
+      A[i] = make_float2(a[2 * i], a[2 * i + 1]);
+      B[i] = make_float2(b[2 * i], b[2 * i + 1]);
+    }
+  }
+  mbar_wait(smem_u32(&bar), 0);
+  const T* t = reinterpret_cast<const T*>(smem);
+  T* ys = y + base + (size_t)pbeg * c;
+#pragma unroll 4
+  for (int row = r; row < m; row += rpp) {
+    const Raw8<T> q = load_raw<T>(t + row * c + c0);
+    Raw8<T> o;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float t = fmaf(a[j], A[j], B[j]);
-          if (SILU) t = __fdividef(t, 1.f + __expf(-t));   // -> 0 as t -> -inf
-          a[j] = t;
-        }
-        Vec8<T>::store(ys + p * c + c0, a);
+    for (int i = 0; i < 4; ++i) {
+      float2 u = f2fma(get_pair<T>(q, i), A[i], B[i]);
+      if (SILU) {   // SiLU(u) = u / (1 + 2^(-u log2 e)) -> 0 as u -> -inf
+        const float2 w = f2mul(u, f2s(-1.4426950408889634f));
+        float2 e;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(w.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(w.y));
+        e = f2add(e, f2s(1.f));
+        float2 rc;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.x) : "f"(e.x));
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.y) : "f"(e.y));
+        u = f2mul(u, rc);
       }
+      set_pair<T>(o, i, u);
     }
+    store_raw<T>(ys + row * c + c0, o);
   }
 }
 
 template <typename T>
 int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, const float* add_nc, int64_t n,
-           int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* ws, cudaStream_t st) {
+           int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* wsv, cudaStream_t st) {
   const T* x = static_cast<const T*>(xv);
   T* y = static_cast<T*>(yv);
-  GnShape s = gn_shape(n, hw, c, groups);
-  unsigned int* counters = static_cast<unsigned int*>(ws);
-  double* acc = reinterpret_cast<double*>(static_cast<uint8_t*>(ws) + 256);
-  float* stats = reinterpret_cast<float*>(acc + n * groups * 2);
+  uint8_t* ws = static_cast<uint8_t*>(wsv);
+  GnShape s = gn_shape(n, hw, c, groups, sizeof(T));
   dim3 grid((unsigned)s.chunks, (unsigned)n);
-  size_t smem = (size_t)s.rpp * c * 2 * sizeof(float);
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(gn_stats_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem_stats = s.tile_bytes + (size_t)s.rpp * c * 2 * sizeof(float);
+  const size_t smem_apply = s.tile_bytes;
+  // opt in to > 48 KB of dynamic shared memory once per device
+  static unsigned long long attr_done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !((attr_done >> dev) & 1ull)) {
+    const int lim = kTileMax + 2 * kMaxThreads * 8 * (int)sizeof(float);
+    cudaFuncSetAttribute(gn_stats_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(gn_apply_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(gn_apply_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    attr_done |= 1ull << dev;
   }
-  gn_stats_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, acc, stats, counters, hw, c, groups, s.cpg,
-                                                    s.rows_per_chunk, s.chunks, s.rpp, eps);
+  const int ihw = (int)hw, ic = (int)c, ig = (int)groups, icpg = (int)s.cpg, irows = (int)s.rows_per_chunk;
+  gn_stats_kernel<T><<<grid, s.threads, smem_stats, st>>>(x, add_nc, ws, ihw, ic, ig, icpg, irows, s.rpp,
+                                                          s.tile_bytes);
   if (int rc = check_launch("gn_stats_kernel")) return rc;
   if (silu)
-    gn_apply_kernel<T, true><<<grid, s.threads, 0, st>>>(x, y, add_nc, stats, gamma, beta, hw, c, groups, s.cpg,
-                                                         s.rows_per_chunk, s.rpp);
+    gn_apply_kernel<T, true><<<grid, s.threads, smem_apply, st>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, ig, icpg,
+                                                                  irows, s.rpp, eps);
   else
-    gn_apply_kernel<T, false><<<grid, s.threads, 0, st>>>(x, y, add_nc, stats, gamma, beta, hw, c, groups, s.cpg,
-                                                          s.rows_per_chunk, s.rpp);
+    gn_apply_kernel<T, false><<<grid, s.threads, smem_apply, st>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, ig,
+                                                                   icpg, irows, s.rpp, eps);
   return check_launch("gn_apply_kernel");
 }
 
 }  // namespace
 
 size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
+  (void)n;
   (void)hw;
   (void)c;
-  return 256 + (size_t)(n * groups * 2) * (sizeof(double) + sizeof(float));
+  (void)groups;
+  return kWsBytes;
 }
 
 int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc, int64_t n,
                    int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, void* ws,
                    cudaStream_t st) {
   if (n <= 0 || hw <= 0 || c <= 0 || groups <= 0) return fail(SDB_EINVAL, "groupnorm: empty shape");
-  if (n > 64) return fail(SDB_EINVAL, "groupnorm: batch > 64 unsupported");
+  if (n > kMaxN) return fail(SDB_EINVAL, "groupnorm: batch > 64 unsupported");
   if (c % groups != 0) return fail(SDB_EINVAL, "groupnorm: channels not divisible by groups");
   if (groups > kMaxGroups) return fail(SDB_EINVAL, "groupnorm: more than 64 groups");
   if (c % 8 != 0) return fail(SDB_EINVAL, "groupnorm: channels must be a multiple of 8");
   if (c / 8 > kMaxThreads) return fail(SDB_EINVAL, "groupnorm: channels > 4096 unsupported");
+  if (hw * c >= (int64_t)INT32_MAX - 8 * c)
+    return fail(SDB_EINVAL, "groupnorm: one sample must hold < 2^31 elements");
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
     return fail(SDB_EINVAL, "groupnorm: x and y must be 16-byte aligned");
   if (ws == nullptr) return fail(SDB_EINVAL, "groupnorm: workspace is NULL");
+  if ((reinterpret_cast<uintptr_t>(ws) & 15) != 0) return fail(SDB_EINVAL, "groupnorm: workspace must be 16-byte aligned");
   switch (dtype) {
     case SDB_BF16: return run_gn<__nv_bfloat16>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
     case SDB_F16: return run_gn<__half>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);

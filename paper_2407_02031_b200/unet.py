@@ -322,7 +322,7 @@ class Net:
         h = self.gn(pre + ".norm2", h, True, add_nc=tproj)       # fused temb add + GN + SiLU
         h = self.conv(pre + ".conv2", h)
         sc = self.conv(pre + ".conv_shortcut", x) if (pre + ".conv_shortcut.weight") in self.t else x
-        return h.add_(sc)
+        return ops.residual_inject(h, [sc], [1.0])          # K3 in-place add (NHWC, vectorised)
 
     def attention(self, pre, x, ctx, heads):
         n, l, c = x.shape
@@ -360,10 +360,10 @@ class Net:
             y = ln("norm2", self.attention(b + ".attn1", y, None, heads))
             y = ln("norm3", self.attention(b + ".attn2", y, ctx, heads))
             delta = self.lin(b + ".ff.out", ops.geglu(self.lin(b + ".ff.proj", y)))   # K5
-        tok = tok + delta
+        tok = ops.residual_inject(tok, [delta], [1.0])
         tok = self.lin(pre + ".proj_out", tok)
         out = tok.view(n, h, w, c).permute(0, 3, 1, 2)            # channels_last view
-        return out + res
+        return ops.residual_inject(out, [res], [1.0])
 
     # -- embeddings ---------------------------------------------------------
     def add_embedding(self, pooled: torch.Tensor, time_ids: torch.Tensor) -> torch.Tensor:

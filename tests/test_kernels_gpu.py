@@ -18,7 +18,7 @@ def cl(t):
 
 # SDXL / SD1.5 GN sites (C, H, W) incl. cpg = 10, 30 (not a multiple of 8)
 GN_SHAPES = [(320, 128, 128), (960, 64, 64), (2560, 32, 32), (640, 32, 32), (1920, 16, 16),
-             (64, 64, 64), (32, 8, 8), (1280, 8, 8)]
+             (64, 64, 64), (32, 8, 8), (1280, 8, 8), (960, 128, 128), (4096, 3, 5)]
 
 
 @pytest.mark.parametrize("c,h,w", GN_SHAPES)
@@ -124,6 +124,20 @@ def test_groupnorm_repeated_launches_reset_counters():
     first = ops.groupnorm_silu(x, g, b)
     for _ in range(5):
         assert torch.equal(ops.groupnorm_silu(x, g, b), first)
+
+
+def test_groupnorm_workspace_shared_across_shapes():
+    """One workspace, alternating batch / group counts: the accumulator banks
+    recycle themselves whatever the previous launch's shape was."""
+    cases = [(2, 320, 64, 64, 32), (1, 640, 16, 16, 16), (4, 128, 32, 32, 64), (2, 1280, 8, 8, 32)]
+    xs = [cl((torch.randn(n, c, h, w, device="cuda") * 2 + 0.5).to(torch.bfloat16)) for n, c, h, w, _ in cases]
+    ws = ops.groupnorm_workspace(xs[0])
+    for rep in range(3):
+        for x, (n, c, h, w, grp) in zip(xs, cases):
+            gamma, beta = torch.ones(c, device="cuda"), torch.zeros(c, device="cuda")
+            y = ops.groupnorm_silu(x, gamma, beta, groups=grp, workspace=ws)
+            ref = F.silu(F.group_norm(x.float(), grp, gamma, beta, 1e-5))
+            assert ((y.float() - ref).abs() <= ref.abs() * 2 ** -8 + 1e-3).all(), (rep, c)
 
 
 @pytest.mark.parametrize("rows,f", [(2 * 4096, 2560), (2 * 1024, 5120), (77, 256), (3, 8)])
