@@ -156,7 +156,7 @@ class LoraSrc(ctypes.Structure):
 
 
 EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_tc_plan",
-                       "sdb_lora_tc_patch", "sdb_geglu", "sdb_add_layernorm")
+                       "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_add_layernorm")
 
 
 def _declare_tc(lib: ctypes.CDLL) -> None:
@@ -172,6 +172,8 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
     lib.sdb_lora_tc_patch.restype = i32
     lib.sdb_lora_tc_patch.argtypes = [vp, i32, i32, i32, i32, f32, i32, vp]
+    lib.sdb_lora_tc_set_mode.restype = i32
+    lib.sdb_lora_tc_set_mode.argtypes = [i32]
     lib.sdb_geglu.restype = i32
     lib.sdb_geglu.argtypes = [vp, vp, i64, i64, i32, vp]
     lib.sdb_add_layernorm.restype = i32

@@ -28,6 +28,7 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
                   cudaStream_t st);
 int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed,
             int* n_units_out, int* kb_max_out);
+int tc_set_mode(int mode);
 int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign,
              int max_ctas, cudaStream_t st);
 // groupnorm_silu.cu
@@ -156,6 +157,10 @@ int sdb_lora_pack_multi(const sdb_lora_src* srcs_host, int n_src, int64_t h1, in
 int sdb_lora_tc_plan(const sdb_lora_tc_job* jobs_host, int n_jobs, void* blob_host, size_t blob_bytes,
                      size_t* needed, int* n_units, int* kb_max) {
   return tc_plan(jobs_host, n_jobs, blob_host, blob_bytes, needed, n_units, kb_max);
+}
+
+int sdb_lora_tc_set_mode(int mode) {
+  return tc_set_mode(mode);
 }
 
 int sdb_lora_tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign,

@@ -27,6 +27,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -46,9 +48,10 @@ constexpr int kBBlockBytes = kBN * 128;   // 32 KB per K block of a B panel
 constexpr int kUnitTiles = 8;             // row tiles per work unit (B panel reuse)
 constexpr int kEpiWarps = 8;              // 2 warps per TMEM lane quadrant (column halves)
 constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kProducerWarp = kEpiWarps;
+constexpr int kProducerWarp = kEpiWarps;       // W boxes
 constexpr int kMmaWarp = kEpiWarps + 1;
-constexpr int kThreads = (kEpiWarps + 2) * 32;
+constexpr int kFactorWarp = kEpiWarps + 2;      // B panel + A K-blocks
+constexpr int kThreads = (kEpiWarps + 3) * 32;
 constexpr int kMaxKB = 4;                 // rank <= 256
 constexpr int kAStages = 2;               // A K-blocks in flight
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
@@ -61,7 +64,8 @@ struct TcJob {
   int32_t kb, rank;
   float scale;
   int32_t map_in, map_out;
-  int32_t pad;
+  int32_t map_a, map_b;   // tensor maps over the packed factors (CTA-pair kernel)
+  int32_t mt, pad;        // row tiles of W
 };
 struct TcUnit {
   int32_t job, n_tile, m_begin, m_end;
@@ -206,19 +210,15 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == kProducerWarp) {
-    // ===================== producer: B panel, A K-blocks, W boxes =====================
+  if (warp == kFactorWarp) {
+    // ===================== factor producer: B panel, A K-blocks =====================
+    // (its own warp: A loads never queue behind a full W ring)
     if (lane == 0) {
-      const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
-      int b_cnt = 0;
-      int a_st = 0, a_round = 0;   // A ring position
-      int w_slot = 0, w_round = 0; // W ring position
+      const uint64_t keep = policy_evict_last();
+      int b_cnt = 0, a_st = 0, a_round = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
-        const CUtensorMap* min = maps + J.map_in;
-        prefetch_map(min);
-        const int nkb = (J.rank + kKB - 1) / kKB;
         if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
         mbar_expect_tx(bar(B_FULL), J.kb * kPanelBlock);
         if (BN == kBN) {
@@ -232,16 +232,31 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
                      keep);
         }
         ++b_cnt;
-        const int64_t ncols = std::min<int64_t>(BN, J.h2 - (int64_t)un.n_tile * BN);
-        const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
         for (int m = un.m_begin; m < un.m_end; ++m) {
-          for (int kb = 0; kb < nkb; ++kb) {
+          for (int kb = 0; kb < J.kb; ++kb) {
             if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
             mbar_expect_tx(bar(A_FULL + a_st), kABlockBytes);
             bulk_g2s(smem_u32(sA + a_st * kABlockBytes), J.a + ((size_t)m * J.kb + kb) * kABlockBytes, kABlockBytes,
                      bar(A_FULL + a_st), keep);
             if (++a_st == kAStages) { a_st = 0; ++a_round; }
           }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kProducerWarp) {
+    // ===================== W producer =====================
+    if (lane == 0) {
+      const uint64_t stream = policy_evict_first();
+      int w_slot = 0, w_round = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const TcUnit un = units[u];
+        const TcJob& J = jobs[un.job];
+        const CUtensorMap* min = maps + J.map_in;
+        prefetch_map(min);
+        const int64_t ncols = std::min<int64_t>(BN, J.h2 - (int64_t)un.n_tile * BN);
+        const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
+        for (int m = un.m_begin; m < un.m_end; ++m) {
           for (int bx = 0; bx < nbox; ++bx) {
             if (w_round > 0) mbar_wait(bar(W_EMPTY + w_slot), (w_round - 1) & 1);
             mbar_expect_tx(bar(W_FULL + w_slot), kBoxBytes);
@@ -353,6 +368,293 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+  }
+}
+
+// ---- CTA-pair variant (cta_group::2) ------------------------------------------
+// The B panel is what limits the W ring at high rank: 256 columns x R bf16 is
+// 128 KB at R = 256, leaving 4 W slots.  A pair of CTAs on one TPC shares it:
+// tcgen05.mma.cta_group::2 computes M = 256 rows (128 per CTA, each CTA's A
+// tile in its own smem) x N = 256 columns, with B split along N — each CTA
+// holds only its half of the panel (64 KB at R = 256), so both keep an 8-slot
+// W ring.  Each CTA's TMEM receives its own 128 rows x 256 columns, so the
+// epilogue and the W traffic are unchanged.  The leader (rank 0) issues the
+// MMAs; factor loads of both CTAs complete on the leader's barriers
+// (cp.async.bulk.tensor .cta_group::2) and the MMA commits multicast to both.
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_idx() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// both CTAs load into their own smem; bytes complete on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t leader_bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(leader_bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit2(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+constexpr int kPairUnitTiles = 16;   // row tiles per pair unit (8 per CTA: same B reuse)
+constexpr int kHalfBlock = 128 * 128; // one K block of half a B panel (128 columns x 64 K)
+constexpr int kMaxSlots = 10;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restrict__ jobs,
+                       const TcUnit* __restrict__ units, int n_units, float sign, int kb_max, int n_slots) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);   // f32 accum, bf16, K-major, M256 x N256
+  uint8_t* sB = smem;                                   // kb_max x 16 KB: this CTA's half of the B panel
+  uint8_t* sA = sB + kb_max * kHalfBlock;               // kAStages x 16 KB
+  uint8_t* sW = sA + kAStages * kABlockBytes;           // n_slots x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + n_slots * kBoxBytes);
+  const int B_FULL = 0, B_EMPTY = 1, A_FULL = 2, A_EMPTY = A_FULL + kAStages, T_FULL = A_EMPTY + kAStages;
+  const int T_EMPTY = T_FULL + 2, W_FULL = T_EMPTY + 2;
+  const int W_EMPTY = W_FULL + n_slots;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + W_EMPTY + n_slots);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int cid = (int)cluster_idx(), ncl = (int)cluster_count();
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_FULL), 1);
+    mbar_init(bar(B_EMPTY), 1);
+    for (int i = 0; i < kAStages; ++i) {
+      mbar_init(bar(A_FULL + i), 1);
+      mbar_init(bar(A_EMPTY + i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(T_FULL + i), 1);
+      mbar_init(bar(T_EMPTY + i), 2 * kEpiWarps);   // both CTAs' epilogue warps
+    }
+    for (int i = 0; i < n_slots; ++i) {
+      mbar_init(bar(W_FULL + i), 1);
+      mbar_init(bar(W_EMPTY + i), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(2 * kBN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == kFactorWarp) {
+    // factor producer: this CTA's half of the B panel and its A K-blocks,
+    // completing on the leader's barriers
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last();
+      int b_cnt = 0, a_st = 0, a_round = 0;
+      for (int u = cid; u < n_units; u += ncl) {
+        const TcUnit un = units[u];
+        const TcJob& J = jobs[un.job];
+        const CUtensorMap* ma = maps + J.map_a;
+        const CUtensorMap* mb = maps + J.map_b;
+        if (b_cnt > 0) mbar_wait_cl(bar(B_EMPTY), (b_cnt - 1) & 1);
+        if (leader) mbar_expect_tx(bar(B_FULL), 2 * J.kb * kHalfBlock);
+        for (int kb = 0; kb < J.kb; ++kb)
+          tma_load_2d_pair(smem_u32(sB + kb * kHalfBlock), mb, 0, (un.n_tile * J.kb + kb) * kBN + (int)cta * 128,
+                           mapa_shared(bar(B_FULL), 0), keep);
+        ++b_cnt;
+        for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2) {
+          // past the last row tile the follower multiplies a valid (ignored) A tile
+          const int mload = std::min(m0 + (int)cta, J.mt - 1);
+          for (int kb = 0; kb < J.kb; ++kb) {
+            if (a_round > 0) mbar_wait_cl(bar(A_EMPTY + a_st), (a_round - 1) & 1);
+            if (leader) mbar_expect_tx(bar(A_FULL + a_st), 2 * kABlockBytes);
+            tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.kb + kb) * kBM,
+                             mapa_shared(bar(A_FULL + a_st), 0), keep);
+            if (++a_st == kAStages) { a_st = 0; ++a_round; }
+          }
+        }
+      }
+      // drain: the leader's last multicast commits must land before this CTA exits
+      for (int s = 0; s < kAStages; ++s) {
+        const int uses = a_round + (s < a_st ? 1 : 0);
+        if (uses > 0) mbar_wait_cl(bar(A_EMPTY + s), (uses - 1) & 1);
+      }
+      if (b_cnt > 0) mbar_wait_cl(bar(B_EMPTY), (b_cnt - 1) & 1);
+    }
+    __syncwarp();
+  } else if (warp == kProducerWarp) {
+    // W producer: this CTA's row tiles only
+    if (lane == 0) {
+      const uint64_t stream = policy_evict_first();
+      int w_slot = 0, w_round = 0;
+      for (int u = cid; u < n_units; u += ncl) {
+        const TcUnit un = units[u];
+        const TcJob& J = jobs[un.job];
+        const CUtensorMap* min = maps + J.map_in;
+        prefetch_map(min);
+        const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
+        const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
+        for (int m = un.m_begin + (int)cta; m < un.m_end; m += 2) {
+          for (int bx = 0; bx < nbox; ++bx) {
+            if (w_round > 0) mbar_wait(bar(W_EMPTY + w_slot), (w_round - 1) & 1);
+            mbar_expect_tx(bar(W_FULL + w_slot), kBoxBytes);
+            tma_load_2d(smem_u32(sW + w_slot * kBoxBytes), min, un.n_tile * kBN + bx * kBoxN, m * kBM,
+                        bar(W_FULL + w_slot), stream);
+            if (++w_slot == n_slots) { w_slot = 0; ++w_round; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMmaWarp) {
+    if (leader && lane == 0) {
+      int tile = 0, b_cnt = 0, a_cnt = 0;
+      for (int u = cid; u < n_units; u += ncl) {
+        const TcUnit un = units[u];
+        const TcJob& J = jobs[un.job];
+        const int nks = (J.rank + 15) / 16;
+        mbar_wait_cl(bar(B_FULL), b_cnt & 1);
+        for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2, ++tile) {
+          const int buf = tile & 1;
+          if (tile >= 2) mbar_wait_cl(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + buf * kBN;
+          for (int kb = 0; kb < J.kb; ++kb, ++a_cnt) {
+            const int st = a_cnt & (kAStages - 1);
+            mbar_wait_cl(bar(A_FULL + st), (a_cnt / kAStages) & 1);
+            tc_fence_after();
+            const int ks_end = std::min(4, nks - kb * 4);
+            for (int ks = 0; ks < ks_end; ++ks) {
+              const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
+              const uint64_t bd = sw128_desc(smem_u32(sB + kb * kHalfBlock + ks * 32));
+              tc_mma2(d, ad, bd, kIdesc2, (kb | ks) ? 1u : 0u);
+            }
+            tc_commit2(bar(A_EMPTY + st));
+          }
+          tc_commit2(bar(T_FULL + buf));
+        }
+        tc_commit2(bar(B_EMPTY));
+        ++b_cnt;
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue: as in the single-CTA kernel, on this CTA's 128 rows
+    const int q = warp & 3, grp = warp >> 2;
+    const int r = (q << 5) | lane;
+    int box = 0, tile = 0, w_slot = 0, w_round = 0, pending = -1;
+    const uint64_t stream = policy_evict_first();
+    for (int u = cid; u < n_units; u += ncl) {
+      const TcUnit un = units[u];
+      const TcJob& J = jobs[un.job];
+      const CUtensorMap* mout = maps + J.map_out;
+      const float ss = sign * J.scale;
+      const int64_t ncols = std::min<int64_t>(kBN, J.h2 - (int64_t)un.n_tile * kBN);
+      const int nbox = (int)((ncols + kBoxN - 1) / kBoxN);
+      for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2, ++tile) {
+        const int m = m0 + (int)cta;
+        const int buf = tile & 1;
+        mbar_wait_cl(bar(T_FULL + buf), (tile >> 1) & 1);
+        tc_fence_after();
+        if (m < un.m_end) {
+          for (int bx = 0; bx < nbox; ++bx) {
+            const int slot = w_slot, round = w_round;
+            if (++w_slot == n_slots) { w_slot = 0; ++w_round; }
+            const bool mine = ((box++ & 1) == grp);
+            if (!mine) continue;
+            mbar_wait(bar(W_FULL + slot), round & 1);
+            uint8_t* row = sW + slot * kBoxBytes + r * 128;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              float v[32];
+              tc_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + buf * kBN + bx * kBoxN + hf * 32, v);
+              rmw32(row, r, hf * 4, v, ss);
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(mout, un.n_tile * kBN + bx * kBoxN, m * kBM + q * 32,
+                           smem_u32(sW + slot * kBoxBytes + q * 32 * 128), stream);
+              if (pending >= 0) {
+                tma_store_wait_read1();
+                mbar_arrive(bar(W_EMPTY + pending));
+              }
+              pending = slot;
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(bar(T_EMPTY + buf));
+          else mbar_arrive_remote(mapa_shared(bar(T_EMPTY + buf), 0));
+        }
+      }
+    }
+    if (lane == 0) {
+      if (pending >= 0) {
+        tma_store_wait_read();
+        mbar_arrive(bar(W_EMPTY + pending));
+      }
+      tma_store_wait_all();
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kBN));
   }
 }
 
@@ -505,6 +807,22 @@ int make_w_map(CUtensorMap* map, void* ptr, int64_t h1, int64_t h2, int64_t ldw,
   return SDB_OK;
 }
 
+
+// packed factors viewed as rows of 128 B (64 bf16); box = one 128-row K block,
+// copied verbatim (the data is already in the SWIZZLE_128B pattern)
+int make_f_map(CUtensorMap* map, const void* ptr, int64_t rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)kKB, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)kKB * 2};
+  cuuint32_t box[2] = {(cuuint32_t)kKB, (cuuint32_t)kBM};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SDB_EINVAL, "cuTensorMapEncodeTiled (factors) failed (" + std::to_string((int)r) + ")");
+  return SDB_OK;
+}
 }  // namespace
 
 int tc_kb(int rank) { return (rank + kKB - 1) / kKB; }
@@ -562,15 +880,22 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
   return check_launch("pack_b_multi_kernel");
 }
 
-// Tile width: the B panel (BN x Rpad bf16) stays resident in shared memory.
-// Up to rank 128 a 256-wide panel (64 KB) leaves room for an 8-slot W ring;
-// above it the 256-wide panel (128 KB) squeezes the ring to 4 slots.  A
-// 128-wide panel (8 slots, but the A tile re-read twice as often) measured
-// slower at R = 232 (3.94 vs 3.36-3.67 ms, round 1), so 256 is kept at every
-// rank; the BN=128 instantiation stays for experiments.
-static int tile_n_for(int /*kb_max*/) { return kBN; }
+// Kernel choice.  The B panel (256 x Rpad bf16) stays resident in shared
+// memory: up to rank 128 (64 KB) the single-CTA kernel keeps an 8-slot W
+// ring; above it the panel (128 KB) would squeeze the ring to 4 slots, so
+// the CTA-pair kernel splits the panel across the two CTAs of a TPC (each
+// keeps 8 slots).  sdb_lora_tc_set_mode forces one kernel (tests, probes).
+// The chosen kernel is folded into the plan's opaque kb_max word
+// (kb | mode << 8) so a plan always launches the kernel it was built for.
+static int g_tc_mode = 0;   // 0 auto, 1 single CTA, 2 CTA pair
+static int pick_mode(int kb_max) {
+  if (g_tc_mode == 1 || g_tc_mode == 2) return g_tc_mode;
+  return kb_max > 2 ? 2 : 1;
+}
 
-// Blob layout: [maps: 2*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]
+// Blob layout: [maps: 4*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]
+// maps per job: W in (128-row load boxes), W out (32-row store boxes),
+// packed A, packed B (128-row K blocks; CTA-pair kernel).
 int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed, int* n_units_out,
             int* kb_max_out) {
   if (n_jobs <= 0 || !jobs) return fail(SDB_EINVAL, "lora_tc_plan: no jobs");
@@ -586,21 +911,22 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": packed factors must be 1024-B aligned");
     kb_max = std::max(kb_max, tc_kb(J.rank));
   }
-  const int bn = tile_n_for(kb_max);
+  const int mode = pick_mode(kb_max);
+  const int unit_tiles = mode == 2 ? kPairUnitTiles : kUnitTiles;
   for (int j = 0; j < n_jobs; ++j) {
     const sdb_lora_tc_job& J = jobs[j];
-    const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + bn - 1) / bn;
+    const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + kBN - 1) / kBN;
     for (int64_t n = 0; n < nt; ++n)
-      for (int64_t m = 0; m < mt; m += kUnitTiles)
-        units.push_back({j, (int32_t)n, (int32_t)m, (int32_t)std::min<int64_t>(mt, m + kUnitTiles)});
+      for (int64_t m = 0; m < mt; m += unit_tiles)
+        units.push_back({j, (int32_t)n, (int32_t)m, (int32_t)std::min<int64_t>(mt, m + unit_tiles)});
   }
-  const size_t maps_b = (size_t)2 * n_jobs * sizeof(CUtensorMap);
+  const size_t maps_b = (size_t)4 * n_jobs * sizeof(CUtensorMap);
   const size_t jobs_b = (size_t)n_jobs * sizeof(TcJob);
   const size_t units_b = units.size() * sizeof(TcUnit);
   const size_t need = maps_b + jobs_b + units_b;
   if (needed) *needed = need;
   if (n_units_out) *n_units_out = (int)units.size();
-  if (kb_max_out) *kb_max_out = kb_max;
+  if (kb_max_out) *kb_max_out = kb_max | (mode << 8);
   if (!blob) return SDB_OK;
   if (blob_bytes < need) return fail(SDB_EINVAL, "lora_tc_plan: blob too small");
   uint8_t* base = static_cast<uint8_t*>(blob);
@@ -608,46 +934,88 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
   TcJob* tj = reinterpret_cast<TcJob*>(base + maps_b);
   for (int j = 0; j < n_jobs; ++j) {
     const sdb_lora_tc_job& J = jobs[j];
+    const int kb = tc_kb(J.rank);
+    const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + kBN - 1) / kBN;
     // loads move whole 128-row boxes; each epilogue warp stores its own 32 rows
-    if (int rc = make_w_map(&maps[2 * j], J.w_in, J.h1, J.h2, J.ldw, kBM)) return rc;
-    if (int rc = make_w_map(&maps[2 * j + 1], J.w_out, J.h1, J.h2, J.ldw, 32)) return rc;
+    if (int rc = make_w_map(&maps[4 * j], J.w_in, J.h1, J.h2, J.ldw, kBM)) return rc;
+    if (int rc = make_w_map(&maps[4 * j + 1], J.w_out, J.h1, J.h2, J.ldw, 32)) return rc;
+    if (int rc = make_f_map(&maps[4 * j + 2], J.a_packed, mt * kb * kBM)) return rc;
+    if (int rc = make_f_map(&maps[4 * j + 3], J.b_packed, nt * kb * kBN)) return rc;
     std::memset(&tj[j], 0, sizeof(TcJob));
     tj[j].a = static_cast<const uint8_t*>(J.a_packed);
     tj[j].b = static_cast<const uint8_t*>(J.b_packed);
     tj[j].h1 = J.h1;
     tj[j].h2 = J.h2;
-    tj[j].kb = tc_kb(J.rank);
+    tj[j].kb = kb;
     tj[j].rank = J.rank;
     tj[j].scale = J.scale;
-    tj[j].map_in = 2 * j;
-    tj[j].map_out = 2 * j + 1;
+    tj[j].map_in = 4 * j;
+    tj[j].map_out = 4 * j + 1;
+    tj[j].map_a = 4 * j + 2;
+    tj[j].map_b = 4 * j + 3;
+    tj[j].mt = (int32_t)mt;
   }
   std::memcpy(base + maps_b + jobs_b, units.data(), units_b);
   return SDB_OK;
 }
 
-int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank, float sign, int max_ctas,
+int tc_set_mode(int mode) {
+  if (mode < 0 || mode > 2) return fail(SDB_EINVAL, "lora_tc_set_mode: mode must be 0 (auto), 1 (single CTA) or 2 (CTA pair)");
+  const int prev = g_tc_mode;
+  g_tc_mode = mode;
+  return prev;
+}
+
+int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int simt_rank, float sign, int max_ctas,
              cudaStream_t st) {
+  const int kb_max = kb_word & 0xFF, mode = kb_word >> 8;
   if (!blob_dev || n_units <= 0) return fail(SDB_EINVAL, "lora_tc_patch: empty plan");
   if (((uintptr_t)blob_dev) & 127) return fail(SDB_EINVAL, "lora_tc_patch: blob must be 128-B aligned");
   if (kb_max < 1 || kb_max > kMaxKB) return fail(SDB_EINVAL, "lora_tc_patch: kb_max out of range");
-  const size_t maps_b = (size_t)2 * n_jobs * sizeof(CUtensorMap);
+  if (mode != 1 && mode != 2) return fail(SDB_EINVAL, "lora_tc_patch: kb_max word is not from sdb_lora_tc_plan");
+  const size_t maps_b = (size_t)4 * n_jobs * sizeof(CUtensorMap);
   const uint8_t* base = static_cast<const uint8_t*>(blob_dev);
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(base);
   const TcJob* jobs = reinterpret_cast<const TcJob*>(base + maps_b);
   const TcUnit* units = reinterpret_cast<const TcUnit*>(base + maps_b + (size_t)n_jobs * sizeof(TcJob));
-  const int bn = tile_n_for(kb_max);
-  const int fixed = 1024 + kb_max * bn * 128 + kAStages * kABlockBytes + 256;
+  (void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
   const int max_smem = 227 * 1024;
+  if (mode == 2) {
+    const int fixed = 1024 + kb_max * kHalfBlock + kAStages * kABlockBytes + 256;
+    const int slots = std::min(kMaxSlots, (max_smem - fixed) / kBoxBytes);
+    const int smem = fixed + slots * kBoxBytes;
+    cudaFuncSetAttribute(lora_patch_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // persistent grid = the CTA pairs that can be co-resident (TPCs usable by
+    // 2-CTA clusters); launching more would leave a second wave doing the tail
+    static int s_pairs = 0, s_smem = -1;
+    if (s_smem != smem) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(kNumSMs & ~1, 1, 1);
+      cfg.blockDim = dim3(kThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, lora_patch_pair_kernel, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        n = kNumSMs / 2;
+      }
+      s_pairs = std::min(n, kNumSMs / 2);
+      s_smem = smem;
+      if (getenv("SDB_DEBUG")) fprintf(stderr, "sdb: lora_patch_pair_kernel smem %d B, co-resident pairs %d\n", smem, n);
+    }
+    int grid = std::min(2 * n_units, 2 * s_pairs);
+    if (max_ctas > 0) grid = std::min(grid, std::max(2, max_ctas));
+    grid &= ~1;
+    lora_patch_pair_kernel<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
+    return check_launch("lora_patch_pair_kernel");
+  }
+  const int fixed = 1024 + kb_max * kBN * 128 + kAStages * kABlockBytes + 256;
   int slots = std::min(8, (max_smem - fixed) / kBoxBytes);
   if (slots < 2) return fail(SDB_EUNSUP, "lora_tc_patch: rank too large for shared memory");
   const int smem = fixed + slots * kBoxBytes;
   int grid = std::min(n_units, kNumSMs);
   if (max_ctas > 0) grid = std::min(grid, max_ctas);
-  (void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
-  auto kfn = bn == kBN ? lora_patch_tma_kernel<kBN> : lora_patch_tma_kernel<128>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kfn<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
+  cudaFuncSetAttribute(lora_patch_tma_kernel<kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  lora_patch_tma_kernel<kBN><<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
   return check_launch("lora_patch_tma_kernel");
 }
 

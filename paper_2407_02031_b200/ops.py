@@ -7,6 +7,7 @@ tensors — there is deliberately no CPU branch (a CPU tensor raises).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from typing import Optional, Sequence
 
@@ -160,6 +161,21 @@ def tma_eligible(w: torch.Tensor) -> bool:
             and _row_stride(w, "weight") % 8 == 0 and w.data_ptr() % 16 == 0)
 
 
+@contextlib.contextmanager
+def lora_kernel_mode(mode: int):
+    """Force the K1 kernel for LoraTmaPlans built inside the block: 0 auto
+    (single CTA up to stacked rank 128, CTA pair above), 1 single CTA, 2 CTA
+    pair (cta_group::2).  A plan keeps the kernel it was built with."""
+    lib = _lib.lib()
+    prev = lib.sdb_lora_tc_set_mode(int(mode))
+    if prev < 0:
+        _lib.check("sdb_lora_tc_set_mode", prev)
+    try:
+        yield
+    finally:
+        lib.sdb_lora_tc_set_mode(prev)
+
+
 class LoraTmaPlan:
     """K1 fast path for bf16 weights: factors packed once (UMMA K-major
     SWIZZLE_128B tiles), W streamed through a TMA ring, rank contraction on
@@ -242,7 +258,8 @@ class LoraTmaPlan:
         self.blob = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
         self.n_jobs = len(entries)
         self.n_units = n_units.value
-        self.kb_max = kb_max.value
+        self.kb_max = kb_max.value                 # opaque: kb | kernel << 8
+        self.kernel = "pair" if (self.kb_max >> 8) == 2 else "single"
         self.simt_rank = self.max_rank if self.max_rank <= simt_max_rank else 0
         self.simt_rank = 0
         self.path = 1   # 1 = TMA + tcgen05 (0 = the generic SIMT kernel of LoraPatchPlan)

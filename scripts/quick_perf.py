@@ -41,9 +41,13 @@ def lora():
     shadow = allocate_shadow(p)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     out = []
-    for ranks, simt in (([8], 0), ([16], 0), ([64], 0), ([64, 64], 0), ([8, 32, 64, 128], 0)):
+    from paper_2407_02031_b200 import ops
+    modes = [int(m) for m in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "2"])]
+    for (ranks, simt), mode in [(x, m) for x in (([8], 0), ([16], 0), ([64], 0), ([64, 64], 0),
+                                                 ([8, 32, 64, 128], 0)) for m in modes]:
         ads = [(synthetic_lora(p, r, seed=i, adapter_id=f"a{i}"), 0.5) for i, r in enumerate(ranks)]
-        ps = PatchSet(p, ads, shadow=shadow, simt_max_rank=simt)
+        with ops.lora_kernel_mode(mode):
+            ps = PatchSet(p, ads, shadow=shadow, simt_max_rank=simt)
 
         def run():
             flush.zero_()
@@ -51,7 +55,7 @@ def lora():
         flush_ms = time_launch(lambda: flush.zero_())
         ms = time_launch(run) - flush_ms
         gbps = ps.alg_bytes / (ms * 1e-3) / 1e9
-        out.append({"ranks": ranks, "R": ps.rank, "path": [pl.path for pl in ps.plans],
+        out.append({"ranks": ranks, "R": ps.rank, "mode": mode, "path": [pl.path for pl in ps.plans],
                     "ms": round(ms, 3), "alg_GB": round(ps.alg_bytes / 1e9, 3), "GBps": round(gbps, 1),
                     "frac": round(gbps / PEAK, 3)})
         print(json.dumps(out[-1]), flush=True)

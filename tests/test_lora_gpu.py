@@ -282,12 +282,19 @@ def test_torch_device_layer_in_place():
     assert (w - before).abs().max().item() <= 1e-5
 
 
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("ranks", [[8], [16], [24], [64], [64, 64], [8, 32, 64, 128]])
-def test_tma_path_bf16_parity(ranks):
+def test_tma_path_bf16_parity(ranks, mode):
     """The TMA / tcgen05 K1 path (LoraTmaPlan) on SDXL-like shapes incl. ragged
-    edges: <= 1 bf16 ulp of bf16(fp64 reference) + the fp32 dot-product bound;
-    in place and out of place agree bitwise; reruns are bitwise identical."""
-    r = sum(ranks)
+    edges, single-CTA kernel (mode 1) and CTA-pair kernel (mode 2, odd row-tile
+    counts included): <= 1 bf16 ulp of bf16(fp64 reference) + the fp32
+    dot-product bound; in place and out of place agree bitwise; reruns are
+    bitwise identical."""
+    with ops.lora_kernel_mode(mode):
+        _tma_parity(sum(ranks), mode)
+
+
+def _tma_parity(r, mode):
     shapes = [(1280, 1280), (640, 2048), (10240, 1280), (1280, 11520), (320, 2880), (4, 2880), (77, 136),
               (200, 72)]
     g = torch.Generator().manual_seed(r)
@@ -297,7 +304,7 @@ def test_tma_path_bf16_parity(ranks):
     wd = [w.cuda() for w in ws]
     outs = [torch.empty_like(w) for w in wd]
     plan = ops.LoraTmaPlan([(w, o, d.cuda(), u.cuda(), 0.7) for w, o, d, u in zip(wd, outs, ds, us)])
-    assert plan.path == 1
+    assert plan.path == 1 and plan.kernel == ("pair" if mode == 2 else "single")
     plan.launch()
     first = [o.clone() for o in outs]
     plan.launch()
@@ -319,12 +326,35 @@ def test_tma_path_bf16_parity(ranks):
     assert all(torch.equal(w, w0) for w, w0 in zip(wd, [x.cuda() for x in ws]))  # w_in untouched
 
 
-def test_tma_path_grid_cap_same_result():
+@pytest.mark.parametrize("mode,rank", [(1, 128), (2, 128), (2, 232)])
+def test_tma_path_grid_cap_same_result(mode, rank):
     g = torch.Generator().manual_seed(1)
     w = (torch.randn(2560, 1280, generator=g) * 0.02).to(torch.bfloat16).cuda()
-    d = (torch.randn(2560, 128, generator=g) / 11).to(torch.bfloat16).cuda()
-    u = torch.randn(128, 1280, generator=g).to(torch.bfloat16).cuda()
+    d = (torch.randn(2560, rank, generator=g) / 11).to(torch.bfloat16).cuda()
+    u = torch.randn(rank, 1280, generator=g).to(torch.bfloat16).cuda()
     o1, o2 = torch.empty_like(w), torch.empty_like(w)
-    ops.LoraTmaPlan([(w, o1, d, u, 1.0)]).launch()
-    ops.LoraTmaPlan([(w, o2, d, u, 1.0)]).launch(max_ctas=7)
+    with ops.lora_kernel_mode(mode):
+        ops.LoraTmaPlan([(w, o1, d, u, 1.0)]).launch()
+        ops.LoraTmaPlan([(w, o2, d, u, 1.0)]).launch(max_ctas=7)
     assert torch.equal(o1, o2)
+
+
+def test_tma_pair_and_single_kernels_agree():
+    """Both K1 kernels on the same SDXL-shaped set at R = 232: each within the
+    1-ulp parity bound (above); against each other at most 1 bf16 ulp apart
+    (the MMA's fp32 summation order may differ between M=128 and M=256)."""
+    g = torch.Generator().manual_seed(5)
+    shapes = [(1280, 1280), (640, 5760), (320, 2880)]
+    ws = [(torch.randn(a, b, generator=g) * 0.02).to(torch.bfloat16).cuda() for a, b in shapes]
+    ds = [(torch.randn(a, 232, generator=g) / 15).to(torch.bfloat16).cuda() for a, _ in shapes]
+    us = [torch.randn(232, b, generator=g).to(torch.bfloat16).cuda() for _, b in shapes]
+    res = {}
+    for mode in (1, 2):
+        outs = [torch.empty_like(w) for w in ws]
+        with ops.lora_kernel_mode(mode):
+            ops.LoraTmaPlan([(w, o, d, u, 0.5) for w, o, d, u in zip(ws, outs, ds, us)]).launch()
+        res[mode] = outs
+    for a, b in zip(res[1], res[2]):
+        diff = (a.float() - b.float()).abs()
+        ulp = torch.maximum(a.float().abs(), b.float().abs()) * 2.0 ** -7
+        assert bool((diff <= ulp + 1e-30).all())
