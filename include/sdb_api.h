@@ -137,8 +137,8 @@ int sdb_lora_tc_plan(const sdb_lora_tc_job* jobs_host, int n_jobs, void* blob_ho
                      size_t* needed, int* n_units, int* kb_max);
 int sdb_lora_tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt_rank,
                       float sign, int max_ctas, void* stream);
-/* Kernel choice for plans built after the call: 0 auto (single CTA up to
- * rank 128, CTA pair above), 1 single CTA, 2 CTA pair (cta_group::2, B panel
+/* Kernel choice for plans built after the call: 0 auto (= CTA pair, fastest
+ * at every rank), 1 single CTA, 2 CTA pair (cta_group::2, B panel
  * split across the two SMs of a TPC).  Returns the previous mode.  The plan
  * records its kernel in the opaque kb_max word (kb | mode << 8). */
 int sdb_lora_tc_set_mode(int mode);

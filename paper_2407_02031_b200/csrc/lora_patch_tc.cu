@@ -405,20 +405,7 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cl(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\n"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 // both CTAs load into their own smem; bytes complete on the leader's barrier
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
@@ -507,7 +494,7 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
         const TcJob& J = jobs[un.job];
         const CUtensorMap* ma = maps + J.map_a;
         const CUtensorMap* mb = maps + J.map_b;
-        if (b_cnt > 0) mbar_wait_cl(bar(B_EMPTY), (b_cnt - 1) & 1);
+        if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
         if (leader) mbar_expect_tx(bar(B_FULL), 2 * J.kb * kHalfBlock);
         for (int kb = 0; kb < J.kb; ++kb)
           tma_load_2d_pair(smem_u32(sB + kb * kHalfBlock), mb, 0, (un.n_tile * J.kb + kb) * kBN + (int)cta * 128,
@@ -517,7 +504,7 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
           // past the last row tile the follower multiplies a valid (ignored) A tile
           const int mload = std::min(m0 + (int)cta, J.mt - 1);
           for (int kb = 0; kb < J.kb; ++kb) {
-            if (a_round > 0) mbar_wait_cl(bar(A_EMPTY + a_st), (a_round - 1) & 1);
+            if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
             if (leader) mbar_expect_tx(bar(A_FULL + a_st), 2 * kABlockBytes);
             tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.kb + kb) * kBM,
                              mapa_shared(bar(A_FULL + a_st), 0), keep);
@@ -528,9 +515,9 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
       // drain: the leader's last multicast commits must land before this CTA exits
       for (int s = 0; s < kAStages; ++s) {
         const int uses = a_round + (s < a_st ? 1 : 0);
-        if (uses > 0) mbar_wait_cl(bar(A_EMPTY + s), (uses - 1) & 1);
+        if (uses > 0) mbar_wait(bar(A_EMPTY + s), (uses - 1) & 1);
       }
-      if (b_cnt > 0) mbar_wait_cl(bar(B_EMPTY), (b_cnt - 1) & 1);
+      if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
     }
     __syncwarp();
   } else if (warp == kProducerWarp) {
@@ -564,15 +551,15 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
         const int nks = (J.rank + 15) / 16;
-        mbar_wait_cl(bar(B_FULL), b_cnt & 1);
+        mbar_wait(bar(B_FULL), b_cnt & 1);
         for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2, ++tile) {
           const int buf = tile & 1;
-          if (tile >= 2) mbar_wait_cl(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
+          if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem_base + buf * kBN;
           for (int kb = 0; kb < J.kb; ++kb, ++a_cnt) {
             const int st = a_cnt & (kAStages - 1);
-            mbar_wait_cl(bar(A_FULL + st), (a_cnt / kAStages) & 1);
+            mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
             tc_fence_after();
             const int ks_end = std::min(4, nks - kb * 4);
             for (int ks = 0; ks < ks_end; ++ks) {
@@ -605,7 +592,7 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
       for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2, ++tile) {
         const int m = m0 + (int)cta;
         const int buf = tile & 1;
-        mbar_wait_cl(bar(T_FULL + buf), (tile >> 1) & 1);
+        mbar_wait(bar(T_FULL + buf), (tile >> 1) & 1);
         tc_fence_after();
         if (m < un.m_end) {
           for (int bx = 0; bx < nbox; ++bx) {
@@ -881,16 +868,18 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
 }
 
 // Kernel choice.  The B panel (256 x Rpad bf16) stays resident in shared
-// memory: up to rank 128 (64 KB) the single-CTA kernel keeps an 8-slot W
-// ring; above it the panel (128 KB) would squeeze the ring to 4 slots, so
-// the CTA-pair kernel splits the panel across the two CTAs of a TPC (each
-// keeps 8 slots).  sdb_lora_tc_set_mode forces one kernel (tests, probes).
-// The chosen kernel is folded into the plan's opaque kb_max word
-// (kb | mode << 8) so a plan always launches the kernel it was built for.
+// memory.  The single-CTA kernel holds all of it (64 KB at rank 128, 128 KB
+// at 256, which squeezes the W ring to 4 slots); the CTA-pair kernel splits
+// it across the two CTAs of a TPC, keeping 8-10 W slots at every rank.  The
+// pair kernel measured faster at every rank (round 1, SDXL all 794 matrices:
+// R=8 1.91 vs 2.04 ms, R=128 2.00 vs 2.20, R=232 2.43 vs 3.61), so auto = pair;
+// sdb_lora_tc_set_mode forces one kernel (tests, probes).  The chosen kernel
+// is folded into the plan's opaque kb_max word (kb | mode << 8) so a plan
+// always launches the kernel it was built for.
 static int g_tc_mode = 0;   // 0 auto, 1 single CTA, 2 CTA pair
-static int pick_mode(int kb_max) {
+static int pick_mode(int /*kb_max*/) {
   if (g_tc_mode == 1 || g_tc_mode == 2) return g_tc_mode;
-  return kb_max > 2 ? 2 : 1;
+  return 2;
 }
 
 // Blob layout: [maps: 4*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]

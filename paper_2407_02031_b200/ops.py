@@ -164,8 +164,8 @@ def tma_eligible(w: torch.Tensor) -> bool:
 @contextlib.contextmanager
 def lora_kernel_mode(mode: int):
     """Force the K1 kernel for LoraTmaPlans built inside the block: 0 auto
-    (single CTA up to stacked rank 128, CTA pair above), 1 single CTA, 2 CTA
-    pair (cta_group::2).  A plan keeps the kernel it was built with."""
+    (= CTA pair), 1 single CTA, 2 CTA pair (cta_group::2, the B panel split
+    across the two SMs of a TPC).  A plan keeps the kernel it was built with."""
     lib = _lib.lib()
     prev = lib.sdb_lora_tc_set_mode(int(mode))
     if prev < 0:
