@@ -176,6 +176,16 @@ int sdb_residual_inject(void* out, const void* hidden, const void* skip,
                         const void* const* res_ptrs_host, const float* scales_host,
                         int n_res, int64_t pixels, int64_t ch, int64_t cs,
                         int dtype, void* stream);
+/* Same, plus optional fp32 per-channel biases (16-B aligned, may be NULL):
+ *   out[p, 0:ch]     += hidden_bias[0:ch]
+ *   out[p, ch:ch+cs] += skip_bias[0:cs]   (added before the residuals)
+ * — the bias of the convolution that produced hidden / skip, folded here so
+ * the conv needs no separate broadcast bias pass. */
+int sdb_residual_inject_bias(void* out, const void* hidden, const void* skip,
+                             const void* const* res_ptrs_host, const float* scales_host,
+                             int n_res, int64_t pixels, int64_t ch, int64_t cs,
+                             const float* hidden_bias, const float* skip_bias,
+                             int dtype, void* stream);
 
 /* ========================================================================
  * K5 — GEGLU: out[m, 0:f] = proj[m, 0:f] * gelu(proj[m, f:2f]) (exact erf).

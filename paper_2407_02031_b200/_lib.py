@@ -35,6 +35,7 @@ EXPORTED = (
     "sdb_groupnorm_workspace",
     "sdb_groupnorm_silu",
     "sdb_residual_inject",
+    "sdb_residual_inject_bias",
     "sdb_cfg_ddim_step",
 )
 
@@ -93,6 +94,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.sdb_residual_inject.restype = i32
     lib.sdb_residual_inject.argtypes = [vp, vp, vp, ctypes.POINTER(ctypes.c_void_p),
                                         ctypes.POINTER(ctypes.c_float), i32, i64, i64, i64, i32, vp]
+    lib.sdb_residual_inject_bias.restype = i32
+    lib.sdb_residual_inject_bias.argtypes = [vp, vp, vp, ctypes.POINTER(ctypes.c_void_p),
+                                             ctypes.POINTER(ctypes.c_float), i32, i64, i64, i64, vp, vp, i32, vp]
     lib.sdb_cfg_ddim_step.restype = i32
     lib.sdb_cfg_ddim_step.argtypes = [vp, i32, vp, vp, vp, i32, i64, vp, vp, vp]
 

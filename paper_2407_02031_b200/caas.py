@@ -275,12 +275,13 @@ class CaaSNode:
         lat = self.msg[: self.L].view(1, h, h, 4).permute(0, 3, 1, 2)
         self.unet_in.copy_(lat.expand(2, 4, h, h))
         t = self.msg[self.L:self.L + 1]
-        outs = [cn.forward(self.unet_in, t, self.ctx, self.hints[i], self.add_emb[i]) for i, cn in enumerate(self.cns)]
-        for j, v in enumerate(self.views[0]):
-            if len(outs) > 1:   # several ControlNets on this GPU: sum them into the send buffer (K3)
-                self.ops.residual_inject(outs[0][j], [o[j] for o in outs[1:]], [1.0] * (len(outs) - 1), out=v)
-            else:
-                v.copy_(outs[0][j])
+        # the first ControlNet's zero convs write straight into the send buffer;
+        # further ControlNets on this GPU are summed into it in place (K3)
+        outs = [cn.forward(self.unet_in, t, self.ctx, self.hints[i], self.add_emb[i],
+                           outs=self.views[0] if i == 0 else None) for i, cn in enumerate(self.cns)]
+        if len(outs) > 1:
+            for j, v in enumerate(self.views[0]):
+                self.ops.residual_inject(v, [o[j] for o in outs[1:]], [1.0] * (len(outs) - 1), out=v)
 
     def _base_encode(self):
         p = self.pipe

@@ -39,7 +39,7 @@ int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta
 // residual_inject.cu
 int residual_inject(void* out, const void* hidden, const void* skip, const void* const* res,
                     const float* scales, int n_res, int64_t pixels, int64_t ch, int64_t cs,
-                    int dtype, cudaStream_t st);
+                    const float* hidden_bias, const float* skip_bias, int dtype, cudaStream_t st);
 // fused_ops.cu
 int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st);
 int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
@@ -183,8 +183,16 @@ int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* 
 int sdb_residual_inject(void* out, const void* hidden, const void* skip,
                         const void* const* res_ptrs_host, const float* scales_host, int n_res,
                         int64_t pixels, int64_t ch, int64_t cs, int dtype, void* stream) {
-  return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, dtype,
-                         as_stream(stream));
+  return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, nullptr, nullptr,
+                         dtype, as_stream(stream));
+}
+
+int sdb_residual_inject_bias(void* out, const void* hidden, const void* skip,
+                             const void* const* res_ptrs_host, const float* scales_host, int n_res,
+                             int64_t pixels, int64_t ch, int64_t cs, const float* hidden_bias,
+                             const float* skip_bias, int dtype, void* stream) {
+  return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, hidden_bias,
+                         skip_bias, dtype, as_stream(stream));
 }
 
 int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, void* stream) {

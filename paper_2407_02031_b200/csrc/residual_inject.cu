@@ -1,8 +1,12 @@
 // residual_inject.cu — K3: ControlNet residual injection fused with the
 // up-block skip concat (NHWC).
 //
-//   out[p, 0:ch]     = hidden[p, :]
-//   out[p, ch:ch+cs] = skip[p, :] + sum_i s_i * res_i[p, :]
+//   out[p, 0:ch]     = hidden[p, :] (+ hidden_bias[:])
+//   out[p, ch:ch+cs] = skip[p, :] (+ skip_bias[:]) + sum_i s_i * res_i[p, :]
+//
+// The optional fp32 per-channel biases fold the bias of the convolution that
+// produced hidden / skip (cuDNN's channels_last bf16 convolutions would add it
+// in a separate broadcast pass), so a conv -> K3 pair costs no extra pass.
 //
 // The paper adds every ControlNet's down/mid outputs to the UNet's skip
 // connections and middle block; the reference
@@ -28,13 +32,21 @@ struct ResArgs {
   float scale[kMaxRes];
 };
 
+__device__ __forceinline__ void add_bias8(float (&a)[8], const float* __restrict__ b) {
+  const float4 b0 = __ldg(reinterpret_cast<const float4*>(b));
+  const float4 b1 = __ldg(reinterpret_cast<const float4*>(b) + 1);
+  a[0] += b0.x; a[1] += b0.y; a[2] += b0.z; a[3] += b0.w;
+  a[4] += b1.x; a[5] += b1.y; a[6] += b1.z; a[7] += b1.w;
+}
+
 // 32-bit index math (callers guarantee pixels * (ch + cs) / 8 < 2^31): the
 // emulated 64-bit division per vector cost more than the memory traffic.
 template <typename T, int NR>
 __global__ void __launch_bounds__(256)
 residual_inject_kernel(T* out, const T* __restrict__ hidden,
                        const T* skip, ResArgs<T> ra, int n_res,
-                       int64_t pixels, int64_t ch, int64_t cs) {
+                       int64_t pixels, int64_t ch, int64_t cs,
+                       const float* __restrict__ hbias, const float* __restrict__ sbias) {
   const uint32_t vh = (uint32_t)(ch / 8), vs = (uint32_t)(cs / 8), vrow = vh + vs;
   const uint32_t total = (uint32_t)(pixels * vrow);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -43,9 +55,11 @@ residual_inject_kernel(T* out, const T* __restrict__ hidden,
     float a[8];
     if (v < vh) {
       Vec8<T>::load(hidden + p * ch + v * 8, a);
+      if (hbias) add_bias8(a, hbias + v * 8);
     } else {
       const int64_t off = p * cs + (v - vh) * 8;
       Vec8<T>::load(skip + off, a);
+      if (sbias) add_bias8(a, sbias + (v - vh) * 8);
       const int nr = NR > 0 ? NR : n_res;
 #pragma unroll
       for (int r = 0; r < (NR > 0 ? NR : kMaxRes); ++r) {
@@ -64,7 +78,7 @@ residual_inject_kernel(T* out, const T* __restrict__ hidden,
 template <typename T>
 int run_inject(void* out, const void* hidden, const void* skip, const void* const* res,
                const float* scales, int n_res, int64_t pixels, int64_t ch, int64_t cs,
-               cudaStream_t st) {
+               const float* hb, const float* sb, cudaStream_t st) {
   ResArgs<T> ra;
   for (int i = 0; i < kMaxRes; ++i) {
     ra.res[i] = i < n_res ? static_cast<const T*>(res[i]) : nullptr;
@@ -81,11 +95,11 @@ int run_inject(void* out, const void* hidden, const void* skip, const void* cons
   const T* h = static_cast<const T*>(hidden);
   const T* s = static_cast<const T*>(skip);
   switch (n_res) {
-    case 0: residual_inject_kernel<T, 0><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 0, pixels, ch, cs); break;
-    case 1: residual_inject_kernel<T, 1><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 1, pixels, ch, cs); break;
-    case 2: residual_inject_kernel<T, 2><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 2, pixels, ch, cs); break;
-    case 3: residual_inject_kernel<T, 3><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 3, pixels, ch, cs); break;
-    default: residual_inject_kernel<T, -1><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, n_res, pixels, ch, cs); break;
+    case 0: residual_inject_kernel<T, 0><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 0, pixels, ch, cs, hb, sb); break;
+    case 1: residual_inject_kernel<T, 1><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 1, pixels, ch, cs, hb, sb); break;
+    case 2: residual_inject_kernel<T, 2><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 2, pixels, ch, cs, hb, sb); break;
+    case 3: residual_inject_kernel<T, 3><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 3, pixels, ch, cs, hb, sb); break;
+    default: residual_inject_kernel<T, -1><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, n_res, pixels, ch, cs, hb, sb); break;
   }
   return check_launch("residual_inject_kernel");
 }
@@ -94,7 +108,7 @@ int run_inject(void* out, const void* hidden, const void* skip, const void* cons
 
 int residual_inject(void* out, const void* hidden, const void* skip, const void* const* res,
                     const float* scales, int n_res, int64_t pixels, int64_t ch, int64_t cs,
-                    int dtype, cudaStream_t st) {
+                    const float* hidden_bias, const float* skip_bias, int dtype, cudaStream_t st) {
   if (n_res < 0 || n_res > kMaxRes) return fail(SDB_EINVAL, "residual_inject: n_res must be in [0, 8]");
   if (n_res > 0 && (res == nullptr || scales == nullptr))
     return fail(SDB_EINVAL, "residual_inject: residual pointers / scales missing");
@@ -105,11 +119,14 @@ int residual_inject(void* out, const void* hidden, const void* skip, const void*
                     reinterpret_cast<uintptr_t>(hidden);
   for (int i = 0; i < n_res; ++i) align |= reinterpret_cast<uintptr_t>(res[i]);
   if (align & 15) return fail(SDB_EINVAL, "residual_inject: pointers must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(hidden_bias) | reinterpret_cast<uintptr_t>(skip_bias)) & 15)
+    return fail(SDB_EINVAL, "residual_inject: bias vectors must be 16-byte aligned fp32");
+  if (hidden_bias && ch == 0) return fail(SDB_EINVAL, "residual_inject: hidden_bias without hidden channels");
   if (pixels == 0) return SDB_OK;
   switch (dtype) {
-    case SDB_BF16: return run_inject<__nv_bfloat16>(out, hidden, skip, res, scales, n_res, pixels, ch, cs, st);
-    case SDB_F16: return run_inject<__half>(out, hidden, skip, res, scales, n_res, pixels, ch, cs, st);
-    case SDB_F32: return run_inject<float>(out, hidden, skip, res, scales, n_res, pixels, ch, cs, st);
+    case SDB_BF16: return run_inject<__nv_bfloat16>(out, hidden, skip, res, scales, n_res, pixels, ch, cs, hidden_bias, skip_bias, st);
+    case SDB_F16: return run_inject<__half>(out, hidden, skip, res, scales, n_res, pixels, ch, cs, hidden_bias, skip_bias, st);
+    case SDB_F32: return run_inject<float>(out, hidden, skip, res, scales, n_res, pixels, ch, cs, hidden_bias, skip_bias, st);
     default: return fail(SDB_EUNSUP, "residual_inject: unsupported dtype");
   }
 }

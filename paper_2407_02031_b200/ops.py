@@ -359,10 +359,14 @@ def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optiona
 # --------------------------------------------------------------------------
 def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scales: Sequence[float],
                     hidden: Optional[torch.Tensor] = None,
-                    out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                    out: Optional[torch.Tensor] = None,
+                    skip_bias: Optional[torch.Tensor] = None,
+                    hidden_bias: Optional[torch.Tensor] = None) -> torch.Tensor:
     """hidden is None: returns skip + sum s_i r_i (in place into ``out`` or skip).
-    otherwise: returns cat([hidden, skip + sum s_i r_i], dim=C) in channels_last."""
-    require_cuda(skip, hidden, out, *residuals)
+    otherwise: returns cat([hidden, skip + sum s_i r_i], dim=C) in channels_last.
+    skip_bias / hidden_bias: optional contiguous fp32 per-channel vectors added
+    to the skip / hidden part (the producing convolution's bias, folded)."""
+    require_cuda(skip, hidden, out, skip_bias, hidden_bias, *residuals)
     if len(residuals) != len(scales):
         raise ValidationError("one scale per residual")
     n, hw, cs = nhwc_view(skip)
@@ -383,13 +387,24 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
                 out = torch.empty((n, hw, ch + cs), dtype=skip.dtype, device=skip.device)
     elif out is None:
         out = skip
+    for b, cnt, what in ((skip_bias, cs, "skip_bias"), (hidden_bias, ch, "hidden_bias")):
+        if b is not None and (b.dtype != torch.float32 or not b.is_contiguous() or b.numel() != cnt):
+            raise ValidationError(f"{what} must be a contiguous fp32 vector of {cnt} channels")
+    if hidden_bias is not None and hidden is None:
+        raise ValidationError("hidden_bias given without hidden")
     k = len(residuals)
     ptrs = (ctypes.c_void_p * max(k, 1))(*[r.data_ptr() for r in residuals])
     sc = (ctypes.c_float * max(k, 1))(*[float(s) for s in scales])
     _count(1)
-    _lib.check("sdb_residual_inject", _lib.lib().sdb_residual_inject(
-        out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),
-        ptrs, sc, k, n * hw, ch, cs, sdb_dtype(skip), _stream_ptr(None)))
+    if skip_bias is None and hidden_bias is None:
+        _lib.check("sdb_residual_inject", _lib.lib().sdb_residual_inject(
+            out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),
+            ptrs, sc, k, n * hw, ch, cs, sdb_dtype(skip), _stream_ptr(None)))
+    else:
+        _lib.check("sdb_residual_inject_bias", _lib.lib().sdb_residual_inject_bias(
+            out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),
+            ptrs, sc, k, n * hw, ch, cs, hidden_bias.data_ptr() if hidden_bias is not None else None,
+            skip_bias.data_ptr() if skip_bias is not None else None, sdb_dtype(skip), _stream_ptr(None)))
     return out
 
 

@@ -294,15 +294,71 @@ class Net:
         self.p = params
         self.t = params.t
         self._gn_ws: dict = {}
+        self.refresh_biases()
+
+    def refresh_biases(self) -> None:
+        """fp32 per-channel conv biases folded into the consumer kernels.
+
+        cuDNN's channels_last bf16 convolutions add their bias in a separate
+        broadcast pass (one full read + write of the output); instead each 3x3
+        conv runs bias-free and its bias rides on the next kernel: the ResNet
+        conv1 bias on the time-embedding projection (K2's per-(n, c) add), the
+        conv2 + shortcut biases, the up/downsample and conv_in biases on K3.
+        Call again whenever a bias tensor changes (CaaS scales the zero convs)."""
+        t, fb = self.t, {}
+        for k, v in t.items():
+            if k.endswith(".bias") and t.get(k[:-5] + ".weight") is not None and t[k[:-5] + ".weight"].dim() == 4:
+                fb[k[:-5]] = v.float().contiguous()
+        for k in list(t):
+            if k.endswith(".time_emb_proj.weight"):
+                pre = k[: -len(".time_emb_proj.weight")]
+                b = t.get(pre + ".time_emb_proj.bias")
+                c1 = fb.get(pre + ".conv1")
+                if b is not None or c1 is not None:
+                    comb = (b.float() if b is not None else 0) + (c1 if c1 is not None else 0)
+                    fb[pre + ".tproj_bias"] = comb.to(self.p.dtype).contiguous()
+                c2, sc = fb.get(pre + ".conv2"), fb.get(pre + ".conv_shortcut")
+                if c2 is not None or sc is not None:
+                    fb[pre + ".out_bias"] = ((c2 if c2 is not None else 0) + (sc if sc is not None else 0)).contiguous()
+        self.fb = fb
 
     # -- primitives -------------------------------------------------------
     def lin(self, name, x):
         return F.linear(x, self.t[name + ".weight"], self.t.get(name + ".bias"))
 
-    def conv(self, name, x, stride=1):
+    def conv(self, name, x, stride=1, bias=True):
+        """bias=False: the caller folds ``self.fb[name]`` into the next kernel."""
         w = self.t[name + ".weight"]
         pad = w.shape[-1] // 2
-        return F.conv2d(x, w, self.t.get(name + ".bias"), stride=stride, padding=pad)
+        return F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=stride, padding=pad)
+
+    def conv1x1(self, name, x, out=None):
+        """A 1x1 convolution on NHWC storage is a GEMM over pixels: cuBLAS with
+        the bias in its epilogue, optionally straight into ``out`` (an NHWC
+        view, e.g. a slot of the CaaS residual buffer)."""
+        w = self.t[name + ".weight"]
+        n, c, hh, ww = x.shape
+        cout = w.shape[0]
+        x2 = x.permute(0, 2, 3, 1).reshape(n * hh * ww, c)
+        w2 = w.reshape(cout, c)              # channels_last [Cout, 1, 1, Cin] memory == (Cout, Cin)
+        b = self.t.get(name + ".bias")
+        if out is None:
+            y = F.linear(x2, w2, b)
+        else:
+            y = out.permute(0, 2, 3, 1).reshape(n * hh * ww, cout)
+            assert y.data_ptr() == out.data_ptr(), "out must be an NHWC (channels_last) buffer"
+            if b is None:
+                torch.mm(x2, w2.t(), out=y)
+            else:
+                torch.addmm(b, x2, w2.t(), out=y)
+        return y.view(n, hh, ww, cout).permute(0, 3, 1, 2)
+
+    def conv_bias_inplace(self, name, x, stride=1):
+        """3x3 conv whose bias has no fusable consumer: bias-free conv + K3's
+        vectorised in-place per-channel add."""
+        h = self.conv(name, x, stride=stride, bias=False)
+        b = self.fb.get(name)
+        return ops.residual_inject(h, [], [], skip_bias=b) if b is not None else h
 
     def gn(self, name, x, silu, eps=None, add_nc=None):
         # one K2 workspace per (site, shape) of THIS network: graphs of different
@@ -317,12 +373,21 @@ class Net:
 
     # -- blocks -----------------------------------------------------------
     def resnet(self, pre, x, temb_act):
-        h = self.conv(pre + ".conv1", self.gn(pre + ".norm1", x, True))
-        tproj = self.lin(pre + ".time_emb_proj", temb_act).float().contiguous()
+        h = self.conv(pre + ".conv1", self.gn(pre + ".norm1", x, True), bias=False)
+        # conv1's bias rides on the time-embedding projection (tproj_bias = b_temb + b_conv1)
+        tproj = F.linear(temb_act, self.t[pre + ".time_emb_proj.weight"],
+                         self.fb.get(pre + ".tproj_bias")).float().contiguous()
         h = self.gn(pre + ".norm2", h, True, add_nc=tproj)       # fused temb add + GN + SiLU
-        h = self.conv(pre + ".conv2", h)
-        sc = self.conv(pre + ".conv_shortcut", x) if (pre + ".conv_shortcut.weight") in self.t else x
-        return ops.residual_inject(h, [sc], [1.0])          # K3 in-place add (NHWC, vectorised)
+        h = self.conv(pre + ".conv2", h, bias=False)
+        if (pre + ".conv_shortcut.weight") in self.t:
+            w = self.t[pre + ".conv_shortcut.weight"]
+            sc = self.conv1x1(pre + ".conv_shortcut", x) if w.shape[-1] == 1 else \
+                self.conv(pre + ".conv_shortcut", x, bias=False)
+            bias = self.fb.get(pre + ".conv2") if w.shape[-1] == 1 else self.fb.get(pre + ".out_bias")
+        else:
+            sc, bias = x, self.fb.get(pre + ".conv2")
+        # K3 in-place add (NHWC, vectorised) with conv2's (+ shortcut's) bias folded
+        return ops.residual_inject(h, [sc], [1.0], skip_bias=bias)
 
     def attention(self, pre, x, ctx, heads):
         n, l, c = x.shape
@@ -385,9 +450,10 @@ class Net:
     def encode(self, x, temb_act, ctx, hint=None):
         """conv_in + down blocks + mid; returns (mid, [skips])."""
         cfg = self.cfg
-        h = self.conv("conv_in", x)
-        if hint is not None:
-            h = h + hint
+        if hint is not None:   # conv_in + bias + the ControlNet hint in one K3 pass
+            h = ops.residual_inject(self.conv("conv_in", x, bias=False), [hint], [1.0], skip_bias=self.fb.get("conv_in"))
+        else:
+            h = self.conv_bias_inplace("conv_in", x)
         skips = [h]
         n = len(cfg.block_channels)
         for i in range(n):
@@ -397,7 +463,7 @@ class Net:
                     h = self.transformer(f"down.{i}.attn.{j}", h, ctx, cfg.attn_depth[i])
                 skips.append(h)
             if i < n - 1:
-                h = self.conv(f"down.{i}.downsample", h, stride=2)
+                h = self.conv_bias_inplace(f"down.{i}.downsample", h, stride=2)
                 skips.append(h)
         h = self.resnet("mid.res.0", h, temb_act)
         h = self.transformer("mid.attn.0", h, ctx, cfg.mid_depth)
@@ -417,18 +483,21 @@ class UNet(Net):
         rev = list(reversed(cfg.block_channels))
         n = len(rev)
         k = len(skips)
+        hb = None   # pending bias of the upsample conv that produced h (folded into K3's hidden part)
         for i, c in enumerate(rev):
             depth = cfg.attn_depth[n - 1 - i]
             for j in range(cfg.layers_per_block + 1):
                 k -= 1
                 res_k = [r[k] for r in residuals] if nres else []
-                h = ops.residual_inject(skips[k], res_k, res_scales if nres else [], hidden=h)
+                h = ops.residual_inject(skips[k], res_k, res_scales if nres else [], hidden=h, hidden_bias=hb)
+                hb = None
                 h = self.resnet(f"up.{i}.res.{j}", h, temb_act)
                 if depth:
                     h = self.transformer(f"up.{i}.attn.{j}", h, ctx, depth)
             if i < n - 1:
                 h = F.interpolate(h, scale_factor=2.0, mode="nearest")
-                h = self.conv(f"up.{i}.upsample", _cl(h))
+                h = self.conv(f"up.{i}.upsample", _cl(h), bias=False)
+                hb = self.fb.get(f"up.{i}.upsample")
         h = self.gn("conv_norm_out", h, True)
         # eps leaves the UNet in fp32: CFG amplifies (eps_c - eps_u) by the
         # guidance scale, so a bf16 rounding here would dominate the latent error
@@ -453,14 +522,25 @@ class ControlNet(Net):
             h = F.silu(self.conv(f"cond_embedding.blocks.{2 * i + 1}", h, stride=2))
         return self.conv("cond_embedding.conv_out", h)
 
-    def forward(self, x, t, ctx, hint, add_emb=None):
+    def forward(self, x, t, ctx, hint, add_emb=None, outs=None):
         """Returns [down residuals..., mid residual] (unscaled; the
-        conditioning scale is applied by K3 on the consumer side)."""
+        conditioning scale is applied by K3 on the consumer side).  The zero
+        convs are 1x1: cuBLAS GEMMs (bias in the epilogue), written straight
+        into ``outs`` (NHWC views, e.g. the CaaS send buffer) when given."""
         temb_act = self.time_embedding(t, x.shape[0], add_emb)
         h, skips = self.encode(x, temb_act, ctx, hint=hint)
-        outs = [self.conv(f"zero_convs.{k}", s) for k, s in enumerate(skips)]
-        outs.append(self.conv("mid_zero_conv", h))
-        return outs
+        names = [f"zero_convs.{k}" for k in range(len(skips))] + ["mid_zero_conv"]
+        srcs = list(skips) + [h]
+        return [self.zero_conv(nm, s, None if outs is None else outs[k]) for k, (nm, s) in enumerate(zip(names, srcs))]
+
+    def zero_conv(self, name, x, out=None):
+        if self.t[name + ".weight"].shape[-1] == 1:
+            return self.conv1x1(name, x, out)
+        y = self.conv(name, x)
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y
 
 
 def patchable_matrices(params: Params) -> list[tuple[str, torch.Tensor]]:
