@@ -188,6 +188,20 @@ int sdb_residual_inject_bias(void* out, const void* hidden, const void* skip,
                              int dtype, void* stream);
 
 /* ========================================================================
+ * K7 — cross-attention against a short, step-invariant context (Lk <= 128,
+ * e.g. the 77 text tokens), bf16, one pass over the queries:
+ *   o[b, i, h*d:(h+1)*d] = softmax(scale * q_h[i] . k_h^T) v_h
+ * q: [n, lq, heads*d] rows of stride ldq; kv: [n, lk, *] rows of stride ldkv
+ * holding K at column 0 and V at column voff; o: rows of stride ldo.
+ * head_dim in 8..160 (% 8); strides % 8; pointers 16-B aligned.
+ * The UNet's attn2 blocks (the SDPA call of a diffusers-style
+ * Attention); the reference has no attention arithmetic (latency model).
+ * ======================================================================== */
+int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o,
+                        int64_t ldo, int n, int lq, int lk, int heads, int head_dim, float scale, int dtype,
+                        void* stream);
+
+/* ========================================================================
  * K5 — GEGLU: out[m, 0:f] = proj[m, 0:f] * gelu(proj[m, f:2f]) (exact erf).
  * The paper's fused GEGLU; in the reference only the
  * 1.06 sub-multiplier of addonsim/model.py:66-70.  f % 8 == 0.

@@ -264,6 +264,9 @@ class CaaSNode:
                           .contiguous(memory_format=torch.channels_last) for _ in mine]
             self.add_emb = [torch.zeros((2, temb), device=self.device, dtype=dtype) if cfg.addition_embed else None
                             for _ in mine]
+            for cn in self.cns:                      # per-request cross-attention K|V (finish_prepare)
+                cn.enable_kv_cache(self.ctx, ("pristine",))
+                cn.kv_slot = "pristine"
         # loopback (all roles in one process, see LoopbackGroup) runs without a communicator
         self.proto = CaaSProtocol(layout, rank, self.msg, self.flats, pg=self.pg) if dist.is_initialized() else None
         self.graphs = {}
@@ -381,6 +384,7 @@ class CaaSNode:
             self.hints[k].copy_(cn.hint_embedding(imgs[i].to(self.ctx.dtype)))
             if cfg.addition_embed:
                 self.add_emb[k].copy_(cn.add_embedding(extra[0], extra[1]))
+            cn.compute_kv(self.ctx, "pristine")
 
     def prepare(self, latent=None, context=None, images=None, pooled=None, time_ids=None) -> None:
         """Base passes the request; services receive it (their args are ignored)."""
@@ -415,7 +419,7 @@ class CaaSNode:
         timing = p.patch_timing is not None
         p0, ev = p.launch_patch(timing=timing, fetch=fetch)
         if timing:
-            p.patch_timing.append((p0, ev))
+            p.patch_timing.append((p0, p.last_patch_k1_event))
         p.last_first_patched_step = first
         return first, ev
 

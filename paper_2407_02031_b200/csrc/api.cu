@@ -44,6 +44,9 @@ int residual_inject(void* out, const void* hidden, const void* skip, const void*
 int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st);
 int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                   float eps, int dtype, cudaStream_t st);
+// cross_attn.cu
+int cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o, int64_t ldo,
+                    int n, int lq, int lk, int heads, int d, float scale, int dtype, cudaStream_t st);
 // cfg_step.cu
 int cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,
                   int in_dtype, int64_t L, const float* coef, int* step_dev, cudaStream_t st);
@@ -202,6 +205,13 @@ int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, v
 int sdb_add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows,
                       int64_t c, float eps, int dtype, void* stream) {
   return add_layernorm(x, d, y, gamma, beta, rows, c, eps, dtype, as_stream(stream));
+}
+
+int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o,
+                        int64_t ldo, int n, int lq, int lk, int heads, int head_dim, float scale, int dtype,
+                        void* stream) {
+  return cross_attention(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, head_dim, scale, dtype,
+                         as_stream(stream));
 }
 
 int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,

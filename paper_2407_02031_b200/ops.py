@@ -440,6 +440,36 @@ def add_layernorm(x: torch.Tensor, d: Optional[torch.Tensor], gamma: torch.Tenso
 
 
 # --------------------------------------------------------------------------
+# K7 — cross-attention against the short text context
+# --------------------------------------------------------------------------
+def cross_attention_supported(q: torch.Tensor, kv: torch.Tensor, heads: int) -> bool:
+    c = q.shape[-1]
+    d = c // heads
+    return (q.dtype == torch.bfloat16 and kv.dtype == torch.bfloat16 and q.dim() == 3 and kv.dim() == 3
+            and 1 <= kv.shape[1] <= 128 and 8 <= d <= 160 and d % 8 == 0 and c % heads == 0)
+
+
+def cross_attention(q: torch.Tensor, kv: torch.Tensor, heads: int, scale: Optional[float] = None,
+                    out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """softmax(scale * Q K^T) V per head.  q [N, Lq, C] (last dim contiguous),
+    kv [N, Lk, 2C] holding K | V (Lk <= 128), bf16; returns [N, Lq, C]."""
+    require_cuda(q, kv, out)
+    n, lq, c = q.shape
+    if kv.shape[0] != n or kv.shape[2] < 2 * c:
+        raise ValidationError(f"kv must be [N, Lk, 2C] (got {tuple(kv.shape)} for C = {c})")
+    if q.stride(2) != 1 or kv.stride(2) != 1 or q.stride(0) != lq * q.stride(1) or kv.stride(0) != kv.shape[1] * kv.stride(1):
+        raise ValidationError("cross_attention: rows must be contiguous and batch-packed")
+    d = c // heads
+    if out is None:
+        out = torch.empty((n, lq, c), dtype=q.dtype, device=q.device)
+    _count(1)
+    _lib.check("sdb_cross_attention", _lib.lib().sdb_cross_attention(
+        q.data_ptr(), q.stride(1), kv.data_ptr(), kv.stride(1), c, out.data_ptr(), out.stride(1), n, lq,
+        kv.shape[1], heads, d, float(scale if scale is not None else d ** -0.5), sdb_dtype(q), _stream_ptr(None)))
+    return out
+
+
+# --------------------------------------------------------------------------
 # K4 — CFG combine + DDIM step (+ CFG re-batch of the next UNet input)
 # --------------------------------------------------------------------------
 def cfg_ddim_step(eps: torch.Tensor, x: torch.Tensor, coef: torch.Tensor, step_dev: torch.Tensor,

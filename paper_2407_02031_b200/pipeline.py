@@ -103,6 +103,10 @@ class AddonPipeline:
         self.add_emb_unet = torch.zeros((2, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
         self.add_emb_cn = [torch.zeros((2, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
                            for _ in self.cns]
+        # cross-attention K|V per request (pristine) and after the LoRA swap (patched)
+        self.unet.enable_kv_cache(self.ctx, ("pristine", "patched"))
+        for cn in self.cns:
+            cn.enable_kv_cache(self.ctx, ("pristine",))
         tab = ddim_tables(steps, guidance)
         pad = 8  # capture warm-ups advance the step counter past the table end
         t_tab = np.concatenate([tab.timesteps.astype(np.float32), np.full(pad, tab.timesteps[-1], np.float32)])
@@ -124,7 +128,8 @@ class AddonPipeline:
         self.step_ms_est = None
         self.patch_ms_est = None
         self.last_first_patched_step = None
-        self.patch_timing: Optional[list] = None   # bench: (start, end) events of each patch launch
+        self.patch_timing: Optional[list] = None   # bench: (start, K1 end) events of each patch launch
+        self.last_patch_k1_event = None
         self.launches_per_step = 0
 
     # ------------------------------------------------------------------
@@ -135,6 +140,9 @@ class AddonPipeline:
         src = self.shadow if which == "patched" else self._pristine
         for name in self._weight_names():
             self.unet_p.t[name + ".weight"] = src[name]
+        self.unet.kv_slot = which            # the matching cross-attention K|V slot
+        for cn in self.cns:
+            cn.kv_slot = "pristine"
 
     @property
     def _pristine(self) -> dict:
@@ -210,7 +218,8 @@ class AddonPipeline:
 
     def launch_patch(self, timing: bool = False, fetch: bool = True):
         """Enqueue the request's patch on the side streams; returns (start, done)
-        events (start is None unless timing).  Host-resident adapters: fetch on
+        events (start is None unless timing; done = the patched weights AND the
+        request's patched cross-attention K|V are ready).  Host-resident adapters: fetch on
         the copy stream (skipped with fetch=False: the staging already holds
         them), then the captured refresh+patch graph."""
         s = torch.cuda.current_stream(self.device)
@@ -230,8 +239,15 @@ class AddonPipeline:
             if timing:
                 p0.record(self.patch_stream)
             self.patchset.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+        k1 = None
+        if timing:   # end of the patch kernel itself (the bench's live K1 roofline)
+            k1 = torch.cuda.Event(enable_timing=True)
+            k1.record(self.patch_stream)
+        with torch.cuda.stream(self.patch_stream):      # the request's K|V under the patched weights
+            self.unet.compute_kv(self.ctx, "patched", weights=self.shadow)
         ev = torch.cuda.Event(enable_timing=timing)
         ev.record(self.patch_stream)
+        self.last_patch_k1_event = k1
         return p0, ev
 
     def setup(self) -> None:
@@ -289,6 +305,11 @@ class AddonPipeline:
             self.hints[i].copy_(cn.hint_embedding(self.images[i]))
             if self.cfg.addition_embed:
                 self.add_emb_cn[i].copy_(cn.add_embedding(self.pooled, self.time_ids))
+            cn.compute_kv(self.ctx, "pristine")
+        self.unet.compute_kv(self.ctx, "pristine", weights=self._pristine)
+        for net in [self.unet] + self.cns:
+            if net.kv_slot is None:
+                net.kv_slot = "pristine"
         self.step_dev.zero_()
 
     def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None,
@@ -312,7 +333,7 @@ class AddonPipeline:
                 first = boundary + 1
             p0, ev = self.launch_patch(timing=self.patch_timing is not None, fetch=fetch)
             if self.patch_timing is not None:
-                self.patch_timing.append((p0, ev))
+                self.patch_timing.append((p0, self.last_patch_k1_event))
         waited = False
         for step in range(1, self.steps + 1):
             use_patched = patch and step >= first
