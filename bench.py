@@ -325,54 +325,94 @@ def k1_traffic():
 
 
 def other_kernels_roofline(hbm: float) -> list:
-    """The step's HBM-bound kernels at their largest SDXL shapes (CFG batch 2),
-    timed with CUDA events one launch at a time, L2 flushed in between (a
-    >126 MB write).  Algorithmic bytes: one read of every input + one write of
-    every output (K2's second read of x, served from L2, is not counted)."""
+    """The step's HBM-bound kernels at their largest SDXL shapes (CFG batch 2).
+
+    Each kernel is captured REPS times into one CUDA graph, every launch on
+    its own copy of the inputs (ROT copies, > 126 MB in total, so each launch
+    finds its inputs outside L2 — what the UNet's freshly evicted activations
+    look like), and timed as graph replays with CUDA events: device time per
+    launch without host launch overhead.  Algorithmic bytes: one read of every
+    input + one write of every output (K2's second read of x, served from L2,
+    is not counted)."""
     import torch
     from paper_2407_02031_b200 import ops
     dev = "cuda"
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     cl = torch.channels_last
+    L2 = 126 << 20
 
-    def timed(fn, reps=10):
-        fn()
-        ts = []
-        for _ in range(reps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b.record()
-            b.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
+    def timed(make, nbytes_in, reps=24):
+        rot = max(2, -(-2 * L2 // max(nbytes_in, 1)))           # copies spanning > 2x L2
+        rot = min(rot, reps)
+        bufs = [make() for _ in range(rot)]                      # each: a zero-arg launch closure
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for f in bufs:
+                f()
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(reps):
+                bufs[i % rot]()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(3):
+            g.replay()
+        b.record()
+        b.synchronize()
+        ms = a.elapsed_time(b) / (3 * reps)
+        del g, bufs
+        torch.cuda.empty_cache()
+        return ms
 
     out = []
-    x = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
     g, bta = torch.ones(320, device=dev), torch.zeros(320, device=dev)
-    add = torch.zeros(2, 320, device=dev)
-    ws = ops.groupnorm_workspace(x)
-    y = torch.empty_like(x)
-    ms = timed(lambda: ops.groupnorm_silu(x, g, bta, out=y, add_nc=add, workspace=ws))
-    out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16", 2 * x.numel() * 2, ms))
-    tok = torch.randn(2, 4096, 640, device=dev).to(torch.bfloat16)
-    d = torch.randn_like(tok)
+
+    def mk_gn():
+        x = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+        add = torch.zeros(2, 320, device=dev)
+        ws = ops.groupnorm_workspace(x)
+        y = torch.empty_like(x)
+        return lambda: ops.groupnorm_silu(x, g, bta, out=y, add_nc=add, workspace=ws)
+    n_gn = 2 * 320 * 128 * 128
+    out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16", 2 * n_gn * 2, timed(mk_gn, n_gn * 2)))
     lw, lb = torch.ones(640, device=dev, dtype=torch.bfloat16), torch.zeros(640, device=dev, dtype=torch.bfloat16)
-    ms = timed(lambda: ops.add_layernorm(tok, d, lw, lb))
-    out.append(("K6 add+layernorm [2,4096,640] bf16", 4 * tok.numel() * 2, ms))
-    proj = torch.randn(2, 4096, 5120, device=dev).to(torch.bfloat16)
-    ms = timed(lambda: ops.geglu(proj))
-    out.append(("K5 geglu [2,4096,5120]->[...,2560] bf16", proj.numel() * 2 * 3 // 2, ms))
-    hid = torch.randn(2, 640, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
-    skip = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
-    res = [torch.randn_like(skip) for _ in range(2)]
-    ms = timed(lambda: ops.residual_inject(skip, res, [0.8, 0.6], hidden=hid))
-    out.append(("K3 inject 2 residuals + concat [2,640|320,128,128] bf16",
-                (hid.numel() + 3 * skip.numel() + hid.numel() + skip.numel()) * 2, ms))
-    del flush
+
+    def mk_ln():
+        tok = torch.randn(2, 4096, 640, device=dev).to(torch.bfloat16)
+        d = torch.randn_like(tok)
+        return lambda: ops.add_layernorm(tok, d, lw, lb)
+    n_ln = 2 * 4096 * 640
+    out.append(("K6 add+layernorm [2,4096,640] bf16", 4 * n_ln * 2, timed(mk_ln, 2 * n_ln * 2)))
+
+    def mk_geglu():
+        proj = torch.randn(2, 4096, 5120, device=dev).to(torch.bfloat16)
+        return lambda: ops.geglu(proj)
+    n_pj = 2 * 4096 * 5120
+    out.append(("K5 geglu [2,4096,5120]->[...,2560] bf16", n_pj * 2 * 3 // 2, timed(mk_geglu, n_pj * 2)))
+
+    def mk_inject():
+        hid = torch.randn(2, 640, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+        skip = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+        res = [torch.randn_like(skip) for _ in range(2)]
+        outb = torch.empty((2, 960, 128, 128), device=dev, dtype=torch.bfloat16, memory_format=cl)
+        return lambda: ops.residual_inject(skip, res, [0.8, 0.6], hidden=hid, out=outb)
+    nh, ns = 2 * 640 * 128 * 128, 2 * 320 * 128 * 128
+    out.append(("K3 inject 2 residuals + concat [2,640|320,128,128] bf16", (nh + 3 * ns + nh + ns) * 2,
+                timed(mk_inject, (nh + 3 * ns) * 2)))
+
+    def mk_xattn():
+        q = torch.randn(2, 4096, 640, device=dev).to(torch.bfloat16)
+        kv = torch.randn(2, 77, 1280, device=dev).to(torch.bfloat16)
+        o = torch.empty_like(q)
+        return lambda: ops.cross_attention(q, kv, 10, out=o)
+    nq = 2 * 4096 * 640
+    out.append(("K7 cross-attention [2,4096,640] x 77 tokens, 10 heads bf16", 2 * nq * 2, timed(mk_xattn, nq * 2)))
     return [{"kernel": k, "achieved": b / (m * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-             "frac": b / (m * 1e-3) / 1e9 / hbm, "alg_bytes": b, "launch_ms": m} for k, b, m in out]
+             "frac": b / (m * 1e-3) / 1e9 / hbm, "alg_bytes": b, "launch_ms": m,
+             "method": "CUDA-graph replay, inputs rotated over > 2x L2"} for k, b, m in out]
 
 
 def run_ours(args):
