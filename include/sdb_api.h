@@ -161,6 +161,12 @@ size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups)
 int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
                        const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups, float eps,
                        int apply_silu, int dtype, void* workspace, void* stream);
+/* Apply half only: the statistics of x were accumulated into `workspace` by
+ * the kernel that produced x (sdb_residual_inject_gn, same groups, ordered
+ * on the same stream); one read of x, one write of y, one launch. */
+int sdb_groupnorm_apply(const void* x, void* y, const float* gamma, const float* beta,
+                        const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups,
+                        float eps, int apply_silu, int dtype, void* workspace, void* stream);
 
 /* ========================================================================
  * K3 — ControlNet residual injection fused with the up-block concat.
@@ -186,6 +192,18 @@ int sdb_residual_inject_bias(void* out, const void* hidden, const void* skip,
                              int n_res, int64_t pixels, int64_t ch, int64_t cs,
                              const float* hidden_bias, const float* skip_bias,
                              int dtype, void* stream);
+/* K3 + the GroupNorm statistics of its output in the same pass: out is
+ * n x hw pixels of [hidden (+hidden_bias) | skip (+skip_bias) + sum_i
+ * scales[i] * res_i] (NHWC), and the per-(sample, group) moments of the
+ * rounded out are accumulated into gn_workspace (a sdb_groupnorm_workspace
+ * buffer) for a following sdb_groupnorm_apply of out.  n_res <= 4; bf16/fp16.
+ * Used where a ResNet / attention block's residual add, the up-block concat
+ * or a folded conv bias writes the next GroupNorm's input (PAPER.md:572-576:
+ * the fused GN+SiLU; here its statistics pass is fused into the producer). */
+int sdb_residual_inject_gn(void* out, const void* hidden, const void* skip,
+                           const void* const* res_ptrs_host, const float* scales_host, int n_res,
+                           int64_t n, int64_t hw, int64_t ch, int64_t cs, const float* hidden_bias,
+                           const float* skip_bias, int64_t groups, void* gn_workspace, int dtype, void* stream);
 
 /* ========================================================================
  * K7 — cross-attention against a short, step-invariant context (Lk <= 128,

@@ -36,6 +36,8 @@ EXPORTED = (
     "sdb_groupnorm_silu",
     "sdb_residual_inject",
     "sdb_residual_inject_bias",
+    "sdb_residual_inject_gn",
+    "sdb_groupnorm_apply",
     "sdb_cfg_ddim_step",
 )
 
@@ -91,6 +93,11 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.sdb_groupnorm_workspace.argtypes = [i64, i64, i64, i64]
     lib.sdb_groupnorm_silu.restype = i32
     lib.sdb_groupnorm_silu.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, f32, i32, i32, vp, vp]
+    lib.sdb_groupnorm_apply.restype = i32
+    lib.sdb_groupnorm_apply.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64, f32, i32, i32, vp, vp]
+    lib.sdb_residual_inject_gn.restype = i32
+    lib.sdb_residual_inject_gn.argtypes = [vp, vp, vp, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(ctypes.c_float),
+                                           i32, i64, i64, i64, i64, vp, vp, i64, vp, i32, vp]
     lib.sdb_residual_inject.restype = i32
     lib.sdb_residual_inject.argtypes = [vp, vp, vp, ctypes.POINTER(ctypes.c_void_p),
                                         ctypes.POINTER(ctypes.c_float), i32, i64, i64, i64, i32, vp]

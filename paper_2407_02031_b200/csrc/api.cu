@@ -35,7 +35,10 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_max, int simt
 size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
 int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
                    const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype,
-                   void* ws, cudaStream_t st);
+                   void* ws, cudaStream_t st, int stats);
+int residual_inject_gn(void* out, const void* hidden, const void* skip, const void* const* res, const float* scales,
+                       int n_res, int64_t n, int64_t hw, int64_t ch, int64_t cs, const float* hidden_bias,
+                       const float* skip_bias, int64_t groups, void* ws, int dtype, cudaStream_t st);
 // residual_inject.cu
 int residual_inject(void* out, const void* hidden, const void* skip, const void* const* res,
                     const float* scales, int n_res, int64_t pixels, int64_t ch, int64_t cs,
@@ -180,7 +183,22 @@ int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* 
                        const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups,
                        float eps, int apply_silu, int dtype, void* workspace, void* stream) {
   return groupnorm_silu(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, apply_silu, dtype, workspace,
-                        as_stream(stream));
+                        as_stream(stream), 1);
+}
+
+int sdb_groupnorm_apply(const void* x, void* y, const float* gamma, const float* beta,
+                        const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups,
+                        float eps, int apply_silu, int dtype, void* workspace, void* stream) {
+  return groupnorm_silu(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, apply_silu, dtype, workspace,
+                        as_stream(stream), 0);
+}
+
+int sdb_residual_inject_gn(void* out, const void* hidden, const void* skip,
+                           const void* const* res_ptrs_host, const float* scales_host, int n_res,
+                           int64_t n, int64_t hw, int64_t ch, int64_t cs, const float* hidden_bias,
+                           const float* skip_bias, int64_t groups, void* gn_workspace, int dtype, void* stream) {
+  return residual_inject_gn(out, hidden, skip, res_ptrs_host, scales_host, n_res, n, hw, ch, cs, hidden_bias,
+                            skip_bias, groups, gn_workspace, dtype, as_stream(stream));
 }
 
 int sdb_residual_inject(void* out, const void* hidden, const void* skip,

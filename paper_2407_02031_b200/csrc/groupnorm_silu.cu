@@ -52,14 +52,47 @@ constexpr int kMaxThreads = 512;
 constexpr int kMaxN = 64;
 constexpr int kMaxGroups = 64;
 constexpr int kTileMax = 80 * 1024;          // chunk bytes per CTA (2 CTAs / SM)
-constexpr int kBankDoubles = kMaxN * kMaxGroups * 2;
+// Statistics bank: kSlots independent copies of the (n, group) fp64 moments;
+// chunk b of a sample adds into slot b % kSlots, so at most
+// ceil(chunks / kSlots) CTAs contend for one L2 atomic address (one copy
+// serialised ~150 fp64 atomics per address at the SDXL 128^2 sites).
+// The layout is fixed ([kMaxN][slot][kMaxGroups][2]); a launch zeroes the
+// idle bank's rows up to the largest batch seen (WsHeader::hwm), so one
+// workspace may serve calls of different shapes.
+constexpr int kSlots = 8;
+constexpr int kBankDoubles = kSlots * kMaxN * kMaxGroups * 2;   // 512 KB
 constexpr size_t kWsHeader = 256;            // epoch (u32) | cur (u32) | pad
-constexpr size_t kWsBytes = kWsHeader + 2 * kBankDoubles * sizeof(double);
+constexpr size_t kWsBytes = kWsHeader + 2 * (size_t)kBankDoubles * sizeof(double);
+__host__ __device__ __forceinline__ size_t bank_index(int slot, int n, int g) {
+  return (((size_t)n * kSlots + slot) * kMaxGroups + g) * 2;   // [n][slot][group][2]
+}
 
 struct WsHeader {
   unsigned int epoch;
   unsigned int cur;
+  unsigned int hwm;   // largest batch ever accumulated: rows >= hwm of both banks are still zero
 };
+
+// Zero rows [0, max(hwm, N)) of the idle bank (a grid-strided slice per CTA)
+// and publish this launch's bank; returns the bank to accumulate into.
+__device__ __forceinline__ double* claim_bank(uint8_t* ws, int nbatch) {
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+  const unsigned int epoch = *reinterpret_cast<volatile unsigned int*>(&hdr->epoch);
+  const int hwm = (int)*reinterpret_cast<volatile unsigned int*>(&hdr->hwm);
+  const int rows = max(hwm, nbatch);
+  double* bank = reinterpret_cast<double*>(ws + kWsHeader) + (size_t)(epoch & 1u) * kBankDoubles;
+  double2* o2 = reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + kWsHeader) +
+                                           (size_t)((epoch + 1u) & 1u) * kBankDoubles);
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  const int ctas = gridDim.x * gridDim.y;
+  const int total = rows * kSlots * kMaxGroups;   // double2 entries
+  for (int i = cta * blockDim.x + threadIdx.x; i < total; i += ctas * blockDim.x) o2[i] = make_double2(0.0, 0.0);
+  if (cta == 0 && threadIdx.x == 0) {
+    hdr->cur = epoch & 1u;
+    hdr->hwm = (unsigned int)rows;
+  }
+  return bank;
+}
 
 struct GnShape {
   int64_t n, hw, c, groups, cv, cpg, es;
@@ -132,16 +165,8 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8
   load_chunk<T>(tile, xs, pbeg, m, c, &bar, policy_evict_last());
 
   // accumulator bank of this launch; zero the other one (a grid-strided slice per CTA)
-  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
-  const unsigned int epoch = *reinterpret_cast<volatile unsigned int*>(&hdr->epoch);
-  double* bank = reinterpret_cast<double*>(ws + kWsHeader) + (size_t)(epoch & 1u) * kBankDoubles;
-  double* other = reinterpret_cast<double*>(ws + kWsHeader) + (size_t)((epoch + 1u) & 1u) * kBankDoubles;
-  {
-    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
-    const int ctas = gridDim.x * gridDim.y;
-    for (int i = cta * blockDim.x + threadIdx.x; i < kBankDoubles; i += ctas * blockDim.x) other[i] = 0.0;
-    if (cta == 0 && threadIdx.x == 0) hdr->cur = epoch & 1u;
-  }
+  double* bank = claim_bank(ws, gridDim.y);
+  double* mine = bank + bank_index(blockIdx.x % kSlots, n, 0);
   int g8[8];
   channel_groups(c0, cpg, g8);
   __syncthreads();            // barrier init visible before anyone waits on it
@@ -205,8 +230,8 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8
       m2 += __shfl_xor_sync(0xffffffffu, m2, o);
     }
     if (lane == 0) {
-      atomicAdd(bank + (n * kMaxGroups + g) * 2 + 0, m1);
-      atomicAdd(bank + (n * kMaxGroups + g) * 2 + 1, m2);
+      atomicAdd(mine + g * 2 + 0, m1);
+      atomicAdd(mine + g * 2 + 1, m2);
     }
   }
 }
@@ -234,8 +259,16 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
   if (threadIdx.x < groups) {
     const unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&hdr->cur);
     const double* bank = reinterpret_cast<const double*>(ws + kWsHeader) + (size_t)cur * kBankDoubles;
-    const double m1 = __ldcg(bank + (n * kMaxGroups + threadIdx.x) * 2 + 0);
-    const double m2 = __ldcg(bank + (n * kMaxGroups + threadIdx.x) * 2 + 1);
+    double2 p[kSlots];
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl)   // all slot loads in flight at once (unused slots are zero)
+      p[sl] = __ldcg(reinterpret_cast<const double2*>(bank + bank_index(sl, n, threadIdx.x)));
+    double m1 = 0.0, m2 = 0.0;
+#pragma unroll
+    for (int sl = 0; sl < kSlots; ++sl) {
+      m1 += p[sl].x;
+      m2 += p[sl].y;
+    }
     const double cnt = (double)hw * (double)cpg;
     const double mean = m1 / cnt;
     double var = m2 / cnt - mean * mean;
@@ -297,16 +330,139 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
   }
 }
 
+// ---- K3 + GroupNorm statistics in one pass ---------------------------------
+// The input of 29 of SDXL's 46 GN sites is written by K3 (a ResNet / attention
+// block's residual add, the up-block concat, a folded conv bias).  This
+// kernel IS that K3 pass — out = [hidden (+hb) | skip (+sb) + sum s_i res_i] —
+// and accumulates the GroupNorm moments of the rounded output into the GN
+// site's workspace bank on the way (fp64 raw moments, same epoch protocol as
+// gn_stats_kernel), so that site runs gn_apply_kernel alone: one full read of
+// the feature map and one launch less per site.  Per thread the sums are raw
+// fp32 over <= ~30 rows (relative error ~1e-6 of sum x^2, i.e. a variance
+// error ~1e-6 (1 + mean^2/var) — the UNet's post-residual activations sit at
+// |mean| / std = O(1); the two-pass gn_stats_kernel keeps shifted sums for
+// arbitrary inputs).  One resident wave of CTAs, each a few row batches whose
+// loads are all issued before any store (out may alias skip).
+constexpr int kInjMaxRes = 4;
 template <typename T>
-int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, const float* add_nc, int64_t n,
-           int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* wsv, cudaStream_t st) {
-  const T* x = static_cast<const T*>(xv);
-  T* y = static_cast<T*>(yv);
-  uint8_t* ws = static_cast<uint8_t*>(wsv);
-  GnShape s = gn_shape(n, hw, c, groups, sizeof(T));
-  dim3 grid((unsigned)s.chunks, (unsigned)n);
-  const size_t smem_stats = s.tile_bytes + (size_t)s.rpp * c * 2 * sizeof(float);
-  const size_t smem_apply = s.tile_bytes;
+struct InjArgs {
+  const T* res[kInjMaxRes];
+  float scale[kInjMaxRes];
+};
+
+template <typename T, int NR>
+__global__ void __launch_bounds__(kMaxThreads)
+inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T> ra, const float* __restrict__ hb,
+                 const float* __restrict__ sb, uint8_t* __restrict__ ws, int hw, int ch, int cs, int groups, int cpg,
+                 int rows_per_chunk, int rpp) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int c = ch + cs;
+  float* red1 = reinterpret_cast<float*>(smem);   // [rpp][c]
+  float* red2 = red1 + rpp * c;                    // [rpp][c]
+  const int n = blockIdx.y;
+  const int cv = c >> 3, vh = ch >> 3;
+  const int v = threadIdx.x % cv;
+  const int r = threadIdx.x / cv;
+  const int c0 = v * 8;
+  const int pbeg = blockIdx.x * rows_per_chunk;
+  const int m = min(hw, pbeg + rows_per_chunk) - pbeg;
+  const int p0 = n * hw + pbeg;                    // first pixel of the chunk (global pixel index)
+  double* bank = claim_bank(ws, gridDim.y);
+
+  constexpr int kB = 4;
+  const bool hid_lane = v < vh;
+  const T* src0 = hid_lane ? hidden + c0 : skip + (c0 - ch);
+  const int ld0 = hid_lane ? ch : cs;
+  const float* bias = hid_lane ? (hb ? hb + c0 : nullptr) : (sb ? sb + (c0 - ch) : nullptr);
+  float bv[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) bv[j] = bias ? bias[j] : 0.f;
+  float2 s1[4], s2[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) s1[i] = s2[i] = make_float2(0.f, 0.f);
+  for (int row0 = r; row0 < m; row0 += kB * rpp) {
+    Raw8<T> q0[kB], qr[kB][NR > 0 ? NR : 1];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const int row = row0 + b * rpp;
+      if (row < m) {
+        const size_t p = (size_t)(p0 + row);
+        q0[b] = load_raw<T>(src0 + p * ld0);
+        if (!hid_lane) {
+#pragma unroll
+          for (int i = 0; i < NR; ++i) qr[b][i] = load_raw<T>(ra.res[i] + p * cs + (c0 - ch));
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const int row = row0 + b * rpp;
+      if (row < m) {
+        float a[8];
+        unpack<T>(q0[b], a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += bv[j];
+        if (!hid_lane) {
+#pragma unroll
+          for (int i = 0; i < NR; ++i) {
+            float rb[8];
+            unpack<T>(qr[b][i], rb);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = fmaf(ra.scale[i], rb[j], a[j]);
+          }
+        }
+        Raw8<T> q;
+        Vec8Half<int>::store(reinterpret_cast<T*>(&q.u), a);   // round once, as stored
+        store_raw<T>(out + (size_t)(p0 + row) * c + c0, q);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = get_pair<T>(q, i);
+          s1[i] = f2add(s1[i], f);
+          s2[i] = f2fma(f, f, s2[i]);
+        }
+      }
+    }
+  }
+  *reinterpret_cast<float4*>(red1 + r * c + c0) = make_float4(s1[0].x, s1[0].y, s1[1].x, s1[1].y);
+  *reinterpret_cast<float4*>(red1 + r * c + c0 + 4) = make_float4(s1[2].x, s1[2].y, s1[3].x, s1[3].y);
+  *reinterpret_cast<float4*>(red2 + r * c + c0) = make_float4(s2[0].x, s2[0].y, s2[1].x, s2[1].y);
+  *reinterpret_cast<float4*>(red2 + r * c + c0 + 4) = make_float4(s2[2].x, s2[2].y, s2[3].x, s2[3].y);
+  __syncthreads();
+  if (rpp > 1) {
+    for (int chn = threadIdx.x; chn < c; chn += blockDim.x) {
+      float a1 = red1[chn], a2 = red2[chn];
+      for (int rr = 1; rr < rpp; ++rr) {
+        a1 += red1[rr * c + chn];
+        a2 += red2[rr * c + chn];
+      }
+      red1[chn] = a1;
+      red2[chn] = a2;
+    }
+    __syncthreads();
+  }
+  // one warp per group: lanes over its channels (fp64), shuffle-reduce, slotted atomics
+  double* mine = bank + bank_index(blockIdx.x % kSlots, n, 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int g = warp; warp < nwarps && g < groups; g += nwarps) {
+    double m1 = 0.0, m2 = 0.0;
+    for (int k = lane; k < cpg; k += 32) {
+      m1 += (double)red1[g * cpg + k];
+      m2 += (double)red2[g * cpg + k];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    }
+    if (lane == 0) {
+      atomicAdd(mine + g * 2 + 0, m1);
+      atomicAdd(mine + g * 2 + 1, m2);
+    }
+  }
+}
+
+template <typename T>
+void gn_attrs() {
   // opt in to > 48 KB of dynamic shared memory once per device
   static unsigned long long attr_done = 0;
   int dev = 0;
@@ -318,17 +474,81 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, cons
     cudaFuncSetAttribute(gn_apply_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     attr_done |= 1ull << dev;
   }
-  const int ihw = (int)hw, ic = (int)c, ig = (int)groups, icpg = (int)s.cpg, irows = (int)s.rows_per_chunk;
-  gn_stats_kernel<T><<<grid, s.threads, smem_stats, st>>>(x, add_nc, ws, ihw, ic, ig, icpg, irows, s.rpp,
-                                                          s.tile_bytes);
-  if (int rc = check_launch("gn_stats_kernel")) return rc;
+}
+
+template <typename T>
+int run_apply(const T* x, T* y, const float* gamma, const float* beta, const float* add_nc, const GnShape& s,
+              float eps, int silu, uint8_t* ws, cudaStream_t st) {
+  dim3 grid((unsigned)s.chunks, (unsigned)s.n);
+  const int ihw = (int)s.hw, ic = (int)s.c, ig = (int)s.groups, icpg = (int)s.cpg, irows = (int)s.rows_per_chunk;
   if (silu)
-    gn_apply_kernel<T, true><<<grid, s.threads, smem_apply, st>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, ig, icpg,
-                                                                  irows, s.rpp, eps);
-  else
-    gn_apply_kernel<T, false><<<grid, s.threads, smem_apply, st>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, ig,
+    gn_apply_kernel<T, true><<<grid, s.threads, s.tile_bytes, st>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, ig,
                                                                    icpg, irows, s.rpp, eps);
+  else
+    gn_apply_kernel<T, false><<<grid, s.threads, s.tile_bytes, st>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, ig,
+                                                                    icpg, irows, s.rpp, eps);
   return check_launch("gn_apply_kernel");
+}
+
+template <typename T>
+int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, const float* add_nc, int64_t n,
+           int64_t hw, int64_t c, int64_t groups, float eps, int silu, void* wsv, cudaStream_t st, bool stats) {
+  const T* x = static_cast<const T*>(xv);
+  T* y = static_cast<T*>(yv);
+  uint8_t* ws = static_cast<uint8_t*>(wsv);
+  GnShape s = gn_shape(n, hw, c, groups, sizeof(T));
+  gn_attrs<T>();
+  if (stats) {
+    dim3 grid((unsigned)s.chunks, (unsigned)n);
+    const size_t smem_stats = s.tile_bytes + (size_t)s.rpp * c * 2 * sizeof(float);
+    gn_stats_kernel<T><<<grid, s.threads, smem_stats, st>>>(x, add_nc, ws, (int)hw, (int)c, (int)groups, (int)s.cpg,
+                                                            (int)s.rows_per_chunk, s.rpp, s.tile_bytes);
+    if (int rc = check_launch("gn_stats_kernel")) return rc;
+  }
+  return run_apply<T>(x, y, gamma, beta, add_nc, s, eps, silu, ws, st);
+}
+
+template <typename T>
+int run_inject_gn(void* out, const void* hidden, const void* skip, const void* const* res, const float* scales,
+                  int n_res, int64_t n, int64_t hw, int64_t ch, int64_t cs, const float* hb, const float* sb,
+                  int64_t groups, void* ws, cudaStream_t st) {
+  const int64_t c = ch + cs;
+  InjArgs<T> ra;
+  for (int i = 0; i < kInjMaxRes; ++i) {
+    ra.res[i] = i < n_res ? static_cast<const T*>(res[i]) : nullptr;
+    ra.scale[i] = i < n_res ? scales[i] : 0.f;
+  }
+  const int cv = (int)(c / 8);
+  const int rpp = std::max(1, 256 / cv);
+  const int threads = cv * rpp;
+  // one resident wave (~2 CTAs per SM over the batch), each CTA a few row
+  // batches: the per-CTA statistics epilogue is paid ~2x per SM, not per row
+  const int64_t want = std::max<int64_t>(1, (2 * kNumSMs + n - 1) / n);
+  const int64_t rpc = std::max<int64_t>(1, (hw + want - 1) / want);
+  const int64_t chunks = (hw + rpc - 1) / rpc;
+  const size_t smem = (size_t)2 * rpp * c * sizeof(float);
+  dim3 grid((unsigned)chunks, (unsigned)n);
+  T* o = static_cast<T*>(out);
+  const T* h = static_cast<const T*>(hidden);
+  const T* sk = static_cast<const T*>(skip);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  const int ihw = (int)hw, ich = (int)ch, ics = (int)cs, ig = (int)groups, icpg = (int)(c / groups), irpc = (int)rpc;
+  switch (n_res) {
+#define SDB_INJ(NR)                                                                                          \
+  case NR:                                                                                                   \
+    cudaFuncSetAttribute(inject_gn_kernel<T, NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    inject_gn_kernel<T, NR><<<grid, threads, smem, st>>>(o, h, sk, ra, hb, sb, w, ihw, ich, ics, ig, icpg, irpc, \
+                                                         rpp);                                               \
+    break;
+    SDB_INJ(0)
+    SDB_INJ(1)
+    SDB_INJ(2)
+    SDB_INJ(3)
+    SDB_INJ(4)
+#undef SDB_INJ
+    default: return fail(SDB_EINVAL, "residual_inject_gn: at most 4 residuals");
+  }
+  return check_launch("inject_gn_kernel");
 }
 
 }  // namespace
@@ -341,26 +561,57 @@ size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
   return kWsBytes;
 }
 
-int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc, int64_t n,
-                   int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, void* ws,
-                   cudaStream_t st) {
+static int gn_checks(const void* x, const void* y, int64_t n, int64_t hw, int64_t c, int64_t groups, const void* ws) {
   if (n <= 0 || hw <= 0 || c <= 0 || groups <= 0) return fail(SDB_EINVAL, "groupnorm: empty shape");
   if (n > kMaxN) return fail(SDB_EINVAL, "groupnorm: batch > 64 unsupported");
   if (c % groups != 0) return fail(SDB_EINVAL, "groupnorm: channels not divisible by groups");
   if (groups > kMaxGroups) return fail(SDB_EINVAL, "groupnorm: more than 64 groups");
   if (c % 8 != 0) return fail(SDB_EINVAL, "groupnorm: channels must be a multiple of 8");
   if (c / 8 > kMaxThreads) return fail(SDB_EINVAL, "groupnorm: channels > 4096 unsupported");
-  if (hw * c >= (int64_t)INT32_MAX - 8 * c)
-    return fail(SDB_EINVAL, "groupnorm: one sample must hold < 2^31 elements");
+  if (n * hw * c >= (int64_t)INT32_MAX - 8 * c)
+    return fail(SDB_EINVAL, "groupnorm: the batch must hold < 2^31 elements");
   if (((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) != 0)
     return fail(SDB_EINVAL, "groupnorm: x and y must be 16-byte aligned");
   if (ws == nullptr) return fail(SDB_EINVAL, "groupnorm: workspace is NULL");
   if ((reinterpret_cast<uintptr_t>(ws) & 15) != 0) return fail(SDB_EINVAL, "groupnorm: workspace must be 16-byte aligned");
+  return SDB_OK;
+}
+
+int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc, int64_t n,
+                   int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, void* ws,
+                   cudaStream_t st, int stats) {
+  if (int rc = gn_checks(x, y, n, hw, c, groups, ws)) return rc;
   switch (dtype) {
-    case SDB_BF16: return run_gn<__nv_bfloat16>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
-    case SDB_F16: return run_gn<__half>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
-    case SDB_F32: return run_gn<float>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st);
+    case SDB_BF16:
+      return run_gn<__nv_bfloat16>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st, stats != 0);
+    case SDB_F16: return run_gn<__half>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st, stats != 0);
+    case SDB_F32: return run_gn<float>(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, ws, st, stats != 0);
     default: return fail(SDB_EUNSUP, "groupnorm: unsupported dtype");
+  }
+}
+
+int residual_inject_gn(void* out, const void* hidden, const void* skip, const void* const* res, const float* scales,
+                       int n_res, int64_t n, int64_t hw, int64_t ch, int64_t cs, const float* hidden_bias,
+                       const float* skip_bias, int64_t groups, void* ws, int dtype, cudaStream_t st) {
+  if (int rc = gn_checks(out, skip, n, hw, ch + cs, groups, ws)) return rc;
+  if (n_res < 0 || n_res > kInjMaxRes) return fail(SDB_EINVAL, "residual_inject_gn: n_res must be in [0, 4]");
+  if (n_res > 0 && (res == nullptr || scales == nullptr))
+    return fail(SDB_EINVAL, "residual_inject_gn: residual pointers / scales missing");
+  if (ch % 8 != 0 || cs % 8 != 0 || cs <= 0)
+    return fail(SDB_EINVAL, "residual_inject_gn: channel counts must be positive multiples of 8");
+  if (ch > 0 && hidden == nullptr) return fail(SDB_EINVAL, "residual_inject_gn: hidden is NULL with ch > 0");
+  uintptr_t align = reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(hidden_bias) |
+                    reinterpret_cast<uintptr_t>(skip_bias);
+  for (int i = 0; i < n_res; ++i) align |= reinterpret_cast<uintptr_t>(res[i]);
+  if (align & 15) return fail(SDB_EINVAL, "residual_inject_gn: pointers must be 16-byte aligned");
+  switch (dtype) {
+    case SDB_BF16:
+      return run_inject_gn<__nv_bfloat16>(out, hidden, skip, res, scales, n_res, n, hw, ch, cs, hidden_bias,
+                                          skip_bias, groups, ws, st);
+    case SDB_F16:
+      return run_inject_gn<__half>(out, hidden, skip, res, scales, n_res, n, hw, ch, cs, hidden_bias, skip_bias,
+                                   groups, ws, st);
+    default: return fail(SDB_EUNSUP, "residual_inject_gn: bf16 / fp16 only");
   }
 }
 

@@ -338,6 +338,16 @@ def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optiona
             raise ValidationError("gamma / beta / add_nc must be contiguous fp32")
     if add_nc is not None and add_nc.numel() != n * c:
         raise ValidationError(f"add_nc must hold N*C = {n * c} values")
+    pending = getattr(x, "_sdb_gn", None)
+    if pending is not None and pending[1] == groups and pending[2] == x.data_ptr():
+        # x's statistics were accumulated by the K3 pass that wrote it: apply only
+        _count(1)
+        _lib.check("sdb_groupnorm_apply", _lib.lib().sdb_groupnorm_apply(
+            x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,
+            beta.data_ptr() if beta is not None else None,
+            add_nc.data_ptr() if add_nc is not None else None, n, hw, c, groups, float(eps), int(silu),
+            sdb_dtype(x), pending[0].data_ptr(), _stream_ptr(None)))
+        return out
     ws_bytes = _lib.lib().sdb_groupnorm_workspace(n, hw, c, groups)
     if workspace is not None:
         if workspace.numel() < ws_bytes:
@@ -361,11 +371,15 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
                     hidden: Optional[torch.Tensor] = None,
                     out: Optional[torch.Tensor] = None,
                     skip_bias: Optional[torch.Tensor] = None,
-                    hidden_bias: Optional[torch.Tensor] = None) -> torch.Tensor:
+                    hidden_bias: Optional[torch.Tensor] = None,
+                    gn_workspace: Optional[torch.Tensor] = None, groups: int = 32) -> torch.Tensor:
     """hidden is None: returns skip + sum s_i r_i (in place into ``out`` or skip).
     otherwise: returns cat([hidden, skip + sum s_i r_i], dim=C) in channels_last.
     skip_bias / hidden_bias: optional contiguous fp32 per-channel vectors added
-    to the skip / hidden part (the producing convolution's bias, folded)."""
+    to the skip / hidden part (the producing convolution's bias, folded).
+    gn_workspace: a ``groupnorm_workspace`` buffer — the same pass also
+    accumulates the GroupNorm(groups) statistics of the output, and the next
+    ``groupnorm_silu`` of the returned tensor runs its apply half only."""
     require_cuda(skip, hidden, out, skip_bias, hidden_bias, *residuals)
     if len(residuals) != len(scales):
         raise ValidationError("one scale per residual")
@@ -396,6 +410,17 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
     ptrs = (ctypes.c_void_p * max(k, 1))(*[r.data_ptr() for r in residuals])
     sc = (ctypes.c_float * max(k, 1))(*[float(s) for s in scales])
     _count(1)
+    if gn_workspace is not None and skip.dim() == 4 and k <= 4 and skip.dtype in (torch.bfloat16, torch.float16) \
+            and (ch + cs) % groups == 0:
+        _lib.check("sdb_residual_inject_gn", _lib.lib().sdb_residual_inject_gn(
+            out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(), ptrs, sc, k,
+            n, hw, ch, cs, hidden_bias.data_ptr() if hidden_bias is not None else None,
+            skip_bias.data_ptr() if skip_bias is not None else None, groups, gn_workspace.data_ptr(),
+            sdb_dtype(skip), _stream_ptr(None)))
+        out._sdb_gn = (gn_workspace, groups, out.data_ptr())
+        return out
+    if hasattr(out, "_sdb_gn"):
+        del out._sdb_gn      # rewritten without statistics
     if skip_bias is None and hidden_bias is None:
         _lib.check("sdb_residual_inject", _lib.lib().sdb_residual_inject(
             out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(),

@@ -385,8 +385,17 @@ class Net:
         """3x3 conv whose bias has no fusable consumer: bias-free conv + K3's
         vectorised in-place per-channel add."""
         h = self.conv(name, x, stride=stride, bias=False)
-        b = self.fb.get(name)
-        return ops.residual_inject(h, [], [], skip_bias=b) if b is not None else h
+        return ops.residual_inject(h, [], [], skip_bias=self.fb.get(name), gn_workspace=self.k3ws(name, h),
+                                   groups=self.cfg.groups)
+
+    def k3ws(self, key, x):
+        """GroupNorm-statistics workspace of one K3 call site whose output is
+        the next GroupNorm's input (the K3 pass accumulates its statistics)."""
+        k = ("k3", key, tuple(x.shape))
+        ws = self._gn_ws.get(k)
+        if ws is None:
+            ws = self._gn_ws[k] = ops.groupnorm_workspace(x, self.cfg.groups)
+        return ws
 
     def gn(self, name, x, silu, eps=None, add_nc=None):
         # one K2 workspace per (site, shape) of THIS network: graphs of different
@@ -414,8 +423,10 @@ class Net:
             bias = self.fb.get(pre + ".conv2") if w.shape[-1] == 1 else self.fb.get(pre + ".out_bias")
         else:
             sc, bias = x, self.fb.get(pre + ".conv2")
-        # K3 in-place add (NHWC, vectorised) with conv2's (+ shortcut's) bias folded
-        return ops.residual_inject(h, [sc], [1.0], skip_bias=bias)
+        # K3 in-place add (NHWC, vectorised) with conv2's (+ shortcut's) bias folded,
+        # accumulating the next GroupNorm's statistics of the block output
+        return ops.residual_inject(h, [sc], [1.0], skip_bias=bias, gn_workspace=self.k3ws(pre, h),
+                                   groups=self.cfg.groups)
 
     def attention(self, pre, x, ctx, heads):
         n, l, c = x.shape
@@ -460,7 +471,7 @@ class Net:
         tok = ops.residual_inject(tok, [delta], [1.0])
         tok = self.lin(pre + ".proj_out", tok)
         out = tok.view(n, h, w, c).permute(0, 3, 1, 2)            # channels_last view
-        return ops.residual_inject(out, [res], [1.0])
+        return ops.residual_inject(out, [res], [1.0], gn_workspace=self.k3ws(pre, out), groups=self.cfg.groups)
 
     # -- embeddings ---------------------------------------------------------
     def add_embedding(self, pooled: torch.Tensor, time_ids: torch.Tensor) -> torch.Tensor:
@@ -483,7 +494,9 @@ class Net:
         """conv_in + down blocks + mid; returns (mid, [skips])."""
         cfg = self.cfg
         if hint is not None:   # conv_in + bias + the ControlNet hint in one K3 pass
-            h = ops.residual_inject(self.conv("conv_in", x, bias=False), [hint], [1.0], skip_bias=self.fb.get("conv_in"))
+            h = self.conv("conv_in", x, bias=False)
+            h = ops.residual_inject(h, [hint], [1.0], skip_bias=self.fb.get("conv_in"),
+                                    gn_workspace=self.k3ws("conv_in", h), groups=self.cfg.groups)
         else:
             h = self.conv_bias_inplace("conv_in", x)
         skips = [h]
@@ -521,7 +534,8 @@ class UNet(Net):
             for j in range(cfg.layers_per_block + 1):
                 k -= 1
                 res_k = [r[k] for r in residuals] if nres else []
-                h = ops.residual_inject(skips[k], res_k, res_scales if nres else [], hidden=h, hidden_bias=hb)
+                h = ops.residual_inject(skips[k], res_k, res_scales if nres else [], hidden=h, hidden_bias=hb,
+                                        gn_workspace=self.k3ws(f"up.{i}.cat.{j}", skips[k]), groups=self.cfg.groups)
                 hb = None
                 h = self.resnet(f"up.{i}.res.{j}", h, temb_act)
                 if depth:

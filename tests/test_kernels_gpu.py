@@ -193,3 +193,39 @@ def test_cross_attention_vs_fp32(n, lq, c, heads, lk):
     assert torch.isfinite(o).all()
     # deterministic
     assert torch.equal(o, ops.cross_attention(q, kv, heads))
+
+
+# K3 + GroupNorm statistics fused (sdb_residual_inject_gn -> sdb_groupnorm_apply)
+@pytest.mark.parametrize("ch,cs,hw,n_res,inplace", [(0, 1280, 32, 1, True), (640, 320, 64, 2, False),
+                                                    (0, 320, 128, 0, True), (32, 32, 16, 1, False),
+                                                    (0, 2560, 8, 3, True), (1280, 640, 32, 0, False)])
+def test_inject_with_groupnorm_stats(ch, cs, hw, n_res, inplace):
+    g = torch.Generator(device="cuda").manual_seed(ch + cs + hw)
+    skip = cl((torch.randn(2, cs, hw, hw, device="cuda", generator=g) * 2 + 0.7).to(torch.bfloat16))
+    res = [cl(torch.randn(2, cs, hw, hw, device="cuda", generator=g).to(torch.bfloat16)) for _ in range(n_res)]
+    hid = cl(torch.randn(2, ch, hw, hw, device="cuda", generator=g).to(torch.bfloat16)) if ch else None
+    sb = torch.randn(cs, device="cuda", generator=g)
+    hb = torch.randn(ch, device="cuda", generator=g) if ch else None
+    scales = [0.8, 0.6, 1.0][:n_res]
+    # plain K3 result (reference for the fused pass's output bits)
+    plain = ops.residual_inject(skip.clone(), res, scales, hidden=hid, skip_bias=sb, hidden_bias=hb)
+    src = skip.clone()
+    ws = ops.groupnorm_workspace(plain)
+    out = ops.residual_inject(src, res, scales, hidden=hid, skip_bias=sb, hidden_bias=hb, gn_workspace=ws)
+    assert torch.equal(out, plain)
+    if inplace and hid is None:
+        assert out.data_ptr() == src.data_ptr()
+    c = ch + cs
+    gamma = torch.rand(c, device="cuda", generator=g) + 0.5
+    beta = torch.randn(c, device="cuda", generator=g)
+    y = ops.groupnorm_silu(out, gamma, beta, groups=32, eps=1e-5, silu=True)      # apply only
+    ref = F.silu(F.group_norm(plain.float(), 32, gamma, beta, 1e-5))
+    err = (y.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 1e-3).all(), float(err.max())
+    # the two-pass path on the same input agrees within one bf16 rounding
+    y2 = ops.groupnorm_silu(plain, gamma, beta, groups=32, eps=1e-5, silu=True)
+    assert ((y.float() - y2.float()).abs() <= y2.float().abs() * 2 ** -7 + 1e-3).all()
+    # repeated use of the same workspace (epoch recycling): same result
+    out2 = ops.residual_inject(skip.clone(), res, scales, hidden=hid, skip_bias=sb, hidden_bias=hb, gn_workspace=ws)
+    y3 = ops.groupnorm_silu(out2, gamma, beta, groups=32, eps=1e-5, silu=True)
+    assert torch.equal(y3, y)
