@@ -266,9 +266,7 @@ int launch(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t vof
   // tiles per warp: enough warps for one resident wave, each walking several
   // tiles so its loads overlap its math (SDXL: 3 at the 64x64 level, 2 at 32x32)
   const int64_t tiles = (int64_t)n * heads * ((lq + kQRows - 1) / kQRows);
-  int tpw = (int)std::max<int64_t>(1, (tiles + kTargetWarps - 1) / kTargetWarps);
-  static const int env_tpw = getenv("SDB_XATTN_TPW") ? atoi(getenv("SDB_XATTN_TPW")) : 0;   // probes only
-  if (env_tpw > 0) tpw = env_tpw;
+  const int tpw = (int)std::max<int64_t>(1, (tiles + kTargetWarps - 1) / kTargetWarps);
   const int cta_q = kWarps * kQRows * tpw;
   dim3 grid((unsigned)((lq + cta_q - 1) / cta_q), (unsigned)heads, (unsigned)n);
   const int smem = (2 * NKP + kWarps * kSlots * kQRows) * (DP + 8) * (int)sizeof(T);

@@ -49,7 +49,7 @@ namespace sdb {
 namespace {
 
 constexpr int kMaxThreads = 512;
-constexpr int kMaxN = 64;
+constexpr int kMaxN = 16;            // batch (x2 for CFG): serving batch 8 with CFG
 constexpr int kMaxGroups = 64;
 constexpr int kTileMax = 80 * 1024;          // chunk bytes per CTA (2 CTAs / SM)
 // Statistics bank: kSlots independent copies of the (n, group) fp64 moments;
@@ -59,7 +59,7 @@ constexpr int kTileMax = 80 * 1024;          // chunk bytes per CTA (2 CTAs / SM
 // The layout is fixed ([kMaxN][slot][kMaxGroups][2]); a launch zeroes the
 // idle bank's rows up to the largest batch seen (WsHeader::hwm), so one
 // workspace may serve calls of different shapes.
-constexpr int kSlots = 8;
+constexpr int kSlots = 32;
 constexpr int kBankDoubles = kSlots * kMaxN * kMaxGroups * 2;   // 512 KB
 constexpr size_t kWsHeader = 256;            // epoch (u32) | cur (u32) | pad
 constexpr size_t kWsBytes = kWsHeader + 2 * (size_t)kBankDoubles * sizeof(double);
@@ -77,8 +77,10 @@ struct WsHeader {
 // and publish this launch's bank; returns the bank to accumulate into.
 __device__ __forceinline__ double* claim_bank(uint8_t* ws, int nbatch) {
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
-  const unsigned int epoch = *reinterpret_cast<volatile unsigned int*>(&hdr->epoch);
-  const int hwm = (int)*reinterpret_cast<volatile unsigned int*>(&hdr->hwm);
+  unsigned int epoch, hwmu;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(epoch) : "l"(&hdr->epoch));
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(hwmu) : "l"(&hdr->hwm));
+  const int hwm = (int)hwmu;
   const int rows = max(hwm, nbatch);
   double* bank = reinterpret_cast<double*>(ws + kWsHeader) + (size_t)(epoch & 1u) * kBankDoubles;
   double2* o2 = reinterpret_cast<double2*>(reinterpret_cast<double*>(ws + kWsHeader) +
@@ -259,15 +261,17 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
   if (threadIdx.x < groups) {
     const unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&hdr->cur);
     const double* bank = reinterpret_cast<const double*>(ws + kWsHeader) + (size_t)cur * kBankDoubles;
-    double2 p[kSlots];
-#pragma unroll
-    for (int sl = 0; sl < kSlots; ++sl)   // all slot loads in flight at once (unused slots are zero)
-      p[sl] = __ldcg(reinterpret_cast<const double2*>(bank + bank_index(sl, n, threadIdx.x)));
     double m1 = 0.0, m2 = 0.0;
 #pragma unroll
-    for (int sl = 0; sl < kSlots; ++sl) {
-      m1 += p[sl].x;
-      m2 += p[sl].y;
+    for (int s0 = 0; s0 < kSlots; s0 += 8) {   // 8 slot loads in flight at a time (unused slots are zero)
+      double2 p[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[k] = __ldcg(reinterpret_cast<const double2*>(bank + bank_index(s0 + k, n, threadIdx.x)));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        m1 += p[k].x;
+        m2 += p[k].y;
+      }
     }
     const double cnt = (double)hw * (double)cpg;
     const double mean = m1 / cnt;
@@ -367,7 +371,6 @@ inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T>
   const int pbeg = blockIdx.x * rows_per_chunk;
   const int m = min(hw, pbeg + rows_per_chunk) - pbeg;
   const int p0 = n * hw + pbeg;                    // first pixel of the chunk (global pixel index)
-  double* bank = claim_bank(ws, gridDim.y);
 
   constexpr int kB = 4;
   const bool hid_lane = v < vh;
@@ -441,6 +444,7 @@ inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T>
     __syncthreads();
   }
   // one warp per group: lanes over its channels (fp64), shuffle-reduce, slotted atomics
+  double* bank = claim_bank(ws, gridDim.y);
   double* mine = bank + bank_index(blockIdx.x % kSlots, n, 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (int g = warp; warp < nwarps && g < groups; g += nwarps) {
@@ -521,8 +525,8 @@ int run_inject_gn(void* out, const void* hidden, const void* skip, const void* c
   const int cv = (int)(c / 8);
   const int rpp = std::max(1, 256 / cv);
   const int threads = cv * rpp;
-  // one resident wave (~2 CTAs per SM over the batch), each CTA a few row
-  // batches: the per-CTA statistics epilogue is paid ~2x per SM, not per row
+  // one resident wave (~2 CTAs per SM over the batch; measured best against
+  // 1, 4, 8 and 16 — the per-CTA statistics epilogue is a serial latency chain)
   const int64_t want = std::max<int64_t>(1, (2 * kNumSMs + n - 1) / n);
   const int64_t rpc = std::max<int64_t>(1, (hw + want - 1) / want);
   const int64_t chunks = (hw + rpc - 1) / rpc;
@@ -563,7 +567,7 @@ size_t groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups) {
 
 static int gn_checks(const void* x, const void* y, int64_t n, int64_t hw, int64_t c, int64_t groups, const void* ws) {
   if (n <= 0 || hw <= 0 || c <= 0 || groups <= 0) return fail(SDB_EINVAL, "groupnorm: empty shape");
-  if (n > kMaxN) return fail(SDB_EINVAL, "groupnorm: batch > 64 unsupported");
+  if (n > kMaxN) return fail(SDB_EINVAL, "groupnorm: batch > 16 unsupported");
   if (c % groups != 0) return fail(SDB_EINVAL, "groupnorm: channels not divisible by groups");
   if (groups > kMaxGroups) return fail(SDB_EINVAL, "groupnorm: more than 64 groups");
   if (c % 8 != 0) return fail(SDB_EINVAL, "groupnorm: channels must be a multiple of 8");

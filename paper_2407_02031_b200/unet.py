@@ -29,11 +29,16 @@ import math
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
+import os
+
 import torch
 import torch.nn.functional as F
 from torch.nn.attention import SDPBackend, sdpa_kernel
 
 from . import ops
+
+# A/B switch for measurements: SDB_K3_GN_STATS=0 keeps the two-pass GroupNorm everywhere
+_NO_K3_STATS = os.environ.get("SDB_K3_GN_STATS", "1") == "0"
 
 
 # --------------------------------------------------------------------------
@@ -391,6 +396,8 @@ class Net:
     def k3ws(self, key, x):
         """GroupNorm-statistics workspace of one K3 call site whose output is
         the next GroupNorm's input (the K3 pass accumulates its statistics)."""
+        if _NO_K3_STATS:
+            return None
         k = ("k3", key, tuple(x.shape))
         ws = self._gn_ws.get(k)
         if ws is None:
