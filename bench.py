@@ -280,9 +280,11 @@ def run_caas(args, world, rank, local):
                         all(not g.services for g in layout.groups))) else 0.0], device=_red_device(),
                        dtype=torch.float64)
     dist.all_reduce(lat, op=dist.ReduceOp.MAX)
-    graph_launches = 0
-    if role == "base":
-        graph_launches = node.pipe.launches_per_step
+    # this repo's kernels launched in the timed region, summed over ranks:
+    # host-issued launches + every graph replay's captured launches
+    mine = host_launches + node.launches_per_step * DENOISE_STEPS * args.steps
+    tot = torch.tensor([float(mine)], device=_red_device(), dtype=torch.float64)
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
     hbm, _, src = peaks()
     line = None
     if rank == 0:
@@ -301,11 +303,12 @@ def run_caas(args, world, rank, local):
                        "l2": "inputs larger than L2 (weights re-read every step)"},
             "e2e": {"value": images / (e2e_ms / 1000.0), "unit": "images/s",
                     "h2d_bytes_per_step": req.nbytes(), "d2h_bytes_per_step": 4 * node.L},
-            "gpu_launches": int(host_launches * world + graph_launches * DENOISE_STEPS * args.steps * world),
+            "gpu_launches": int(tot.item()),
             "roofline": {"kernel": "sdb lora_patch (K1, stacked R=128, all 794 SDXL matrices)", "bound": "hbm",
                          "achieved": alg / (p.patch_ms_est * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                         "frac": alg / (p.patch_ms_est * 1e-3) / 1e9 / hbm, "traffic": None,
-                         "launch_ms_isolated": p.patch_ms_est, "peak_source": src},
+                         "frac": alg / (p.patch_ms_est * 1e-3) / 1e9 / hbm, "traffic": k1_traffic(),
+                         "alg_bytes_per_launch": alg, "launch_ms_isolated": p.patch_ms_est,
+                         "peak_source": src},
             "clocks": clk,
             "detail": {"layout": [list(g.ranks) for g in layout.groups],
                        "first_patched_step": p.last_first_patched_step, "step_ms_est": p.step_ms_est},
