@@ -220,6 +220,20 @@ int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv
                         void* stream);
 
 /* ========================================================================
+ * Peer step handshakes (ControlNet-as-a-service over NVLink, caas.py):
+ * enqueue on `stream` a wait until the 32-bit word at addr (local, IPC- or
+ * peer-mapped device memory) is >= value, or a write of value to addr that
+ * is ordered after every earlier store/copy of the stream (system-scope
+ * fence).  Replaces the per-step transfer steps modelled as comm_ms in
+ * addonsim/model.py:151-158 (orchestrator.py:621-660) with GPU-side flags.
+ * ======================================================================== */
+int sdb_stream_wait_value32(void* stream, void* addr, uint32_t value);
+int sdb_stream_write_value32(void* stream, void* addr, uint32_t value);
+/* Stream-ordered copy between any two device addresses (local, peer over
+ * NVLink, or CUDA-IPC mapped): the residual push / latent pull of caas.py. */
+int sdb_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
+
+/* ========================================================================
  * K5 — GEGLU: out[m, 0:f] = proj[m, 0:f] * gelu(proj[m, f:2f]) (exact erf).
  * The paper's fused GEGLU; in the reference only the
  * 1.06 sub-multiplier of addonsim/model.py:66-70.  f % 8 == 0.

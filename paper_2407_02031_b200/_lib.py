@@ -168,7 +168,8 @@ class LoraSrc(ctypes.Structure):
 
 EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_tc_plan",
                        "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_add_layernorm",
-                       "sdb_cross_attention")
+                       "sdb_cross_attention", "sdb_stream_wait_value32", "sdb_stream_write_value32",
+                       "sdb_memcpy_async")
 
 
 def _declare_tc(lib: ctypes.CDLL) -> None:
@@ -188,6 +189,12 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
     lib.sdb_lora_tc_set_mode.argtypes = [i32]
     lib.sdb_geglu.restype = i32
     lib.sdb_geglu.argtypes = [vp, vp, i64, i64, i32, vp]
+    lib.sdb_stream_wait_value32.restype = i32
+    lib.sdb_stream_wait_value32.argtypes = [vp, vp, ctypes.c_uint32]
+    lib.sdb_stream_write_value32.restype = i32
+    lib.sdb_stream_write_value32.argtypes = [vp, vp, ctypes.c_uint32]
+    lib.sdb_memcpy_async.restype = i32
+    lib.sdb_memcpy_async.argtypes = [vp, vp, ctypes.c_size_t, vp]
     lib.sdb_cross_attention.restype = i32
     lib.sdb_cross_attention.argtypes = [vp, i64, vp, i64, i64, vp, i64, i32, i32, i32, i32, i32, f32, i32, vp]
     lib.sdb_add_layernorm.restype = i32

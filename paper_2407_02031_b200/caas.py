@@ -174,6 +174,122 @@ class CaaSProtocol:
         return dist.batch_isend_irecv([dist.P2POp(dist.isend, self.flats[0], peer=self.group.base, group=self.pg)])
 
 
+class CaaSPeerProtocol(CaaSProtocol):
+    """The per-step exchange with no collective on the data path: GPU-to-GPU
+    copies through CUDA IPC mappings (NVLink peer copies across GPUs) ordered
+    by GPU-side sequence flags (``sdb_stream_write_value32`` /
+    ``sdb_stream_wait_value32``, stream memory operations — no NCCL call and
+    no host round trip per step).
+
+    base     owns msg, one receive buffer per service and one int32 "residuals
+             ready" flag per service; writes each service's "message ready"
+             flag (step k) once the previous decoder + K4 wrote msg, and makes
+             its decoder stream wait for every service's flag >= k.
+    service  waits for its flag >= k, copies the base's msg (256 KiB), runs its
+             ControlNets into its local buffer, copies that buffer into its
+             receive buffer on the base (107.5 MB for SDXL) and writes the
+             base's flag = k (the write is fenced after the copy).
+    A service writes step k+1's residuals only after its k+1 message flag,
+    which the base raises after decoder k consumed step k's — no extra fence.
+    Setup (IPC handle exchange) and the per-request conditioning broadcast use
+    the group's communicator (NCCL or gloo)."""
+
+    def __init__(self, layout: CaaSLayout, rank: int, msg: torch.Tensor, flats: Sequence[torch.Tensor], pg=None):
+        super().__init__(layout, rank, msg, flats, pg)
+        from torch.multiprocessing.reductions import reduce_tensor
+        dev = msg.device
+        self.step = 0
+        services = list(self.group.services)
+        if self.role == "base":
+            self.res_flags = torch.zeros(len(services), dtype=torch.int32, device=dev)
+            export = {"msg": reduce_tensor(msg), "flats": [reduce_tensor(f) for f in self.flats],
+                      "flags": reduce_tensor(self.res_flags)}
+        else:
+            self.msg_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+            export = {"flag": reduce_tensor(self.msg_flag)}
+        objs = [None] * len(self.group.ranks)
+        dist.all_gather_object(objs, export, group=self.pg)
+
+        def rebuild(x):
+            fn, args = x
+            return fn(*args)
+        if self.role == "base":
+            self.peer_msg_flags = [rebuild(objs[1 + i]["flag"]) for i in range(len(services))]
+        else:
+            k = services.index(rank)
+            b = objs[0]
+            self.peer_msg = rebuild(b["msg"])
+            self.peer_flat = rebuild(b["flats"][k])
+            self.peer_res_flag = rebuild(b["flags"])[k:k + 1]
+        self._export = export     # keep the exported tensors' IPC records alive
+
+    def _lib(self):
+        from . import _lib
+        return _lib
+
+    def _write(self, flag: torch.Tensor, value: int) -> None:
+        _lib = self._lib()
+        _lib.check("sdb_stream_write_value32", _lib.lib().sdb_stream_write_value32(
+            torch.cuda.current_stream().cuda_stream, flag.data_ptr(), value & 0xFFFFFFFF))
+
+    def _copy(self, dst: torch.Tensor, src: torch.Tensor) -> None:
+        _lib = self._lib()
+        _lib.check("sdb_memcpy_async", _lib.lib().sdb_memcpy_async(
+            dst.data_ptr(), src.data_ptr(), src.numel() * src.element_size(), torch.cuda.current_stream().cuda_stream))
+
+    def _wait(self, flag: torch.Tensor, value: int) -> None:
+        _lib = self._lib()
+        _lib.check("sdb_stream_wait_value32", _lib.lib().sdb_stream_wait_value32(
+            torch.cuda.current_stream().cuda_stream, flag.data_ptr(), value & 0xFFFFFFFF))
+
+    def base_step_begin(self) -> list:
+        self.step += 1
+        for f in self.peer_msg_flags:          # msg (latent, t) of this step is written
+            self._write(f, self.step)
+        return [_FlagWait(self, i, self.step) for i in range(len(self.peer_msg_flags))]
+
+    def service_receive(self) -> None:
+        self.step += 1
+        self._wait(self.msg_flag, self.step)
+        self._copy(self.msg, self.peer_msg)
+
+    def service_send(self):
+        self._copy(self.peer_flat, self.flats[0])
+        self._write(self.peer_res_flag, self.step)
+        return []
+
+
+class _FlagWait:
+    """Base side: the current stream waits for service i's residuals of a step."""
+
+    def __init__(self, proto: CaaSPeerProtocol, i: int, step: int):
+        self.proto, self.i, self.step = proto, i, step
+
+    def wait(self):
+        self.proto._wait(self.proto.res_flags[self.i:self.i + 1], self.step)
+
+
+def make_protocol(layout: CaaSLayout, rank: int, msg: torch.Tensor, flats: Sequence[torch.Tensor], pg,
+                  transport: Optional[str] = None):
+    """The group's transport: ``p2p`` (CaaSPeerProtocol; default when every
+    GPU of the group can map its peers' memory) or ``nccl`` (CaaSProtocol:
+    broadcast + send/recv; gloo-staged on CPU-only process groups)."""
+    import os
+    transport = transport or os.environ.get("SDB_CAAS_TRANSPORT", "auto")
+    if transport == "auto":
+        dev = torch.tensor([msg.device.index if msg.is_cuda else -1])
+        devs = [None] * len(layout.group_of(rank).ranks)
+        dist.all_gather_object(devs, int(dev.item()), group=pg)
+        ok = all(d >= 0 for d in devs) and all(
+            a == b or torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs)
+        transport = "p2p" if ok else "nccl"
+    if transport == "p2p":
+        return CaaSPeerProtocol(layout, rank, msg, flats, pg)
+    if transport == "nccl":
+        return CaaSProtocol(layout, rank, msg, flats, pg)
+    raise ValueError(f"unknown CaaS transport {transport!r} (p2p | nccl | auto)")
+
+
 class _StagedWork:
     """gloo receive into host buffers, then the device copy the decoder reads."""
 
@@ -267,8 +383,9 @@ class CaaSNode:
             for cn in self.cns:                      # per-request cross-attention K|V (finish_prepare)
                 cn.enable_kv_cache(self.ctx, ("pristine",))
                 cn.kv_slot = "pristine"
-        # loopback (all roles in one process, see LoopbackGroup) runs without a communicator
-        self.proto = CaaSProtocol(layout, rank, self.msg, self.flats, pg=self.pg) if dist.is_initialized() else None
+        # loopback (all roles in one process, see LoopbackGroup) and solo ranks run without a transport
+        self.proto = (make_protocol(layout, rank, self.msg, self.flats, self.pg)
+                      if dist.is_initialized() and self.role != "solo" else None)
         self.graphs = {}
         self.graph_launches = {}
 
@@ -319,6 +436,8 @@ class CaaSNode:
     @property
     def launches_per_step(self) -> int:
         """This repo's kernels issued per denoising step by this node's graphs."""
+        if self.role == "solo":
+            return self.pipe.launches_per_step
         g = self.graph_launches
         if self.role == "base":
             return g.get("enc_pristine", 0) + g.get("dec_pristine", 0)

@@ -50,6 +50,10 @@ int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void
 // cross_attn.cu
 int cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o, int64_t ldo,
                     int n, int lq, int lk, int heads, int d, float scale, int dtype, cudaStream_t st);
+// peer_sync.cu
+int stream_wait_value32(cudaStream_t st, void* addr, uint32_t value);
+int stream_write_value32(cudaStream_t st, void* addr, uint32_t value);
+int memcpy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // cfg_step.cu
 int cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,
                   int in_dtype, int64_t L, const float* coef, int* step_dev, cudaStream_t st);
@@ -230,6 +234,18 @@ int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv
                         void* stream) {
   return cross_attention(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, head_dim, scale, dtype,
                          as_stream(stream));
+}
+
+int sdb_stream_wait_value32(void* stream, void* addr, uint32_t value) {
+  return stream_wait_value32(as_stream(stream), addr, value);
+}
+
+int sdb_stream_write_value32(void* stream, void* addr, uint32_t value) {
+  return stream_write_value32(as_stream(stream), addr, value);
+}
+
+int sdb_memcpy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  return memcpy_async(dst, src, bytes, as_stream(stream));
 }
 
 int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,

@@ -26,13 +26,13 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, transport):
     import torch.distributed as dist
     from paper_2407_02031_b200 import unet as U
     from paper_2407_02031_b200.caas import CaaSNode, caas_layout
     from paper_2407_02031_b200.patcher import synthetic_lora
     from paper_2407_02031_b200.pipeline import synthetic_request
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SDB_CAAS_TRANSPORT=transport)
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     torch.cuda.set_device(0)
@@ -42,12 +42,17 @@ def _worker(rank, world, port, out):
         node.load_loras([(synthetic_lora(node.pipe.unet_p, 8, seed=7), 0.75)])
     node.setup()
     req = synthetic_request(U.TOY, 2)
-    if node.role == "base":
+    if node.role in ("base", "solo"):
+        if node.role == "solo":
+            node.load_loras([(synthetic_lora(node.pipe.unet_p, 8, seed=7), 0.75)])
+            node.setup()
         node.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context),
                      [torch.from_numpy(i) for i in req.images])
         node.denoise(patch=True, boundary=1)
         torch.cuda.synchronize()
-        out["latent"] = node.latent_nchw().cpu().clone()
+        out["latent" if node.role == "base" else f"solo{rank}"] = node.latent_nchw().cpu().clone()
+        if node.role == "base":
+            out["transport"] = type(node.proto).__name__
     else:
         node.prepare()
         node.denoise()
@@ -72,20 +77,29 @@ def single_gpu():
     return pipe.latent_nchw().cpu().clone()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_multiprocess_caas_matches_single_gpu(world):
+@pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (4, "p2p"), (3, "nccl")])
+def test_multiprocess_caas_matches_single_gpu(world, transport):
+    """transport p2p: CaaSPeerProtocol (IPC mappings + GPU-side step flags; on
+    one GPU the 'peer' copies are same-device copies); nccl: CaaSProtocol
+    (here gloo, device buffers staged through the host).  world 4 adds a solo
+    rank (serves whole images alone, no transport)."""
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, out)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out, transport)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(600)
         assert p.exitcode == 0
     got = out["latent"]
+    assert out["transport"] == ("CaaSPeerProtocol" if transport == "p2p" else "CaaSProtocol")
     ref = single_gpu()
     rel = float((got.double() - ref.double()).norm() / ref.double().norm())
     print(f"world {world}: multi-process CaaS vs single GPU rel-L2 {rel:.2e}")
     assert rel <= 1e-5
+    for k in out.keys():
+        if k.startswith("solo"):    # a solo rank runs the whole pipeline itself
+            r2 = float((out[k].double() - ref.double()).norm() / ref.double().norm())
+            assert r2 <= 1e-5, (k, r2)
