@@ -36,7 +36,7 @@ def launches(path):
     T = sum(tot.values())
     ours = sum(v for k, v in tot.items() if "sdb::" in k)
     print(f"Source: `{path}` — every launch, `ncu --metrics gpu__time_duration.sum --clock-control none` "
-          f"(cold-cache, serialised: compare SHARES).\n")
+          f"(serialised one launch at a time: compare SHARES, not the step time).\n")
     print(f"Total {T:.3f} ms over {sum(cnt.values())} launches; this repo's kernels (sdb::) "
           f"{ours:.3f} ms = {100 * ours / T:.1f}%.\n")
     print("| ms | share | launches | kernel |\n|---:|---:|---:|---|")
