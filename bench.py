@@ -412,7 +412,17 @@ def other_kernels_roofline(hbm: float) -> list:
         o = torch.empty_like(q)
         return lambda: ops.cross_attention(q, kv, 10, out=o)
     nq = 2 * 4096 * 640
-    out.append(("K7 cross-attention [2,4096,640] x 77 tokens, 10 heads bf16", 2 * nq * 2, timed(mk_xattn, nq * 2)))
+    out.append(("K7 cross-attention [2,4096,640] x 77 tokens, 10 heads bf16 (mma.sync form)", 2 * nq * 2,
+                timed(mk_xattn, nq * 2)))
+
+    def mk_xattn_tc():
+        q = torch.randn(2, 1024, 1280, device=dev).to(torch.bfloat16)
+        kv = torch.randn(2, 77, 2560, device=dev).to(torch.bfloat16)
+        o = torch.empty_like(q)
+        return lambda: ops.cross_attention(q, kv, 20, out=o)
+    nq = 2 * 1024 * 1280
+    out.append(("K7 cross-attention [2,1024,1280] x 77 tokens, 20 heads bf16 (tcgen05 form)", 2 * nq * 2,
+                timed(mk_xattn_tc, nq * 2)))
     return [{"kernel": k, "achieved": b / (m * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
              "frac": b / (m * 1e-3) / 1e9 / hbm, "alg_bytes": b, "launch_ms": m,
              "method": "CUDA-graph replay, inputs rotated over > 2x L2"} for k, b, m in out]

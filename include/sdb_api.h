@@ -218,6 +218,10 @@ int sdb_residual_inject_gn(void* out, const void* hidden, const void* skip,
 int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o,
                         int64_t ldo, int n, int lq, int lk, int heads, int head_dim, float scale, int dtype,
                         void* stream);
+/* 1 (default): head_dim 64 runs the tcgen05 form (TMEM accumulators, one
+ * query row per thread); 0: every head dim runs the mma.sync form.  Returns
+ * the previous setting. */
+int sdb_cross_attention_set_mode(int tcgen05);
 
 /* ========================================================================
  * Peer step handshakes (ControlNet-as-a-service over NVLink, caas.py):

@@ -50,6 +50,7 @@ int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void
 // cross_attn.cu
 int cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o, int64_t ldo,
                     int n, int lq, int lk, int heads, int d, float scale, int dtype, cudaStream_t st);
+int cross_attention_set_mode(int tc);
 // peer_sync.cu
 int stream_wait_value32(cudaStream_t st, void* addr, uint32_t value);
 int stream_write_value32(cudaStream_t st, void* addr, uint32_t value);
@@ -235,6 +236,8 @@ int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv
   return cross_attention(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, head_dim, scale, dtype,
                          as_stream(stream));
 }
+
+int sdb_cross_attention_set_mode(int tcgen05) { return cross_attention_set_mode(tcgen05); }
 
 int sdb_stream_wait_value32(void* stream, void* addr, uint32_t value) {
   return stream_wait_value32(as_stream(stream), addr, value);

@@ -170,8 +170,20 @@ XATTN = [(2, 4096, 640, 10, 77), (2, 1024, 1280, 20, 77), (2, 4096, 320, 8, 77),
          (2, 17, 64, 1, 1)]
 
 
+@pytest.mark.parametrize("tc", [1, 0])
 @pytest.mark.parametrize("n,lq,c,heads,lk", XATTN)
-def test_cross_attention_vs_fp32(n, lq, c, heads, lk):
+def test_cross_attention_vs_fp32(n, lq, c, heads, lk, tc):
+    """K7 vs fp32 SDPA; tc=1 runs head dim 64 through the tcgen05 form, tc=0
+    through the mma.sync form (other head dims always use the latter)."""
+    lib = ops._lib.lib()
+    prev = lib.sdb_cross_attention_set_mode(tc)
+    try:
+        _xattn_case(n, lq, c, heads, lk)
+    finally:
+        lib.sdb_cross_attention_set_mode(prev)
+
+
+def _xattn_case(n, lq, c, heads, lk):
     g = torch.Generator(device="cuda").manual_seed(lq + c + lk)
     q = torch.randn(n, lq, c, device="cuda", generator=g).to(torch.bfloat16)
     kv = torch.randn(n, lk, 2 * c, device="cuda", generator=g).to(torch.bfloat16)
