@@ -222,6 +222,8 @@ class CaaSPeerProtocol(CaaSProtocol):
             self.peer_flat = rebuild(b["flats"][k])
             self.peer_res_flag = rebuild(b["flags"])[k:k + 1]
         self._export = export     # keep the exported tensors' IPC records alive
+        self._push_stream = None
+        self._pushed = False
 
     def _lib(self):
         from . import _lib
@@ -253,8 +255,29 @@ class CaaSPeerProtocol(CaaSProtocol):
         self._wait(self.msg_flag, self.step)
         self._copy(self.msg, self.peer_msg)
 
+    def push_level(self, k: int, out: torch.Tensor) -> None:
+        """Inside the service graph: copy residual level k (just written by
+        its zero conv into the local buffer) into the base's buffer on a side
+        stream, overlapping the deeper levels' compute."""
+        if self._push_stream is None:
+            self._push_stream = torch.cuda.Stream(device=out.device)
+            self._levels = None
+        cur = torch.cuda.current_stream()
+        self._push_stream.wait_stream(cur)
+        off = out.data_ptr() - self.flats[0].data_ptr()
+        nbytes = out.numel() * out.element_size()
+        _lib = self._lib()
+        _lib.check("sdb_memcpy_async", _lib.lib().sdb_memcpy_async(
+            self.peer_flat.data_ptr() + off, out.data_ptr(), nbytes, self._push_stream.cuda_stream))
+        self._pushed = True
+
+    def join_pushes(self) -> None:
+        if self._push_stream is not None:
+            torch.cuda.current_stream().wait_stream(self._push_stream)
+
     def service_send(self):
-        self._copy(self.peer_flat, self.flats[0])
+        if not self._pushed:      # the graph did not push per level: one copy of the whole buffer
+            self._copy(self.peer_flat, self.flats[0])
         self._write(self.peer_res_flag, self.step)
         return []
 
@@ -396,9 +419,16 @@ class CaaSNode:
         self.unet_in.copy_(lat.expand(2, 4, h, h))
         t = self.msg[self.L:self.L + 1]
         # the first ControlNet's zero convs write straight into the send buffer;
-        # further ControlNets on this GPU are summed into it in place (K3)
+        # further ControlNets on this GPU are summed into it in place (K3).
+        # With the peer transport and one ControlNet per service, each level
+        # is pushed to the base over NVLink the moment its zero conv is done
+        # (a copy on a side stream, inside this graph), shallow levels first.
+        push = getattr(self.proto, "push_level", None) if len(self.cns) == 1 else None
         outs = [cn.forward(self.unet_in, t, self.ctx, self.hints[i], self.add_emb[i],
-                           outs=self.views[0] if i == 0 else None) for i, cn in enumerate(self.cns)]
+                           outs=self.views[0] if i == 0 else None, on_level=push if i == 0 else None)
+                for i, cn in enumerate(self.cns)]
+        if push is not None:
+            self.proto.join_pushes()
         if len(outs) > 1:
             for j, v in enumerate(self.views[0]):
                 self.ops.residual_inject(v, [o[j] for o in outs[1:]], [1.0] * (len(outs) - 1), out=v)

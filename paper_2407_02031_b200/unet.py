@@ -497,8 +497,10 @@ class Net:
         return F.silu(emb)   # every consumer (time_emb_proj) applies SiLU first
 
     # -- encoder ------------------------------------------------------------
-    def encode(self, x, temb_act, ctx, hint=None):
-        """conv_in + down blocks + mid; returns (mid, [skips])."""
+    def encode(self, x, temb_act, ctx, hint=None, on_skip=None):
+        """conv_in + down blocks + mid; returns (mid, [skips]).  on_skip(k, h)
+        is called as soon as skip k exists (the ControlNet's zero convs and
+        per-level pushes hang off it)."""
         cfg = self.cfg
         if hint is not None:   # conv_in + bias + the ControlNet hint in one K3 pass
             h = self.conv("conv_in", x, bias=False)
@@ -506,17 +508,23 @@ class Net:
                                     gn_workspace=self.k3ws("conv_in", h), groups=self.cfg.groups)
         else:
             h = self.conv_bias_inplace("conv_in", x)
-        skips = [h]
+        skips = []
+
+        def skip(h):
+            skips.append(h)
+            if on_skip is not None:
+                on_skip(len(skips) - 1, h)
+        skip(h)
         n = len(cfg.block_channels)
         for i in range(n):
             for j in range(cfg.layers_per_block):
                 h = self.resnet(f"down.{i}.res.{j}", h, temb_act)
                 if cfg.attn_depth[i]:
                     h = self.transformer(f"down.{i}.attn.{j}", h, ctx, cfg.attn_depth[i])
-                skips.append(h)
+                skip(h)
             if i < n - 1:
                 h = self.conv_bias_inplace(f"down.{i}.downsample", h, stride=2)
-                skips.append(h)
+                skip(h)
         h = self.resnet("mid.res.0", h, temb_act)
         h = self.transformer("mid.attn.0", h, ctx, cfg.mid_depth)
         h = self.resnet("mid.res.1", h, temb_act)
@@ -575,16 +583,26 @@ class ControlNet(Net):
             h = F.silu(self.conv(f"cond_embedding.blocks.{2 * i + 1}", h, stride=2))
         return self.conv("cond_embedding.conv_out", h)
 
-    def forward(self, x, t, ctx, hint, add_emb=None, outs=None):
+    def forward(self, x, t, ctx, hint, add_emb=None, outs=None, on_level=None):
         """Returns [down residuals..., mid residual] (unscaled; the
         conditioning scale is applied by K3 on the consumer side).  The zero
         convs are 1x1: cuBLAS GEMMs (bias in the epilogue), written straight
-        into ``outs`` (NHWC views, e.g. the CaaS send buffer) when given."""
+        into ``outs`` (NHWC views, e.g. the CaaS send buffer) when given.
+        Each level's zero conv runs as soon as its skip exists, and
+        on_level(k, out_k) lets the caller push it to the base right away —
+        shallow levels (the largest) first, overlapped with the deeper levels'
+        compute (SURVEY App. B pitfall 7)."""
         temb_act = self.time_embedding(t, x.shape[0], add_emb)
-        h, skips = self.encode(x, temb_act, ctx, hint=hint)
-        names = [f"zero_convs.{k}" for k in range(len(skips))] + ["mid_zero_conv"]
-        srcs = list(skips) + [h]
-        return [self.zero_conv(nm, s, None if outs is None else outs[k]) for k, (nm, s) in enumerate(zip(names, srcs))]
+        res = []
+
+        def level(k, s, name):
+            r = self.zero_conv(name, s, None if outs is None else outs[k])
+            res.append(r)
+            if on_level is not None:
+                on_level(k, r)
+        h, skips = self.encode(x, temb_act, ctx, hint=hint, on_skip=lambda k, s: level(k, s, f"zero_convs.{k}"))
+        level(len(skips), h, "mid_zero_conv")
+        return res
 
     def zero_conv(self, name, x, out=None):
         if self.t[name + ".weight"].shape[-1] == 1:
