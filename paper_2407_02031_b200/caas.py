@@ -356,7 +356,7 @@ class CaaSNode:
     """
 
     def __init__(self, cfg, layout: CaaSLayout, rank: int, cn_scales: Sequence[float], steps: int = 30,
-                 guidance: float = 7.5, dtype=torch.bfloat16, seed: int = 0, device=None):
+                 guidance: float = 7.5, dtype=torch.bfloat16, seed: int = 0, device=None, batch: int = 1):
         from . import ops
         from .pipeline import AddonPipeline
         from .unet import ControlNet, init_controlnet, skip_shapes
@@ -368,14 +368,16 @@ class CaaSNode:
         n_cn = layout.n_cn
         self.ops = ops
         h = cfg.latent_hw
-        self.L = 4 * h * h
+        self.batch = batch                   # serving batch of B images: CFG batch 2B
+        nb = 2 * batch
+        self.L = batch * 4 * h * h
         # communicators are created collectively by every rank, solo ones included
         self.pg = make_groups(layout, rank) if dist.is_initialized() else None
         if self.role == "solo":
             self.pipe = AddonPipeline(cfg, n_controlnets=n_cn, cn_scales=cn_scales, steps=steps, guidance=guidance,
-                                      device=self.device, dtype=dtype, seed=seed)
+                                      device=self.device, dtype=dtype, seed=seed, batch=batch)
             return
-        self.shapes = skip_shapes(cfg, 2)
+        self.shapes = skip_shapes(cfg, nb)
         _, total = residual_layout(self.shapes)
         self.msg = torch.zeros(self.L + 1, device=self.device, dtype=torch.float32)
         n_flat = len(self.group.services) if self.role == "base" else 1
@@ -384,7 +386,7 @@ class CaaSNode:
         if self.role == "base":
             # UNet only (no ControlNet weights on the base GPU)
             self.pipe = AddonPipeline(cfg, n_controlnets=0, steps=steps, guidance=guidance, device=self.device,
-                                      dtype=dtype, seed=seed, use_graphs=False)   # the node captures its own
+                                      dtype=dtype, seed=seed, use_graphs=False, batch=batch)   # own graphs
             self.pipe.x = self.msg[: self.L]            # K4 writes the latent straight into the message
         else:
             mine = self.group.cn_of_service[self.group.services.index(rank)]
@@ -396,12 +398,12 @@ class CaaSNode:
                         p.t[k] = (p.t[k].float() * float(cn_scales[i])).to(p.t[k].dtype)
             self.cns = [ControlNet(cfg, p) for p in self.cn_p]
             temb = cfg.time_embed_dim
-            self.unet_in = torch.zeros((2, 4, h, h), device=self.device, dtype=dtype).contiguous(
+            self.unet_in = torch.zeros((nb, 4, h, h), device=self.device, dtype=dtype).contiguous(
                 memory_format=torch.channels_last)
-            self.ctx = torch.zeros((2, cfg.context_len, cfg.context_dim), device=self.device, dtype=dtype)
-            self.hints = [torch.zeros((2, cfg.block_channels[0], h, h), device=self.device, dtype=dtype)
+            self.ctx = torch.zeros((nb, cfg.context_len, cfg.context_dim), device=self.device, dtype=dtype)
+            self.hints = [torch.zeros((nb, cfg.block_channels[0], h, h), device=self.device, dtype=dtype)
                           .contiguous(memory_format=torch.channels_last) for _ in mine]
-            self.add_emb = [torch.zeros((2, temb), device=self.device, dtype=dtype) if cfg.addition_embed else None
+            self.add_emb = [torch.zeros((nb, temb), device=self.device, dtype=dtype) if cfg.addition_embed else None
                             for _ in mine]
             for cn in self.cns:                      # per-request cross-attention K|V (finish_prepare)
                 cn.enable_kv_cache(self.ctx, ("pristine",))
@@ -414,9 +416,10 @@ class CaaSNode:
 
     # -- capture --------------------------------------------------------------
     def _service_step(self):
-        h = self.cfg.latent_hw
-        lat = self.msg[: self.L].view(1, h, h, 4).permute(0, 3, 1, 2)
-        self.unet_in.copy_(lat.expand(2, 4, h, h))
+        h, B = self.cfg.latent_hw, self.batch
+        lat = self.msg[: self.L].view(B, h, h, 4).permute(0, 3, 1, 2)
+        self.unet_in[:B].copy_(lat)
+        self.unet_in[B:].copy_(lat)
         t = self.msg[self.L:self.L + 1]
         # the first ControlNet's zero convs write straight into the send buffer;
         # further ControlNets on this GPU are summed into it in place (K3).
@@ -436,7 +439,7 @@ class CaaSNode:
     def _base_encode(self):
         p = self.pipe
         t = p.t_table.index_select(0, p.step_dev[:1].long())
-        temb = p.unet.time_embedding(t, 2, p.add_emb_unet)
+        temb = p.unet.time_embedding(t, 2 * self.batch, p.add_emb_unet)
         h, skips = p.unet.encode(p.unet_in, temb, p.ctx)
         self._enc = (temb, h, skips)
 
@@ -505,10 +508,10 @@ class CaaSNode:
     def request_tensors(self, context=None, images=None, pooled=None, time_ids=None) -> list:
         """The conditioning tensors shipped base -> services once per request
         (filled on the base, receive buffers elsewhere)."""
-        cfg, dev, h = self.cfg, self.device, self.cfg.latent_hw
-        ctx = torch.empty((2, cfg.context_len, cfg.context_dim), device=dev, dtype=torch.float32)
-        imgs = [torch.empty((2, 3, 8 * h, 8 * h), device=dev, dtype=torch.float32) for _ in range(self.layout.n_cn)]
-        extra = [torch.empty((2, cfg.pooled_dim), device=dev), torch.empty((2, cfg.time_ids), device=dev)] \
+        cfg, dev, h, nb = self.cfg, self.device, self.cfg.latent_hw, 2 * self.batch
+        ctx = torch.empty((nb, cfg.context_len, cfg.context_dim), device=dev, dtype=torch.float32)
+        imgs = [torch.empty((nb, 3, 8 * h, 8 * h), device=dev, dtype=torch.float32) for _ in range(self.layout.n_cn)]
+        extra = [torch.empty((nb, cfg.pooled_dim), device=dev), torch.empty((nb, cfg.time_ids), device=dev)] \
             if cfg.addition_embed else []
         if self.role == "base":
             ctx.copy_(context.to(dev, non_blocking=True))
@@ -619,10 +622,11 @@ class LoopbackGroup:
 
     def __init__(self, cfg, n_cn: int, cn_scales: Sequence[float], steps: int = 30, guidance: float = 7.5,
                  dtype=torch.bfloat16, seed: int = 0, n_services: Optional[int] = None,
-                 concurrent: bool = False):
+                 concurrent: bool = False, batch: int = 1):
         world = 1 + (n_cn if n_services is None else n_services)
         self.layout = caas_layout(world, n_cn)
-        self.nodes = [CaaSNode(cfg, self.layout, r, cn_scales, steps, guidance, dtype, seed) for r in range(world)]
+        self.nodes = [CaaSNode(cfg, self.layout, r, cn_scales, steps, guidance, dtype, seed, batch=batch)
+                      for r in range(world)]
         self.base, self.services = self.nodes[0], self.nodes[1:]
         for k, svc in enumerate(self.services):   # alias before any graph is captured
             svc.msg = self.base.msg

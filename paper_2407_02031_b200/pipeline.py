@@ -41,13 +41,14 @@ from .unet import ControlNet, UNet, UNetConfig, init_controlnet, init_unet
 
 @dataclass
 class Request:
-    """Host-side inputs of one image (CFG batch of 2 = [uncond; cond])."""
+    """Host-side inputs of one image — or of a serving batch of B images —
+    with the CFG batch laid out [uncond x B; cond x B] (B = 1: [uncond; cond])."""
 
-    latent: np.ndarray          # [4, H, W] float32 initial noise
-    context: np.ndarray         # [2, ctx_len, ctx_dim] float32 text embeddings
-    images: list                # per ControlNet: [2, 3, 8H, 8W] float32 in [0, 1]
-    pooled: Optional[np.ndarray] = None    # [2, 1280] (SDXL)
-    time_ids: Optional[np.ndarray] = None  # [2, 6]    (SDXL)
+    latent: np.ndarray          # [4, H, W] (or [B, 4, H, W]) float32 initial noise
+    context: np.ndarray         # [2B, ctx_len, ctx_dim] float32 text embeddings
+    images: list                # per ControlNet: [2B, 3, 8H, 8W] float32 in [0, 1]
+    pooled: Optional[np.ndarray] = None    # [2B, 1280] (SDXL)
+    time_ids: Optional[np.ndarray] = None  # [2B, 6]    (SDXL)
 
     def nbytes(self) -> int:
         n = self.latent.nbytes + self.context.nbytes + sum(i.nbytes for i in self.images)
@@ -71,12 +72,27 @@ def synthetic_request(cfg: UNetConfig, n_controlnets: int, seed: int = 0) -> Req
     return Request(lat, ctx, imgs, pooled, time_ids)
 
 
+def synthetic_batch(cfg: UNetConfig, n_controlnets: int, batch: int, seed: int = 0) -> Request:
+    """B independent images (image i = synthetic_request(seed + 1000 i)) in
+    the batched CFG layout [uncond_0 .. uncond_B-1, cond_0 .. cond_B-1]."""
+    reqs = [synthetic_request(cfg, n_controlnets, seed + 1000 * i) for i in range(batch)]
+    if batch == 1:
+        return reqs[0]
+
+    def cfg_cat(arrs):
+        return np.concatenate([a[0:1] for a in arrs] + [a[1:2] for a in arrs], axis=0)
+    return Request(np.stack([r.latent for r in reqs]), cfg_cat([r.context for r in reqs]),
+                   [cfg_cat([r.images[i] for r in reqs]) for i in range(n_controlnets)],
+                   cfg_cat([r.pooled for r in reqs]) if cfg.addition_embed else None,
+                   cfg_cat([r.time_ids for r in reqs]) if cfg.addition_embed else None)
+
+
 class AddonPipeline:
     """SD-style UNet + N ControlNets + LoRA on one B200."""
 
     def __init__(self, cfg: UNetConfig, n_controlnets: int = 1, cn_scales: Optional[Sequence[float]] = None,
                  steps: int = 30, guidance: float = 7.5, device="cuda", dtype=torch.bfloat16,
-                 seed: int = 0, use_graphs: bool = True, patch_max_ctas: int = 0):
+                 seed: int = 0, use_graphs: bool = True, patch_max_ctas: int = 0, batch: int = 1):
         ops.require_cuda(torch.empty(1, device=device))
         self.cfg, self.steps, self.guidance = cfg, steps, guidance
         self.device = torch.device(device)
@@ -90,18 +106,22 @@ class AddonPipeline:
         self.patch_max_ctas = patch_max_ctas
         h = cfg.latent_hw
         dev = self.device
-        self.L = 4 * h * h
+        # a serving batch of B images shares the step (and the LoRA set): the
+        # CFG batch is [uncond x B; cond x B], the fp32 master latents [B, H, W, 4]
+        self.batch = batch
+        nb = 2 * batch
+        self.L = batch * 4 * h * h
         self.x = torch.zeros(self.L, device=dev, dtype=torch.float32)
-        self.unet_in = torch.zeros((2, 4, h, h), device=dev, dtype=dtype).contiguous(memory_format=torch.channels_last)
-        self.ctx = torch.zeros((2, cfg.context_len, cfg.context_dim), device=dev, dtype=dtype)
-        self.pooled = torch.zeros((2, cfg.pooled_dim), device=dev, dtype=torch.float32)
-        self.time_ids = torch.zeros((2, cfg.time_ids), device=dev, dtype=torch.float32)
-        self.images = [torch.zeros((2, 3, 8 * h, 8 * h), device=dev, dtype=dtype) for _ in self.cns]
-        self.hints = [torch.zeros((2, cfg.block_channels[0], h, h), device=dev, dtype=dtype)
+        self.unet_in = torch.zeros((nb, 4, h, h), device=dev, dtype=dtype).contiguous(memory_format=torch.channels_last)
+        self.ctx = torch.zeros((nb, cfg.context_len, cfg.context_dim), device=dev, dtype=dtype)
+        self.pooled = torch.zeros((nb, cfg.pooled_dim), device=dev, dtype=torch.float32)
+        self.time_ids = torch.zeros((nb, cfg.time_ids), device=dev, dtype=torch.float32)
+        self.images = [torch.zeros((nb, 3, 8 * h, 8 * h), device=dev, dtype=dtype) for _ in self.cns]
+        self.hints = [torch.zeros((nb, cfg.block_channels[0], h, h), device=dev, dtype=dtype)
                       .contiguous(memory_format=torch.channels_last) for _ in self.cns]
         temb = cfg.time_embed_dim
-        self.add_emb_unet = torch.zeros((2, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
-        self.add_emb_cn = [torch.zeros((2, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
+        self.add_emb_unet = torch.zeros((nb, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
+        self.add_emb_cn = [torch.zeros((nb, temb), device=dev, dtype=dtype) if cfg.addition_embed else None
                            for _ in self.cns]
         # cross-attention K|V per request (pristine) and after the LoRA swap (patched)
         self.unet.enable_kv_cache(self.ctx, ("pristine", "patched"))
@@ -290,10 +310,14 @@ class AddonPipeline:
         """Load one request's (device or pinned-host) inputs into the static
         buffers and compute the step-invariant pieces (hint embeddings, SDXL
         added-condition embeddings)."""
-        h = self.cfg.latent_hw
+        h, B = self.cfg.latent_hw, self.batch
         nb = True
-        self.x.view(h, h, 4).copy_(latent.to(self.device, non_blocking=nb).permute(1, 2, 0))
-        self.unet_in.copy_(self.x.view(1, h, h, 4).permute(0, 3, 1, 2).expand(2, 4, h, h))
+        lat = latent.to(self.device, non_blocking=nb)
+        lat = lat.unsqueeze(0) if lat.dim() == 3 else lat
+        self.x.view(B, h, h, 4).copy_(lat.permute(0, 2, 3, 1))
+        xv = self.x.view(B, h, h, 4).permute(0, 3, 1, 2)
+        self.unet_in[:B].copy_(xv)
+        self.unet_in[B:].copy_(xv)
         self.ctx.copy_(context.to(self.device, non_blocking=nb))
         for buf, img in zip(self.images, images):
             buf.copy_(img.to(self.device, non_blocking=nb))
@@ -349,8 +373,11 @@ class AddonPipeline:
         return first
 
     def latent_nchw(self) -> torch.Tensor:
+        """[4, H, W] (B = 1) or [B, 4, H, W] view of the fp32 master latents."""
         h = self.cfg.latent_hw
-        return self.x.view(h, h, 4).permute(2, 0, 1)
+        if self.batch == 1:
+            return self.x.view(h, h, 4).permute(2, 0, 1)
+        return self.x.view(self.batch, h, h, 4).permute(0, 3, 1, 2)
 
     # ------------------------------------------------------------------
     def generate(self, req: Request, patch: bool = False, boundary: Optional[int] = None,

@@ -177,3 +177,45 @@ def test_sd15_shaped_config2_runs():
     pipe.denoise(patch=True, boundary=1)
     torch.cuda.synchronize()
     assert torch.isfinite(pipe.x).all()
+
+
+def test_serving_batch_matches_single_images(fp32_mode):
+    """A serving batch of B = 3 images (CFG batch 6, one shared LoRA set,
+    BASELINE config 5's batching) equals the 3 images run one at a time
+    (fp32, per-image rel-L2 <= 1e-5); the CaaS split (loopback, batch 3)
+    equals the batched pipeline."""
+    from paper_2407_02031_b200.caas import LoopbackGroup
+    from paper_2407_02031_b200.pipeline import synthetic_batch
+    B, steps = 3, 4
+
+    def lora_for(p):
+        return synthetic_lora(p.unet_p, 8, seed=7, adapter_id="l0", scale=LORA_SCALE)
+
+    def tensors(req):
+        return (torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(i) for i in req.images])
+
+    pipe = AddonPipeline(U.TOY, n_controlnets=1, cn_scales=[CN_SCALE], steps=steps, guidance=GUIDANCE,
+                         dtype=torch.float32, seed=0, batch=B)
+    pipe.load_loras([(lora_for(pipe), LORA_SCALE)])
+    pipe.setup()
+    pipe.prepare(*tensors(synthetic_batch(U.TOY, 1, B)))
+    pipe.denoise(patch=True, boundary=1)
+    torch.cuda.synchronize()
+    got = pipe.latent_nchw().cpu().clone()
+    assert got.shape == (B, 4, 64, 64)
+    single = AddonPipeline(U.TOY, n_controlnets=1, cn_scales=[CN_SCALE], steps=steps, guidance=GUIDANCE,
+                           dtype=torch.float32, seed=0)
+    single.load_loras([(lora_for(single), LORA_SCALE)])
+    single.setup()
+    for i in range(B):
+        single.prepare(*tensors(synthetic_request(U.TOY, 1, seed=1000 * i)))
+        single.denoise(patch=True, boundary=1)
+        torch.cuda.synchronize()
+        assert rel_l2(got[i], single.latent_nchw()) <= 1e-5, i
+    grp = LoopbackGroup(U.TOY, 1, [CN_SCALE], steps=steps, guidance=GUIDANCE, dtype=torch.float32, seed=0, batch=B)
+    grp.load_loras([(lora_for(grp.base.pipe), LORA_SCALE)])
+    grp.setup()
+    grp.prepare(*tensors(synthetic_batch(U.TOY, 1, B)))
+    grp.denoise(patch=True, boundary=1)
+    torch.cuda.synchronize()
+    assert rel_l2(grp.latent_nchw(), got) <= 1e-5
