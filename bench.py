@@ -196,17 +196,19 @@ def run_caas(args, world, rank, local):
     from paper_2407_02031_b200 import unet as U
     from paper_2407_02031_b200.caas import CaaSNode, caas_layout
     from paper_2407_02031_b200.patcher import synthetic_lora
-    from paper_2407_02031_b200.pipeline import synthetic_request
+    from paper_2407_02031_b200.pipeline import synthetic_batch
 
     cfg = U.SDXL
+    B = args.batch
     layout = caas_layout(world, N_CN)
-    node = CaaSNode(cfg, layout, rank, [0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16, seed=0)
+    node = CaaSNode(cfg, layout, rank, [0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16, seed=0,
+                    batch=B)
     role = node.role
     if role in ("base", "solo"):
         node.load_loras([(synthetic_lora(node.pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7)
                          for i, r in enumerate(LORA_RANKS)])
     node.setup()
-    req = synthetic_request(cfg, N_CN, seed=rank)
+    req = synthetic_batch(cfg, N_CN, B, seed=rank)
     dev_in = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
                   images=[torch.from_numpy(i).cuda() for i in req.images],
                   pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
@@ -273,7 +275,7 @@ def run_caas(args, world, rank, local):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
     clk = clocks.stop()
     producers = sum(1 for g in layout.groups)
-    images = args.steps * producers
+    images = args.steps * producers * B
     # per-image latency of group bases (not solos) for p50, gathered to rank 0
     import torch.distributed as dist
     lat = torch.tensor([statistics.median(per_image) if (role == "base" or (role == "solo" and
@@ -297,7 +299,7 @@ def run_caas(args, world, rank, local):
             "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
                                    "30 DDIM steps, CFG batch 2, async LoRA patch",
                        "model": "sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init",
-                       "global_batch": producers, "seq_len": None,
+                       "global_batch": producers * B, "seq_len": None,
                        "parallelism": "ControlNet-as-a-service groups " +
                                       "; ".join(str(g.ranks) for g in layout.groups),
                        "l2": "inputs larger than L2 (weights re-read every step)"},
