@@ -374,16 +374,17 @@ constexpr int kMaxSlots = 10;
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restrict__ jobs,
-                       const TcUnit* __restrict__ units, int n_units, float sign, int kb_max, int n_slots) {
+                       const TcUnit* __restrict__ units, int n_units, float sign, int kb_max, int n_slots,
+                       int na) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
                                ((uint32_t)(256 >> 4) << 24);   // f32 accum, bf16, K-major, M256 x N256
   uint8_t* sB = smem;                                   // kb_max x 16 KB: this CTA's half of the B panel
-  uint8_t* sA = sB + kb_max * kHalfBlock;               // kAStages x 16 KB
-  uint8_t* sW = sA + kAStages * kABlockBytes;           // n_slots x 16 KB
+  uint8_t* sA = sB + kb_max * kHalfBlock;               // na x 16 KB: streamed A K-blocks
+  uint8_t* sW = sA + na * kABlockBytes;                 // n_slots x 16 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + n_slots * kBoxBytes);
-  const int B_FULL = 0, B_EMPTY = 1, A_FULL = 2, A_EMPTY = A_FULL + kAStages, T_FULL = A_EMPTY + kAStages;
+  const int B_FULL = 0, B_EMPTY = 1, A_FULL = 2, A_EMPTY = A_FULL + na, T_FULL = A_EMPTY + na;
   const int T_EMPTY = T_FULL + 2, W_FULL = T_EMPTY + 2;
   const int W_EMPTY = W_FULL + n_slots;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + W_EMPTY + n_slots);
@@ -398,7 +399,7 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
   if (threadIdx.x == 0) {
     mbar_init(bar(B_FULL), 1);
     mbar_init(bar(B_EMPTY), 1);
-    for (int i = 0; i < kAStages; ++i) {
+    for (int i = 0; i < na; ++i) {
       mbar_init(bar(A_FULL + i), 1);
       mbar_init(bar(A_EMPTY + i), 1);
     }
@@ -447,12 +448,12 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
             if (leader) mbar_expect_tx(bar(A_FULL + a_st), 2 * kABlockBytes);
             tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.kb + kb) * kBM,
                              mapa_shared(bar(A_FULL + a_st), 0), keep);
-            if (++a_st == kAStages) { a_st = 0; ++a_round; }
+            if (++a_st == na) { a_st = 0; ++a_round; }
           }
         }
       }
       // drain: the leader's last multicast commits must land before this CTA exits
-      for (int s = 0; s < kAStages; ++s) {
+      for (int s = 0; s < na; ++s) {
         const int uses = a_round + (s < a_st ? 1 : 0);
         if (uses > 0) mbar_wait(bar(A_EMPTY + s), (uses - 1) & 1);
       }
@@ -485,7 +486,7 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
     __syncwarp();
   } else if (warp == kMmaWarp) {
     if (leader && lane == 0) {
-      int tile = 0, b_cnt = 0, a_cnt = 0;
+      int tile = 0, b_cnt = 0, a_st = 0, a_round = 0;
       for (int u = cid; u < n_units; u += ncl) {
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
@@ -496,9 +497,10 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem_base + buf * kBN;
-          for (int kb = 0; kb < J.kb; ++kb, ++a_cnt) {
-            const int st = a_cnt & (kAStages - 1);
-            mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
+          for (int kb = 0; kb < J.kb; ++kb) {
+            const int st = a_st;
+            mbar_wait(bar(A_FULL + st), a_round & 1);
+            if (++a_st == na) { a_st = 0; ++a_round; }
             tc_fence_after();
             const int ks_end = std::min(4, nks - kb * 4);
             for (int ks = 0; ks < ks_end; ++ks) {
@@ -905,7 +907,12 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int sim
   (void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
   const int max_smem = 227 * 1024;
   if (mode == 2) {
-    const int fixed = 1024 + kb_max * kHalfBlock + kAStages * kABlockBytes + 256;
+    // A K-blocks in flight = the K blocks of one tile (2..4): a tile's MMAs
+    // consume them in sequence, so at high rank a deeper A ring beats the
+    // last W slots (round 1, R = 232: 4 stages + 6 slots 2.04 ms = 89% of the
+    // copy peak vs 2 stages + 8 slots 2.42 ms; R <= 128: 2 stages best)
+    const int na = std::min(4, std::max(2, kb_max));
+    const int fixed = 1024 + kb_max * kHalfBlock + na * kABlockBytes + 320;
     const int slots = std::min(kMaxSlots, (max_smem - fixed) / kBoxBytes);
     const int smem = fixed + slots * kBoxBytes;
     cudaFuncSetAttribute(lora_patch_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -929,7 +936,7 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int sim
     int grid = std::min(2 * n_units, 2 * s_pairs);
     if (max_ctas > 0) grid = std::min(grid, std::max(2, max_ctas));
     grid &= ~1;
-    lora_patch_pair_kernel<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
+    lora_patch_pair_kernel<<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots, na);
     return check_launch("lora_patch_pair_kernel");
   }
   const int fixed = 1024 + kb_max * kBN * 128 + kAStages * kABlockBytes + 256;
