@@ -223,6 +223,16 @@ int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv
  * the previous setting. */
 int sdb_cross_attention_set_mode(int tcgen05);
 
+/* K8 — self-attention, head dim 64, non-causal, bf16, flash-style on tcgen05
+ * (S and PV in TMEM, online softmax one query row per thread):
+ *   o[b, i, h*64:(h+1)*64] = softmax(scale * q_h[i] . k_h^T) v_h
+ * qkv: [n, seq_len, *] rows of stride ldqkv holding Q | K | V (heads*64
+ * columns each, the fused to_qkv GEMM output); o rows of stride ldo;
+ * seq_len % 128 == 0.  The UNet's attn1 blocks (the SDPA call of a
+ * diffusers-style Attention); the reference has no attention arithmetic. */
+int sdb_self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, int seq_len, int heads,
+                       int head_dim, float scale, int dtype, void* stream);
+
 /* ========================================================================
  * Peer step handshakes (ControlNet-as-a-service over NVLink, caas.py):
  * enqueue on `stream` a wait until the 32-bit word at addr (local, IPC- or

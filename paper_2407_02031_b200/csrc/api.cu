@@ -51,6 +51,9 @@ int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void
 int cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o, int64_t ldo,
                     int n, int lq, int lk, int heads, int d, float scale, int dtype, cudaStream_t st);
 int cross_attention_set_mode(int tc);
+// self_attn.cu
+int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, int L, int heads, int head_dim,
+                   float scale, int dtype, cudaStream_t st);
 // peer_sync.cu
 int stream_wait_value32(cudaStream_t st, void* addr, uint32_t value);
 int stream_write_value32(cudaStream_t st, void* addr, uint32_t value);
@@ -238,6 +241,11 @@ int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv
 }
 
 int sdb_cross_attention_set_mode(int tcgen05) { return cross_attention_set_mode(tcgen05); }
+
+int sdb_self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, int seq_len, int heads,
+                       int head_dim, float scale, int dtype, void* stream) {
+  return self_attention(qkv, ldqkv, o, ldo, n, seq_len, heads, head_dim, scale, dtype, as_stream(stream));
+}
 
 int sdb_stream_wait_value32(void* stream, void* addr, uint32_t value) {
   return stream_wait_value32(as_stream(stream), addr, value);

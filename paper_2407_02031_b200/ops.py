@@ -495,6 +495,31 @@ def cross_attention(q: torch.Tensor, kv: torch.Tensor, heads: int, scale: Option
 
 
 # --------------------------------------------------------------------------
+# K8 — self-attention (head dim 64) on tcgen05
+# --------------------------------------------------------------------------
+def self_attention_supported(qkv: torch.Tensor, heads: int) -> bool:
+    n, l, c3 = qkv.shape
+    return (qkv.dtype == torch.bfloat16 and c3 % 3 == 0 and (c3 // 3) == heads * 64 and l % 128 == 0
+            and qkv.stride(2) == 1 and qkv.stride(1) % 8 == 0 and qkv.stride(0) == l * qkv.stride(1))
+
+
+def self_attention(qkv: torch.Tensor, heads: int, scale: Optional[float] = None,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """softmax(scale * Q K^T) V per head from the fused q|k|v projection
+    [N, L, 3C] (C = heads * 64, L % 128 == 0), bf16; returns [N, L, C]."""
+    require_cuda(qkv, out)
+    n, l, c3 = qkv.shape
+    c = c3 // 3
+    if out is None:
+        out = torch.empty((n, l, c), dtype=qkv.dtype, device=qkv.device)
+    _count(1)
+    _lib.check("sdb_self_attention", _lib.lib().sdb_self_attention(
+        qkv.data_ptr(), qkv.stride(1), out.data_ptr(), out.stride(1), n, l, heads, 64,
+        float(scale if scale is not None else 64 ** -0.5), sdb_dtype(qkv), _stream_ptr(None)))
+    return out
+
+
+# --------------------------------------------------------------------------
 # K4 — CFG combine + DDIM step (+ CFG re-batch of the next UNet input)
 # --------------------------------------------------------------------------
 def cfg_ddim_step(eps: torch.Tensor, x: torch.Tensor, coef: torch.Tensor, step_dev: torch.Tensor,

@@ -39,6 +39,9 @@ from . import ops
 
 # A/B switch for measurements: SDB_K3_GN_STATS=0 keeps the two-pass GroupNorm everywhere
 _NO_K3_STATS = os.environ.get("SDB_K3_GN_STATS", "1") == "0"
+# K8 (tcgen05 flash-style self-attention) is opt-in: SDB_SELF_ATTN=1 (round 1: slower than
+# the library SDPA at SDXL's shapes, see csrc/self_attn.cu)
+_SELF_ATTN = os.environ.get("SDB_SELF_ATTN", "0") == "1"
 
 
 # --------------------------------------------------------------------------
@@ -438,7 +441,11 @@ class Net:
     def attention(self, pre, x, ctx, heads):
         n, l, c = x.shape
         if ctx is None:   # self-attention: one GEMM for q, k, v (fused weight storage)
-            q, k, v = F.linear(x, self.t[pre + ".to_qkv.weight"]).split(c, dim=-1)
+            qkv = F.linear(x, self.t[pre + ".to_qkv.weight"])
+            if _SELF_ATTN and qkv.is_cuda and ops.self_attention_supported(qkv, heads):
+                # K8: flash-style tcgen05 attention straight off the fused projection
+                return self.lin(pre + ".to_out", ops.self_attention(qkv, heads))
+            q, k, v = qkv.split(c, dim=-1)
         else:             # cross-attention: q from x, one GEMM for k, v from the context
             q = self.lin(pre + ".to_q", x)
             kv = self.kv[self.kv_slot][pre] if self.kv_slot is not None else F.linear(ctx, self.t[pre + ".to_kv.weight"])

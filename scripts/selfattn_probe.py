@@ -59,5 +59,22 @@ def main():
         print(name, "torch_sdpa", round(res["torch_sdpa"], 2), "us;", "TFLOP/s", round(flops / res["torch_sdpa"] / 1e6, 1), flush=True)
 
 
+
+
+def k8():
+    import sys as _s
+    from pathlib import Path
+    _s.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from paper_2407_02031_b200 import ops
+    for name, (n, L, h) in {"self64": (2, 4096, 10), "self32": (2, 1024, 20)}.items():
+        qkv = torch.randn(n, L, 3 * h * 64, device="cuda", dtype=torch.bfloat16)
+        q, k, v = (t.reshape(n, L, h, 64).transpose(1, 2) for t in qkv.split(h * 64, dim=-1))
+        t_k8 = graph_time(lambda: ops.self_attention(qkv, h))
+        t_sdpa = graph_time(lambda: F.scaled_dot_product_attention(q, k, v))
+        flops = 4 * n * h * L * L * 64
+        print(name, "K8", round(t_k8, 2), "us", round(flops / t_k8 / 1e6, 1), "TF/s | sdpa", round(t_sdpa, 2), "us",
+              round(flops / t_sdpa / 1e6, 1), "TF/s", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    k8() if len(sys.argv) > 1 and sys.argv[1] == "k8" else main()

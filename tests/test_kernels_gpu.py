@@ -241,3 +241,25 @@ def test_inject_with_groupnorm_stats(ch, cs, hw, n_res, inplace):
     out2 = ops.residual_inject(skip.clone(), res, scales, hidden=hid, skip_bias=sb, hidden_bias=hb, gn_workspace=ws)
     y3 = ops.groupnorm_silu(out2, gamma, beta, groups=32, eps=1e-5, silu=True)
     assert torch.equal(y3, y)
+
+
+# K8 self-attention (head dim 64): SDXL's 32x32 and 64x64 levels, small / odd batch
+SATTN = [(2, 1024, 20), (2, 4096, 10), (1, 128, 2), (3, 256, 4), (2, 512, 5)]
+
+
+@pytest.mark.parametrize("n,l,heads", SATTN)
+def test_self_attention_vs_fp32(n, l, heads):
+    c = heads * 64
+    g = torch.Generator(device="cuda").manual_seed(l + heads)
+    qkv = (torch.randn(n, l, 3 * c, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    o = ops.self_attention(qkv, heads)
+
+    def split(t):
+        return t.reshape(n, l, heads, 64).transpose(1, 2)
+    q, k, v = (split(t) for t in qkv.split(c, dim=-1))
+    ref = F.scaled_dot_product_attention(q.float(), k.float(), v.float()).transpose(1, 2).reshape(n, l, c)
+    lib = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(n, l, c)
+    err = (o.float() - ref).abs().max().item()
+    lib_err = (lib.float() - ref).abs().max().item()
+    assert err <= 2 * lib_err + 2e-3, (err, lib_err)
+    assert torch.equal(o, ops.self_attention(qkv, heads))
