@@ -59,7 +59,7 @@ constexpr int kTileMax = 80 * 1024;          // chunk bytes per CTA (2 CTAs / SM
 // The layout is fixed ([kMaxN][slot][kMaxGroups][2]); a launch zeroes the
 // idle bank's rows up to the largest batch seen (WsHeader::hwm), so one
 // workspace may serve calls of different shapes.
-constexpr int kSlots = 32;
+constexpr int kSlots = 8;
 constexpr int kBankDoubles = kSlots * kMaxN * kMaxGroups * 2;   // 512 KB
 constexpr size_t kWsHeader = 256;            // epoch (u32) | cur (u32) | pad
 constexpr size_t kWsBytes = kWsHeader + 2 * (size_t)kBankDoubles * sizeof(double);
@@ -142,6 +142,32 @@ __device__ __forceinline__ void load_chunk(uint8_t* tile, const T* xs, int pbeg,
     const uint32_t bytes = (uint32_t)m * (uint32_t)c * (uint32_t)sizeof(T);
     mbar_expect_tx(b, bytes);
     bulk_g2s(smem_u32(tile), xs + (size_t)pbeg * c, bytes, b, pol);
+  }
+}
+
+// Apply kernel: the chunk arrives as kSlabs row slabs, each on its own
+// mbarrier, so the stores of slab k overlap the arrival of slabs k+1.. (a
+// single copy makes every CTA wait for all of its input before its first
+// store: read and write phases would never overlap inside the CTA).
+constexpr int kSlabs = 4;
+template <typename T>
+__device__ __forceinline__ void load_chunk_slabs(uint8_t* tile, const T* xs, int pbeg, int m, int c, uint64_t* bars,
+                                                 uint64_t pol) {
+  if (threadIdx.x == 0) {
+    const int rs = (m + kSlabs - 1) / kSlabs;
+    for (int k = 0; k < kSlabs; ++k) mbar_init(smem_u32(bars + k), 1);
+    mbar_fence_init();
+    for (int k = 0; k < kSlabs; ++k) {
+      const int r0 = k * rs, r1 = min(m, r0 + rs);
+      if (r1 <= r0) {
+        mbar_arrive(smem_u32(bars + k));
+        continue;
+      }
+      const uint32_t bytes = (uint32_t)(r1 - r0) * (uint32_t)c * (uint32_t)sizeof(T);
+      mbar_expect_tx(smem_u32(bars + k), bytes);
+      bulk_g2s(smem_u32(tile + (size_t)r0 * c * sizeof(T)), xs + (size_t)(pbeg + r0) * c, bytes, smem_u32(bars + k),
+               pol);
+    }
   }
 }
 
@@ -245,7 +271,7 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
                 const float* __restrict__ beta, int hw, int c, int groups, int cpg, int rows_per_chunk, int rpp,
                 float eps) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bars[kSlabs];
   __shared__ float2 gstat[kMaxGroups];   // (mean, rstd)
   const int n = blockIdx.y;
   const int cv = c >> 3;
@@ -255,23 +281,26 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
   const size_t base = (size_t)n * hw * c;
   const int pbeg = blockIdx.x * rows_per_chunk;
   const int m = min(hw, pbeg + rows_per_chunk) - pbeg;
-  load_chunk<T>(smem, x + base, pbeg, m, c, &bar, policy_evict_first());
+  load_chunk_slabs<T>(smem, x + base, pbeg, m, c, bars, policy_evict_first());
 
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
   if (threadIdx.x < groups) {
-    const unsigned int cur = *reinterpret_cast<volatile unsigned int*>(&hdr->cur);
-    const double* bank = reinterpret_cast<const double*>(ws + kWsHeader) + (size_t)cur * kBankDoubles;
+    // one memory round trip: the bank index and every slot of BOTH banks are
+    // loaded together (unused slots are zero), then the current bank is summed
+    unsigned int cur;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&hdr->cur));
+    const double* banks = reinterpret_cast<const double*>(ws + kWsHeader);
+    double2 p0[kSlots], p1[kSlots];
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+      p0[k] = __ldcg(reinterpret_cast<const double2*>(banks + bank_index(k, n, threadIdx.x)));
+      p1[k] = __ldcg(reinterpret_cast<const double2*>(banks + kBankDoubles + bank_index(k, n, threadIdx.x)));
+    }
     double m1 = 0.0, m2 = 0.0;
 #pragma unroll
-    for (int s0 = 0; s0 < kSlots; s0 += 8) {   // 8 slot loads in flight at a time (unused slots are zero)
-      double2 p[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) p[k] = __ldcg(reinterpret_cast<const double2*>(bank + bank_index(s0 + k, n, threadIdx.x)));
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        m1 += p[k].x;
-        m2 += p[k].y;
-      }
+    for (int k = 0; k < kSlots; ++k) {
+      m1 += (cur & 1u) ? p1[k].x : p0[k].x;
+      m2 += (cur & 1u) ? p1[k].y : p0[k].y;
     }
     const double cnt = (double)hw * (double)cpg;
     const double mean = m1 / cnt;
@@ -307,11 +336,13 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
       B[i] = make_float2(b[2 * i], b[2 * i + 1]);
     }
   }
-  mbar_wait(smem_u32(&bar), 0);
+  const int slab_rows = (m + kSlabs - 1) / kSlabs;
+  int ready = -1;
   const T* t = reinterpret_cast<const T*>(smem);
   T* ys = y + base + (size_t)pbeg * c;
 #pragma unroll 4
   for (int row = r; row < m; row += rpp) {
+    while (ready < row / slab_rows) mbar_wait(smem_u32(bars + ++ready), 0);
     const Raw8<T> q = load_raw<T>(t + row * c + c0);
     Raw8<T> o;
 #pragma unroll
