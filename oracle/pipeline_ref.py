@@ -191,11 +191,32 @@ def merge_loras(p: dict, adapters, matrices) -> dict:
 
 
 def denoise(cfg, unet_p: dict, cn_ps: list, req, cn_scales, steps: int, guidance: float,
-            adapters=None, matrices=None, boundary=None, bf16_acts: bool = False) -> list:
-    """Returns the fp32 [4, H, W] latent after every step."""
+            adapters=None, matrices=None, boundary=None, bf16_acts: bool = False,
+            groups=None, group_boundaries=None) -> list:
+    """Returns the fp32 [4, H, W] latent after every step.
+
+    groups / group_boundaries: group-pipelined patching
+    (addonsim/orchestrator.py:244-278) — matrix group m (a set of names) is
+    patched after step group_boundaries[m] (None = never); the steps in
+    between run a UNet with only the groups patched so far merged."""
     unet = RefUNet(cfg, unet_p, bf16_acts)
-    patched = RefUNet(cfg, merge_loras(unet_p, adapters, matrices), bf16_acts) if adapters else None
-    first = (boundary + 1) if (adapters and boundary is not None) else steps + 1
+    if groups is not None and adapters:
+        nets, firsts = [unet], []
+        for v in range(1, len(groups) + 1):
+            names = set().union(*groups[:v])
+            nets.append(RefUNet(cfg, merge_loras(unet_p, adapters, [m for m in matrices if m[0] in names]),
+                                bf16_acts))
+            b = group_boundaries[v - 1]
+            firsts.append(steps + 1 if b is None else b + 1)
+
+        def pick(s):
+            return nets[sum(1 for f in firsts if s >= f)]
+    else:
+        patched = RefUNet(cfg, merge_loras(unet_p, adapters, matrices), bf16_acts) if adapters else None
+        first = (boundary + 1) if (adapters and boundary is not None) else steps + 1
+
+        def pick(s):
+            return patched if (patched is not None and s >= first) else unet
     cns = [RefControlNet(cfg, p, bf16_acts) for p in cn_ps]
     ctx = torch.from_numpy(req.context).float()
     add_u = add_c = None
@@ -209,7 +230,7 @@ def denoise(cfg, unet_p: dict, cn_ps: list, req, cn_scales, steps: int, guidance
     for s, (t, a_t, a_p) in enumerate(ddim_coefs(steps, guidance), start=1):
         inp = x.float()[None].expand(2, -1, -1, -1)
         res = [cn.forward(inp, t, ctx, hints[i], add_c[i] if add_c else None) for i, cn in enumerate(cns)]
-        net = patched if (patched is not None and s >= first) else unet
+        net = pick(s)
         eps = net.forward(inp, t, ctx, add_u, res, cn_scales).double()
         e = eps[0] + guidance * (eps[1] - eps[0])
         x0 = (x - math.sqrt(1 - a_t) * e) / math.sqrt(a_t)

@@ -108,13 +108,17 @@ class PatchSet:
     device-resident K1 job table."""
 
     def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]],
-                 shadow: Optional[dict] = None, use_tma: bool = True, simt_max_rank: int = 0):
+                 shadow: Optional[dict] = None, use_tma: bool = True, simt_max_rank: int = 0,
+                 only: Optional[set] = None):
         if not adapters:
             raise ValidationError("PatchSet needs at least one adapter")
         self.params = params
         self.shadow = shadow
         self.adapters = list(adapters)
-        names = [n for n, _ in params.matrices if any(n in a.factors for a, _ in adapters)]
+        names = [n for n, _ in params.matrices if any(n in a.factors for a, _ in adapters)
+                 and (only is None or n in only)]
+        if not names:
+            raise ValidationError("PatchSet: no adapter touches the selected matrices")
         self.touched = set(names)
         ranks = {n: sum(a.factors[n][0].shape[1] for a, _ in adapters if n in a.factors) for n in names}
         self.rank = max(ranks.values())
@@ -201,35 +205,84 @@ class AdapterBank:
     device views it fills are what a PatchSet packs from, so fetch -> repack ->
     patch is a stream-ordered chain that needs no host round trip."""
 
-    def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]], device=None):
+    def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]], device=None,
+                 groups: Optional[Sequence[set]] = None):
+        """groups: optional partition of the matrix names (patch groups, see
+        ``split_patch_groups``): each adapter's factors are laid out group by
+        group so ``fetch(stream, group=m)`` copies one group's slice."""
         device = torch.device(device) if device is not None else params.device
         self.host, self.dev, self.adapters = [], [], []
         self.nbytes = 0
+        self.group_spans = []          # per adapter: [(begin, end)] element range of each group
+        gidx = {}
+        for m, g in enumerate(groups or []):
+            for name in g:
+                gidx[name] = m
+        order = {n: i for i, (n, _) in enumerate(params.matrices)}
         for a, s in adapters:
             dtype = next(iter(a.factors.values()))[0].dtype
             items = []
-            for name, (d, u) in a.factors.items():
+            for name, (d, u) in sorted(a.factors.items(), key=lambda kv: (gidx.get(kv[0], 0), order.get(kv[0], 0))):
                 up = u if a.up_physical else physical_up(params, name, u.to(params.device))
                 items.append((name, d, up))
             total = sum(d.numel() + up.numel() for _, d, up in items)
             host = torch.empty(total, dtype=dtype).pin_memory()
             dev = torch.empty(total, dtype=dtype, device=device)
             views, off = {}, 0
+            n_groups = max(1, len(groups or []))
+            spans = [[None, None] for _ in range(n_groups)]
             for name, d, up in items:
                 nd, nu = d.numel(), up.numel()
                 host[off:off + nd].copy_(d.reshape(-1).cpu())
                 host[off + nd:off + nd + nu].copy_(up.reshape(-1).cpu())
                 views[name] = (dev[off:off + nd].view(d.shape), dev[off + nd:off + nd + nu].view(up.shape))
+                m = gidx.get(name, 0)
+                spans[m][0] = off if spans[m][0] is None else spans[m][0]
+                spans[m][1] = off + nd + nu
                 off += nd + nu
+            self.group_spans.append([(b or 0, e or 0) for b, e in spans])
             self.host.append(host)
             self.dev.append(dev)
             self.nbytes += total * host.element_size()
             self.adapters.append((UNetLora(a.adapter_id, views, a.scale, up_physical=True), s))
 
-    def fetch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+    def fetch(self, stream: Optional[torch.cuda.Stream] = None, group: Optional[int] = None) -> None:
         with torch.cuda.stream(stream) if stream is not None else _nullctx():
-            for h, d in zip(self.host, self.dev):
-                d.copy_(h, non_blocking=True)
+            for h, d, spans in zip(self.host, self.dev, self.group_spans):
+                if group is None:
+                    d.copy_(h, non_blocking=True)
+                else:
+                    b, e = spans[group]
+                    if e > b:
+                        d[b:e].copy_(h[b:e], non_blocking=True)
+
+
+def split_patch_groups(params: Params, n_groups: int) -> list:
+    """Partition the patchable matrices into n_groups contiguous runs of the
+    UNet order with ~equal weight bytes (the pipelined loading of
+    orchestrator.py:244-278 / PAPER.md:520-528: group m can be patched as soon
+    as its own slice of the adapters has arrived).  Members of a fused storage
+    (q|k|v, k|v) stay in one group: they are swapped together."""
+    if n_groups < 1:
+        raise ValidationError("n_groups must be >= 1")
+    parent_of = {}
+    for parent, members in params.fused.items():
+        for m in members:
+            parent_of[m] = parent
+    names = [n for n, _ in params.matrices]
+    sizes = {n: params.t[n + ".weight"].numel() for n in names}
+    total = sum(sizes.values())
+    groups, cur, acc = [], [], 0
+    for i, n in enumerate(names):
+        cur.append(n)
+        acc += sizes[n]
+        nxt = names[i + 1] if i + 1 < len(names) else None
+        same_parent = nxt is not None and n in parent_of and parent_of.get(nxt) == parent_of[n]
+        if (len(groups) < n_groups - 1 and acc >= total * (len(groups) + 1) / n_groups and not same_parent):
+            groups.append(set(cur))
+            cur = []
+    groups.append(set(cur))
+    return [g for g in groups if g]
 
 
 class _nullctx:

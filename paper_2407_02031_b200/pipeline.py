@@ -33,9 +33,9 @@ import numpy as np
 import torch
 
 from . import ops
-from .patcher import AdapterBank, PatchSet, UNetLora, allocate_shadow
+from .patcher import AdapterBank, PatchSet, UNetLora, allocate_shadow, split_patch_groups
 from .scheduler import ddim_tables
-from .schedule import plan_lora_patch
+from .schedule import plan_lora_patch, plan_pipeline_patch
 from .unet import ControlNet, UNet, UNetConfig, init_controlnet, init_unet
 
 
@@ -151,13 +151,37 @@ class AddonPipeline:
         self.patch_timing: Optional[list] = None   # bench: (start, K1 end) events of each patch launch
         self.last_patch_k1_event = None
         self.launches_per_step = 0
+        # group-pipelined patching (orchestrator.py:244-278): M contiguous
+        # matrix groups, each fetched / patched / swapped in on its own
+        self.patch_groups: Optional[list] = None
+        self.group_patchsets: list = []
+        self.group_graphs: list = []
+        self.group_loads_ms: Optional[list] = None
+        self.last_group_boundaries: Optional[list] = None
 
     # ------------------------------------------------------------------
     def _weight_names(self) -> list:
         return [n for n, _ in self.unet_p.matrices] + list(self.unet_p.fused)
 
+    def _variant_weights(self, which: str) -> dict:
+        """{weight name: tensor} of a weight set: "pristine", "patched" (every
+        LoRA group swapped in) or "pg<v>" (the first v patch groups swapped in,
+        the rest pristine — group-pipelined patching)."""
+        if which == "pristine":
+            return self._pristine
+        if which == "patched":
+            return self.shadow
+        if not which.startswith("pg") or self.patch_groups is None:
+            raise ValueError(f"unknown weight set {which!r}")
+        v = int(which[2:])
+        swapped = set().union(*self.patch_groups[:v])
+        for parent, members in self.unet_p.fused.items():
+            if all(m in swapped for m in members):
+                swapped.add(parent)
+        return {n: (self.shadow[n] if n in swapped else self._pristine[n]) for n in self._weight_names()}
+
     def _use_weights(self, which: str) -> None:
-        src = self.shadow if which == "patched" else self._pristine
+        src = self._variant_weights(which)
         for name in self._weight_names():
             self.unet_p.t[name + ".weight"] = src[name]
         self.unet.kv_slot = which            # the matching cross-attention K|V slot
@@ -204,7 +228,8 @@ class AddonPipeline:
         torch.cuda.synchronize(self.device)
 
     # ------------------------------------------------------------------
-    def load_loras(self, adapters: Sequence[tuple[UNetLora, float]], host_resident: bool = False) -> PatchSet:
+    def load_loras(self, adapters: Sequence[tuple[UNetLora, float]], host_resident: bool = False,
+                   groups: int = 1) -> PatchSet:
         """Stack the request's adapters into one planned K1 launch writing the
         shadow weights (allocated once).
 
@@ -213,10 +238,20 @@ class AddonPipeline:
         (orchestrator.py:509-528): H2D on a copy stream,
         then ONE CUDA graph on the patch stream re-stacks/re-packs them and
         runs K1, all overlapped with the first denoising steps; the plan's
-        "load" time is fetch + pack + patch."""
+        "load" time is fetch + pack + patch.
+
+        groups > 1: group-pipelined patching (orchestrator.py:244-278,
+        PAPER.md:520-528) — the matrices split into ``groups`` contiguous runs
+        (split_patch_groups); each group is fetched, packed and patched by its
+        own K1 launch and swapped in at its own step boundary
+        (plan_pipeline_patch), so the early groups need not wait for the whole
+        adapter set.  One extra step graph per partial weight set."""
         if self.shadow is None:
             _ = self._pristine
             self.shadow = allocate_shadow(self.unet_p)
+        if groups > 1:
+            return self._load_groups(adapters, host_resident, groups)
+        self.patch_groups, self.group_patchsets, self.group_graphs = None, [], []
         self.bank = AdapterBank(self.unet_p, adapters, self.device) if host_resident else None
         if self.bank is not None:
             adapters = self.bank.adapters
@@ -235,6 +270,136 @@ class AddonPipeline:
         if self.use_graphs and "patched" not in self.graphs:
             self._capture("patched")
         return self.patchset
+
+    def _load_groups(self, adapters, host_resident: bool, n_groups: int) -> PatchSet:
+        touched = {n for a, _ in adapters for n in a.factors}
+        split = [g for g in split_patch_groups(self.unet_p, n_groups) if g & touched]
+        self.patch_groups = split
+        self.group_loads_ms = None
+        self.bank = AdapterBank(self.unet_p, adapters, self.device, groups=split) if host_resident else None
+        if self.bank is not None:
+            adapters = self.bank.adapters
+            self.bank.fetch()
+        self.group_patchsets = [PatchSet(self.unet_p, adapters, shadow=self.shadow, only=g) for g in split]
+        covered = set().union(*(ps.touched for ps in self.group_patchsets))
+        for name, _ in self.unet_p.matrices:          # untouched shadow entries mirror pristine
+            if name not in covered:
+                self.shadow[name].copy_(self.unet_p.t[name + ".weight"])
+        self.patchset = self.group_patchsets[-1]
+        self.patch_graph = None
+        self.group_graphs = []
+        if self.bank is not None:
+            torch.cuda.synchronize(self.device)
+            self.patch_stream.wait_stream(torch.cuda.current_stream(self.device))
+            for ps in self.group_patchsets:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.patch_stream):
+                    ps.refresh(self.patch_stream)
+                    ps.launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+                self.group_graphs.append(g)
+        key = tuple(frozenset(g) for g in split)
+        if getattr(self, "_graph_split", None) != key:      # partial sets changed: recapture
+            for k in [k for k in self.graphs if k.startswith("pg")]:
+                del self.graphs[k]
+            self._graph_split = key
+        variants = [f"pg{v}" for v in range(1, len(split))] + ["patched"]
+        for v in variants:
+            self.unet.ensure_kv_slot(v)
+            if self.use_graphs and v not in self.graphs:
+                self._capture(v)
+        return self.patchset
+
+    def launch_patch_groups(self, timing: bool = False, fetch: bool = True):
+        """Enqueue every group's fetch -> pack -> K1 -> K|V chain on the side
+        streams (group m's fetch overlaps group m-1's patch); returns (start
+        event, [ready event per group]).  Group m's ready event also covers
+        the K|V slot of weight set m+1."""
+        s = torch.cuda.current_stream(self.device)
+        M = len(self.patch_groups)
+        p0 = torch.cuda.Event(enable_timing=True) if timing else None
+        self.copy_stream.wait_stream(s)
+        self.copy_stream.wait_stream(self.patch_stream)       # previous request's packs done
+        self.patch_stream.wait_stream(s)                      # shadow free once earlier steps finished
+        if timing:
+            p0.record(self.copy_stream if self.bank is not None else self.patch_stream)
+            if self.bank is None:
+                self.copy_stream.wait_event(p0)
+        ready = []
+        for m in range(M):
+            if self.bank is not None:
+                if fetch:
+                    self.bank.fetch(self.copy_stream, group=m)
+                fe = torch.cuda.Event()
+                fe.record(self.copy_stream)
+                self.patch_stream.wait_event(fe)
+                with torch.cuda.stream(self.patch_stream):
+                    self.group_graphs[m].replay()
+            else:
+                self.group_patchsets[m].launch(stream=self.patch_stream, max_ctas=self.patch_max_ctas)
+            v = "patched" if m == M - 1 else f"pg{m + 1}"
+            with torch.cuda.stream(self.patch_stream):
+                self.unet.compute_kv(self.ctx, v, weights=self._variant_weights(v))
+            ev = torch.cuda.Event(enable_timing=timing)
+            ev.record(self.patch_stream)
+            ready.append(ev)
+        return p0, ready
+
+    def calibrate_groups(self) -> list:
+        """Measured ready time (ms after the request's start) of each patch
+        group — plan_pipeline_patch's group_loads_ms."""
+        if self.step_ms_est is None:
+            return self.calibrate() and self.group_loads_ms
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.stream(self.main_stream):
+            p0, ready = self.launch_patch_groups(timing=True)
+        ready[-1].synchronize()
+        loads = [p0.elapsed_time(e) for e in ready]
+        for i in range(1, len(loads)):      # events on one stream: guard float noise
+            loads[i] = max(loads[i], loads[i - 1])
+        self.group_loads_ms = loads
+        return loads
+
+    def denoise_pipelined(self, boundaries: Optional[Sequence[int]] = None, on_step=None,
+                          fetch: bool = True) -> list:
+        """Group-pipelined patching: group m is swapped in after step
+        boundaries[m] (forced, non-decreasing) or at the boundary
+        plan_pipeline_patch picks from the calibrated group ready times
+        (per_group_patch_ms = 0: the patch runs on the side stream into the
+        shadow weights).  Returns the boundary of each group (None = the group
+        missed the request)."""
+        if not self.patch_groups:
+            raise RuntimeError("denoise_pipelined needs load_loras(groups > 1) first")
+        M = len(self.patch_groups)
+        if boundaries is None:
+            if self.group_loads_ms is None:
+                self.calibrate_groups()
+            plan = plan_pipeline_patch(self.group_loads_ms, self.step_ms_est, 0.0, self.steps)
+            bounds = [g.boundary_step for g in plan.groups] + [None] * (M - len(plan.groups))
+        else:
+            bounds = list(boundaries)
+            if len(bounds) != M or any(b is not None and b < 0 for b in bounds):
+                raise ValueError(f"need {M} non-negative boundaries")
+            live = [b for b in bounds if b is not None]
+            if any(b2 < b1 for b1, b2 in zip(live, live[1:])) or (None in bounds and
+                                                                  any(b is not None for b in bounds[bounds.index(None):])):
+                raise ValueError("group boundaries must be non-decreasing (None only as a suffix)")
+        s = torch.cuda.current_stream(self.device)
+        p0, ready = self.launch_patch_groups(timing=self.patch_timing is not None, fetch=fetch)
+        waited = 0
+        for step in range(1, self.steps + 1):
+            v = sum(1 for b in bounds if b is not None and b + 1 <= step)
+            while waited < v:
+                s.wait_event(ready[waited])
+                waited += 1
+            which = "pristine" if v == 0 else ("patched" if v == M else f"pg{v}")
+            self._replay(which)
+            if on_step is not None:
+                on_step(step, self.latent_nchw().clone())
+        s.wait_event(ready[-1])              # never leave the side streams dangling
+        self.last_group_boundaries = bounds
+        live = [b for b in bounds if b is not None]
+        self.last_first_patched_step = bounds[-1] + 1 if len(live) == M else self.steps + 1
+        return bounds
 
     def launch_patch(self, timing: bool = False, fetch: bool = True):
         """Enqueue the request's patch on the side streams; returns (start, done)
@@ -290,7 +455,9 @@ class AddonPipeline:
             e1.record(s)
         e1.synchronize()
         self.step_ms_est = e0.elapsed_time(e1) / reps
-        if self.patchset is not None:
+        if self.patch_groups:
+            self.patch_ms_est = self.calibrate_groups()[-1]
+        elif self.patchset is not None:
             p0, p1 = self.launch_patch(timing=True)
             p1.synchronize()
             self.patch_ms_est = p0.elapsed_time(p1)   # the plan's "load": fetch + pack + patch

@@ -320,6 +320,12 @@ class Net:
         self.kv = {s: {pre: torch.zeros((n, l, self.t[pre + ".to_kv.weight"].shape[0]), device=ctx.device,
                                         dtype=self.p.dtype) for pre in self.kv_prefixes()} for s in slots}
 
+    def ensure_kv_slot(self, slot: str) -> None:
+        """Add one more static K|V slot (e.g. a partially patched weight set)."""
+        if slot not in self.kv:
+            ref = next(iter(self.kv.values()))
+            self.kv[slot] = {pre: torch.zeros_like(buf) for pre, buf in ref.items()}
+
     def compute_kv(self, ctx: torch.Tensor, slot: str, weights: Optional[dict] = None) -> None:
         """Fill ``slot`` from ctx (stream-ordered on the current stream);
         weights: optional {"<prefix>.to_kv": tensor} override (e.g. the LoRA

@@ -219,3 +219,70 @@ def test_serving_batch_matches_single_images(fp32_mode):
     grp.denoise(patch=True, boundary=1)
     torch.cuda.synchronize()
     assert rel_l2(grp.latent_nchw(), got) <= 1e-5
+
+
+def test_group_pipelined_patch_matches_oracle(fp32_mode):
+    """Group-pipelined patching (orchestrator.py:244-278): 3 matrix groups
+    swapped in at boundaries 2, 4, 7 — every step matches the oracle run with
+    the same partial merges; host-resident groups are bitwise the device-
+    resident ones (same kernels on the same packed operands)."""
+    bounds = [2, 4, 7]
+
+    def run(host):
+        pipe = AddonPipeline(U.TOY, n_controlnets=1, cn_scales=[CN_SCALE], steps=10, guidance=GUIDANCE,
+                             dtype=torch.float32, seed=0)
+        lora = synthetic_lora(pipe.unet_p, 8, seed=7, adapter_id="l0", scale=LORA_SCALE)
+        pipe.load_loras([(lora, LORA_SCALE)], host_resident=host, groups=3)
+        assert len(pipe.patch_groups) == 3
+        pipe.setup()
+        req = synthetic_request(U.TOY, 1, seed=0)
+        pipe.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context),
+                     [torch.from_numpy(req.images[0])])
+        per = []
+        got = pipe.denoise_pipelined(bounds, on_step=lambda s, x: per.append(x.float().cpu()))
+        torch.cuda.synchronize()
+        assert got == bounds and pipe.last_first_patched_step == bounds[-1] + 1
+        return pipe, lora, req, per
+
+    pipe, lora, req, dev = run(False)
+    up = R.to_cpu_params(pipe.unet_p)
+    cps = [R.to_cpu_params(p) for p in pipe.cn_p]
+    ref = R.denoise(U.TOY, up, cps, req, [CN_SCALE], 10, GUIDANCE, adapters=[(lora.factors, LORA_SCALE)],
+                    matrices=pipe.unet_p.matrices, groups=pipe.patch_groups, group_boundaries=bounds)
+    errs = [rel_l2(a, b) for a, b in zip(dev, ref)]
+    print("grouped fp32 per-step rel-L2:", ["%.1e" % e for e in errs])
+    assert max(errs) <= 1e-5
+    # the partial weight sets are really different: all-at-once at the last boundary diverges
+    once = R.denoise(U.TOY, up, cps, req, [CN_SCALE], 10, GUIDANCE, adapters=[(lora.factors, LORA_SCALE)],
+                     matrices=pipe.unet_p.matrices, boundary=bounds[-1])
+    assert rel_l2(dev[-1], once[-1]) > 1e-4
+    _, _, _, host = run(True)
+    for a, b in zip(dev, host):
+        assert torch.equal(a, b)
+
+
+def test_group_pipelined_equal_boundaries_is_single_patch():
+    """All groups at one boundary == the single-launch patch at that boundary, bitwise."""
+    def run(groups):
+        pipe = AddonPipeline(U.TOY, n_controlnets=1, steps=6, dtype=torch.bfloat16, seed=0)
+        los = [(synthetic_lora(pipe.unet_p, r, seed=7 + r, adapter_id=f"l{r}"), 0.6) for r in (8, 16)]
+        pipe.load_loras(los, host_resident=True, groups=groups)
+        pipe.setup()
+        req = synthetic_request(U.TOY, 1)
+        pipe.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(req.images[0])])
+        if groups == 1:
+            pipe.denoise(patch=True, boundary=2)
+        else:
+            pipe.denoise_pipelined([2] * len(pipe.patch_groups))
+        return pipe.latent_nchw().clone(), pipe
+    a, _ = run(1)
+    b, pipe = run(4)
+    assert torch.equal(a, b)
+    loads = pipe.calibrate_groups()            # planned path: measured group ready times
+    assert len(loads) == len(pipe.patch_groups) and all(x > 0 for x in loads)
+    req = synthetic_request(U.TOY, 1)
+    pipe.prepare(torch.from_numpy(req.latent), torch.from_numpy(req.context), [torch.from_numpy(req.images[0])])
+    bounds = pipe.denoise_pipelined()
+    plan = __import__("paper_2407_02031_b200.schedule", fromlist=["x"]).plan_pipeline_patch(
+        loads, pipe.step_ms_est, 0.0, pipe.steps)
+    assert bounds[:len(plan.groups)] == [g.boundary_step for g in plan.groups]
