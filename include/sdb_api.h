@@ -278,6 +278,18 @@ int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_o
                       void* unet_in, int in_dtype, int64_t latent_elems,
                       const float* coef, int* step_dev, void* stream);
 
+/* ========================================================================
+ * K9 — the UNet output convolution: 3x3, pad 1, C -> 4 channels, fp32 out.
+ *   out[n, y, x, o] = bias[o] + sum_{dy, dx, c} x[n, y+dy-1, x+dx-1, c] * w[o, dy, dx, c]
+ * x: NHWC (channels_last) [n, h, width, c] of `dtype` (SDB_BF16 / SDB_F32);
+ * w: the weight's physical channels_last layout [cout, 3, 3, c], same dtype;
+ * bias: fp32 [cout] or NULL; out: fp32 NHWC [n, h, width, cout].
+ * fp32 accumulation.  cout must be 4, width a multiple of 16, c even <= 1280.
+ * Replaces the UNet's conv_out (no reference counterpart: SURVEY §0.2).
+ * ======================================================================== */
+int sdb_conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h,
+                 int64_t width, int64_t c, int64_t cout, int dtype, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

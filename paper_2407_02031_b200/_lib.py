@@ -39,6 +39,7 @@ EXPORTED = (
     "sdb_residual_inject_gn",
     "sdb_groupnorm_apply",
     "sdb_cfg_ddim_step",
+    "sdb_conv_out",
 )
 
 
@@ -106,6 +107,8 @@ def _declare(lib: ctypes.CDLL) -> None:
                                              ctypes.POINTER(ctypes.c_float), i32, i64, i64, i64, vp, vp, i32, vp]
     lib.sdb_cfg_ddim_step.restype = i32
     lib.sdb_cfg_ddim_step.argtypes = [vp, i32, vp, vp, vp, i32, i64, vp, vp, vp]
+    lib.sdb_conv_out.restype = i32
+    lib.sdb_conv_out.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, i32, vp]
 
 
 def lib() -> ctypes.CDLL:

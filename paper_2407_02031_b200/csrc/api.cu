@@ -58,6 +58,9 @@ int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, 
 int stream_wait_value32(cudaStream_t st, void* addr, uint32_t value);
 int stream_write_value32(cudaStream_t st, void* addr, uint32_t value);
 int memcpy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// conv_out.cu
+int conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h, int64_t w_,
+             int64_t c, int64_t cout, int dtype, cudaStream_t st);
 // cfg_step.cu
 int cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_out, void* unet_in,
                   int in_dtype, int64_t L, const float* coef, int* step_dev, cudaStream_t st);
@@ -264,6 +267,11 @@ int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_o
                       void* stream) {
   return cfg_ddim_step(eps, eps_dtype, x, x_out, unet_in, in_dtype, latent_elems, coef, step_dev,
                        as_stream(stream));
+}
+
+int sdb_conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h,
+                 int64_t width, int64_t c, int64_t cout, int dtype, void* stream) {
+  return conv_out(x, w, bias, out, n, h, width, c, cout, dtype, as_stream(stream));
 }
 
 }  // extern "C"

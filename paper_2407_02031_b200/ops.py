@@ -522,6 +522,42 @@ def self_attention(qkv: torch.Tensor, heads: int, scale: Optional[float] = None,
 # --------------------------------------------------------------------------
 # K4 — CFG combine + DDIM step (+ CFG re-batch of the next UNet input)
 # --------------------------------------------------------------------------
+def conv_out_supported(x: torch.Tensor, w: torch.Tensor) -> bool:
+    return (x.dim() == 4 and w.dim() == 4 and w.shape[0] == 4 and tuple(w.shape[2:]) == (3, 3)
+            and x.dtype in (torch.bfloat16, torch.float32) and w.dtype == x.dtype
+            and x.shape[3] % 16 == 0 and x.shape[1] % 2 == 0 and x.shape[1] <= 1280
+            and x.is_contiguous(memory_format=torch.channels_last))
+
+
+def conv_out(x: torch.Tensor, w: torch.Tensor, bias: Optional[torch.Tensor] = None,
+             out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """K9: 3x3 pad-1 convolution C -> 4 with an fp32 result (the UNet's
+    conv_out), x channels_last bf16/fp32, fp32 accumulation.  Returns an fp32
+    channels_last [N, 4, H, W] tensor."""
+    require_cuda(x, w, bias, out)
+    n, c, h, wd = x.shape
+    if not conv_out_supported(x, w) or w.shape[1] != c:
+        raise ValidationError("conv_out: needs channels_last x [N, C, H, W] (W % 16 == 0, C even <= 1280) "
+                              "and a same-dtype [4, C, 3, 3] weight")
+    wp = w.permute(0, 2, 3, 1)
+    if not wp.is_contiguous():
+        wp = wp.contiguous()
+    b = None
+    if bias is not None:
+        b = bias if bias.dtype == torch.float32 and bias.is_contiguous() else bias.float().contiguous()
+    if out is None:
+        out = torch.empty((n, 4, h, wd), device=x.device, dtype=torch.float32,
+                          memory_format=torch.channels_last)
+    elif out.dtype != torch.float32 or not out.is_contiguous(memory_format=torch.channels_last) \
+            or tuple(out.shape) != (n, 4, h, wd):
+        raise ValidationError("conv_out: out must be fp32 channels_last [N, 4, H, W]")
+    _count(1)
+    _lib.check("sdb_conv_out", _lib.lib().sdb_conv_out(
+        x.data_ptr(), wp.data_ptr(), b.data_ptr() if b is not None else None, out.data_ptr(),
+        n, h, wd, c, 4, sdb_dtype(x), _stream_ptr(None)))
+    return out
+
+
 def cfg_ddim_step(eps: torch.Tensor, x: torch.Tensor, coef: torch.Tensor, step_dev: torch.Tensor,
                   x_out: Optional[torch.Tensor] = None,
                   unet_in: Optional[torch.Tensor] = None) -> torch.Tensor:

@@ -577,6 +577,8 @@ class UNet(Net):
         # guidance scale, so a bf16 rounding here would dominate the latent error
         w = self.t["conv_out.weight"]
         b = self.t.get("conv_out.bias")
+        if ops.conv_out_supported(h, w):
+            return ops.conv_out(h, w, self.fb.get("conv_out"))       # K9, fp32 accumulate
         return F.conv2d(h.float(), w.float(), None if b is None else b.float(), padding=w.shape[-1] // 2)
 
     def forward(self, x, t, ctx, add_emb=None, residuals=None, res_scales=None):

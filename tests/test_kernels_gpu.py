@@ -263,3 +263,24 @@ def test_self_attention_vs_fp32(n, l, heads):
     lib_err = (lib.float() - ref).abs().max().item()
     assert err <= 2 * lib_err + 2e-3, (err, lib_err)
     assert torch.equal(o, ops.self_attention(qkv, heads))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n,c,h,w", [(2, 320, 128, 128), (2, 320, 64, 64), (4, 32, 16, 48), (1, 1280, 8, 16),
+                                     (2, 66, 5, 16)])
+@pytest.mark.parametrize("with_bias", [True, False])
+def test_conv_out_vs_fp64(dtype, n, c, h, w, with_bias):
+    """K9: 3x3 pad-1 conv C -> 4 with fp32 accumulation vs an fp64 torch
+    conv of the same (bf16-exact) operands."""
+    g = torch.Generator(device="cuda").manual_seed(c + h)
+    x = cl(torch.randn(n, c, h, w, device="cuda", generator=g).to(dtype))
+    wt = cl((torch.randn(4, c, 3, 3, device="cuda", generator=g) / math.sqrt(9 * c)).to(dtype))
+    b = torch.randn(4, device="cuda", generator=g) if with_bias else None
+    y = ops.conv_out(x, wt, b)
+    ref = F.conv2d(x.double(), wt.double(), None if b is None else b.double(), padding=1)
+    assert y.dtype == torch.float32 and y.is_contiguous(memory_format=torch.channels_last)
+    err = (y.double() - ref).abs().max().item()
+    # fp32 accumulation of 9C exact products: |err| <~ 9C * 2^-24 * sum|terms|
+    bound = 9 * c * 2 ** -24 * (x.double().abs().amax() * wt.double().abs().amax() * 9 * c).item() + 1e-6
+    assert err <= bound, (err, bound)
+    assert err <= 1e-4 * ref.abs().max().item() + 1e-5
