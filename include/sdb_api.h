@@ -158,6 +158,14 @@ int sdb_lora_tc_set_mode(int mode);
  * workspace must be ordered on one stream.  y may alias x.
  * ======================================================================== */
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
+/* K2 form selection: mode 0 (default) runs the single-pass cluster form
+ * (the whole map of one (sample, channel slab) in the shared memory of a
+ * thread-block cluster: one read, one write, one launch) wherever the shape
+ * fits (bf16, C/G >= 8, slab rows <= 200 KB per CTA, <= 16 CTAs), else the
+ * two-pass form; mode 1 forces the two-pass form.  sdb_groupnorm_launches
+ * returns the kernel launches sdb_groupnorm_silu will make for a shape. */
+void sdb_groupnorm_set_mode(int mode);
+int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
 int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
                        const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups, float eps,
                        int apply_silu, int dtype, void* workspace, void* stream);

@@ -40,6 +40,8 @@ EXPORTED = (
     "sdb_groupnorm_apply",
     "sdb_cfg_ddim_step",
     "sdb_conv_out",
+    "sdb_groupnorm_set_mode",
+    "sdb_groupnorm_launches",
 )
 
 
@@ -107,6 +109,10 @@ def _declare(lib: ctypes.CDLL) -> None:
                                              ctypes.POINTER(ctypes.c_float), i32, i64, i64, i64, vp, vp, i32, vp]
     lib.sdb_cfg_ddim_step.restype = i32
     lib.sdb_cfg_ddim_step.argtypes = [vp, i32, vp, vp, vp, i32, i64, vp, vp, vp]
+    lib.sdb_groupnorm_set_mode.restype = None
+    lib.sdb_groupnorm_set_mode.argtypes = [i32]
+    lib.sdb_groupnorm_launches.restype = i32
+    lib.sdb_groupnorm_launches.argtypes = [i64, i64, i64, i64, i32]
     lib.sdb_conv_out.restype = i32
     lib.sdb_conv_out.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, i32, vp]
 

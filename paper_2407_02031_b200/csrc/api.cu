@@ -58,6 +58,9 @@ int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, 
 int stream_wait_value32(cudaStream_t st, void* addr, uint32_t value);
 int stream_write_value32(cudaStream_t st, void* addr, uint32_t value);
 int memcpy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// gn_cluster.cu
+extern int g_gn_cluster_mode;
+int gn_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
 // conv_out.cu
 int conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h, int64_t w_,
              int64_t c, int64_t cout, int dtype, cudaStream_t st);
@@ -267,6 +270,12 @@ int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_o
                       void* stream) {
   return cfg_ddim_step(eps, eps_dtype, x, x_out, unet_in, in_dtype, latent_elems, coef, step_dev,
                        as_stream(stream));
+}
+
+void sdb_groupnorm_set_mode(int mode) { g_gn_cluster_mode = mode; }
+
+int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype) {
+  return gn_launches(n, hw, c, groups, dtype);
 }
 
 int sdb_conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h,

@@ -309,6 +309,17 @@ def nhwc_view(x: torch.Tensor) -> tuple[int, int, int]:
     raise ValidationError(f"expected a 3-d or 4-d tensor, got {x.dim()}-d")
 
 
+@contextlib.contextmanager
+def groupnorm_mode(mode: int):
+    """K2 form for calls inside the block: 0 = single-pass cluster form where
+    eligible (default), 1 = two-pass form (tests / probes)."""
+    _lib.lib().sdb_groupnorm_set_mode(int(mode))
+    try:
+        yield
+    finally:
+        _lib.lib().sdb_groupnorm_set_mode(0)
+
+
 def groupnorm_workspace(x: torch.Tensor, groups: int = 32) -> torch.Tensor:
     """A zeroed K2 workspace sized for x (its counters must start at zero;
     every launch leaves them at zero)."""
@@ -355,7 +366,7 @@ def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optiona
         ws = workspace
     else:
         ws = _workspace(ws_bytes, x.device)
-    _count(3)
+    _count(_lib.lib().sdb_groupnorm_launches(n, hw, c, groups, sdb_dtype(x)))
     _lib.check("sdb_groupnorm_silu", _lib.lib().sdb_groupnorm_silu(
         x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,
         beta.data_ptr() if beta is not None else None,

@@ -284,3 +284,40 @@ def test_conv_out_vs_fp64(dtype, n, c, h, w, with_bias):
     bound = 9 * c * 2 ** -24 * (x.double().abs().amax() * wt.double().abs().amax() * 9 * c).item() + 1e-6
     assert err <= bound, (err, bound)
     assert err <= 1e-4 * ref.abs().max().item() + 1e-5
+
+
+@pytest.mark.parametrize("c,h,w", [(1280, 32, 32), (640, 32, 32), (1920, 16, 16), (2560, 16, 16), (4096, 3, 5),
+                                   (320, 64, 64), (960, 32, 32)])
+@pytest.mark.parametrize("n", [1, 2, 4])
+@pytest.mark.parametrize("with_add", [True, False])
+def test_groupnorm_single_pass_cluster_form(c, h, w, n, with_add):
+    """K2 single-pass cluster form (gn_cluster.cu) vs the fp32 torch GN and
+    vs the two-pass form; one launch where the plan says so; bitwise
+    reproducible (fixed-order reductions, no atomics)."""
+    if n * c * h * w * 2 > 6 << 20:
+        pytest.skip("above the cluster form's size class")
+    g = torch.Generator(device="cuda").manual_seed(c + h + n)
+    x = cl((torch.randn(n, c, h, w, device="cuda", generator=g) * 2 + 0.7).to(torch.bfloat16))
+    gamma = torch.rand(c, device="cuda", generator=g) + 0.5
+    beta = torch.randn(c, device="cuda", generator=g)
+    add = torch.randn(n, c, device="cuda", generator=g) if with_add else None
+    assert ops._lib.lib().sdb_groupnorm_launches(n, h * w, c, 32, ops.sdb_dtype(x)) == 1
+    y = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+    y2 = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+    assert torch.equal(y, y2)
+    xin = x.float() + (add[:, :, None, None] if add is not None else 0)
+    ref = F.silu(F.group_norm(xin, 32, gamma, beta, 1e-5))
+    err = (y.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 2e-3).all(), float(err.max())
+    with ops.groupnorm_mode(1):
+        assert ops._lib.lib().sdb_groupnorm_launches(n, h * w, c, 32, ops.sdb_dtype(x)) == 2
+        yt = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+    assert (y.float() - yt.float()).abs().max().item() <= 2 ** -7 * (ref.abs().max().item() + 1)
+
+
+def test_groupnorm_large_maps_take_the_two_pass_form():
+    lib = ops._lib.lib()
+    bf16 = ops.sdb_dtype(torch.empty(0, dtype=torch.bfloat16))
+    assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 2
+    assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, bf16) == 1
+    assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, ops.sdb_dtype(torch.empty(0))) == 2   # fp32
