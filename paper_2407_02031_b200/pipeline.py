@@ -87,18 +87,34 @@ def synthetic_batch(cfg: UNetConfig, n_controlnets: int, batch: int, seed: int =
                    cfg_cat([r.time_ids for r in reqs]) if cfg.addition_embed else None)
 
 
+@dataclass
+class SharedWeights:
+    """One UNet + ControlNet weight set (and its LoRA shadow copy) shared by
+    engines of different shapes (serving.EngineCache)."""
+    unet_p: object
+    cn_p: list
+    shadow: Optional[dict] = None
+
+
 class AddonPipeline:
     """SD-style UNet + N ControlNets + LoRA on one B200."""
 
     def __init__(self, cfg: UNetConfig, n_controlnets: int = 1, cn_scales: Optional[Sequence[float]] = None,
                  steps: int = 30, guidance: float = 7.5, device="cuda", dtype=torch.bfloat16,
-                 seed: int = 0, use_graphs: bool = True, patch_max_ctas: int = 0, batch: int = 1):
+                 seed: int = 0, use_graphs: bool = True, patch_max_ctas: int = 0, batch: int = 1,
+                 weights: Optional["SharedWeights"] = None):
         ops.require_cuda(torch.empty(1, device=device))
         self.cfg, self.steps, self.guidance = cfg, steps, guidance
         self.device = torch.device(device)
         self.dtype = dtype
-        self.unet_p = init_unet(cfg, self.device, dtype, seed)
-        self.cn_p = [init_controlnet(cfg, self.device, dtype, seed=1000 + i) for i in range(n_controlnets)]
+        self.weights = weights
+        if weights is not None:   # engines of other shapes over the same weights (serving.EngineCache)
+            if len(weights.cn_p) != n_controlnets:
+                raise ValueError("shared weights hold a different number of ControlNets")
+            self.unet_p, self.cn_p = weights.unet_p, weights.cn_p
+        else:
+            self.unet_p = init_unet(cfg, self.device, dtype, seed)
+            self.cn_p = [init_controlnet(cfg, self.device, dtype, seed=1000 + i) for i in range(n_controlnets)]
         self.unet = UNet(cfg, self.unet_p)
         self.cns = [ControlNet(cfg, p) for p in self.cn_p]
         self.cn_scales = list(cn_scales) if cn_scales is not None else [0.8] * n_controlnets
@@ -248,7 +264,12 @@ class AddonPipeline:
         adapter set.  One extra step graph per partial weight set."""
         if self.shadow is None:
             _ = self._pristine
-            self.shadow = allocate_shadow(self.unet_p)
+            if self.weights is not None:      # one shadow copy per weight set, not per engine
+                if self.weights.shadow is None:
+                    self.weights.shadow = allocate_shadow(self.unet_p)
+                self.shadow = self.weights.shadow
+            else:
+                self.shadow = allocate_shadow(self.unet_p)
         if groups > 1:
             return self._load_groups(adapters, host_resident, groups)
         self.patch_groups, self.group_patchsets, self.group_graphs = None, [], []

@@ -12,7 +12,7 @@ import torch
 from oracle import pipeline_ref as R
 from paper_2407_02031_b200 import unet as U
 from paper_2407_02031_b200.patcher import synthetic_lora
-from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_request
+from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_batch, synthetic_request
 from paper_2407_02031_b200.schedule import plan_lora_patch
 
 pytestmark = pytest.mark.gpu
@@ -286,3 +286,26 @@ def test_group_pipelined_equal_boundaries_is_single_patch():
     plan = __import__("paper_2407_02031_b200.schedule", fromlist=["x"]).plan_pipeline_patch(
         loads, pipe.step_ms_est, 0.0, pipe.steps)
     assert bounds[:len(plan.groups)] == [g.boundary_step for g in plan.groups]
+
+
+def test_engine_cache_shapes_share_weights_and_match_standalone():
+    """serving.EngineCache: engines per (batch, resolution) over one weight
+    set, LRU-evicted; each shape's output is bitwise the standalone engine's."""
+    import dataclasses
+
+    from paper_2407_02031_b200.serving import EngineCache
+    cache = EngineCache(U.TOY, n_controlnets=1, steps=4, dtype=torch.bfloat16, capacity=2)
+    lora = synthetic_lora(cache.weights.unet_p, 8, seed=7)
+    cache.load_loras([(lora, 0.8)])
+    small = dataclasses.replace(U.TOY, latent_hw=32)
+    reqs = [synthetic_request(U.TOY, 1, seed=1), synthetic_batch(U.TOY, 1, 2, seed=2),
+            synthetic_request(small, 1, seed=3)]
+    outs = [cache.generate(r, patch=True, boundary=1) for r in reqs]
+    assert cache.cache.evictions == 1 and cache.cache.keys() == [(2, 64), (1, 32)]
+    again = cache.generate(reqs[0], patch=True, boundary=1)       # rebuilt after eviction
+    assert (again == outs[0]).all()
+    for r, o, cfg, b in zip(reqs, outs, (U.TOY, U.TOY, small), (1, 2, 1)):
+        ref = AddonPipeline(cfg, n_controlnets=1, steps=4, dtype=torch.bfloat16, batch=b)
+        ref.load_loras([(synthetic_lora(ref.unet_p, 8, seed=7), 0.8)])
+        ref.setup()
+        assert (ref.generate(r, patch=True, boundary=1) == o).all()
