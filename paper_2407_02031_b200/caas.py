@@ -347,6 +347,34 @@ def flat_views(flat: torch.Tensor, shapes: Sequence[tuple]) -> list:
 # ---------------------------------------------------------------------------
 # the real node: graph-captured compute on B200 around the protocol
 # ---------------------------------------------------------------------------
+class PatchSchedule:
+    """Which base weight set each step runs — "pristine", "pg<v>" (the first
+    v patch groups swapped in) or "patched" — given each group's boundary
+    (None = the group missed this request) and its ready event; the stream
+    waits for a group's event before the first step that uses it."""
+
+    def __init__(self, bounds: Sequence[Optional[int]], ready: Sequence, steps: int):
+        self.bounds, self.ready, self.M = list(bounds), list(ready), len(bounds)
+        self.waited = 0
+        live = [b for b in self.bounds if b is not None]
+        self.first_full = (self.bounds[-1] + 1) if self.M and len(live) == self.M else steps + 1
+
+    def weights_at(self, step: int, stream) -> str:
+        v = sum(1 for b in self.bounds if b is not None and b + 1 <= step)
+        while self.waited < v:
+            stream.wait_event(self.ready[self.waited])
+            self.waited += 1
+        if v == 0:
+            return "pristine"
+        return "patched" if v == self.M else f"pg{v}"
+
+    def finish(self, stream) -> None:
+        """Never leave the side streams dangling past the request."""
+        if self.ready:
+            stream.wait_event(self.ready[-1])
+        self.waited = self.M
+
+
 class CaaSNode:
     """One rank of the ControlNet-as-a-service deployment.
 
@@ -478,10 +506,11 @@ class CaaSNode:
             return g.get("svc", 0)
         return self.pipe.launches_per_step
 
-    def load_loras(self, adapters, host_resident: bool = False) -> None:
-        """LoRA lives on the base UNet only (ControlNets are not patched)."""
+    def load_loras(self, adapters, host_resident: bool = False, groups: int = 1) -> None:
+        """LoRA lives on the base UNet only (ControlNets are not patched).
+        groups > 1: group-pipelined patching (AddonPipeline.load_loras)."""
         if self.role in ("base", "solo"):
-            self.pipe.load_loras(adapters, host_resident=host_resident)
+            self.pipe.load_loras(adapters, host_resident=host_resident, groups=groups)
 
     def setup(self) -> None:
         if self.role == "solo":
@@ -491,6 +520,8 @@ class CaaSNode:
             p = self.pipe
             _ = p._pristine
             variants = ["pristine"] + (["patched"] if p.patchset is not None else [])
+            if p.patch_groups:           # partially patched weight sets of the grouped patch
+                variants += [f"pg{v}" for v in range(1, len(p.patch_groups))]
             for which in variants:
                 # one memory pool per (encoder, decoder) pair: the pair hands its
                 # activations over inside the pool, pairs never share one
@@ -575,19 +606,52 @@ class CaaSNode:
         p.last_first_patched_step = first
         return first, ev
 
-    def denoise(self, patch: bool = False, boundary: Optional[int] = None, fetch: bool = True) -> None:
-        if self.role == "solo":
-            self.pipe.denoise(patch=patch, boundary=boundary, fetch=fetch)
-            return
-        first, ev = (self.steps + 1, None)
-        if self.role == "base" and patch:
+    def start_patch_schedule(self, patch: bool, boundary: Optional[int] = None, fetch: bool = True,
+                             boundaries: Optional[Sequence[int]] = None) -> "PatchSchedule":
+        """Base: launch the request's patch — one K1 launch, or with grouped
+        adapters every group's fetch -> pack -> K1 chain — and return the
+        per-step weight-set schedule (forced boundary / boundaries, or planned
+        by plan_lora_patch / plan_pipeline_patch from the calibrated times)."""
+        p = self.pipe
+        if not patch:
+            return PatchSchedule([], [], self.steps)
+        if not p.patch_groups:
             first, ev = self.start_patch(boundary, fetch=fetch)
+            return PatchSchedule([first - 1 if first <= self.steps else None], [ev], self.steps)
+        from .schedule import plan_pipeline_patch
+        M = len(p.patch_groups)
+        if boundaries is not None:
+            bounds = list(boundaries)
+        elif boundary is not None:
+            bounds = [boundary] * M
+        else:
+            if p.step_ms_est is None or p.group_loads_ms is None:
+                raise RuntimeError("calibrate the base (step_ms_est / calibrate_groups) or pass boundaries")
+            plan = plan_pipeline_patch(p.group_loads_ms, p.step_ms_est, 0.0, self.steps)
+            bounds = [g.boundary_step for g in plan.groups] + [None] * (M - len(plan.groups))
+        if len(bounds) != M:
+            raise ValueError(f"need {M} group boundaries")
+        _, ready = p.launch_patch_groups(timing=False, fetch=fetch)
+        p.last_group_boundaries = bounds
+        sched = PatchSchedule(bounds, ready, self.steps)
+        p.last_first_patched_step = sched.first_full
+        return sched
+
+    def denoise(self, patch: bool = False, boundary: Optional[int] = None, fetch: bool = True,
+                boundaries: Optional[Sequence[int]] = None) -> None:
+        if self.role == "solo":
+            if self.pipe.patch_groups and patch:
+                self.pipe.denoise_pipelined(boundaries or ([boundary] * len(self.pipe.patch_groups)
+                                                           if boundary is not None else None), fetch=fetch)
+            else:
+                self.pipe.denoise(patch=patch, boundary=boundary, fetch=fetch)
+            return
+        sched = (self.start_patch_schedule(patch, boundary, fetch, boundaries) if self.role == "base"
+                 else PatchSchedule([], [], self.steps))
         s = torch.cuda.current_stream(self.device)
         for step in range(1, self.steps + 1):
             if self.role == "base":
-                which = "patched" if step >= first else "pristine"
-                if step == first:
-                    s.wait_event(ev)
+                which = sched.weights_at(step, s)
                 works = self.proto.base_step_begin()
                 self.base_encode(which)               # overlaps the services' ControlNets
                 for w in works:
@@ -597,8 +661,7 @@ class CaaSNode:
                 self.proto.service_receive()
                 self.service_step()
                 self.proto.service_send()
-        if ev is not None and first > self.steps:
-            s.wait_event(ev)
+        sched.finish(s)
 
     def latent_nchw(self) -> Optional[torch.Tensor]:
         if self.role == "service":
@@ -649,15 +712,11 @@ class LoopbackGroup:
             s.finish_prepare([t.clone() for t in shared])
 
     def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None,
-                fetch: bool = True) -> None:
-        first, ev = (self.steps + 1, None)
-        if patch:
-            first, ev = self.base.start_patch(boundary, fetch=fetch)
+                fetch: bool = True, boundaries: Optional[Sequence[int]] = None) -> None:
+        sched = self.base.start_patch_schedule(patch, boundary, fetch, boundaries)
         s = torch.cuda.current_stream()
         for step in range(1, self.steps + 1):
-            which = "patched" if step >= first else "pristine"
-            if step == first:
-                s.wait_event(ev)
+            which = sched.weights_at(step, s)
             if self.concurrent:
                 done = []
                 for svc, st in zip(self.services, self.streams):
@@ -677,11 +736,10 @@ class LoopbackGroup:
             self.base.base_decode(which)
             if on_step is not None:
                 on_step(step, self.latent_nchw().clone())
-        if ev is not None and first > self.steps:
-            s.wait_event(ev)
+        sched.finish(s)
 
-    def load_loras(self, adapters, host_resident: bool = False) -> None:
-        self.base.load_loras(adapters, host_resident=host_resident)
+    def load_loras(self, adapters, host_resident: bool = False, groups: int = 1) -> None:
+        self.base.load_loras(adapters, host_resident=host_resident, groups=groups)
 
     def latent_nchw(self) -> torch.Tensor:
         return self.base.latent_nchw()

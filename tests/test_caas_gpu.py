@@ -90,3 +90,31 @@ def test_caas_split_bf16_within_the_bf16_floor(fp32_mode):
     print("bf16 single vs fp32:", ["%.1e" % e for e in e_single])
     print("bf16 caas   vs fp32:", ["%.1e" % e for e in e_caas])
     assert max(e_caas) <= 2e-2 and max(e_single) <= 2e-2
+
+
+def test_caas_group_pipelined_patch_matches_single_gpu(fp32_mode):
+    """Group-pipelined patching on the CaaS base (encoder/decoder graphs per
+    partial weight set) == the single-GPU pipeline's denoise_pipelined at the
+    same group boundaries."""
+    bounds = [1, 2, 4]
+    lora_of = lambda p: [(synthetic_lora(p.unet_p, 8, seed=7), 0.75)]   # noqa: E731
+    pipe = AddonPipeline(U.TOY, n_controlnets=2, cn_scales=SCALES, steps=STEPS, dtype=torch.float32, seed=0)
+    pipe.load_loras(lora_of(pipe), host_resident=True, groups=3)
+    pipe.setup()
+    req = synthetic_request(U.TOY, 2)
+    pipe.prepare(*inputs(req))
+    ref = []
+    pipe.denoise_pipelined(bounds, on_step=lambda s, x: ref.append(x.float().cpu()))
+    grp = LoopbackGroup(U.TOY, 2, SCALES, steps=STEPS, dtype=torch.float32, seed=0, concurrent=True)
+    grp.load_loras(lora_of(grp.base.pipe), host_resident=True, groups=3)
+    grp.setup()
+    grp.prepare(*inputs(req))
+    got = []
+    grp.denoise(patch=True, boundaries=bounds, on_step=lambda s, x: got.append(x.float().cpu()))
+    assert grp.base.pipe.last_group_boundaries == bounds
+    errs = [rel(a, b) for a, b in zip(got, ref)]
+    print("caas grouped vs single grouped (fp32):", ["%.1e" % e for e in errs])
+    assert max(errs) <= 1e-5
+    # and the partial sets really differ from an all-at-once patch at the last boundary
+    once = loopback(torch.float32, patch=True, n_services=2)
+    assert rel(got[2], once[2]) > 1e-6 or rel(got[3], once[3]) > 1e-6
