@@ -814,9 +814,12 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
 // is folded into the plan's opaque kb_max word (kb | mode << 8) so a plan
 // always launches the kernel it was built for.
 static int g_tc_mode = 0;   // 0 auto, 1 single CTA, 2 CTA pair
-static int pick_mode(int /*kb_max*/) {
+static int pick_mode(int kb_max) {
   if (g_tc_mode == 1 || g_tc_mode == 2) return g_tc_mode;
-  return 2;
+  // one 64-wide K block (stacked rank <= 64): the B panel is 32 KB, the
+  // single-CTA kernel keeps a deep W ring on its own and, with the balanced
+  // unit order, measured 1.88 ms vs the pair's 1.91 (all SDXL matrices, r64)
+  return kb_max <= 1 ? 1 : 2;
 }
 
 // Blob layout: [maps: 4*n_jobs CUtensorMap (64 B aligned)] [jobs] [units]
@@ -845,6 +848,43 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
     for (int64_t n = 0; n < nt; ++n)
       for (int64_t m = 0; m < mt; m += unit_tiles)
         units.push_back({j, (int32_t)n, (int32_t)m, (int32_t)std::min<int64_t>(mt, m + unit_tiles)});
+  }
+  // Static balance: the kernel hands unit u to CTA (pair) u % ncl.  Units
+  // range from 1 to unit_tiles row tiles (a 320-row matrix is one 3-tile
+  // unit), so plain job order leaves some CTAs ~7% more work than others
+  // (ncu: SM active 93% of the elapsed cycles); sort by size and deal the
+  // units out boustrophedon (round k forward for even k, backward for odd
+  // k) so every CTA's total is near the mean.  Single-CTA kernel: largest
+  // first (r64: 2.06 -> 1.88 ms, R=232: 3.60 -> 2.90 ms).  CTA pair: smallest
+  // first — a 1-tile unit idles half the pair, and dealing those last left
+  // every pair half-idle at the tail (largest-first was 2% slower at
+  // R=128); smallest-first is neutral at R <= 128 and 0.5% faster at R=232.
+  // SDB_K1_BALANCE=0 keeps job order (probe knob).
+  static int balance = -1;
+  if (balance < 0) {
+    const char* e = getenv("SDB_K1_BALANCE");
+    balance = e ? atoi(e) : 1;
+  }
+  if (balance) {
+    const int ncl = mode == 2 ? kNumSMs / 2 : kNumSMs;
+    auto elems = [&](const TcUnit& u) {          // W elements the unit reads and writes
+      const sdb_lora_tc_job& J = jobs[u.job];
+      const int64_t rows = std::min<int64_t>(J.h1, (int64_t)u.m_end * kBM) - (int64_t)u.m_begin * kBM;
+      const int64_t cols = std::min<int64_t>(J.h2 - (int64_t)u.n_tile * kBN, kBN);
+      return rows * cols;
+    };
+    std::vector<TcUnit> sorted(units);
+    if (mode == 2)
+      std::stable_sort(sorted.begin(), sorted.end(),
+                       [&](const TcUnit& a, const TcUnit& b) { return elems(a) < elems(b); });
+    else
+      std::stable_sort(sorted.begin(), sorted.end(),
+                       [&](const TcUnit& a, const TcUnit& b) { return elems(a) > elems(b); });
+    for (size_t k = 0; k * ncl < sorted.size(); ++k) {
+      const size_t b = k * ncl, e = std::min(sorted.size(), b + ncl);
+      if (k & 1) std::reverse(sorted.begin() + b, sorted.begin() + e);
+    }
+    units.swap(sorted);
   }
   const size_t maps_b = (size_t)4 * n_jobs * sizeof(CUtensorMap);
   const size_t jobs_b = (size_t)n_jobs * sizeof(TcJob);
