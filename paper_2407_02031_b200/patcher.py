@@ -182,8 +182,21 @@ class PatchSet:
         return sum(p.alg_flops for p in self.plans)
 
     def launch(self, sign: float = 1.0, stream: Optional[torch.cuda.Stream] = None, max_ctas: int = 0):
-        for p in self.plans:
-            p.launch(sign=sign, stream=stream, max_ctas=max_ctas)
+        """One K1 launch for the tcgen05 plan; the few matrices the generic
+        kernel takes (SDXL's 320 x 36 conv_in: a 5-CTA, ~30 us launch) run on
+        a forked stream beside it instead of after it (graph-capturable
+        fork / join)."""
+        if len(self.plans) == 1:
+            self.plans[0].launch(sign=sign, stream=stream, max_ctas=max_ctas)
+            return
+        main = stream if stream is not None else torch.cuda.current_stream()
+        if getattr(self, "_side", None) is None or self._side.device != main.device:
+            self._side = torch.cuda.Stream(device=main.device)
+        self._side.wait_stream(main)
+        for p in self.plans[1:]:
+            p.launch(sign=sign, stream=self._side, max_ctas=max_ctas)
+        self.plans[0].launch(sign=sign, stream=main, max_ctas=max_ctas)
+        main.wait_stream(self._side)
 
     def copy_unpatched(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Shadow entries not touched by any adapter must mirror the pristine
