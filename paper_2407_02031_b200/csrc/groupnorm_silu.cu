@@ -367,7 +367,14 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every CTA reads its chunk into 
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(w.x));
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(w.y));
         e = f2add(e, f2s(1.f));
-        u = f2mul(u, make_float2(rcp_nr(e.x), rcp_nr(e.y)));
+        if constexpr (sizeof(T) == 4) {   // fp32 output: keep the full-precision MUFU reciprocal
+          float2 rc;
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.x) : "f"(e.x));
+          asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rc.y) : "f"(e.y));
+          u = f2mul(u, rc);
+        } else {                           // 16-bit output: 2 Newton steps (6.7e-6) are far below its ulp
+          u = f2mul(u, make_float2(rcp_nr(e.x), rcp_nr(e.y)));
+        }
       }
       set_pair<T>(o, i, u);
     }
