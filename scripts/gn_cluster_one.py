@@ -7,7 +7,7 @@ import torch  # noqa: E402
 
 from paper_2407_02031_b200 import ops  # noqa: E402
 
-for n, c, h in ((2, 320, 128), (2, 1280, 32)):
+for n, c, h in ((2, 1280, 32),):
     x = torch.randn(n, c, h, h, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
     gamma = torch.rand(c, device="cuda") + 0.5
     beta = torch.randn(c, device="cuda")
