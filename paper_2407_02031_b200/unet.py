@@ -372,20 +372,22 @@ class Net:
         """bias=False: the caller folds ``self.fb[name]`` into the next kernel."""
         w = self.t[name + ".weight"]
         pad = w.shape[-1] // 2
-        if name == "conv_in" and w.shape[1] % 8 != 0 and x.dtype != torch.float32:
+        if w.shape[1] % 8 != 0 and x.dtype != torch.float32:
             x, w = self._pad_cin(name, x, w)
         return F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=stride, padding=pad)
 
     def _pad_cin(self, name, x, w):
-        """conv_in's 4 latent channels: cuDNN has no bf16 tensor-op kernel for
-        C_in % 8 != 0 and falls back to convert -> TF32 conv -> convert
-        (49 us per SDXL call, 3 calls per step; 26 us padded, incl. the copies:
-        scripts/convin_probe.py).  Zero-pad C_in to a multiple
-        of 8 in persistent buffers (the padding channels stay zero; each call
+        """conv_in's 4 latent channels (and the ControlNet hint's 3 image
+        channels): cuDNN has no bf16 tensor-op kernel for C_in % 8 != 0 and
+        falls back to convert -> TF32 conv -> convert (49 us per SDXL conv_in,
+        3 per step; 152 us per hint conv).  Padded to 16 channels, incl. the
+        copies: ~24 us and ~90 us (scripts/convin_probe.py; 16 beat 8, which
+        still made cuDNN insert its own padding pass).  Zero-pad C_in to a multiple
+        of 16 in persistent buffers (the padding channels stay zero; each call
         copies the live input and the live weight — the LoRA shadow or the
         pristine one, whichever the graph captured — into the first C_in)."""
         cin = w.shape[1]
-        cp = (cin + 7) // 8 * 8
+        cp = (cin + 15) // 16 * 16
         key = (name, tuple(x.shape), tuple(w.shape), x.dtype)
         bufs = getattr(self, "_cin_pad", None)
         if bufs is None:

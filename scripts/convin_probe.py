@@ -34,6 +34,8 @@ for cin, cout, n, hw in ((4, 320, 2, 128), (3, 16, 2, 1024), (4, 320, 16, 128)):
     w = cl(torch.randn(cout, cin, 3, 3, device="cuda").bfloat16())
     xp = cl(torch.zeros(n, 8, hw, hw, device="cuda").bfloat16())
     wp = cl(torch.zeros(cout, 8, 3, 3, device="cuda").bfloat16())
+    xp16 = cl(torch.zeros(n, 16, hw, hw, device="cuda").bfloat16())
+    wp16 = cl(torch.zeros(cout, 16, 3, 3, device="cuda").bfloat16())
 
     def pad():
         xp[:, :cin].copy_(x)
@@ -46,5 +48,6 @@ for cin, cout, n, hw in ((4, 320, 2, 128), (3, 16, 2, 1024), (4, 320, 16, 128)):
     t0 = gt(lambda: F.conv2d(x, w, padding=1))
     t1 = gt(pad)
     t2 = gt(pad_conv_only)
+    t3 = gt(lambda: F.conv2d(xp16, wp16, padding=1))
     print(f"[{n},{cin},{hw},{hw}] -> {cout}: cin={cin} {t0:.1f} us | padded to 8 incl. copies {t1:.1f} us "
-          f"(conv alone {t2:.1f} us)")
+          f"(conv alone {t2:.1f} us; 16 channels {t3:.1f} us)")
