@@ -25,7 +25,6 @@ Latents are NHWC end to end (the fp32 master latent is [H, W, 4] flat).
 
 from __future__ import annotations
 
-import time
 from dataclasses import dataclass
 from typing import Optional, Sequence
 

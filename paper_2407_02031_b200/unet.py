@@ -26,7 +26,7 @@ N(0, 0.02) so residual parity is not vacuous, SURVEY §7 hard part 9).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional, Sequence
 
 import os
