@@ -374,6 +374,13 @@ class Net:
         pad = w.shape[-1] // 2
         if w.shape[1] % 8 != 0 and x.dtype != torch.float32:
             x, w = self._pad_cin(name, x, w)
+        if stride == 2 and w.shape[-1] == 3 and x.dim() == 4 and x.shape[-1] >= 128 and x.dtype != torch.float32:
+            # cuDNN has no good bf16 kernel for the 3x3 stride-2 downsample at
+            # 128x128 (SDXL's first: 155 us, a TF32 fallback with conversions);
+            # the stride-1 conv + subsample computes 4x the outputs and still
+            # takes 59 us (scripts/convds_probe.py)
+            y = F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=1, padding=pad)
+            return y[:, :, ::2, ::2].contiguous(memory_format=torch.channels_last)
         return F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=stride, padding=pad)
 
     def _pad_cin(self, name, x, w):

@@ -321,3 +321,22 @@ def test_groupnorm_large_maps_take_the_two_pass_form():
     assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 2
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, bf16) == 1
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, ops.sdb_dtype(torch.empty(0))) == 2   # fp32
+
+
+@pytest.mark.parametrize("c,hw", [(320, 128), (64, 130)])
+def test_strided_conv_via_subsample(c, hw):
+    """Net.conv's stride-2 3x3 at >= 128x128 runs as stride-1 conv + subsample
+    (cuDNN's strided bf16 kernel is a TF32 fallback there): same values as
+    the strided conv within the bf16 output rounding, vs an fp64 reference."""
+    from paper_2407_02031_b200 import unet as U
+    net = object.__new__(U.Net)
+    g = torch.Generator(device="cuda").manual_seed(c)
+    x = cl(torch.randn(2, c, hw, hw, device="cuda", generator=g).to(torch.bfloat16))
+    w = cl((torch.randn(c, c, 3, 3, device="cuda", generator=g) / math.sqrt(9 * c)).to(torch.bfloat16))
+    b = torch.randn(c, device="cuda", generator=g).to(torch.bfloat16)
+    net.t = {"ds.weight": w, "ds.bias": b}
+    y = net.conv("ds", x, stride=2)
+    ref = F.conv2d(x.double(), w.double(), b.double(), stride=2, padding=1)
+    assert y.shape == ref.shape and y.is_contiguous(memory_format=torch.channels_last)
+    err = (y.double() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -7 + 1e-2).all(), float(err.max())
