@@ -262,6 +262,13 @@ int sdb_memcpy_async(void* dst, const void* src, size_t bytes, void* stream);
  * ======================================================================== */
 int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, void* stream);
 
+/* K10 — nearest 2x upsample of an NHWC map: y[n, 2i+a, 2j+b, :] = x[n, i, j, :]
+ * (the UNet decoder's upsample before its 3x3 conv).  x [n, h, w, c], y
+ * [n, 2h, 2w, c], c * elem_bytes a multiple of 16, 16-B aligned pointers.
+ * No reference counterpart (addonsim has no UNet arithmetic). */
+int sdb_upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t c, int elem_bytes,
+                   void* stream);
+
 /* ========================================================================
  * K6 — residual add + LayerNorm of the transformer blocks:
  *   x[m] += d[m] (in place; d may be NULL), y[m] = LN(x[m]) * gamma + beta.

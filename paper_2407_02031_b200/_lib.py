@@ -178,7 +178,8 @@ class LoraSrc(ctypes.Structure):
 EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_tc_plan",
                        "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_add_layernorm",
                        "sdb_cross_attention", "sdb_stream_wait_value32", "sdb_stream_write_value32",
-                       "sdb_memcpy_async", "sdb_cross_attention_set_mode", "sdb_self_attention")
+                       "sdb_memcpy_async", "sdb_cross_attention_set_mode", "sdb_self_attention",
+                       "sdb_upsample2x")
 
 
 def _declare_tc(lib: ctypes.CDLL) -> None:
@@ -196,6 +197,8 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
     lib.sdb_lora_tc_patch.argtypes = [vp, i32, i32, i32, i32, f32, i32, vp]
     lib.sdb_lora_tc_set_mode.restype = i32
     lib.sdb_lora_tc_set_mode.argtypes = [i32]
+    lib.sdb_upsample2x.restype = i32
+    lib.sdb_upsample2x.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
     lib.sdb_geglu.restype = i32
     lib.sdb_geglu.argtypes = [vp, vp, i64, i64, i32, vp]
     lib.sdb_stream_wait_value32.restype = i32

@@ -45,6 +45,7 @@ int residual_inject(void* out, const void* hidden, const void* skip, const void*
                     const float* hidden_bias, const float* skip_bias, int dtype, cudaStream_t st);
 // fused_ops.cu
 int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st);
+int upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t c, int elem_bytes, cudaStream_t st);
 int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                   float eps, int dtype, cudaStream_t st);
 // cross_attn.cu
@@ -228,6 +229,11 @@ int sdb_residual_inject_bias(void* out, const void* hidden, const void* skip,
                              const float* skip_bias, int dtype, void* stream) {
   return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, hidden_bias,
                          skip_bias, dtype, as_stream(stream));
+}
+
+int sdb_upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t c, int elem_bytes,
+                   void* stream) {
+  return upsample2x(x, y, n, h, w, c, elem_bytes, as_stream(stream));
 }
 
 int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, void* stream) {

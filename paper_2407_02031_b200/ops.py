@@ -460,6 +460,19 @@ def geglu(proj: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def upsample2x(x: torch.Tensor) -> torch.Tensor:
+    """K10: nearest 2x upsample of a channels_last [N, C, H, W] map."""
+    require_cuda(x)
+    n, c, h, w = x.shape
+    if not x.is_contiguous(memory_format=torch.channels_last) or (c * x.element_size()) % 16:
+        raise ValidationError("upsample2x: channels_last input with C * element size a multiple of 16")
+    y = torch.empty((n, c, 2 * h, 2 * w), device=x.device, dtype=x.dtype, memory_format=torch.channels_last)
+    _count(1)
+    _lib.check("sdb_upsample2x", _lib.lib().sdb_upsample2x(x.data_ptr(), y.data_ptr(), n, h, w, c,
+                                                           x.element_size(), _stream_ptr(None)))
+    return y
+
+
 def add_layernorm(x: torch.Tensor, d: Optional[torch.Tensor], gamma: torch.Tensor, beta: torch.Tensor,
                   eps: float = 1e-5) -> torch.Tensor:
     """x += d (in place, d may be None); returns LayerNorm(x) * gamma + beta."""

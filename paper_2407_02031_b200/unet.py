@@ -604,8 +604,8 @@ class UNet(Net):
                 if depth:
                     h = self.transformer(f"up.{i}.attn.{j}", h, ctx, depth)
             if i < n - 1:
-                h = F.interpolate(h, scale_factor=2.0, mode="nearest")
-                h = self.conv(f"up.{i}.upsample", _cl(h), bias=False)
+                h = ops.upsample2x(_cl(h))                      # K10 (nearest 2x, NHWC)
+                h = self.conv(f"up.{i}.upsample", h, bias=False)
                 hb = self.fb.get(f"up.{i}.upsample")
         h = self.gn("conv_norm_out", h, True)
         # eps leaves the UNet in fp32: CFG amplifies (eps_c - eps_u) by the

@@ -340,3 +340,12 @@ def test_strided_conv_via_subsample(c, hw):
     assert y.shape == ref.shape and y.is_contiguous(memory_format=torch.channels_last)
     err = (y.double() - ref).abs()
     assert (err <= ref.abs() * 2 ** -7 + 1e-2).all(), float(err.max())
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("n,c,h,w", [(2, 1280, 32, 32), (2, 640, 64, 64), (1, 8, 3, 5), (3, 64, 7, 16)])
+def test_upsample2x_equals_nearest_interpolate(dtype, n, c, h, w):
+    x = cl(torch.randn(n, c, h, w, device="cuda").to(dtype))
+    y = ops.upsample2x(x)
+    assert y.is_contiguous(memory_format=torch.channels_last)
+    assert torch.equal(y, F.interpolate(x, scale_factor=2.0, mode="nearest"))
