@@ -463,8 +463,13 @@ class Net:
     def resnet(self, pre, x, temb_act):
         h = self.conv(pre + ".conv1", self.gn(pre + ".norm1", x, True), bias=False)
         # conv1's bias rides on the time-embedding projection (tproj_bias = b_temb + b_conv1)
-        tproj = F.linear(temb_act, self.t[pre + ".time_emb_proj.weight"],
-                         self.fb.get(pre + ".tproj_bias")).float().contiguous()
+        wt, tb = self.t[pre + ".time_emb_proj.weight"], self.fb.get(pre + ".tproj_bias")
+        if temb_act.dtype == torch.float32:
+            tproj = F.linear(temb_act, wt, tb).contiguous()
+        elif tb is not None:   # fp32 straight out of cuBLAS: no separate cast kernel (33 per SDXL+2CN step)
+            tproj = torch.addmm(tb, temb_act, wt.t(), out_dtype=torch.float32)
+        else:
+            tproj = torch.mm(temb_act, wt.t(), out_dtype=torch.float32)
         h = self.gn(pre + ".norm2", h, True, add_nc=tproj)       # fused temb add + GN + SiLU
         h = self.conv(pre + ".conv2", h, bias=False)
         if (pre + ".conv_shortcut.weight") in self.t:
