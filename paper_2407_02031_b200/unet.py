@@ -359,6 +359,8 @@ class Net:
                 if b is not None or c1 is not None:
                     comb = (b.float() if b is not None else 0) + (c1 if c1 is not None else 0)
                     fb[pre + ".tproj_bias"] = comb.to(self.p.dtype).contiguous()
+                    # the same sum in the param dtype, held in fp32: the bias of the fp32-output addmm
+                    fb[pre + ".tproj_bias_f32"] = fb[pre + ".tproj_bias"].float()
                 c2, sc = fb.get(pre + ".conv2"), fb.get(pre + ".conv_shortcut")
                 if c2 is not None or sc is not None:
                     fb[pre + ".out_bias"] = ((c2 if c2 is not None else 0) + (sc if sc is not None else 0)).contiguous()
@@ -466,8 +468,8 @@ class Net:
         wt, tb = self.t[pre + ".time_emb_proj.weight"], self.fb.get(pre + ".tproj_bias")
         if temb_act.dtype == torch.float32:
             tproj = F.linear(temb_act, wt, tb).contiguous()
-        elif tb is not None:   # fp32 straight out of cuBLAS: no separate cast kernel (33 per SDXL+2CN step)
-            tproj = torch.addmm(tb, temb_act, wt.t(), out_dtype=torch.float32)
+        elif tb is not None:   # fp32 accumulate-and-store in cuBLAS (torch still broadcasts the bias first)
+            tproj = torch.addmm(self.fb[pre + ".tproj_bias_f32"], temb_act, wt.t(), out_dtype=torch.float32)
         else:
             tproj = torch.mm(temb_act, wt.t(), out_dtype=torch.float32)
         h = self.gn(pre + ".norm2", h, True, add_nc=tproj)       # fused temb add + GN + SiLU
