@@ -376,7 +376,8 @@ class Net:
         pad = w.shape[-1] // 2
         if w.shape[1] % 8 != 0 and x.dtype != torch.float32:
             x, w = self._pad_cin(name, x, w)
-        if stride == 2 and w.shape[-1] == 3 and x.dim() == 4 and x.shape[-1] >= 128 and x.dtype != torch.float32:
+        if (stride == 2 and w.shape[-1] == 3 and x.dim() == 4 and x.shape[-1] >= 128 and x.shape[1] >= 256
+                and x.dtype != torch.float32):
             # cuDNN has no good bf16 kernel for the 3x3 stride-2 downsample at
             # 128x128 (SDXL's first: 155 us, a TF32 fallback with conversions);
             # the stride-1 conv + subsample computes 4x the outputs and still
@@ -634,11 +635,21 @@ class ControlNet(Net):
         """Conditioning image (N, 3, 8H, 8W) -> (N, C0, H, W).  Step-invariant:
         computed once per request (SURVEY App. B pitfall 8)."""
         hc = self.cfg.hint_channels
-        h = F.silu(self.conv("cond_embedding.conv_in", _cl(image)))
+        h = F.silu(self._conv_bias("cond_embedding.conv_in", _cl(image)), inplace=True)
         for i in range(len(hc) - 1):
-            h = F.silu(self.conv(f"cond_embedding.blocks.{2 * i}", h))
-            h = F.silu(self.conv(f"cond_embedding.blocks.{2 * i + 1}", h, stride=2))
-        return self.conv("cond_embedding.conv_out", h)
+            h = F.silu(self._conv_bias(f"cond_embedding.blocks.{2 * i}", h), inplace=True)
+            h = F.silu(self._conv_bias(f"cond_embedding.blocks.{2 * i + 1}", h, stride=2), inplace=True)
+        return self._conv_bias("cond_embedding.conv_out", h)
+
+    def _conv_bias(self, name, x, stride=1):
+        """Bias-free cuDNN conv + K3's vectorised in-place per-channel bias add
+        (cuDNN's own channels_last bias pass is a non-vectorised broadcast add:
+        ~70 us per 1024x1024 hint map)."""
+        h = self.conv(name, x, stride=stride, bias=False)
+        b = self.fb.get(name)
+        if b is None or h.shape[1] % 8 != 0:
+            return h if b is None else h.add_(self.t[name + ".bias"].view(1, -1, 1, 1))
+        return ops.residual_inject(h, [], [], skip_bias=b, out=h)
 
     def forward(self, x, t, ctx, hint, add_emb=None, outs=None, on_level=None):
         """Returns [down residuals..., mid residual] (unscaled; the
