@@ -376,6 +376,11 @@ class Net:
         pad = w.shape[-1] // 2
         if w.shape[1] % 8 != 0 and x.dtype != torch.float32:
             x, w = self._pad_cin(name, x, w)
+        elif tuple(w.shape[:2]) == (320, 256) and w.shape[-1] == 3 and x.dtype != torch.float32:
+            # the hint embedding's conv_out: cuDNN's heuristic picks a TF32
+            # fallback for 256 -> 320 (~410 us at 128x128); padded to 320
+            # input channels it takes 54 us (scripts/condout_probe.py)
+            x, w = self._pad_cin(name, x, w, to=320)
         if (stride == 2 and w.shape[-1] == 3 and x.dim() == 4 and x.shape[-1] >= 128 and x.shape[1] >= 256
                 and x.dtype != torch.float32):
             # cuDNN has no good bf16 kernel for the 3x3 stride-2 downsample at
@@ -386,7 +391,7 @@ class Net:
             return y[:, :, ::2, ::2].contiguous(memory_format=torch.channels_last)
         return F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=stride, padding=pad)
 
-    def _pad_cin(self, name, x, w):
+    def _pad_cin(self, name, x, w, to=None):
         """conv_in's 4 latent channels (and the ControlNet hint's 3 image
         channels): cuDNN has no bf16 tensor-op kernel for C_in % 8 != 0 and
         falls back to convert -> TF32 conv -> convert (49 us per SDXL conv_in,
@@ -397,7 +402,7 @@ class Net:
         copies the live input and the live weight — the LoRA shadow or the
         pristine one, whichever the graph captured — into the first C_in)."""
         cin = w.shape[1]
-        cp = (cin + 15) // 16 * 16
+        cp = to if to is not None else (cin + 15) // 16 * 16
         key = (name, tuple(x.shape), tuple(w.shape), x.dtype)
         bufs = getattr(self, "_cin_pad", None)
         if bufs is None:
