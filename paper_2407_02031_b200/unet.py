@@ -376,17 +376,20 @@ class Net:
         pad = w.shape[-1] // 2
         if w.shape[1] % 8 != 0 and x.dtype != torch.float32:
             x, w = self._pad_cin(name, x, w)
-        elif tuple(w.shape[:2]) == (320, 256) and w.shape[-1] == 3 and x.dtype != torch.float32:
+        elif (tuple(w.shape[:2]) == (320, 256) and w.shape[-1] == 3 and x.shape[0] <= 4
+              and x.dtype != torch.float32):
             # the hint embedding's conv_out: cuDNN's heuristic picks a TF32
-            # fallback for 256 -> 320 (~410 us at 128x128); padded to 320
-            # input channels it takes 54 us (scripts/condout_probe.py)
+            # fallback for 256 -> 320 (~410 us at 128x128, CFG batch 2; not at
+            # batch 16); padded to 320 input channels it takes 54 us
+            # (scripts/condout_probe.py)
             x, w = self._pad_cin(name, x, w, to=320)
         if (stride == 2 and w.shape[-1] == 3 and x.dim() == 4 and x.shape[-1] >= 128 and x.shape[1] >= 256
-                and x.dtype != torch.float32):
+                and x.shape[0] <= 4 and x.dtype != torch.float32):
             # cuDNN has no good bf16 kernel for the 3x3 stride-2 downsample at
             # 128x128 (SDXL's first: 155 us, a TF32 fallback with conversions);
             # the stride-1 conv + subsample computes 4x the outputs and still
-            # takes 59 us (scripts/convds_probe.py)
+            # takes 59 us (scripts/convds_probe.py).  At CFG batch 16 cuDNN's
+            # strided kernel is fine (104 us, scripts/conv_shapes_probe.py NB=16)
             y = F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=1, padding=pad)
             return y[:, :, ::2, ::2].contiguous(memory_format=torch.channels_last)
         return F.conv2d(x, w, self.t.get(name + ".bias") if bias else None, stride=stride, padding=pad)

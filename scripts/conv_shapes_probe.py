@@ -30,14 +30,16 @@ def gt(fn, reps=10):
     return a.elapsed_time(b) / reps * 1000
 
 
-shapes = [(320, 320, 128, 1), (640, 320, 128, 1), (960, 320, 128, 1), (640, 640, 128, 1),
+shapes = [(4, 320, 128, 1), (320, 320, 128, 2), (256, 320, 128, 1), (320, 320, 128, 1), (640, 320, 128, 1), (960, 320, 128, 1), (640, 640, 128, 1),
           (320, 640, 64, 1), (640, 640, 64, 1), (640, 640, 64, 2), (1280, 640, 64, 1), (1920, 640, 64, 1),
           (960, 640, 64, 1), (1280, 1280, 64, 1),
           (640, 1280, 32, 1), (1280, 1280, 32, 1), (2560, 1280, 32, 1), (1920, 1280, 32, 1)]
+import os
+NB = int(os.environ.get("NB", "2"))
 for cin, cout, hw, st in shapes:
-    x = cl(torch.randn(2, cin, hw, hw, device="cuda").bfloat16())
+    x = cl(torch.randn(NB, cin, hw, hw, device="cuda").bfloat16())
     w = cl(torch.randn(cout, cin, 3, 3, device="cuda").bfloat16() * 0.02)
     t = gt(lambda: F.conv2d(x, w, stride=st, padding=1))
     ho = hw // st
-    fl = 2 * 2 * ho * ho * cout * cin * 9
-    print(f"[2,{cin},{hw},{hw}] -> {cout} s{st}: {t:7.1f} us {fl / t / 1e6:6.0f} TF/s")
+    fl = 2 * NB * ho * ho * cout * cin * 9
+    print(f"[{NB},{cin},{hw},{hw}] -> {cout} s{st}: {t:7.1f} us {fl / t / 1e6:6.0f} TF/s")
