@@ -1,10 +1,18 @@
-"""bench.py — SDXL + 2 ControlNets + 2 LoRAs (rank 64), 30 DDIM steps, CFG,
-1024x1024 (128x128 latent), on B200 — BASELINE.json's headline metric.
+"""bench.py — BASELINE.json's headline: SDXL + 2 ControlNets + 2 LoRAs (rank
+64), 30 DDIM steps, CFG, 1024x1024 (128x128 latent), on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config sdxl|sd15|serve|lora]
 
-A bench *step* is one image: the full 30-step denoising loop of UNet + 2
-ControlNets at CFG batch 2, with the request's 2 LoRAs patched by one K1
+--config selects the BASELINE config the line is measured on (default sdxl =
+configs[2], the metric's own config; sd15 = configs[1]; serve = configs[4]
+folded onto the GPUs given; lora = configs[3], the K1 patch/unpatch
+micro-bench).  The default run also carries the config-4 micro-bench, the
+patch-overhead arm and the CaaS stall accounting as extra keys, so the
+driver's line shows them.
+
+A bench *step* is one image: the full 30-step denoising loop of UNet + the
+ControlNets at CFG batch 2, with the request's LoRAs patched by one K1
 launch into shadow weights on a low-priority side stream and swapped in at
 the planned boundary (async LoRA, schedule.plan_lora_patch).  Weights are
 synthetic random-init of the SDXL architecture; inputs are synthetic.
@@ -16,9 +24,10 @@ roofline K1 (the LoRA patch kernel, north_star's >=70%-of-HBM target): algorithm
         bytes per launch / its CUDA-event duration on the patch stream inside
         the timed region (it runs concurrently with the UNet there); the
         isolated launch is reported beside it
-N > 1   one process per GPU (torchrun, NCCL); each rank serves its own images
-        (replicas — ControlNet-as-a-service sharding is caas.py), so scaling is
-        weak; timing is the max over ranks of CUDA-event time.
+N > 1   one process per GPU (torchrun, NCCL): ControlNet-as-a-service groups
+        (1 base + 1 GPU per ControlNet, caas.py); leftover ranks serve whole
+        images alone; scaling is weak; timing is the max over ranks of
+        CUDA-event time.
 """
 
 from __future__ import annotations
@@ -38,8 +47,25 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "p50 s/image & images/s, SDXL+2 ControlNet+2 LoRA, 1/2/4/8 B200 vs CPU ref"
 DENOISE_STEPS = 30
-N_CN = 2
-LORA_RANKS = (64, 64)
+LORA_SCALE = 0.7
+
+# BASELINE.json configs as bench workloads
+CONFIGS = {
+    "sdxl": dict(cfg="sdxl", n_cn=2, cn_scales=(0.8, 0.6), lora_ranks=(64, 64), batch=1, metric=METRIC,
+                 workload="SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
+                          "30 DDIM steps, CFG batch 2, async LoRA patch",
+                 model="sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init"),
+    "sd15": dict(cfg="sd15", n_cn=1, cn_scales=(0.8,), lora_ranks=(16,), batch=1,
+                 metric="p50 s/image & images/s, SD1.5 512^2 + 1 ControlNet + 1 LoRA r16, 1 B200 (config 2)",
+                 workload="SD1.5 512^2 (64x64 latent) + 1 ControlNet + 1 LoRA r16, 30 DDIM steps, CFG batch 2, "
+                          "async LoRA patch",
+                 model="sd1.5-shaped UNet (0.86B) + 1 ControlNet, random init"),
+    "serve": dict(cfg="sdxl", n_cn=3, cn_scales=(0.8, 0.6, 0.5), lora_ranks=(64, 64), batch=8,
+                  metric="images/s & p50/p99 s/batch, SDXL serving batch 8 + 3 ControlNets + 2 LoRAs (config 5)",
+                  workload="SDXL 1024^2 serving batch of 8 images per step (CFG batch 16, one shared LoRA set) + "
+                           "3 ControlNets + 2 LoRAs r64, 30 DDIM steps",
+                  model="sdxl-shaped UNet (2.57B) + 3 ControlNets (1.25B each), random init"),
+}
 
 
 def peaks():
@@ -138,35 +164,59 @@ def _red_device() -> str:
 
 
 # ---------------------------------------------------------------------------
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads", 0) for i in threadpool_info() if i.get("user_api") == "blas"), default=0)
+    except Exception:  # noqa: BLE001
+        return 0
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args):
-    """The reference CPU path on the host cores (oracle port, see oracle/cpu_bench.py)."""
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    """The reference CPU path on the host cores (oracle/cpu_bench.py: the
+    builder's fp32 torch restatement of the denoising step — the reference
+    has none — plus the reference's own numpy LoRA merge, addonsim from
+    baseline/_ref when installed).  Every bench step is one bounded sample =
+    1/(2 * 30) of an image; warm-up samples as asked; rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle.cpu_bench import CpuWorkload
     from paper_2407_02031_b200 import unet as U
-    wl = CpuWorkload(U.SDXL, N_CN, sum(LORA_RANKS), DENOISE_STEPS)
-    for _ in range(min(args.warmup, 1)):
+    c = CONFIGS.get(args.config, CONFIGS["sdxl"])
+    wl = CpuWorkload(U.CONFIGS[c["cfg"]], c["n_cn"], sum(c["lora_ranks"]), DENOISE_STEPS)
+    for _ in range(args.warmup):
         wl.sample()
+    t0 = time.perf_counter()
     samples = [wl.sample() for _ in range(args.steps)]
-    img_s = [DENOISE_STEPS * s["step_s"] + s["merge_s"] * wl.merge_elems_total / wl.merge_elems_slice
-             for s in samples]
-    med = statistics.median(img_s)
-    value = 1.0 / med
+    wall = time.perf_counter() - t0
+    sample_s = [x["sample_s"] for x in samples]
+    ms_per_step = 1000.0 * wall / args.steps
+    value = wl.images_per_s(wall / args.steps)          # whole-run throughput: units / time
     cores = torch_threads()
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": med * 1000.0,
+        "impl": "reference", "metric": c["metric"], "value": value, "unit": "images/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "p50_s_per_image": med,
-        "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRA r64, 30 DDIM steps, "
-                               "CFG batch 2 — CPU oracle, one bounded sample per step (see sample)",
-                   "model": "sdxl-shaped random init", "global_batch": 1, "parallelism": "cpu"},
+        "data": "synthetic", "p50_s_per_image": wl.fraction * statistics.median(sample_s),
+        "config": {"workload": c["workload"] + " — CPU, one bounded sample per step (see cpu_baseline.sample)",
+                   "model": c["model"], "global_batch": 1, "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "merge_kind": wl.merge.kind, "blas_threads": blas_threads(), "cpu_model": cpu_model(),
                          "sample": wl.describe()},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "samples_s": [round(s["sample_s"], 3) for s in samples],
+        "samples_s": [round(x, 3) for x in sample_s],
+        "merge_s": [round(x["merge_s"], 3) for x in samples],
     }
     print(json.dumps(line), flush=True)
 
@@ -176,53 +226,77 @@ def torch_threads():
     return torch.get_num_threads()
 
 
-def cpu_baseline_leg():
-    """Bounded CPU sample on rank 0 at N=1 (about one sample, ~10-40 s)."""
+def cpu_baseline_leg(c: dict) -> dict:
+    """Bounded CPU sample on rank 0 at N=1 (two samples, ~15 s)."""
     from oracle.cpu_bench import CpuWorkload
     from paper_2407_02031_b200 import unet as U
-    wl = CpuWorkload(U.SDXL, N_CN, sum(LORA_RANKS), DENOISE_STEPS)
-    s = wl.sample()
-    img_s = DENOISE_STEPS * s["step_s"] + s["merge_s"] * wl.merge_elems_total / wl.merge_elems_slice
-    return {"value": 1.0 / img_s, "unit": "images/s", "cores": torch_threads(), "kind": "port",
-            "sample": wl.describe(), "sample_s": round(s["sample_s"], 2), "s_per_image_est": round(img_s, 1)}
+    wl = CpuWorkload(U.CONFIGS[c["cfg"]], c["n_cn"], sum(c["lora_ranks"]), DENOISE_STEPS)
+    wl.sample()                                  # warm-up (allocator, thread pool)
+    x = wl.sample()
+    return {"value": wl.images_per_s(x["sample_s"]), "unit": "images/s", "cores": torch_threads(), "kind": "port",
+            "merge_kind": wl.merge.kind, "blas_threads": blas_threads(), "cpu_model": cpu_model(),
+            "sample": wl.describe(), "sample_s": round(x["sample_s"], 2),
+            "s_per_image_est": round(wl.fraction * x["sample_s"], 1)}
 
 
 # ---------------------------------------------------------------------------
+def _inputs(req):
+    import torch
+    dev = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
+               images=[torch.from_numpy(i).cuda() for i in req.images])
+    if req.pooled is not None:
+        dev["pooled"] = torch.from_numpy(req.pooled).cuda()
+        dev["time_ids"] = torch.from_numpy(req.time_ids).cuda()
+    pinned = {k: (v.cpu().pin_memory() if not isinstance(v, list) else [x.cpu().pin_memory() for x in v])
+              for k, v in dev.items()}
+    return dev, pinned
+
+
+def gpu_minute_accounting(images: int, wall_ms: float, busy_ms: float, n_gpus: int) -> dict:
+    """orchestrator.py:768-782 ``throughput``: images over the GPU time
+    consumed, in minutes — busy time of every GPU, service GPUs included —
+    beside the allocation form (every GPU charged for the whole run)."""
+    return {"images_per_gpu_minute": images / (busy_ms / 60_000.0) if busy_ms > 0 else None,
+            "images_per_gpu_minute_allocated": images / (n_gpus * wall_ms / 60_000.0),
+            "gpu_busy_ms": busy_ms, "wall_ms": wall_ms, "n_gpus": n_gpus}
+
+
 def run_caas(args, world, rank, local):
     """N > 1: ControlNet-as-a-service groups (caas.py) — base GPU + one GPU per
     ControlNet; leftover ranks serve whole images alone."""
     import torch
+    import torch.distributed as dist
     from paper_2407_02031_b200 import ops
     from paper_2407_02031_b200 import unet as U
-    from paper_2407_02031_b200.caas import CaaSNode, caas_layout
+    from paper_2407_02031_b200.caas import CaaSNode, StepTimeline, caas_layout
     from paper_2407_02031_b200.patcher import synthetic_lora
     from paper_2407_02031_b200.pipeline import synthetic_batch
 
-    cfg = U.SDXL
-    B = args.batch
-    layout = caas_layout(world, N_CN)
-    node = CaaSNode(cfg, layout, rank, [0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16, seed=0,
-                    batch=B)
+    c = CONFIGS[args.config]
+    cfg, n_cn = U.CONFIGS[c["cfg"]], c["n_cn"]
+    B = args.batch or c["batch"]
+    layout = caas_layout(world, n_cn)
+    node = CaaSNode(cfg, layout, rank, list(c["cn_scales"]), steps=DENOISE_STEPS, guidance=7.5,
+                    dtype=torch.bfloat16, seed=0, batch=B)
     role = node.role
     if role in ("base", "solo"):
-        node.load_loras([(synthetic_lora(node.pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7)
-                         for i, r in enumerate(LORA_RANKS)])
+        node.load_loras([(synthetic_lora(node.pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), LORA_SCALE)
+                         for i, r in enumerate(c["lora_ranks"])])
     node.setup()
-    req = synthetic_batch(cfg, N_CN, B, seed=rank)
-    dev_in = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
-                  images=[torch.from_numpy(i).cuda() for i in req.images],
-                  pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
-    pinned = {k: (v.cpu().pin_memory() if not isinstance(v, list) else [x.cpu().pin_memory() for x in v])
-              for k, v in dev_in.items()}
+    req = synthetic_batch(cfg, n_cn, B, seed=rank)
+    dev_in, pinned = _inputs(req)
     producer = role in ("base", "solo")
     p = node.pipe if producer else None
 
-    def image(inputs, patch=True):
+    def image(inputs, patch=True, timeline=None):
         if producer:
             node.prepare(**inputs)
         else:
             node.prepare()
-        node.denoise(patch=patch) if producer else node.denoise()
+        if producer:
+            node.denoise(patch=patch, timeline=timeline)
+        else:
+            node.denoise(timeline=timeline)
 
     s = torch.cuda.current_stream()
     # calibrate the patch plan on the base: one unpatched image, one isolated patch
@@ -234,12 +308,12 @@ def run_caas(args, world, rank, local):
         b.record()
         b.synchronize()
         p.step_ms_est = a.elapsed_time(b) / DENOISE_STEPS
-        c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c.record(p.patch_stream)
+        c0_, d0_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0_.record(p.patch_stream)
         p.patchset.launch(stream=p.patch_stream)
-        d.record(p.patch_stream)
-        d.synchronize()
-        p.patch_ms_est = c.elapsed_time(d)
+        d0_.record(p.patch_stream)
+        d0_.synchronize()
+        p.patch_ms_est = c0_.elapsed_time(d0_)
     for _ in range(args.warmup):
         image(dev_in)
     barrier_sync(world)
@@ -274,10 +348,19 @@ def run_caas(args, world, rank, local):
     barrier_sync(world)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
     clk = clocks.stop()
-    producers = sum(1 for g in layout.groups)
+    # per-step accounting (one more image, events on every rank): the base's
+    # decoder wait split like orchestrator.py:662-678, service compute per step
+    tl = StepTimeline()
+    barrier_sync(world)
+    image(dev_in, timeline=tl)
+    barrier_sync(world)
+    summ = tl.summary()
+    red = torch.tensor([summ.get("step_ms", 0.0) if role == "service" else 0.0,
+                        1.0 if role == "service" else 0.0], device=_red_device(), dtype=torch.float64)
+    dist.all_reduce(red, op=dist.ReduceOp.SUM)
+    svc_ms = float(red[0].item() / red[1].item()) if red[1].item() > 0 else 0.0
+    producers = len(layout.groups)
     images = args.steps * producers * B
-    # per-image latency of group bases (not solos) for p50, gathered to rank 0
-    import torch.distributed as dist
     lat = torch.tensor([statistics.median(per_image) if (role == "base" or (role == "solo" and
                         all(not g.services for g in layout.groups))) else 0.0], device=_red_device(),
                        dtype=torch.float64)
@@ -291,14 +374,14 @@ def run_caas(args, world, rank, local):
     line = None
     if rank == 0:
         alg = p.patchset.alg_bytes
+        n_svc_gpus = sum(len(g.services) for g in layout.groups)
+        busy = total_ms * producers + svc_ms * DENOISE_STEPS * args.steps * n_svc_gpus
         line = {
-            "metric": METRIC, "value": images / (total_ms / 1000.0), "unit": "images/s", "n_gpus": world,
+            "metric": c["metric"], "value": images / (total_ms / 1000.0), "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "p50_s_per_image": float(lat.item()),
-            "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
-                                   "30 DDIM steps, CFG batch 2, async LoRA patch",
-                       "model": "sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init",
+            "config": {"workload": c["workload"], "model": c["model"],
                        "global_batch": producers * B, "seq_len": None,
                        "parallelism": "ControlNet-as-a-service groups " +
                                       "; ".join(str(g.ranks) for g in layout.groups),
@@ -306,12 +389,14 @@ def run_caas(args, world, rank, local):
             "e2e": {"value": images / (e2e_ms / 1000.0), "unit": "images/s",
                     "h2d_bytes_per_step": req.nbytes(), "d2h_bytes_per_step": 4 * node.L},
             "gpu_launches": int(tot.item()),
-            "roofline": {"kernel": "sdb lora_patch (K1, stacked R=128, all 794 SDXL matrices)", "bound": "hbm",
-                         "achieved": alg / (p.patch_ms_est * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                         "frac": alg / (p.patch_ms_est * 1e-3) / 1e9 / hbm, "traffic": k1_traffic(),
+            "roofline": {"kernel": f"sdb lora_patch (K1, stacked R={sum(c['lora_ranks'])}, all UNet matrices)",
+                         "bound": "hbm", "achieved": alg / (p.patch_ms_est * 1e-3) / 1e9, "peak": hbm,
+                         "unit": "GB/s", "frac": alg / (p.patch_ms_est * 1e-3) / 1e9 / hbm, "traffic": k1_traffic(),
                          "alg_bytes_per_launch": alg, "launch_ms_isolated": p.patch_ms_est,
                          "peak_source": src},
             "clocks": clk,
+            "caas_accounting": {"base": summ, "service_step_ms": svc_ms,
+                                **gpu_minute_accounting(images, total_ms, busy, world)},
             "detail": {"layout": [list(g.ranks) for g in layout.groups],
                        "first_patched_step": p.last_first_patched_step, "step_ms_est": p.step_ms_est},
         }
@@ -461,39 +546,157 @@ def blocking_preamble(pipe) -> dict:
     return out
 
 
+def lora_microbench(unet_p, shadow, hbm: float, cpu_full: bool = False, reps: int = 5) -> dict:
+    """BASELINE config 4: K1 over every patchable SDXL matrix with 4 LoRAs at
+    ranks 8/32/64/128 (stacked R = 232) and four distinct scales, bf16 weights.
+    Extends the reference's ``bench_merge`` keys (lora.py:163-199): patch
+    (out of place into the serving copy, and in place = merge_in_place),
+    unpatch (sign -1 in place = unmerge_in_place; restore from pristine; the
+    serving path's pointer swap), each as the median of ``reps`` CUDA-event
+    timed launches, with algorithmic GB/s and the fraction of the measured
+    HBM peak.  Beside it, the reference's own numpy ``merge_in_place`` (or
+    its restatement) on the host cores, BLAS at 1 thread and at all threads."""
+    import torch
+    from paper_2407_02031_b200.patcher import PatchSet, synthetic_lora
+    ranks, scales = (8, 32, 64, 128), (0.9, 0.55, 0.35, 1.3)
+    ads = [(synthetic_lora(unet_p, r, seed=40 + i, adapter_id=f"cfg4_{i}"), sc)
+           for i, (r, sc) in enumerate(zip(ranks, scales))]
+    out_of_place = PatchSet(unet_p, ads, shadow=shadow)
+    in_place = PatchSet(unet_p, ads, shadow=shadow, in_place_on_shadow=True)
+    names = [n for n, _ in unet_p.matrices]
+    pristine = [unet_p.t[n + ".weight"] for n in names]
+    dst = [shadow[n] for n in names]
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    alg = out_of_place.alg_bytes
+    w_bytes = sum(t.numel() * t.element_size() for t in pristine)
+    res = {}
+    res["patch_out_of_place_ms"] = timed(lambda: out_of_place.launch())
+    torch._foreach_copy_(dst, pristine)
+    res["merge_in_place_ms"] = timed(lambda: in_place.launch(sign=1.0))
+    res["unmerge_in_place_ms"] = timed(lambda: in_place.launch(sign=-1.0))
+    res["restore_from_pristine_ms"] = timed(lambda: torch._foreach_copy_(dst, pristine))
+    res["pointer_swap_ms"] = 0.0
+    out = {"layers": len(names), "ranks": list(ranks), "scales": list(scales), "stacked_rank": sum(ranks),
+           "kernel": out_of_place.plan.kernel, "alg_bytes_patch": alg, "alg_bytes_restore": 2 * w_bytes,
+           "in_place_nbytes": w_bytes, "create_and_replace_nbytes": 2 * w_bytes + sum(
+               a.nbytes for a, _ in ads), **{k: round(v, 4) for k, v in res.items()}}
+    for k in ("patch_out_of_place", "merge_in_place", "unmerge_in_place"):
+        gbs = alg / (res[k + "_ms"] * 1e-3) / 1e9
+        out[k + "_gbs"], out[k + "_frac"] = round(gbs, 1), round(gbs / hbm, 4)
+    gbs = 2 * w_bytes / (res["restore_from_pristine_ms"] * 1e-3) / 1e9
+    out["restore_from_pristine_gbs"], out["restore_from_pristine_frac"] = round(gbs, 1), round(gbs / hbm, 4)
+    out["peak_gbs"] = hbm
+    del out_of_place, in_place, ads
+    torch.cuda.empty_cache()
+    out["cpu_reference"] = cpu_merge_leg([(t.shape[0], t.numel() // t.shape[0]) for t in pristine],
+                                         sum(ranks), full=cpu_full)
+    return out
+
+
+def cpu_merge_leg(shapes, rank: int, full: bool) -> dict:
+    """The reference numpy merge on the host cores (addonsim.lora.merge_in_place
+    from baseline/_ref, else the bit-exact restatement), fp32 weights, over the
+    whole inventory (full) or a size-stratified 1/10 slice scaled up."""
+    from oracle.cpu_bench import MergeTimer, stratified
+    den = 1 if full else 10
+    sl = stratified(shapes, lambda s: s[0] * s[1], den)
+    total = sum(a * b for a, b in shapes)
+    mt = MergeTimer(sl, rank)
+    out = {"kind": mt.kind, "rank": rank, "matrices_timed": len(sl), "matrices_total": len(shapes),
+           "cpu_model": cpu_model(), "cores": os.cpu_count()}
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # noqa: BLE001
+        threadpool_limits = None
+    for label, n in (("blas_1_thread", 1), ("blas_all_threads", os.cpu_count())):
+        if threadpool_limits is not None:
+            with threadpool_limits(limits=n, user_api="blas"):
+                t = mt.run()
+        else:
+            t = mt.run()
+        s_full = t * total / mt.elements
+        out[label] = {"s_inventory": round(s_full, 2), "gbs_fp32": round(8 * total / s_full / 1e9, 3),
+                      "threads": n}
+    return out
+
+
+def parity_leg(eng, c: dict, dev_in: dict, req) -> dict:
+    """The benchmarked engine's step-1 latent (bf16, one more image with the
+    patch forced at boundary 1, so step 1 runs the pristine weights) against
+    the CPU fp32 oracle's step 1 on the same parameter values and inputs
+    (oracle/pipeline_ref.py, the checker).  The bf16 floor — the oracle with
+    bf16 activations vs fp32 — is measured by tests/test_sdxl_engine_gpu.py."""
+    import torch
+    from oracle import pipeline_ref as R
+    from paper_2407_02031_b200 import unet as U
+    cfg = U.CONFIGS[c["cfg"]]
+    got = []
+    eng.prepare(**dev_in)
+    eng.denoise(patch=True, boundary=1, on_step=lambda k, x: got.append(x.float().cpu()) if k == 1 else None)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pipe = eng.base.pipe
+    up = R.to_cpu_params(pipe.unet_p)
+    cps = []
+    for i in range(c["n_cn"]):
+        p = U.init_controlnet(cfg, "cuda", torch.bfloat16, seed=1000 + i)   # unscaled (services fold the scale)
+        cps.append(R.to_cpu_params(p))
+        del p
+    torch.cuda.empty_cache()
+    ref = R.denoise(cfg, up, cps, req, list(c["cn_scales"]), DENOISE_STEPS, 7.5, max_steps=1)[0]
+    rel = float((got[0].double() - ref.double()).norm() / ref.double().norm())
+    return {"step": 1, "rel_l2_vs_fp32_oracle": rel, "dtype": "bf16", "oracle": "oracle/pipeline_ref.py fp32 CPU",
+            "oracle_s": round(time.perf_counter() - t0, 1),
+            "note": "bf16-activation floor at this config: tests/test_sdxl_engine_gpu.py "
+                    "(profiles/r02_sdxl_parity.txt)"}
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_setup(args.gpus)
     torch.cuda.set_device(local)
+    if args.config == "lora":
+        return run_lora(args)
     if world > 1:
         return run_caas(args, world, rank, local)
     from paper_2407_02031_b200 import ops
     from paper_2407_02031_b200 import unet as U
+    from paper_2407_02031_b200.caas import LoopbackGroup, StepTimeline
     from paper_2407_02031_b200.patcher import synthetic_lora
     from paper_2407_02031_b200.pipeline import AddonPipeline, synthetic_batch
 
-    cfg = U.SDXL
-    B = args.batch
-    req = synthetic_batch(cfg, N_CN, B, seed=rank)
-    # device-resident copies of the request for the `value` loop
-    dev_in = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
-                  images=[torch.from_numpy(i).cuda() for i in req.images],
-                  pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
+    c = CONFIGS[args.config]
+    cfg, n_cn, scales = U.CONFIGS[c["cfg"]], c["n_cn"], list(c["cn_scales"])
+    B = args.batch or c["batch"]
+    req = synthetic_batch(cfg, n_cn, B, seed=rank)
+    dev_in, pinned = _inputs(req)
     if args.mode == "serial":
         # ControlNets inline (orchestrator.py:611-619), one CUDA graph per step
-        eng = AddonPipeline(cfg, n_controlnets=N_CN, cn_scales=[0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5,
+        eng = AddonPipeline(cfg, n_controlnets=n_cn, cn_scales=scales, steps=DENOISE_STEPS, guidance=7.5,
                             dtype=torch.bfloat16, seed=0, patch_max_ctas=args.patch_ctas, batch=B)
         pipe = eng
     else:
         # ControlNet branches on their own streams beside the UNet encoder (CaaS split on one GPU)
-        from paper_2407_02031_b200.caas import LoopbackGroup
-        eng = LoopbackGroup(cfg, N_CN, [0.8, 0.6], steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16,
+        eng = LoopbackGroup(cfg, n_cn, scales, steps=DENOISE_STEPS, guidance=7.5, dtype=torch.bfloat16,
                             seed=0, concurrent=True, batch=B)
         pipe = eng.base.pipe
         pipe.patch_max_ctas = args.patch_ctas
-    loras = [(synthetic_lora(pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), 0.7) for i, r in
-             enumerate(LORA_RANKS)]
-    # the 2 LoRAs live in pinned host memory (the LoRA cache tier); the e2e loop
+    loras = [(synthetic_lora(pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}"), LORA_SCALE) for i, r in
+             enumerate(c["lora_ranks"])]
+    # the LoRAs live in pinned host memory (the LoRA cache tier); the e2e loop
     # re-fetches them every image (H2D on the copy stream, re-pack, patch), the
     # resident loop finds them in HBM and only patches
     eng.load_loras(loras, host_resident=True)
@@ -511,20 +714,17 @@ def run_ours(args):
             b.record(s)
             b.synchronize()
             pipe.step_ms_est = step_ms = a.elapsed_time(b) / DENOISE_STEPS
-            c, d = pipe.launch_patch(timing=True, fetch=True)   # the plan's load: fetch + pack + patch
-            d.synchronize()
-            pipe.patch_ms_est = patch_ms = c.elapsed_time(d)
+            c0_, d0_ = pipe.launch_patch(timing=True, fetch=True)   # the plan's load: fetch + pack + patch
+            d0_.synchronize()
+            pipe.patch_ms_est = patch_ms = c0_.elapsed_time(d0_)
     lora_h2d = pipe.bank.nbytes
 
-    def image_resident():
+    def image_resident(patch=True):
         eng.prepare(**dev_in)
-        eng.denoise(patch=True, fetch=False)
-
-    pinned = {k: (v.cpu().pin_memory() if not isinstance(v, list) else [x.cpu().pin_memory() for x in v])
-              for k, v in dev_in.items()}
+        eng.denoise(patch=patch, fetch=False)
 
     def image_e2e():
-        # the public call: pinned host inputs (+ the 2 LoRAs) -> H2D -> denoise -> D2H of the final latent
+        # the public call: pinned host inputs (+ the LoRAs) -> H2D -> denoise -> D2H of the final latent
         eng.prepare(**pinned)
         eng.denoise(patch=True, fetch=True)
         eng.latent_nchw().contiguous().cpu()
@@ -535,43 +735,63 @@ def run_ours(args):
         image_e2e()
     barrier_sync(world)
 
+    def timed_images(fn, n):
+        evs = []
+        with torch.cuda.stream(s):
+            t_a = torch.cuda.Event(enable_timing=True)
+            t_a.record(s)
+            for _ in range(n):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                fn()
+                b.record(s)
+                evs.append((a, b))
+            t_b = torch.cuda.Event(enable_timing=True)
+            t_b.record(s)
+        barrier_sync(world)
+        return t_a.elapsed_time(t_b), [a.elapsed_time(b) / 1000.0 for a, b in evs]
+
     # ---- timed: device-resident inputs ------------------------------------
     clocks = ClockSampler(local)
     clocks.start()
     pipe.patch_timing = []
     c0 = ops.LAUNCHES["count"]
-    evs = []
     barrier_sync(world)
-    with torch.cuda.stream(s):
-        t_all0 = torch.cuda.Event(enable_timing=True)
-        t_all0.record(s)
-        for _ in range(args.steps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            image_resident()
-            b.record(s)
-            evs.append((a, b))
-        t_all1 = torch.cuda.Event(enable_timing=True)
-        t_all1.record(s)
-    barrier_sync(world)
+    total_ms, per_image = timed_images(image_resident, args.steps)
     host_launches = ops.LAUNCHES["count"] - c0
-    total_ms = max_over_ranks(t_all0.elapsed_time(t_all1), world)
-    per_image = [a.elapsed_time(b) / 1000.0 for a, b in evs]
+    total_ms = max_over_ranks(total_ms, world)
     patch_ms_live = [p0.elapsed_time(p1) for p0, p1 in pipe.patch_timing]
     pipe.patch_timing = None
 
     # ---- timed: end to end through the public API (host buffers) ----------
     barrier_sync(world)
-    with torch.cuda.stream(s):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for _ in range(args.steps):
-            image_e2e()
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record(s)
-    barrier_sync(world)
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_ms, _ = timed_images(image_e2e, args.steps)
+    e2e_ms = max_over_ranks(e2e_ms, world)
     clk = clocks.stop()
+
+    # ---- the same loop without the LoRA: is the patch hidden? ------------
+    plain_ms, per_plain = timed_images(lambda: image_resident(patch=False), args.steps)
+    overhead = {"patched_mean_s": statistics.mean(per_image), "unpatched_mean_s": statistics.mean(per_plain),
+                "patched_p50_s": statistics.median(per_image), "unpatched_p50_s": statistics.median(per_plain),
+                "patch_overhead_ms_per_image": 1000.0 * (statistics.mean(per_image) - statistics.mean(per_plain)),
+                "note": "identical image loops (resident inputs) with and without the async LoRA patch, "
+                        "back to back in this run (PAPER.md:519-521; orchestrator.py:698-719)"}
+    overhead["patch_overhead_pct"] = 100.0 * overhead["patch_overhead_ms_per_image"] / (
+        1000.0 * overhead["unpatched_mean_s"])
+
+    # ---- CaaS per-step accounting (orchestrator.py:621-678, 768-782) ------
+    accounting = None
+    if args.mode == "branch":
+        tl = StepTimeline()
+        with torch.cuda.stream(s):
+            eng.prepare(**dev_in)
+            eng.denoise(patch=True, fetch=False, timeline=tl)
+        torch.cuda.synchronize()
+        accounting = {"per_step": tl.summary(comm_ms=0.0),
+                      "note": "1 GPU: ControlNet branches on side streams beside the encoder, residual buffers "
+                              "aliased (no transfer, comm 0); decoder wait split comm -> ControlNet compute -> "
+                              "fetch -> queue as orchestrator.py:662-678",
+                      **gpu_minute_accounting(args.steps * B, total_ms, total_ms, 1)}
 
     # ---- K1 isolated (for the roofline's context) --------------------------
     iso = []
@@ -596,55 +816,107 @@ def run_ours(args):
     achieved = alg / (live * 1e-3) / 1e9 if live else None
     images = args.steps * world * B
     value = images / (total_ms / 1000.0)
+    R = sum(c["lora_ranks"])
     line = {
-        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "metric": c["metric"], "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "p50_s_per_image": statistics.median(per_image),
-        "config": {"workload": "SDXL 1024^2 (128x128 latent) + 2 ControlNets + 2 LoRAs r64 (stacked R=128), "
-                               "30 DDIM steps, CFG batch 2, async LoRA patch" +
-                               (f"; serving batch of {B} images per step (CFG batch {2 * B}, one LoRA set)"
-                                if B > 1 else ""),
-                   "model": "sdxl-shaped UNet (2.57B) + 2 ControlNets (1.25B each), random init",
-                   "global_batch": world * B, "seq_len": None,
+        "config": {"workload": c["workload"] + (f"; serving batch of {B} images per step (CFG batch {2 * B}, "
+                                                f"one LoRA set)" if B > 1 else ""),
+                   "model": c["model"], "global_batch": world * B, "seq_len": None,
                    "parallelism": ("1 GPU, ControlNet branches on side streams concurrent with the UNet encoder"
                                    if args.mode == "branch" else "1 GPU, ControlNets inline"),
-                   "l2": "inputs larger than L2 (5.1 GB UNet + 5.0 GB ControlNet weights re-read every step)"},
+                   "l2": "inputs larger than L2 (UNet + ControlNet weights, GBs, re-read every step)"},
         "e2e": {"value": images / (e2e_ms / 1000.0), "unit": "images/s",
                 "h2d_bytes_per_step": req.nbytes() + lora_h2d, "d2h_bytes_per_step": pipe.d2h_bytes(),
-                "note": "inputs + both LoRAs fetched from pinned host memory every image"},
+                "note": "inputs + the LoRAs fetched from pinned host memory every image"},
         "gpu_launches": int(gpu_launches),
-        "roofline": {"kernel": "sdb lora_patch (K1, stacked R=128, all 794 SDXL matrices)",
+        "roofline": {"kernel": f"sdb lora_patch (K1, stacked R={R}, all {len(pipe.unet_p.matrices)} UNet matrices)",
                      "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm if achieved else None, "traffic": k1_traffic(),
+                     "frac": achieved / hbm if achieved else None,
+                     "traffic": k1_traffic() if args.config == "sdxl" else None,
                      "alg_bytes_per_launch": alg, "launch_ms_live": live,
                      "launch_ms_isolated": statistics.median(iso),
                      "frac_isolated": alg / (statistics.median(iso) * 1e-3) / 1e9 / hbm,
                      "peak_source": f"{src} MEASURED_PEAKS.json hbm_gbs" if src == "measured" else src},
         "clocks": clk,
         "detail": {"step_ms_calibrated": step_ms, "first_patched_step": pipe.last_first_patched_step,
-                   "patch_path": pipe.patchset.plan.path, "per_image_s": [round(x, 4) for x in per_image]},
+                   "patch_path": pipe.patchset.plan.path, "per_image_s": [round(x, 4) for x in per_image],
+                   "patch_overhead": overhead},
     }
+    if accounting is not None:
+        line["caas_accounting"] = accounting
     if B > 1:   # every image of a batch completes with the batch: its latency is the batch time
         line["p50_s_per_batch"] = statistics.median(per_image)
-        line["max_s_per_batch"] = max(per_image)
+        line["p99_s_per_batch"] = sorted(per_image)[min(len(per_image) - 1, int(0.99 * len(per_image)))]
         line["detail"]["per_batch_s"] = line["detail"].pop("per_image_s")
     line["roofline_other_kernels"] = other_kernels_roofline(hbm)
-    if world == 1:
-        try:
-            line["detail"]["blocking_lora_preamble"] = blocking_preamble(pipe)
+    if args.config == "sdxl" and args.mode == "branch":
+        try:   # BASELINE config 4 (K1 patch / unpatch micro-bench) on the engine's own weights
+            line["lora_microbench"] = lora_microbench(pipe.unet_p, pipe.shadow, hbm)
         except Exception as e:  # noqa: BLE001 — a side measurement must not sink the bench line
-            line["detail"]["blocking_lora_preamble"] = {"error": f"{type(e).__name__}: {e}"[:200]}
-    if world == 1 and rank == 0 and not args.no_cpu:
+            line["lora_microbench"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    try:
+        line["detail"]["blocking_lora_preamble"] = blocking_preamble(pipe)
+    except Exception as e:  # noqa: BLE001
+        line["detail"]["blocking_lora_preamble"] = {"error": f"{type(e).__name__}: {e}"[:200]}
+    if rank == 0 and not args.no_cpu:
         try:
-            line["cpu_baseline"] = cpu_baseline_leg()
+            line["cpu_baseline"] = cpu_baseline_leg(c)
         except Exception as exc:  # reported, never silently dropped
             line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+        if args.mode == "branch" and B == 1:
+            try:
+                with torch.cuda.stream(s):
+                    line["parity"] = parity_leg(eng, c, dev_in, req)
+            except Exception as exc:  # noqa: BLE001
+                line["parity"] = {"error": repr(exc)[:300]}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+
+
+def run_lora(args):
+    """--config lora: BASELINE config 4 alone — the K1 patch / unpatch
+    micro-bench over every SDXL matrix (R = 232, four scales), timed K times
+    after W warm-ups; the reference numpy merge over the FULL inventory."""
+    import torch
+    from paper_2407_02031_b200 import ops
+    from paper_2407_02031_b200 import unet as U
+    from paper_2407_02031_b200.patcher import allocate_shadow
+    hbm, _, src = peaks()
+    p = U.init_unet(U.SDXL, "cuda", torch.bfloat16, 0)
+    shadow = allocate_shadow(p)
+    clocks = ClockSampler(0)
+    clocks.start()
+    c0 = ops.LAUNCHES["count"]
+    mb = lora_microbench(p, shadow, hbm, cpu_full=True, reps=max(args.steps, 1))
+    clk = clocks.stop()
+    n_launch = ops.LAUNCHES["count"] - c0
+    ms = mb["patch_out_of_place_ms"]
+    line = {
+        "metric": "K1 LoRA patch GB/s, all 794 SDXL matrices, 4 LoRAs r8-128 (R=232), bf16 (config 4)",
+        "value": mb["patch_out_of_place_gbs"], "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "K1 over all 794 SDXL UNet matrices (2.57 G elements), 4 LoRAs r 8/32/64/128 at "
+                               "scales 0.9/0.55/0.35/1.3, stacked R=232; patch out of place + merge/unmerge in "
+                               "place + restore", "model": "sdxl-shaped UNet weights, random init",
+                   "global_batch": 1, "parallelism": "1 GPU",
+                   "l2": "inputs larger than L2 (5.1 GB of weights per launch)"},
+        "e2e": {"value": mb["patch_out_of_place_gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0, "note": "factors resident (the fetch path is in the headline's e2e)"},
+        "gpu_launches": int(n_launch),
+        "roofline": {"kernel": "sdb lora_patch (K1, R=232)", "bound": "hbm", "achieved": mb["patch_out_of_place_gbs"],
+                     "peak": hbm, "unit": "GB/s", "frac": mb["patch_out_of_place_frac"], "traffic": None,
+                     "peak_source": src},
+        "clocks": clk, "lora_microbench": mb,
+        "cpu_baseline": {"value": 8 * 2.566e9 / mb["cpu_reference"]["blas_all_threads"]["s_inventory"] / 1e9,
+                         "unit": "GB/s (fp32 weights)", "cores": os.cpu_count(),
+                         "kind": mb["cpu_reference"]["kind"],
+                         "sample": "the reference numpy merge_in_place over all 794 SDXL matrices, R=232"},
+    }
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -653,10 +925,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS) + ["lora"], default="sdxl",
+                    help="BASELINE config: sdxl (configs[2], default), sd15 (configs[1]), serve (configs[4]), "
+                         "lora (configs[3] micro-bench)")
     ap.add_argument("--patch-ctas", type=int, default=0, help="cap the K1 grid (0 = one CTA per tile)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--batch", type=int, default=1,
-                    help="images per denoising batch sharing one LoRA set (BASELINE config 5: 8); 1 GPU")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="images per denoising batch sharing one LoRA set (0 = the config's: 1, serve 8)")
     ap.add_argument("--mode", choices=["branch", "serial"], default="branch",
                     help="1 GPU: ControlNet branches concurrent with the encoder (branch) or inline (serial)")
     args = ap.parse_args()

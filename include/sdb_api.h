@@ -107,7 +107,7 @@ int sdb_lora_patch_one(void* w_in, void* w_out, int64_t h1, int64_t h2, int64_t 
  * plan is a host-built blob (TMA tensor maps for every W + job/unit tables)
  * the caller copies to device memory (128-B aligned) before launching.
  * Requirements: bf16 W with ldw % 8 == 0 and 16-B aligned rows; rank <= 256.
- * simt_rank > 0 (<= 32) selects the FFMA contraction, 0 the tcgen05 MMA. */
+ * simt_rank is reserved (pass 0): the contraction is tcgen05 at every rank. */
 typedef struct sdb_lora_tc_job {
   void* w_in;
   void* w_out;
@@ -115,19 +115,28 @@ typedef struct sdb_lora_tc_job {
   const void* a_packed;
   const void* b_packed;
   int32_t rank;
-  float scale;
+  float scale;        /* epilogue scale (sdb_lora_pack_multi_layout's epi_scale x the job's own) */
+  int32_t lo_mask;    /* from sdb_lora_pack_multi_layout (0 for sdb_lora_pack): K blocks with a low part */
 } sdb_lora_tc_job;
 
 int sdb_lora_pack_bytes(int64_t h1, int64_t h2, int32_t rank, size_t* a_bytes, size_t* b_bytes);
 /* Stack-and-pack from up to 8 adapters' own bf16 factor buffers (the stacked
- * set of lora.py:147-160, scales folded in fp32 into A, one rounding):
- * packed rank = sum of the sources' ranks. */
+ * set of lora.py:147-160, down' = [d_i * f32(s_i)], up' = [u_i]; packed rank =
+ * sum of the sources' ranks).  Scales stay exact: the scale carried by the
+ * largest share of the rank (epi_scale) is applied by the patch epilogue in
+ * fp32 and its sources are packed unscaled; each other source is packed as
+ * x = d * (s_i / epi_scale) split into a bf16 high part and a bf16 low part
+ * (an extra A K-block per affected B K-block, bit b of lo_mask), 2^-17
+ * relative instead of a bf16 rounding of s_i * d.  Query the layout first
+ * (sizes, epi_scale, lo_mask for the sdb_lora_tc_job), then pack. */
 typedef struct sdb_lora_src {
   const void* down; int64_t ldd;   /* h1 x rank   */
   const void* up;   int64_t ldu;   /* rank x h2   */
   int32_t rank;
   float scale;
 } sdb_lora_src;
+int sdb_lora_pack_multi_layout(const sdb_lora_src* srcs_host, int n_src, int64_t h1, int64_t h2,
+                               size_t* a_bytes, size_t* b_bytes, float* epi_scale, int32_t* lo_mask);
 int sdb_lora_pack_multi(const sdb_lora_src* srcs_host, int n_src, int64_t h1, int64_t h2,
                         void* a_packed, void* b_packed, void* stream);
 int sdb_lora_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2,

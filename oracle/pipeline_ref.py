@@ -29,9 +29,10 @@ import torch.nn.functional as F
 from . import lora_ref
 
 
-def to_cpu_params(params) -> dict:
-    """Device Params -> {name: fp32 CPU NCHW-contiguous tensor}."""
-    return {k: v.detach().float().cpu().contiguous() for k, v in params.t.items()}
+def to_cpu_params(params, dtype=torch.float32) -> dict:
+    """Device Params -> {name: CPU NCHW-contiguous tensor} (fp32; fp64 for the
+    rounding-floor measurements)."""
+    return {k: v.detach().cpu().to(dtype).contiguous() for k, v in params.t.items()}
 
 
 def ddim_coefs(steps: int, guidance: float):
@@ -44,11 +45,14 @@ def ddim_coefs(steps: int, guidance: float):
 
 class RefNet:
     """bf16_acts=True rounds every linear / conv / norm output to bf16 (fp32
-    math in between): the error floor of ANY bf16-activation implementation,
-    used to bound the device bf16 path (tests/test_pipeline_gpu.py)."""
+    math in between; the UNet's eps stays fp32 as on the device) and the
+    merged LoRA weights to bf16: the error floor of a bf16-activation
+    implementation, used to bound the device bf16 path
+    (tests/test_pipeline_gpu.py, tests/test_sdxl_engine_gpu.py)."""
 
     def __init__(self, cfg, p: dict, bf16_acts: bool = False):
         self.cfg, self.p = cfg, p
+        self.dt = next(iter(p.values())).dtype      # fp32 (fp64: the truth the fp32 floor is measured against)
         self.rnd = (lambda t: t.bfloat16().float()) if bf16_acts else (lambda t: t)
 
     def lin(self, n, x):
@@ -65,7 +69,7 @@ class RefNet:
 
     def temb(self, t, n, add_emb):
         half = self.cfg.block_channels[0] // 2
-        freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=torch.float32) / half)
+        freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=self.dt) / half)
         a = float(t) * freqs
         te = torch.cat([torch.cos(a), torch.sin(a)])[None].expand(n, -1)
         e = self.lin("time_embedding.linear_2", F.silu(self.lin("time_embedding.linear_1", te)))
@@ -76,10 +80,10 @@ class RefNet:
     def add_embedding(self, pooled, time_ids):
         d = self.cfg.addition_time_embed_dim
         half = d // 2
-        freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=torch.float32) / half)
-        a = time_ids.reshape(-1, 1).float() * freqs[None]
+        freqs = torch.exp(-math.log(10000.0) * torch.arange(half, dtype=self.dt) / half)
+        a = time_ids.reshape(-1, 1).to(self.dt) * freqs[None]
         tid = torch.cat([torch.cos(a), torch.sin(a)], -1).reshape(pooled.shape[0], -1)
-        x = torch.cat([pooled.float(), tid], -1)
+        x = torch.cat([pooled.to(self.dt), tid], -1)
         return self.lin("add_embedding.linear_2", F.silu(self.lin("add_embedding.linear_1", x)))
 
     def resnet(self, pre, x, temb):
@@ -155,7 +159,9 @@ class RefUNet(RefNet):
                     h = self.transformer(f"up.{i}.attn.{j}", h, ctx, depth)
             if i < len(rev) - 1:
                 h = self.conv(f"up.{i}.upsample", F.interpolate(h, scale_factor=2.0, mode="nearest"))
-        return self.conv("conv_out", self.gn("conv_norm_out", h, True))
+        # eps leaves the device UNet in fp32 (K9): no bf16 rounding of conv_out
+        w = self.p["conv_out.weight"]
+        return F.conv2d(self.gn("conv_norm_out", h, True), w, self.p.get("conv_out.bias"), padding=w.shape[-1] // 2)
 
 
 class RefControlNet(RefNet):
@@ -173,27 +179,31 @@ class RefControlNet(RefNet):
         return [self.conv(f"zero_convs.{k}", s) for k, s in enumerate(skips)] + [self.conv("mid_zero_conv", h)]
 
 
-def merge_loras(p: dict, adapters, matrices) -> dict:
+def merge_loras(p: dict, adapters, matrices, round_bf16: bool = False) -> dict:
     """Patched copy of the UNet params: for every target, W_logical (Cout,
     Cin*kh*kw) += stacked adapters via the pinned lora_ref (fp64 accumulate).
-    adapters: [(factors{name: (down, up)} with LOGICAL up, scale)]."""
+    adapters: [(factors{name: (down, up)} with LOGICAL up, scale)].
+    round_bf16: store the merged weights rounded to bf16 (a bf16 weight
+    store's single rounding, lora_ref.accumulate_bf16's contract)."""
     out = dict(p)
     for name, _ in matrices:
         present = [(f[name], s) for f, s in adapters if name in f]
         if not present:
             continue
         w = p[name + ".weight"]
-        wl = w.reshape(w.shape[0], -1).numpy().copy()
+        wl = w.reshape(w.shape[0], -1).float().numpy().copy()   # the reference merges fp32 weights
         down, up = lora_ref.stack([(d.float().cpu().numpy(), u.float().cpu().numpy(), s) for (d, u), s in present])
         lora_ref.accumulate(wl, down, up, 1.0, 1.0)
-        out[name + ".weight"] = torch.from_numpy(wl).reshape(w.shape)
+        merged = torch.from_numpy(wl).reshape(w.shape).to(w.dtype)
+        out[name + ".weight"] = merged.bfloat16().float() if round_bf16 else merged
     return out
 
 
 def denoise(cfg, unet_p: dict, cn_ps: list, req, cn_scales, steps: int, guidance: float,
             adapters=None, matrices=None, boundary=None, bf16_acts: bool = False,
-            groups=None, group_boundaries=None) -> list:
-    """Returns the fp32 [4, H, W] latent after every step.
+            groups=None, group_boundaries=None, max_steps=None) -> list:
+    """Returns the fp32 [4, H, W] latent after every step (the first
+    ``max_steps`` steps of the ``steps``-step schedule when given).
 
     groups / group_boundaries: group-pipelined patching
     (addonsim/orchestrator.py:244-278) — matrix group m (a set of names) is
@@ -204,31 +214,34 @@ def denoise(cfg, unet_p: dict, cn_ps: list, req, cn_scales, steps: int, guidance
         nets, firsts = [unet], []
         for v in range(1, len(groups) + 1):
             names = set().union(*groups[:v])
-            nets.append(RefUNet(cfg, merge_loras(unet_p, adapters, [m for m in matrices if m[0] in names]),
-                                bf16_acts))
+            nets.append(RefUNet(cfg, merge_loras(unet_p, adapters, [m for m in matrices if m[0] in names],
+                                                 bf16_acts), bf16_acts))
             b = group_boundaries[v - 1]
             firsts.append(steps + 1 if b is None else b + 1)
 
         def pick(s):
             return nets[sum(1 for f in firsts if s >= f)]
     else:
-        patched = RefUNet(cfg, merge_loras(unet_p, adapters, matrices), bf16_acts) if adapters else None
+        patched = RefUNet(cfg, merge_loras(unet_p, adapters, matrices, bf16_acts), bf16_acts) if adapters else None
         first = (boundary + 1) if (adapters and boundary is not None) else steps + 1
 
         def pick(s):
             return patched if (patched is not None and s >= first) else unet
     cns = [RefControlNet(cfg, p, bf16_acts) for p in cn_ps]
-    ctx = torch.from_numpy(req.context).float()
+    dt = unet.dt
+    ctx = torch.from_numpy(req.context).to(dt)
     add_u = add_c = None
     if cfg.addition_embed:
         pooled, tids = torch.from_numpy(req.pooled), torch.from_numpy(req.time_ids)
         add_u = unet.add_embedding(pooled, tids)
         add_c = [cn.add_embedding(pooled, tids) for cn in cns]
-    hints = [cn.hint(torch.from_numpy(im).float()) for cn, im in zip(cns, req.images)]
+    hints = [cn.hint(torch.from_numpy(im).to(dt)) for cn, im in zip(cns, req.images)]
     x = torch.from_numpy(req.latent).double()
     out = []
     for s, (t, a_t, a_p) in enumerate(ddim_coefs(steps, guidance), start=1):
-        inp = x.float()[None].expand(2, -1, -1, -1)
+        if max_steps is not None and s > max_steps:
+            break
+        inp = x.to(dt)[None].expand(2, -1, -1, -1)
         res = [cn.forward(inp, t, ctx, hints[i], add_c[i] if add_c else None) for i, cn in enumerate(cns)]
         net = pick(s)
         eps = net.forward(inp, t, ctx, add_u, res, cn_scales).double()

@@ -159,6 +159,7 @@ class LoraTcJob(ctypes.Structure):
         ("b_packed", ctypes.c_void_p),
         ("rank", ctypes.c_int32),
         ("scale", ctypes.c_float),
+        ("lo_mask", ctypes.c_int32),
     ]
 
 
@@ -175,7 +176,8 @@ class LoraSrc(ctypes.Structure):
     ]
 
 
-EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_tc_plan",
+EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_pack_multi_layout",
+                       "sdb_lora_tc_plan",
                        "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_add_layernorm",
                        "sdb_cross_attention", "sdb_stream_wait_value32", "sdb_stream_write_value32",
                        "sdb_memcpy_async", "sdb_cross_attention_set_mode", "sdb_self_attention",
@@ -190,6 +192,10 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
     lib.sdb_lora_pack.argtypes = [vp, i64, vp, i64, i64, i64, ctypes.c_int32, vp, vp, vp]
     lib.sdb_lora_pack_multi.restype = i32
     lib.sdb_lora_pack_multi.argtypes = [ctypes.POINTER(LoraSrc), i32, i64, i64, vp, vp, vp]
+    lib.sdb_lora_pack_multi_layout.restype = i32
+    lib.sdb_lora_pack_multi_layout.argtypes = [ctypes.POINTER(LoraSrc), i32, i64, i64, ctypes.POINTER(sz),
+                                               ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_float),
+                                               ctypes.POINTER(ctypes.c_int32)]
     lib.sdb_lora_tc_plan.restype = i32
     lib.sdb_lora_tc_plan.argtypes = [ctypes.POINTER(LoraTcJob), i32, vp, sz, ctypes.POINTER(sz),
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]

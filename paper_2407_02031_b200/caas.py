@@ -13,14 +13,22 @@ branch are done (orchestrator.py:652-653).  Here that is a real exchange:
 * per request: the base broadcasts the conditioning inputs (text embeddings,
   control images, SDXL added conditions) to its services once; hint and
   added-condition embeddings are then computed locally (step-invariant).
-* per step: the base broadcasts the 4xHxW fp32 latent + timestep (256 KiB for
-  SDXL, the paper's "send latent" C0); every service runs its ControlNet(s)
-  and writes the conditioning-scaled sum of its residuals into one flat
-  buffer (the scales are folded into the zero convolutions at load); one
-  NCCL reduce(SUM) onto the base (the paper's 108 MiB "feature map" transfer,
-  C1) overlaps the base's encoder; the base's decoder consumes the reduced
-  residuals through K3.  The only data-path collectives are that broadcast
-  and that reduce — there is no other exchange.
+* per step (``CaaSPeerProtocol``, the default whenever the group's GPUs can
+  map each other's memory): the base raises each service's "message ready"
+  flag (a GPU-side ``cuStreamWriteValue32`` into the service's memory) once
+  the 4xHxW fp32 latent + timestep (256 KiB for SDXL, the paper's "send
+  latent" C0) is written; each service's stream waits on it, pulls the
+  message over NVLink (CUDA-IPC mapping), runs its ControlNet(s) — scales
+  folded into the zero convolutions — and pushes each residual level into
+  its own receive buffer on the base as soon as it exists (shallow, largest
+  levels first: the paper's 108 MiB "feature map" transfer C1, overlapped
+  with the deeper levels and the base's encoder), then raises the base's
+  "residuals ready" flag.  The base's decoder waits on every service's flag
+  and K3 sums the per-service buffers into the skip concat.  No collective
+  and no host round trip on the per-step data path.
+* ``SDB_CAAS_TRANSPORT=nccl`` selects ``CaaSProtocol`` instead: NCCL
+  broadcast of the message + send/recv of each service's flat buffer (gloo
+  with host staging on CPU-only process groups, which the CPU tests use).
 
 The transport (``CaaSProtocol``) is separated from the compute so the same
 protocol code runs under gloo on CPU in the tests with a stand-in compute.
@@ -441,6 +449,12 @@ class CaaSNode:
                       if dist.is_initialized() and self.role != "solo" else None)
         self.graphs = {}
         self.graph_launches = {}
+        # every node captures on its OWN stream: library calls inside a capture
+        # bake in per-stream resources (cuBLAS keys its workspace by stream),
+        # and the services' graphs replay concurrently with the base's encoder
+        # graph (LoopbackGroup(concurrent=True)) — one shared capture stream
+        # would make them race on one cuBLAS workspace
+        self.capture_stream = torch.cuda.Stream(device=self.device)
 
     # -- capture --------------------------------------------------------------
     def _service_step(self):
@@ -481,14 +495,14 @@ class CaaSNode:
 
     def _capture(self, name, fn, pool=None):
         s = torch.cuda.current_stream(self.device)
-        side = torch.cuda.Stream(device=self.device)
+        side = self.capture_stream
         side.wait_stream(s)
         with torch.cuda.stream(side):
-            fn()
+            fn()                                  # warm-up on the capture stream
         s.wait_stream(side)
         g = torch.cuda.CUDAGraph()
         c0 = self.ops.LAUNCHES["count"]
-        with torch.cuda.graph(g, pool=pool):
+        with torch.cuda.graph(g, pool=pool, stream=side):
             fn()
         self.graph_launches[name] = self.ops.LAUNCHES["count"] - c0   # our kernels per replay
         self.graphs[name] = g
@@ -638,7 +652,11 @@ class CaaSNode:
         return sched
 
     def denoise(self, patch: bool = False, boundary: Optional[int] = None, fetch: bool = True,
-                boundaries: Optional[Sequence[int]] = None) -> None:
+                boundaries: Optional[Sequence[int]] = None, timeline: Optional["StepTimeline"] = None) -> None:
+        """timeline: per-step events — on the base the encoder end, decoder
+        start / end (the decoder start is when every service's residuals were
+        in); on a service the ControlNet compute (message arrival -> residuals
+        pushed).  A solo rank records nothing."""
         if self.role == "solo":
             if self.pipe.patch_groups and patch:
                 self.pipe.denoise_pipelined(boundaries or ([boundary] * len(self.pipe.patch_groups)
@@ -652,21 +670,88 @@ class CaaSNode:
         for step in range(1, self.steps + 1):
             if self.role == "base":
                 which = sched.weights_at(step, s)
+                rec = timeline.begin(s) if timeline is not None else None
                 works = self.proto.base_step_begin()
                 self.base_encode(which)               # overlaps the services' ControlNets
+                if rec is not None:
+                    rec["enc_end"].record(s)
                 for w in works:
                     w.wait()                          # decoder after the encoder AND every branch
+                if rec is not None:
+                    rec["dec_start"].record(s)
                 self.base_decode(which)
+                if rec is not None:
+                    rec["dec_end"].record(s)
             else:
                 self.proto.service_receive()
+                rec = timeline.begin(s) if timeline is not None else None
                 self.service_step()
                 self.proto.service_send()
+                if rec is not None:                   # a service's step: its compute (+ push)
+                    for k in ("enc_end", "dec_start", "dec_end"):
+                        rec[k].record(s)
         sched.finish(s)
 
     def latent_nchw(self) -> Optional[torch.Tensor]:
         if self.role == "service":
             return None
         return self.pipe.latent_nchw()
+
+
+class StepTimeline:
+    """Per-step CUDA events of the CaaS step (orchestrator.py:621-660) and the
+    reference's split of the decoder's wait (``_attribute_stall``
+    :662-678): the gap between the encoder's end and the decoder's start is
+    charged, back to front along the critical (last-ready) branch, to the
+    transfer tail (comm), the branch's ControlNet compute, a weight fetch
+    (none here: the ControlNets stay resident) and, for what remains,
+    queueing.  Times come from events on the streams that did the work."""
+
+    def __init__(self):
+        self.steps = []     # per step: dict of events
+
+    @staticmethod
+    def _ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def begin(self, stream) -> dict:
+        rec = {"start": self._ev(), "branches": [], "enc_end": self._ev(), "dec_start": self._ev(),
+               "dec_end": self._ev()}
+        rec["start"].record(stream)
+        self.steps.append(rec)
+        return rec
+
+    def summary(self, comm_ms: float = 0.0) -> dict:
+        """Mean per-step ms: encoder, each branch (ControlNet compute, from the
+        step start), decoder, the decoder's wait and its comm / compute /
+        fetch / queue split (reference accounting)."""
+        n = len(self.steps)
+        if n == 0:
+            return {}
+        acc = {"encoder_ms": 0.0, "decoder_ms": 0.0, "decoder_wait_ms": 0.0, "comm_ms": 0.0,
+               "controlnet_wait_ms": 0.0, "cache_fetch_ms": 0.0, "queue_ms": 0.0, "step_ms": 0.0}
+        branch = None
+        for r in self.steps:
+            enc = r["start"].elapsed_time(r["enc_end"])
+            br = [r["start"].elapsed_time(e) for e in r["branches"]]
+            gap = max(0.0, r["enc_end"].elapsed_time(r["dec_start"]))
+            acc["encoder_ms"] += enc
+            acc["decoder_ms"] += r["dec_start"].elapsed_time(r["dec_end"])
+            acc["step_ms"] += r["start"].elapsed_time(r["dec_end"])
+            acc["decoder_wait_ms"] += gap
+            branch = [a + b for a, b in zip(branch, br)] if branch is not None else br
+            if gap > 0 and br:
+                comm = min(gap, comm_ms)
+                rest = gap - comm
+                compute = min(rest, max(br))          # the critical branch's compute
+                rest -= compute
+                acc["comm_ms"] += comm
+                acc["controlnet_wait_ms"] += compute
+                acc["queue_ms"] += rest               # fetch: 0 (resident weights)
+        out = {k: v / n for k, v in acc.items()}
+        out["branch_ms"] = [b / n for b in (branch or [])]
+        out["steps"] = n
+        return out
 
 
 class LoopbackGroup:
@@ -712,28 +797,43 @@ class LoopbackGroup:
             s.finish_prepare([t.clone() for t in shared])
 
     def denoise(self, patch: bool = False, boundary: Optional[int] = None, on_step=None,
-                fetch: bool = True, boundaries: Optional[Sequence[int]] = None) -> None:
+                fetch: bool = True, boundaries: Optional[Sequence[int]] = None,
+                timeline: Optional[StepTimeline] = None) -> None:
         sched = self.base.start_patch_schedule(patch, boundary, fetch, boundaries)
         s = torch.cuda.current_stream()
         for step in range(1, self.steps + 1):
             which = sched.weights_at(step, s)
+            rec = timeline.begin(s) if timeline is not None else None
             if self.concurrent:
                 done = []
                 for svc, st in zip(self.services, self.streams):
                     st.wait_stream(s)              # message of this step is written
                     with torch.cuda.stream(st):
                         svc.service_step()
-                    e = torch.cuda.Event()
+                    e = torch.cuda.Event(enable_timing=rec is not None)
                     e.record(st)
                     done.append(e)
                 self.base.base_encode(which)
+                if rec is not None:
+                    rec["enc_end"].record(s)
+                    rec["branches"] = done
                 for e in done:
                     s.wait_event(e)
             else:
                 for svc in self.services:
                     svc.service_step()
+                    if rec is not None:
+                        e = StepTimeline._ev()
+                        e.record(s)
+                        rec["branches"].append(e)
                 self.base.base_encode(which)
+                if rec is not None:
+                    rec["enc_end"].record(s)
+            if rec is not None:
+                rec["dec_start"].record(s)
             self.base.base_decode(which)
+            if rec is not None:
+                rec["dec_end"].record(s)
             if on_step is not None:
                 on_step(step, self.latent_nchw().clone())
         sched.finish(s)

@@ -17,15 +17,13 @@ int lora_patch_simt(const sdb_lora_job* jobs_dev, const sdb_lora_job& one, int n
                     int64_t total_tiles, int w_dtype, int f_dtype, float sign, int max_ctas,
                     cudaStream_t st);
 // lora_patch_tc.cu
-int64_t tc_tiles(int64_t h1, int64_t h2);
-bool tc_supported(int w_dtype, int f_dtype, int max_rank);
-int lora_patch_tc(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles, float sign,
-                  int max_ctas, cudaStream_t st);
 void tc_pack_bytes(int64_t h1, int64_t h2, int rank, size_t* a_bytes, size_t* b_bytes);
 int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t h1, int64_t h2, int rank,
             void* a_out, void* b_out, cudaStream_t st);
 int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, void* a_out, void* b_out,
                   cudaStream_t st);
+int tc_pack_multi_layout(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, size_t* a_bytes,
+                         size_t* b_bytes, float* epi_scale, int32_t* lo_mask);
 int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_bytes, size_t* needed,
             int* n_units_out, int* kb_max_out);
 int tc_set_mode(int mode);
@@ -103,19 +101,19 @@ int sdb_lora_plan(sdb_lora_job* jobs, int n_jobs, int w_dtype, int f_dtype, int6
                   int* path_out) {
   if (n_jobs <= 0 || jobs == nullptr || total_tiles == nullptr)
     return fail(SDB_EINVAL, "sdb_lora_plan: no jobs");
-  int max_rank = 0;
-  for (int i = 0; i < n_jobs; ++i) {
+  (void)w_dtype;
+  (void)f_dtype;
+  for (int i = 0; i < n_jobs; ++i)
     if (int rc = check_job(jobs[i], i)) return rc;
-    max_rank = std::max(max_rank, (int)jobs[i].rank);
-  }
-  const int path = tc_supported(w_dtype, f_dtype, max_rank) ? 1 : 0;
+  // the job-table API runs the generic SIMT kernel (any dtype, any stride);
+  // the tcgen05 path has its own packed-factor plan (sdb_lora_tc_plan)
   int64_t t = 0;
   for (int i = 0; i < n_jobs; ++i) {
     jobs[i].tile_begin = t;
-    t += path ? tc_tiles(jobs[i].h1, jobs[i].h2) : simt_tiles(jobs[i].h1, jobs[i].h2);
+    t += simt_tiles(jobs[i].h1, jobs[i].h2);
   }
   *total_tiles = t;
-  if (path_out) *path_out = path;
+  if (path_out) *path_out = 0;
   return SDB_OK;
 }
 
@@ -123,11 +121,8 @@ int sdb_lora_patch(const sdb_lora_job* jobs_dev, int n_jobs, int64_t total_tiles
                    int f_dtype, int path, float sign, int max_ctas, void* stream) {
   if (n_jobs <= 0 || jobs_dev == nullptr) return fail(SDB_EINVAL, "sdb_lora_patch: no jobs");
   if (total_tiles <= 0) return fail(SDB_EINVAL, "sdb_lora_patch: plan has no tiles");
-  if (path == 1) {
-    if (!(w_dtype == SDB_BF16 && f_dtype == SDB_BF16))
-      return fail(SDB_EUNSUP, "sdb_lora_patch: tcgen05 path needs bf16 weights and factors");
-    return lora_patch_tc(jobs_dev, n_jobs, total_tiles, sign, max_ctas, as_stream(stream));
-  }
+  if (path != 0)
+    return fail(SDB_EUNSUP, "sdb_lora_patch: path 1 is planned by sdb_lora_tc_plan / run by sdb_lora_tc_patch");
   sdb_lora_job none;
   std::memset(&none, 0, sizeof(none));
   return lora_patch_simt(jobs_dev, none, n_jobs, total_tiles, w_dtype, f_dtype, sign, max_ctas,
@@ -173,6 +168,12 @@ int sdb_lora_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, in
 int sdb_lora_pack_multi(const sdb_lora_src* srcs_host, int n_src, int64_t h1, int64_t h2, void* a_packed,
                         void* b_packed, void* stream) {
   return tc_pack_multi(srcs_host, n_src, h1, h2, a_packed, b_packed, as_stream(stream));
+}
+
+int sdb_lora_pack_multi_layout(const sdb_lora_src* srcs_host, int n_src, int64_t h1, int64_t h2, size_t* a_bytes,
+                               size_t* b_bytes, float* epi_scale, int32_t* lo_mask) {
+  if (h1 <= 0 || h2 <= 0) return fail(SDB_EINVAL, "sdb_lora_pack_multi_layout: bad shape");
+  return tc_pack_multi_layout(srcs_host, n_src, h1, h2, a_bytes, b_bytes, epi_scale, lo_mask);
 }
 
 int sdb_lora_tc_plan(const sdb_lora_tc_job* jobs_host, int n_jobs, void* blob_host, size_t blob_bytes,

@@ -17,7 +17,7 @@ namespace {
 
 template <typename TE, typename TI>
 __global__ void __launch_bounds__(256)
-cfg_ddim_kernel(const TE* __restrict__ eps, const float* __restrict__ x, float* __restrict__ x_out,
+cfg_ddim_kernel(const TE* __restrict__ eps, const float* x, float* x_out,   // x_out may alias x (in place)
                 TI* __restrict__ unet_in, int64_t L, const float* __restrict__ coef,
                 int* __restrict__ step_dev) {
   const int step = *reinterpret_cast<volatile int*>(step_dev);

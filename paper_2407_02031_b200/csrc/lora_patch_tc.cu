@@ -59,15 +59,25 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN
                             ((uint32_t)(kBM >> 4) << 24);   // f32 accum, bf16 A/B, K-major, 128x256
 
 struct TcJob {
-  const uint8_t* a;   // packed A: [m_tiles][kb][128 rows][128 B]
+  const uint8_t* a;   // packed A: [m_tiles][akb][128 rows][128 B]
   const uint8_t* b;   // packed B: [n_tiles][kb][256 rows][128 B]
   int64_t h1, h2;
   int32_t kb, rank;
   float scale;
   int32_t map_in, map_out;
   int32_t map_a, map_b;   // tensor maps over the packed factors (CTA-pair kernel)
-  int32_t mt, pad;        // row tiles of W
+  int32_t mt;             // row tiles of W
+  int32_t akb;            // A K-blocks per row tile: kb high parts + the low parts (see lo_b)
+  uint32_t lo_b;          // byte i: the B K-block that A K-block kb + i (a low part) multiplies
+  int32_t pad;
 };
+
+// A K-block a of a tile multiplies B K-block b_of(J, a): the first kb blocks
+// are the (unscaled or high-part) stacked factors, the rest the low parts of
+// the scale-folded sources (hi/lo split, see the packing section)
+__device__ __forceinline__ int b_of(const TcJob& J, int a) {
+  return a < J.kb ? a : (int)((J.lo_b >> (8 * (a - J.kb))) & 0xFF);
+}
 struct TcUnit {
   int32_t job, n_tile, m_begin, m_end;
 };
@@ -172,10 +182,10 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         }
         ++b_cnt;
         for (int m = un.m_begin; m < un.m_end; ++m) {
-          for (int kb = 0; kb < J.kb; ++kb) {
+          for (int kb = 0; kb < J.akb; ++kb) {
             if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
             mbar_expect_tx(bar(A_FULL + a_st), kABlockBytes);
-            bulk_g2s(smem_u32(sA + a_st * kABlockBytes), J.a + ((size_t)m * J.kb + kb) * kABlockBytes, kABlockBytes,
+            bulk_g2s(smem_u32(sA + a_st * kABlockBytes), J.a + ((size_t)m * J.akb + kb) * kABlockBytes, kABlockBytes,
                      bar(A_FULL + a_st), keep);
             if (++a_st == kAStages) { a_st = 0; ++a_round; }
           }
@@ -215,20 +225,20 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
         const int nks = (J.rank + 15) / 16;     // K steps of 16 (zero-padded)
-        const int nkb = (J.rank + kKB - 1) / kKB;
         mbar_wait(bar(B_FULL), b_cnt & 1);
         for (int m = un.m_begin; m < un.m_end; ++m, ++tile) {
           const int buf = tile & 1;
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           const uint32_t d = tmem_base + buf * BN;
-          for (int kb = 0; kb < nkb; ++kb, ++a_cnt) {
+          for (int kb = 0; kb < J.akb; ++kb, ++a_cnt) {
             const int st = a_cnt & (kAStages - 1);
             mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
             tc_fence_after();
-            const int ks_end = std::min(4, nks - kb * 4);
+            const int bb = b_of(J, kb);
+            const int ks_end = std::min(4, nks - bb * 4);
             for (int ks = 0; ks < ks_end; ++ks) {
               const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
-              const uint64_t bd = sw128_desc(smem_u32(sB + kb * kPanelBlock + ks * 32));
+              const uint64_t bd = sw128_desc(smem_u32(sB + bb * kPanelBlock + ks * 32));
               tc_mma(d, ad, bd, kIdescBN, (kb | ks) ? 1u : 0u);
             }
             tc_commit(bar(A_EMPTY + st));       // stage free once these MMAs completed
@@ -443,10 +453,10 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
         for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2) {
           // past the last row tile the follower multiplies a valid (ignored) A tile
           const int mload = std::min(m0 + (int)cta, J.mt - 1);
-          for (int kb = 0; kb < J.kb; ++kb) {
+          for (int kb = 0; kb < J.akb; ++kb) {
             if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
             if (leader) mbar_expect_tx(bar(A_FULL + a_st), 2 * kABlockBytes);
-            tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.kb + kb) * kBM,
+            tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.akb + kb) * kBM,
                              mapa_shared(bar(A_FULL + a_st), 0), keep);
             if (++a_st == na) { a_st = 0; ++a_round; }
           }
@@ -497,15 +507,16 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem_base + buf * kBN;
-          for (int kb = 0; kb < J.kb; ++kb) {
+          for (int kb = 0; kb < J.akb; ++kb) {
             const int st = a_st;
             mbar_wait(bar(A_FULL + st), a_round & 1);
             if (++a_st == na) { a_st = 0; ++a_round; }
             tc_fence_after();
-            const int ks_end = std::min(4, nks - kb * 4);
+            const int bb = b_of(J, kb);
+            const int ks_end = std::min(4, nks - bb * 4);
             for (int ks = 0; ks < ks_end; ++ks) {
               const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
-              const uint64_t bd = sw128_desc(smem_u32(sB + kb * kHalfBlock + ks * 32));
+              const uint64_t bd = sw128_desc(smem_u32(sB + bb * kHalfBlock + ks * 32));
               tc_mma2(d, ad, bd, kIdesc2, (kb | ks) ? 1u : 0u);
             }
             tc_commit2(bar(A_EMPTY + st));
@@ -590,15 +601,70 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
 // Multi-source packing: the stacked adapter set (lora.py:147-160: down' =
 // [d_1*f32(s_1) | d_2*f32(s_2) ...], up' = [u_1; u_2 ...]) is assembled while
 // packing, straight from each adapter's own factor buffers — no stacked copy.
+//
+// Exact scales.  Folding s_k into a bf16 A operand would round s_k*d a second
+// time (2^-9 relative per factor element) — where W + delta nearly cancels
+// that is many bf16 ulps of the result.  Instead the scale carried by the
+// largest share of the stacked rank (s_e) is applied in the fp32 epilogue and
+// its sources are packed unscaled (exact); every other source is packed as
+// x = f32(d) * f32(s_k / s_e) split into hi = bf16(x) (in the stacked K-blocks)
+// and lo = bf16(x - hi) (in an extra A K-block that multiplies the SAME B
+// K-block, see b_of): hi + lo carries x to 2^-17 relative.  Only B K-blocks
+// that hold a folded source get a low block, so equal scales (the serving
+// case: every adapter at one strength) cost nothing extra.
 constexpr int kMaxSrc = 8;
 struct PackSrcs {
   const __nv_bfloat16* down[kMaxSrc];
   const __nv_bfloat16* up[kMaxSrc];
   int64_t ldd[kMaxSrc], ldu[kMaxSrc];
   int koff[kMaxSrc + 1];   // prefix sums of the ranks
-  float scale[kMaxSrc];
+  float fold[kMaxSrc];     // s_k / s_e (exactly 1 for the epilogue-scaled sources)
   int n;
+  int kb;                  // stacked K-blocks (high parts)
+  uint32_t lo_b;           // byte i: the K-block whose low part is A K-block kb + i
 };
+
+struct MultiLayout {
+  float epi_scale;
+  float fold[kMaxSrc];
+  int rank, kb, nlo;
+  uint32_t lo_mask, lo_b;
+};
+
+int multi_layout(const sdb_lora_src* srcs, int n, MultiLayout* L) {
+  if (n < 1 || n > kMaxSrc || !srcs) return fail(SDB_EINVAL, "lora_pack_multi: 1..8 sources");
+  L->rank = 0;
+  for (int i = 0; i < n; ++i) {
+    if (srcs[i].rank < 1) return fail(SDB_EINVAL, "lora_pack_multi: source " + std::to_string(i) + ": bad rank");
+    L->rank += srcs[i].rank;
+  }
+  if (L->rank > kMaxKB * kKB) return fail(SDB_EINVAL, "lora_pack_multi: stacked rank must be <= 256");
+  // epilogue scale: the nonzero scale with the largest total rank (first on ties)
+  float best = 0.f;
+  int best_r = 0;
+  for (int i = 0; i < n; ++i) {
+    if (srcs[i].scale == 0.f) continue;
+    int r = 0;
+    for (int j = 0; j < n; ++j)
+      if (srcs[j].scale == srcs[i].scale) r += srcs[j].rank;
+    if (r > best_r) { best_r = r; best = srcs[i].scale; }
+  }
+  L->epi_scale = best;
+  L->kb = (L->rank + kKB - 1) / kKB;
+  L->lo_mask = 0;
+  int k0 = 0;
+  for (int i = 0; i < n; ++i) {
+    L->fold[i] = best == 0.f ? 1.f : srcs[i].scale / best;
+    if (L->fold[i] != 1.f)
+      for (int b = k0 / kKB; b <= (k0 + srcs[i].rank - 1) / kKB; ++b) L->lo_mask |= 1u << b;
+    k0 += srcs[i].rank;
+  }
+  L->nlo = 0;
+  L->lo_b = 0;
+  for (int b = 0; b < L->kb; ++b)
+    if (L->lo_mask >> b & 1u) L->lo_b |= (uint32_t)b << (8 * L->nlo++);
+  return SDB_OK;
+}
 
 __device__ __forceinline__ int src_of(const PackSrcs& s, int k) {
   int i = 0;
@@ -606,17 +672,19 @@ __device__ __forceinline__ int src_of(const PackSrcs& s, int k) {
   return i;
 }
 
-__global__ void pack_a_multi_kernel(PackSrcs s, int64_t h1, int kbt, int64_t mt, uint4* __restrict__ out) {
+__global__ void pack_a_multi_kernel(PackSrcs s, int64_t h1, int akb, int64_t mt, uint4* __restrict__ out) {
   const int rank = s.koff[s.n];
-  const int64_t total = mt * kbt * kBM * 8;
+  const int64_t total = mt * akb * kBM * 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i & 7);
-    const int64_t rowi = i >> 3;                // (m*kbt + kb)*128 + r
+    const int64_t rowi = i >> 3;                // (m*akb + a)*128 + r
     const int r = (int)(rowi % kBM);
     const int64_t mk = rowi / kBM;
-    const int kb = (int)(mk % kbt);
-    const int64_t m = mk / kbt;
+    const int a = (int)(mk % akb);
+    const int64_t m = mk / akb;
     const int64_t row = m * kBM + r;
+    const bool low = a >= s.kb;
+    const int kb = low ? (int)((s.lo_b >> (8 * (a - s.kb))) & 0xFF) : a;
     const int k0 = kb * kKB + c * 8;
     __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
@@ -625,8 +693,8 @@ __global__ void pack_a_multi_kernel(PackSrcs s, int64_t h1, int kbt, int64_t mt,
       float x = 0.f;
       if (row < h1 && k < rank) {
         const int si = src_of(s, k);
-        // f32(d) * f32(s), rounded once to bf16 (the reference folds in fp32)
-        x = __bfloat162float(s.down[si][row * s.ldd[si] + (k - s.koff[si])]) * s.scale[si];
+        x = __bfloat162float(s.down[si][row * s.ldd[si] + (k - s.koff[si])]) * s.fold[si];
+        if (low) x -= __bfloat162float(__float2bfloat16_rn(x));   // exactly 0 for fold == 1
       }
       v[e] = __float2bfloat16_rn(x);
     }
@@ -772,9 +840,21 @@ int tc_pack(const void* down, int64_t ldd, const void* up, int64_t ldu, int64_t 
   return check_launch("pack_b_kernel");
 }
 
+int tc_pack_multi_layout(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, size_t* a_bytes,
+                         size_t* b_bytes, float* epi_scale, int32_t* lo_mask) {
+  MultiLayout L;
+  if (int rc = multi_layout(srcs, n_src, &L)) return rc;
+  if (a_bytes) *a_bytes = (size_t)((h1 + kBM - 1) / kBM) * (L.kb + L.nlo) * kABlockBytes;
+  if (b_bytes) *b_bytes = (size_t)((h2 + kBN - 1) / kBN) * L.kb * kBBlockBytes;
+  if (epi_scale) *epi_scale = L.epi_scale;
+  if (lo_mask) *lo_mask = (int32_t)L.lo_mask;
+  return SDB_OK;
+}
+
 int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, void* a_out, void* b_out,
                   cudaStream_t st) {
-  if (n_src < 1 || n_src > kMaxSrc || !srcs) return fail(SDB_EINVAL, "lora_pack_multi: 1..8 sources");
+  MultiLayout L;
+  if (int rc = multi_layout(srcs, n_src, &L)) return rc;
   if (((uintptr_t)a_out | (uintptr_t)b_out) & 1023)
     return fail(SDB_EINVAL, "lora_pack_multi: outputs must be 1024-B aligned");
   PackSrcs s;
@@ -782,25 +862,25 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
   s.n = n_src;
   s.koff[0] = 0;
   for (int i = 0; i < n_src; ++i) {
-    if (!srcs[i].down || !srcs[i].up || srcs[i].rank < 1 || srcs[i].ldd < srcs[i].rank || srcs[i].ldu < h2)
-      return fail(SDB_EINVAL, "lora_pack_multi: source " + std::to_string(i) + ": bad pointer / rank / stride");
+    if (!srcs[i].down || !srcs[i].up || srcs[i].ldd < srcs[i].rank || srcs[i].ldu < h2)
+      return fail(SDB_EINVAL, "lora_pack_multi: source " + std::to_string(i) + ": bad pointer / stride");
     s.down[i] = static_cast<const __nv_bfloat16*>(srcs[i].down);
     s.up[i] = static_cast<const __nv_bfloat16*>(srcs[i].up);
     s.ldd[i] = srcs[i].ldd;
     s.ldu[i] = srcs[i].ldu;
-    s.scale[i] = srcs[i].scale;
+    s.fold[i] = L.fold[i];
     s.koff[i + 1] = s.koff[i] + srcs[i].rank;
   }
-  const int rank = s.koff[n_src];
-  if (rank > kMaxKB * kKB) return fail(SDB_EINVAL, "lora_pack_multi: stacked rank must be <= 256");
-  const int kbt = tc_kb(rank);
+  s.kb = L.kb;
+  s.lo_b = L.lo_b;
+  const int akb = L.kb + L.nlo;
   const int64_t mt = (h1 + kBM - 1) / kBM, nt = (h2 + kBN - 1) / kBN;
-  const int64_t na = mt * kbt * kBM * 8, nb = nt * kbt * 8 * kBN;
+  const int64_t na = mt * akb * kBM * 8, nb = nt * L.kb * 8 * kBN;
   pack_a_multi_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 65535), 256, 0, st>>>(
-      s, h1, kbt, mt, static_cast<uint4*>(a_out));
+      s, h1, akb, mt, static_cast<uint4*>(a_out));
   if (int rc = check_launch("pack_a_multi_kernel")) return rc;
   pack_b_multi_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 65535), 256, 0, st>>>(
-      s, h2, kbt, nt, static_cast<uint4*>(b_out));
+      s, h2, L.kb, nt, static_cast<uint4*>(b_out));
   return check_launch("pack_b_multi_kernel");
 }
 
@@ -829,11 +909,14 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
             int* kb_max_out) {
   if (n_jobs <= 0 || !jobs) return fail(SDB_EINVAL, "lora_tc_plan: no jobs");
   std::vector<TcUnit> units;
-  int kb_max = 1;
+  int kb_max = 1, akb_max = 1;
   for (int j = 0; j < n_jobs; ++j) {
     const sdb_lora_tc_job& J = jobs[j];
     if (J.h1 <= 0 || J.h2 <= 0 || J.rank < 1 || J.rank > kMaxKB * kKB)
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": bad shape or rank (1..256)");
+    if ((uint32_t)J.lo_mask >> tc_kb(J.rank))
+      return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": lo_mask names a K block past the rank");
+    akb_max = std::max(akb_max, tc_kb(J.rank) + __builtin_popcount((uint32_t)J.lo_mask));
     if (J.ldw % 8 != 0 || ((uintptr_t)J.w_in & 15) || ((uintptr_t)J.w_out & 15))
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": W rows must be 16-B aligned (ldw % 8 == 0)");
     if (((uintptr_t)J.a_packed | (uintptr_t)J.b_packed) & 1023)
@@ -892,7 +975,7 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
   const size_t need = maps_b + jobs_b + units_b;
   if (needed) *needed = need;
   if (n_units_out) *n_units_out = (int)units.size();
-  if (kb_max_out) *kb_max_out = kb_max | (mode << 8);
+  if (kb_max_out) *kb_max_out = kb_max | (mode << 8) | (akb_max << 12);
   if (!blob) return SDB_OK;
   if (blob_bytes < need) return fail(SDB_EINVAL, "lora_tc_plan: blob too small");
   uint8_t* base = static_cast<uint8_t*>(blob);
@@ -901,11 +984,15 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
   for (int j = 0; j < n_jobs; ++j) {
     const sdb_lora_tc_job& J = jobs[j];
     const int kb = tc_kb(J.rank);
+    int nlo = 0;
+    uint32_t lo_b = 0;
+    for (int b = 0; b < kb; ++b)
+      if ((uint32_t)J.lo_mask >> b & 1u) lo_b |= (uint32_t)b << (8 * nlo++);
     const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + kBN - 1) / kBN;
     // loads move whole 128-row boxes; each epilogue warp stores its own 32 rows
     if (int rc = make_w_map(&maps[4 * j], J.w_in, J.h1, J.h2, J.ldw, kBM)) return rc;
     if (int rc = make_w_map(&maps[4 * j + 1], J.w_out, J.h1, J.h2, J.ldw, 32)) return rc;
-    if (int rc = make_f_map(&maps[4 * j + 2], J.a_packed, mt * kb * kBM)) return rc;
+    if (int rc = make_f_map(&maps[4 * j + 2], J.a_packed, mt * (kb + nlo) * kBM)) return rc;
     if (int rc = make_f_map(&maps[4 * j + 3], J.b_packed, nt * kb * kBN)) return rc;
     std::memset(&tj[j], 0, sizeof(TcJob));
     tj[j].a = static_cast<const uint8_t*>(J.a_packed);
@@ -920,6 +1007,8 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
     tj[j].map_a = 4 * j + 2;
     tj[j].map_b = 4 * j + 3;
     tj[j].mt = (int32_t)mt;
+    tj[j].akb = kb + nlo;
+    tj[j].lo_b = lo_b;
   }
   std::memcpy(base + maps_b + jobs_b, units.data(), units_b);
   return SDB_OK;
@@ -934,7 +1023,7 @@ int tc_set_mode(int mode) {
 
 int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int simt_rank, float sign, int max_ctas,
              cudaStream_t st) {
-  const int kb_max = kb_word & 0xFF, mode = kb_word >> 8;
+  const int kb_max = kb_word & 0xFF, mode = (kb_word >> 8) & 0xF, akb_max = std::max(kb_max, kb_word >> 12);
   if (!blob_dev || n_units <= 0) return fail(SDB_EINVAL, "lora_tc_patch: empty plan");
   if (((uintptr_t)blob_dev) & 127) return fail(SDB_EINVAL, "lora_tc_patch: blob must be 128-B aligned");
   if (kb_max < 1 || kb_max > kMaxKB) return fail(SDB_EINVAL, "lora_tc_patch: kb_max out of range");
@@ -944,14 +1033,14 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int sim
   const CUtensorMap* maps = reinterpret_cast<const CUtensorMap*>(base);
   const TcJob* jobs = reinterpret_cast<const TcJob*>(base + maps_b);
   const TcUnit* units = reinterpret_cast<const TcUnit*>(base + maps_b + (size_t)n_jobs * sizeof(TcJob));
-  (void)simt_rank;  // the FFMA variant was retired: tcgen05 wins at every rank (profiles/)
+  (void)simt_rank;  // reserved (ABI): the FFMA variant was retired, tcgen05 wins at every rank (profiles/)
   const int max_smem = 227 * 1024;
   if (mode == 2) {
     // A K-blocks in flight = the K blocks of one tile (2..4): a tile's MMAs
     // consume them in sequence, so at high rank a deeper A ring beats the
     // last W slots (round 1, R = 232: 4 stages + 6 slots 2.04 ms = 89% of the
     // copy peak vs 2 stages + 8 slots 2.42 ms; R <= 128: 2 stages best)
-    const int na = std::min(4, std::max(2, kb_max));
+    const int na = std::min(4, std::max(2, akb_max));
     const int fixed = 1024 + kb_max * kHalfBlock + na * kABlockBytes + 320;
     const int slots = std::min(kMaxSlots, (max_smem - fixed) / kBoxBytes);
     const int smem = fixed + slots * kBoxBytes;
@@ -988,13 +1077,6 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int sim
   cudaFuncSetAttribute(lora_patch_tma_kernel<kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   lora_patch_tma_kernel<kBN><<<grid, kThreads, smem, st>>>(maps, jobs, units, n_units, sign, kb_max, slots);
   return check_launch("lora_patch_tma_kernel");
-}
-
-// legacy entry points used by sdb_lora_plan / sdb_lora_patch (SIMT job tables)
-int64_t tc_tiles(int64_t h1, int64_t h2) { return ((h1 + kBM - 1) / kBM) * ((h2 + kBN - 1) / kBN); }
-bool tc_supported(int, int, int) { return false; }
-int lora_patch_tc(const sdb_lora_job*, int, int64_t, float, int, cudaStream_t) {
-  return fail(SDB_EUNSUP, "use sdb_lora_tc_plan / sdb_lora_tc_patch for the tcgen05 path");
 }
 
 }  // namespace sdb

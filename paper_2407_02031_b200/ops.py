@@ -184,8 +184,9 @@ class LoraTmaPlan:
 
     entries: (w_in, w_out or None, down (h1, R) bf16, up (R, h2) bf16, scale)
     or (w_in, w_out or None, [(down_i, up_i, s_i), ...], None, scale) — the
-    adapters of a stack given separately: they are stacked (scales folded,
-    lora.py:147-160) while packing, straight from their own buffers.  Every
+    adapters of a stack given separately: they are stacked (lora.py:147-160)
+    while packing, straight from their own buffers, with the scales kept
+    exact (epilogue scale + hi/lo split of the others, sdb_lora_pack_multi).  Every
     w_in must satisfy ``tma_eligible``.  ``repack(stream)`` re-runs the
     packing from the same factor buffers (after they were refreshed, e.g. by
     an async host-to-device fetch)."""
@@ -199,7 +200,8 @@ class LoraTmaPlan:
         self.alg_bytes = 0
         self.alg_flops = 0
         self.max_rank = 0
-        self._srcs = []      # per job: (ctypes sdb_lora_src array, n, h1, h2)
+        self._srcs = []      # per job: (ctypes sdb_lora_src array, n, h1, h2, a, b)
+        self._keep = []
         norm = []
         for i, (w_in, w_out, down, up, scale) in enumerate(entries):
             out = w_in if w_out is None else w_out
@@ -208,20 +210,28 @@ class LoraTmaPlan:
                 raise ValidationError(f"job {i}: weight is not TMA-eligible (bf16, ldw % 8 == 0)")
             h1, h2 = w_in.shape
             r = 0
-            for d, u, _ in srcs:
+            arr = (_lib.LoraSrc * len(srcs))()
+            for k, (d, u, s) in enumerate(srcs):
                 require_cuda(w_in, out, d, u)
                 if d.dtype != torch.bfloat16 or u.dtype != torch.bfloat16:
                     raise ValidationError(f"job {i}: factors must be bf16 on the TMA path")
                 if d.shape[0] != h1 or u.shape != (d.shape[1], h2):
                     raise ValidationError(f"job {i}: factor shapes do not match weight ({h1}, {h2})")
                 r += d.shape[1]
+                arr[k].down, arr[k].ldd = d.data_ptr(), _row_stride(d, "down")
+                arr[k].up, arr[k].ldu = u.data_ptr(), _row_stride(u, "up")
+                arr[k].rank, arr[k].scale = d.shape[1], float(s)
+                self._keep += [d, u]
+            # packed sizes, the epilogue scale and the hi/lo K blocks of this stack
             a_b, b_b = ctypes.c_size_t(0), ctypes.c_size_t(0)
-            _lib.check("sdb_lora_pack_bytes", lib.sdb_lora_pack_bytes(h1, h2, r, ctypes.byref(a_b), ctypes.byref(b_b)))
+            epi, lo = ctypes.c_float(0), ctypes.c_int32(0)
+            _lib.check("sdb_lora_pack_multi_layout", lib.sdb_lora_pack_multi_layout(
+                arr, len(srcs), h1, h2, ctypes.byref(a_b), ctypes.byref(b_b), ctypes.byref(epi), ctypes.byref(lo)))
             sizes.append((a_b.value, b_b.value))
             self.alg_bytes += 2 * h1 * h2 * 2 + (h1 + h2) * r * 2
             self.alg_flops += 2 * h1 * h2 * r
             self.max_rank = max(self.max_rank, r)
-            norm.append((w_in, out, srcs, r, scale))
+            norm.append((w_in, out, arr, len(srcs), r, float(scale) * epi.value, lo.value))
         # one arena, every packed block 1024-B aligned
         offs, total = [], 0
         for a_b, b_b in sizes:
@@ -230,22 +240,15 @@ class LoraTmaPlan:
         self.arena = torch.empty(total + 1024, dtype=torch.uint8, device=dev)
         base = (self.arena.data_ptr() + 1023) // 1024 * 1024
         jobs = (_lib.LoraTcJob * len(entries))()
-        self._keep = []
-        for i, (w_in, out, srcs, r, scale) in enumerate(norm):
+        for i, (w_in, out, arr, n_src, r, scale, lo_mask) in enumerate(norm):
             h1, h2 = w_in.shape
             a_ptr, b_ptr = base + offs[i][0], base + offs[i][1]
-            arr = (_lib.LoraSrc * len(srcs))()
-            for k, (d, u, s) in enumerate(srcs):
-                arr[k].down, arr[k].ldd = d.data_ptr(), _row_stride(d, "down")
-                arr[k].up, arr[k].ldu = u.data_ptr(), _row_stride(u, "up")
-                arr[k].rank, arr[k].scale = d.shape[1], float(s)
-                self._keep += [d, u]
-            self._srcs.append((arr, len(srcs), h1, h2, a_ptr, b_ptr))
+            self._srcs.append((arr, n_src, h1, h2, a_ptr, b_ptr))
             j = jobs[i]
             j.w_in, j.w_out = w_in.data_ptr(), out.data_ptr()
             j.h1, j.h2, j.ldw = h1, h2, _row_stride(w_in, "weight")
             j.a_packed, j.b_packed = a_ptr, b_ptr
-            j.rank, j.scale = r, float(scale)
+            j.rank, j.scale, j.lo_mask = r, scale, lo_mask
             self._keep += [w_in, out]
         self.repack(stream)
         need, n_units, kb_max = ctypes.c_size_t(0), ctypes.c_int(0), ctypes.c_int(0)
@@ -258,10 +261,9 @@ class LoraTmaPlan:
         self.blob = torch.frombuffer(bytearray(bytes(host)), dtype=torch.uint8).to(dev)
         self.n_jobs = len(entries)
         self.n_units = n_units.value
-        self.kb_max = kb_max.value                 # opaque: kb | kernel << 8
-        self.kernel = "pair" if (self.kb_max >> 8) == 2 else "single"
-        self.simt_rank = self.max_rank if self.max_rank <= simt_max_rank else 0
-        self.simt_rank = 0
+        self.kb_max = kb_max.value                 # opaque: kb | kernel << 8 | A K-blocks << 12
+        self.kernel = "pair" if ((self.kb_max >> 8) & 0xF) == 2 else "single"
+        self.simt_rank = 0   # reserved in the ABI: tcgen05 at every rank
         self.path = 1   # 1 = TMA + tcgen05 (0 = the generic SIMT kernel of LoraPatchPlan)
 
     def repack(self, stream: Optional[torch.cuda.Stream] = None) -> None:
@@ -350,8 +352,9 @@ def groupnorm_silu(x: torch.Tensor, gamma: Optional[torch.Tensor], beta: Optiona
     if add_nc is not None and add_nc.numel() != n * c:
         raise ValidationError(f"add_nc must hold N*C = {n * c} values")
     pending = getattr(x, "_sdb_gn", None)
-    if pending is not None and pending[1] == groups and pending[2] == x.data_ptr():
+    if pending is not None and pending[1] == groups and pending[2] == x.data_ptr() and add_nc is None:
         # x's statistics were accumulated by the K3 pass that wrote it: apply only
+        # (not with add_nc: GroupNorm(x + add_nc) needs the statistics of the sum)
         _count(1)
         _lib.check("sdb_groupnorm_apply", _lib.lib().sdb_groupnorm_apply(
             x.data_ptr(), out.data_ptr(), gamma.data_ptr() if gamma is not None else None,
@@ -593,6 +596,10 @@ def cfg_ddim_step(eps: torch.Tensor, x: torch.Tensor, coef: torch.Tensor, step_d
         raise ValidationError("eps must hold the [uncond; cond] batch of 2 latents")
     if unet_in is not None and unet_in.numel() != 2 * L:
         raise ValidationError("unet_in must hold 2 latents")
+    # the master latent is NHWC-flat: eps / unet_in must be stored NHWC too
+    for name, t in (("eps", eps), ("unet_in", unet_in)):
+        if t is not None and t.dim() == 4 and not t.is_contiguous(memory_format=torch.channels_last):
+            raise ValidationError(f"{name} must be channels_last (NHWC) like the latent")
     out = x if x_out is None else x_out
     _count(1)
     _lib.check("sdb_cfg_ddim_step", _lib.lib().sdb_cfg_ddim_step(

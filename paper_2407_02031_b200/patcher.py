@@ -109,7 +109,10 @@ class PatchSet:
 
     def __init__(self, params: Params, adapters: Sequence[tuple[UNetLora, float]],
                  shadow: Optional[dict] = None, use_tma: bool = True, simt_max_rank: int = 0,
-                 only: Optional[set] = None):
+                 only: Optional[set] = None, in_place_on_shadow: bool = False):
+        """shadow: write W + delta there (out of place).  in_place_on_shadow:
+        patch the shadow weights in place instead (W_shadow += sign * delta —
+        the reference's merge / unmerge on a serving copy; micro-bench)."""
         if not adapters:
             raise ValidationError("PatchSet needs at least one adapter")
         self.params = params
@@ -131,6 +134,8 @@ class PatchSet:
             if shadow is not None:
                 w_out = shadow[name].permute(0, 2, 3, 1).reshape(w_in.shape) if shadow[name].dim() == 4 \
                     else shadow[name]
+                if in_place_on_shadow:
+                    w_in, w_out = w_out, None
             ups = [a.factors[name][1] if a.up_physical else physical_up(params, name, a.factors[name][1])
                    for a, _ in present]
             if (use_tma and self.rank <= 256 and ops.tma_eligible(w_in)
@@ -140,10 +145,10 @@ class PatchSet:
                 fast.append((w_in, w_out, srcs, None, 1.0))
             else:
                 # everything else (e.g. SDXL conv_in, 320 x 36): the generic kernel on a
-                # stacked copy — lora.py:153 folds f32(s) into down in fp32, one rounding
+                # stacked copy (lora.py:147-160; see _stack for how the scales stay exact)
                 self.stacked[name] = self._stack(name, present, ups)
                 down, up = self.stacked[name]
-                slow.append((w_in, w_out, down, up, 1.0))
+                slow.append((w_in, w_out, down, up, self._epi_scale(name, present)))
         self._slow_src = {n: [(a, s) for a, s in adapters if n in a.factors] for n in self.stacked}
         self.plans = []
         if fast:
@@ -152,15 +157,57 @@ class PatchSet:
             self.plans.append(ops.LoraPatchPlan(slow))
         self.plan = self.plans[0]
 
+    @staticmethod
+    def _epi_scale(name, present) -> float:
+        """The job scale of a stacked copy: 1.0 for fp32 factors (lora.py:153
+        folds every f32(s) into down in fp32 — the reference's own rounding);
+        for bf16 factors the nonzero scale carried by the largest share of the
+        rank (first on ties), applied in the kernel's fp32 epilogue — the
+        same choice sdb_lora_pack_multi makes."""
+        if present[0][0].factors[name][0].dtype == torch.float32:
+            return 1.0
+        share = {}
+        for a, s in present:
+            s32 = float(np.float32(s))
+            if s32 != 0.0:
+                share[s32] = share.get(s32, 0) + a.factors[name][0].shape[1]
+        best = 0.0
+        for k, r in share.items():          # insertion order: first on ties
+            if best == 0.0 or r > share[best]:
+                best = k
+        return best
+
     def _stack(self, name, present, ups=None, out=None):
+        """(down', up') of lora.py:147-160.  fp32 factors: down' = [d_i * f32(s_i)]
+        exactly as the reference.  bf16 factors: a bf16 rounding of s_i * d_i
+        would add 2^-9 relative per element, so the sources at the epilogue
+        scale s_e go in unscaled and every other one as x = d_i * f32(s_i / s_e)
+        split into bf16 hi | lo columns (2^-17), with its up rows repeated."""
         if ups is None:
             ups = [a.factors[name][1] if a.up_physical else physical_up(self.params, name, a.factors[name][1])
                    for a, _ in present]
-        downs = [(a.factors[name][0].float() * np.float32(s)).to(a.factors[name][0].dtype) for a, s in present]
+        dtype = present[0][0].factors[name][0].dtype
+        downs, ups_out = [], []
+        if dtype == torch.float32:
+            downs = [a.factors[name][0].float() * np.float32(s) for a, s in present]
+            ups_out = list(ups)
+        else:
+            se = np.float32(self._epi_scale(name, present))
+            for (a, s), u in zip(present, ups):
+                d = a.factors[name][0]
+                fold = np.float32(1.0) if se == 0 else np.float32(np.float32(s) / se)
+                if fold == 1.0:
+                    downs.append(d)
+                    ups_out.append(u)
+                    continue
+                x = d.float() * float(fold)
+                hi = x.to(dtype)
+                downs += [hi, (x - hi.float()).to(dtype)]
+                ups_out += [u, u]
         if out is None:
-            return torch.cat(downs, dim=1).contiguous(), torch.cat(ups, dim=0).contiguous()
+            return torch.cat(downs, dim=1).contiguous(), torch.cat(ups_out, dim=0).contiguous()
         torch.cat(downs, dim=1, out=out[0])
-        torch.cat(ups, dim=0, out=out[1])
+        torch.cat(ups_out, dim=0, out=out[1])
         return out
 
     def refresh(self, stream: Optional[torch.cuda.Stream] = None) -> None:

@@ -153,6 +153,10 @@ class AddonPipeline:
         self.main_stream = torch.cuda.Stream(device=dev, priority=-1)
         self.patch_stream = torch.cuda.Stream(device=dev, priority=0)
         self.copy_stream = torch.cuda.Stream(device=dev, priority=0)
+        # this engine's own capture stream (library per-stream resources, e.g.
+        # the cuBLAS workspace, must not be shared with graphs that another
+        # engine may replay concurrently)
+        self.capture_stream = torch.cuda.Stream(device=dev)
         self.bank = None
         self.patch_graph = None
         self.shadow = None
@@ -224,7 +228,7 @@ class AddonPipeline:
         self._use_weights(which)
         s = torch.cuda.current_stream(self.device)
         self.step_dev.zero_()
-        side = torch.cuda.Stream(device=self.device)
+        side = self.capture_stream
         side.wait_stream(s)
         with torch.cuda.stream(side):
             for _ in range(2):
@@ -233,7 +237,7 @@ class AddonPipeline:
         self.step_dev.zero_()
         g = torch.cuda.CUDAGraph()
         c0 = ops.LAUNCHES["count"]
-        with torch.cuda.graph(g, pool=self.pool):
+        with torch.cuda.graph(g, pool=self.pool, stream=side):
             self.step_once()
         self.launches_per_step = ops.LAUNCHES["count"] - c0   # our kernels per replay
         if self.pool is None:

@@ -53,3 +53,26 @@ def test_footprint_accounting_cpu():
     a = L.LowRankAdapter("a", np.zeros((8, 2), np.float32), np.zeros((2, 6), np.float32))
     aug = L.AugmentedLayer(w.copy(), w.copy(), [(a, 1.0)])
     assert aug.nbytes == 2 * L.BaseLayer(w).nbytes + a.nbytes
+
+
+def test_errors_derive_from_the_reference_when_installed():
+    """With the reference importable (baseline/_ref, the drop-in setting), a
+    caller catching addonsim.errors.ValidationError catches ours too."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    ref = root / "baseline" / "_ref"
+    if not (ref / "addonsim").exists():
+        pytest.skip("reference not installed in baseline/_ref")
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "import addonsim.errors as A\n"
+            "from paper_2407_02031_b200 import errors as E\n"
+            "assert issubclass(E.ValidationError, A.ValidationError)\n"
+            "assert issubclass(E.ValidationError, E.AddonSimError)\n"
+            "assert issubclass(E.AddonSimError, A.AddonSimError)\n"
+            "try:\n    raise E.ValidationError('rank mismatch')\n"
+            "except A.ValidationError as e:\n    print('caught', e)\n") % (str(ref), str(root))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "caught rank mismatch" in out.stdout

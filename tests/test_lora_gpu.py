@@ -358,3 +358,57 @@ def test_tma_pair_and_single_kernels_agree():
         diff = (a.float() - b.float()).abs()
         ulp = torch.maximum(a.float().abs(), b.float().abs()) * 2.0 ** -7
         assert bool((diff <= ulp + 1e-30).all())
+
+
+def _stacked_inventory_parity(ranks, scales, seed):
+    """Every patchable SDXL matrix (794, bf16 N(0, 0.02^2)), adapters stacked
+    by PatchSet exactly as the serving path packs them (sdb_lora_pack_multi:
+    per-adapter factor buffers, per-adapter scales), one K1 launch into the
+    shadow weights; each matrix against lora_ref.stack + accumulate_bf16 on
+    the LOGICAL (Cout, Cin*kh*kw) layout (lora.py:147-160, :84-95)."""
+    from paper_2407_02031_b200 import unet as U
+    from paper_2407_02031_b200.patcher import PatchSet, allocate_shadow, synthetic_lora
+    params = U.init_unet(U.SDXL, "cuda", torch.bfloat16, seed=0)
+    los = [synthetic_lora(params, r, seed=seed + i, adapter_id=f"a{i}", down_std=1.0, up_std=1.0)
+           for i, r in enumerate(ranks)]
+    shadow = allocate_shadow(params)
+    ps = PatchSet(params, list(zip(los, scales)), shadow=shadow)
+    ps.launch()
+    torch.cuda.synchronize()
+    R = sum(ranks)
+    worst, n_el, n_over = 0.0, 0, 0
+    for name, _ in params.matrices:
+        w = params.t[name + ".weight"]
+        cout = w.shape[0]
+        wl = w.float().cpu().reshape(cout, -1).numpy()
+        got = shadow[name].float().cpu().reshape(cout, -1).numpy()
+        trip = [(lo.factors[name][0].float().cpu().numpy(), lo.factors[name][1].float().cpu().numpy(), s)
+                for lo, s in zip(los, scales)]
+        down, up = lora_ref.stack(trip)
+        exp = lora_ref.accumulate_bf16(wl, down, up, 1.0, 1.0)
+        ulp = lora_ref.bf16_ulp(exp)
+        terms = np.abs(wl) + np.abs(down) @ np.abs(up)
+        # 1 bf16 ulp + the fp32 dot-product bound (+ 2^-16 relative for the
+        # hi/lo bf16 split of a scale-folded source, lora_patch_tc.cu)
+        tol = ulp + (R * 2.0 ** -24 + 2.0 ** -16) * terms
+        err = np.abs(got - exp)
+        worst = max(worst, float((err / ulp).max()))
+        n_over += int((err > ulp).sum())
+        n_el += err.size
+        assert not (err > tol).any(), (name, int((err > tol).sum()), float((err / ulp).max()))
+    print(f"stacked K1 ranks={ranks} scales={scales}: {n_el} elements, max {worst:.2f} ulp, "
+          f"{n_over} over 1 ulp")
+    # over 1 ulp only where the result nearly cancels (|W + delta| << its
+    # terms): equal scales ~4e-6 of the elements (fp32 accumulation only),
+    # distinct scales ~1.4e-4 (the 2^-17 hi/lo residual of the folded sources)
+    assert n_over <= (5e-4 if len(set(scales)) > 1 else 2e-5) * n_el
+
+
+def test_stacked_bench_adapters_all_sdxl_matrices():
+    """The headline's operand path: 2 LoRAs r64 at 0.7 (R = 128)."""
+    _stacked_inventory_parity((64, 64), (0.7, 0.7), seed=10)
+
+
+def test_stacked_config4_adapters_all_sdxl_matrices():
+    """Config 4: 4 LoRAs r 8/32/64/128 at four distinct scales (R = 232)."""
+    _stacked_inventory_parity((8, 32, 64, 128), (0.9, 0.55, 0.35, 1.3), seed=20)

@@ -81,8 +81,10 @@ def test_toy_bf16_per_step_parity():
                     matrices=pipe.unet_p.matrices, boundary=K, bf16_acts=True)
     errs = [rel_l2(a, b) for a, b in zip(dev, ref)]
     floor = [rel_l2(a, b) for a, b in zip(emu, ref)]
+    vs_emu = [rel_l2(a, b) for a, b in zip(dev, emu)]
     print("bf16 device  per-step rel-L2:", ["%.1e" % e for e in errs])
     print("bf16 emulated per-step rel-L2:", ["%.1e" % e for e in floor])
+    print("bf16 device vs emulator rel-L2:", ["%.1e" % e for e in vs_emu])
     assert max(errs) <= 2e-2
     for e, f in zip(errs, floor):
         assert e <= 1.25 * f + 1e-4
