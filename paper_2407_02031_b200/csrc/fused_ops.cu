@@ -89,7 +89,17 @@ geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int rows, int f) {
       if (m < rows) {
         Raw8<T> o;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) set_pair<T>(o, i, f2mul(get_pair<T>(h[u], i), gelu2(get_pair<T>(g[u], i))));
+        for (int i = 0; i < 4; ++i) {
+          const float2 gv = get_pair<T>(g[u], i);
+          float2 ge;
+          if constexpr (sizeof(T) == 4) {   // fp32 parity mode: libdevice erff (torch's exact GELU)
+            ge = make_float2(0.5f * gv.x * (1.f + erff(gv.x * 0.70710678118654752f)),
+                             0.5f * gv.y * (1.f + erff(gv.y * 0.70710678118654752f)));
+          } else {
+            ge = gelu2(gv);
+          }
+          set_pair<T>(o, i, f2mul(get_pair<T>(h[u], i), ge));
+        }
         store_raw<T>(dst + (unsigned)m * (unsigned)f, o);
       }
     }
@@ -153,7 +163,8 @@ add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* 
     float sq = q.x + q.y;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-    const float2 rstd = f2s(rsqrtf(sq / (float)c + eps));
+    // fp32 parity mode: an IEEE square root and division (rsqrtf is ~2 ulp)
+    const float2 rstd = f2s(sizeof(T) == 4 ? 1.f / sqrtf(sq / (float)c + eps) : rsqrtf(sq / (float)c + eps));
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const int col = (k * 32 + lane) * 8;

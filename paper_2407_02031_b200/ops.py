@@ -322,10 +322,12 @@ def groupnorm_mode(mode: int):
         _lib.lib().sdb_groupnorm_set_mode(0)
 
 
-def groupnorm_workspace(x: torch.Tensor, groups: int = 32) -> torch.Tensor:
-    """A zeroed K2 workspace sized for x (its counters must start at zero;
-    every launch leaves them at zero)."""
+def groupnorm_workspace(x: torch.Tensor, groups: int = 32, channels: Optional[int] = None) -> torch.Tensor:
+    """A zeroed K2 workspace sized for x — or for x's batch and pixels with
+    ``channels`` channels (a K3 concat's output) — (its arrival counters must
+    start at zero; every launch leaves them at zero)."""
     n, hw, c = nhwc_view(x)
+    c = c if channels is None else int(channels)
     return torch.zeros(max(_lib.lib().sdb_groupnorm_workspace(n, hw, c, groups), 256), dtype=torch.uint8,
                        device=x.device)
 
@@ -426,6 +428,10 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
     _count(1)
     if gn_workspace is not None and skip.dim() == 4 and k <= 4 and skip.dtype in (torch.bfloat16, torch.float16) \
             and (ch + cs) % groups == 0:
+        need = _lib.lib().sdb_groupnorm_workspace(n, hw, ch + cs, groups)
+        if gn_workspace.numel() < need:       # sized for the OUTPUT (hidden | skip) map
+            raise ValidationError(f"gn_workspace holds {gn_workspace.numel()} B, the {ch + cs}-channel output "
+                                  f"needs {need} B (groupnorm_workspace of the output shape)")
         _lib.check("sdb_residual_inject_gn", _lib.lib().sdb_residual_inject_gn(
             out.data_ptr(), hidden.data_ptr() if hidden is not None else None, skip.data_ptr(), ptrs, sc, k,
             n, hw, ch, cs, hidden_bias.data_ptr() if hidden_bias is not None else None,

@@ -448,15 +448,17 @@ class Net:
         return ops.residual_inject(h, [], [], skip_bias=self.fb.get(name), gn_workspace=self.k3ws(name, h),
                                    groups=self.cfg.groups)
 
-    def k3ws(self, key, x):
+    def k3ws(self, key, x, channels: Optional[int] = None):
         """GroupNorm-statistics workspace of one K3 call site whose output is
-        the next GroupNorm's input (the K3 pass accumulates its statistics)."""
+        the next GroupNorm's input (the K3 pass publishes its statistics).
+        Sized for the K3 OUTPUT: x's batch and pixels with ``channels``
+        channels (the concat's hidden + skip) when given."""
         if _NO_K3_STATS:
             return None
-        k = ("k3", key, tuple(x.shape))
+        k = ("k3", key, tuple(x.shape), channels)
         ws = self._gn_ws.get(k)
         if ws is None:
-            ws = self._gn_ws[k] = ops.groupnorm_workspace(x, self.cfg.groups)
+            ws = self._gn_ws[k] = ops.groupnorm_workspace(x, self.cfg.groups, channels)
         return ws
 
     def gn(self, name, x, silu, eps=None, add_nc=None):
@@ -471,7 +473,10 @@ class Net:
                                   silu=silu, add_nc=add_nc, workspace=ws)
 
     # -- blocks -----------------------------------------------------------
-    def resnet(self, pre, x, temb_act):
+    def resnet(self, pre, x, temb_act, gn_next: bool = True):
+        """gn_next: the block's output is the input of a GroupNorm (the next
+        ResNet's norm1 or a transformer's norm): only then does the closing K3
+        pass also publish that GroupNorm's statistics."""
         h = self.conv(pre + ".conv1", self.gn(pre + ".norm1", x, True), bias=False)
         # conv1's bias rides on the time-embedding projection (tproj_bias = b_temb + b_conv1)
         wt, tb = self.t[pre + ".time_emb_proj.weight"], self.fb.get(pre + ".tproj_bias")
@@ -492,8 +497,8 @@ class Net:
             sc, bias = x, self.fb.get(pre + ".conv2")
         # K3 in-place add (NHWC, vectorised) with conv2's (+ shortcut's) bias folded,
         # accumulating the next GroupNorm's statistics of the block output
-        return ops.residual_inject(h, [sc], [1.0], skip_bias=bias, gn_workspace=self.k3ws(pre, h),
-                                   groups=self.cfg.groups)
+        return ops.residual_inject(h, [sc], [1.0], skip_bias=bias,
+                                   gn_workspace=self.k3ws(pre, h) if gn_next else None, groups=self.cfg.groups)
 
     def attention(self, pre, x, ctx, heads):
         n, l, c = x.shape
@@ -524,7 +529,7 @@ class Net:
         o = o.transpose(1, 2).reshape(n, l, c)
         return self.lin(pre + ".to_out", o)
 
-    def transformer(self, pre, x, ctx, depth):
+    def transformer(self, pre, x, ctx, depth, gn_next: bool = True):
         n, c, h, w = x.shape
         res = x
         hs = self.gn(pre + ".norm", x, False, eps=self.cfg.tf_gn_eps)
@@ -542,7 +547,8 @@ class Net:
         tok = ops.residual_inject(tok, [delta], [1.0])
         tok = self.lin(pre + ".proj_out", tok)
         out = tok.view(n, h, w, c).permute(0, 3, 1, 2)            # channels_last view
-        return ops.residual_inject(out, [res], [1.0], gn_workspace=self.k3ws(pre, out), groups=self.cfg.groups)
+        return ops.residual_inject(out, [res], [1.0], gn_workspace=self.k3ws(pre, out) if gn_next else None,
+                                   groups=self.cfg.groups)
 
     # -- embeddings ---------------------------------------------------------
     def add_embedding(self, pooled: torch.Tensor, time_ids: torch.Tensor) -> torch.Tensor:
@@ -582,16 +588,19 @@ class Net:
         n = len(cfg.block_channels)
         for i in range(n):
             for j in range(cfg.layers_per_block):
-                h = self.resnet(f"down.{i}.res.{j}", h, temb_act)
+                # a GroupNorm reads this output next unless a downsample conv does
+                nxt_gn = j < cfg.layers_per_block - 1 or i == n - 1
+                h = self.resnet(f"down.{i}.res.{j}", h, temb_act, gn_next=nxt_gn or bool(cfg.attn_depth[i]))
                 if cfg.attn_depth[i]:
-                    h = self.transformer(f"down.{i}.attn.{j}", h, ctx, cfg.attn_depth[i])
+                    h = self.transformer(f"down.{i}.attn.{j}", h, ctx, cfg.attn_depth[i], gn_next=nxt_gn)
                 skip(h)
             if i < n - 1:
                 h = self.conv_bias_inplace(f"down.{i}.downsample", h, stride=2)
                 skip(h)
         h = self.resnet("mid.res.0", h, temb_act)
         h = self.transformer("mid.attn.0", h, ctx, cfg.mid_depth)
-        h = self.resnet("mid.res.1", h, temb_act)
+        # the UNet decoder adds the mid residuals / the ControlNet's zero conv reads it: no GroupNorm
+        h = self.resnet("mid.res.1", h, temb_act, gn_next=False)
         return h, skips
 
 
@@ -614,11 +623,16 @@ class UNet(Net):
                 k -= 1
                 res_k = [r[k] for r in residuals] if nres else []
                 h = ops.residual_inject(skips[k], res_k, res_scales if nres else [], hidden=h, hidden_bias=hb,
-                                        gn_workspace=self.k3ws(f"up.{i}.cat.{j}", skips[k]), groups=self.cfg.groups)
+                                        gn_workspace=self.k3ws(f"up.{i}.cat.{j}", skips[k],
+                                                               h.shape[1] + skips[k].shape[1]),
+                                        groups=self.cfg.groups)
                 hb = None
-                h = self.resnet(f"up.{i}.res.{j}", h, temb_act)
+                # next: the transformer's norm, the next concat (K3, computes its own
+                # statistics), the upsample conv, or conv_norm_out after the last block
+                last = i == n - 1 and j == cfg.layers_per_block
+                h = self.resnet(f"up.{i}.res.{j}", h, temb_act, gn_next=bool(depth) or last)
                 if depth:
-                    h = self.transformer(f"up.{i}.attn.{j}", h, ctx, depth)
+                    h = self.transformer(f"up.{i}.attn.{j}", h, ctx, depth, gn_next=last)
             if i < n - 1:
                 h = ops.upsample2x(_cl(h))                      # K10 (nearest 2x, NHWC)
                 h = self.conv(f"up.{i}.upsample", h, bias=False)

@@ -35,7 +35,7 @@ def run():
 
 
 res = {}
-for mode in ("default", "deterministic", "default_again", "nocudnn"):
+for mode in ("default", "deterministic", "default_again"):
     torch.backends.cudnn.deterministic = mode == "deterministic"
     torch.backends.cudnn.enabled = mode != "nocudnn"
     res[mode], up = run()

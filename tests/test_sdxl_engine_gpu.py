@@ -1,5 +1,6 @@
 """The benchmarked engine itself against the CPU oracle, at the headline
-config (BASELINE config 3): SDXL-shaped UNet at 128x128 latent + 2
+config (BASELINE config 3) and at config 2 (SD1.5 512^2 + 1 ControlNet + 1
+LoRA r16, same engine).  Config 3: SDXL-shaped UNet at 128x128 latent + 2
 ControlNets (scales 0.8 / 0.6) on their own streams beside the UNet encoder
 (``caas.LoopbackGroup(concurrent=True)``, exactly what ``bench.py`` times) +
 2 LoRAs r64 at 0.7, host-resident (``AdapterBank`` -> H2D -> ``pack_multi``
@@ -38,8 +39,9 @@ from paper_2407_02031_b200.pipeline import synthetic_request
 pytestmark = pytest.mark.gpu
 
 STEPS, BOUNDARY, GUIDANCE = 2, 1, 7.5
-CN_SCALES = [0.8, 0.6]
-LORA_RANKS, LORA_SCALE = (64, 64), 0.7
+LORA_SCALE = 0.7
+# BASELINE config 3 (the headline) and config 2 (SD1.5 + 1 ControlNet + 1 LoRA r16)
+ENGINES = {"sdxl": (U.SDXL, [0.8, 0.6], (64, 64)), "sd15": (U.SD15, [0.8], (16,))}
 
 
 def rel(a, b):
@@ -47,18 +49,20 @@ def rel(a, b):
     return float((a - b).norm() / b.norm())
 
 
-def run_engine(dtype):
-    cfg = U.SDXL
-    grp = LoopbackGroup(cfg, 2, CN_SCALES, steps=STEPS, guidance=GUIDANCE, dtype=dtype, seed=0, concurrent=True)
+def run_engine(dtype, name="sdxl"):
+    cfg, scales, ranks = ENGINES[name]
+    n_cn = len(scales)
+    grp = LoopbackGroup(cfg, n_cn, scales, steps=STEPS, guidance=GUIDANCE, dtype=dtype, seed=0, concurrent=True)
     pipe = grp.base.pipe
     loras = [synthetic_lora(pipe.unet_p, r, seed=10 + i, adapter_id=f"lora{i}", scale=LORA_SCALE)
-             for i, r in enumerate(LORA_RANKS)]
+             for i, r in enumerate(ranks)]
     grp.load_loras([(lo, LORA_SCALE) for lo in loras], host_resident=True)
     grp.setup()
-    req = synthetic_request(cfg, 2, seed=0)
+    req = synthetic_request(cfg, n_cn, seed=0)
     dev = dict(latent=torch.from_numpy(req.latent).cuda(), context=torch.from_numpy(req.context).cuda(),
-               images=[torch.from_numpy(i).cuda() for i in req.images],
-               pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
+               images=[torch.from_numpy(i).cuda() for i in req.images])
+    if req.pooled is not None:
+        dev.update(pooled=torch.from_numpy(req.pooled).cuda(), time_ids=torch.from_numpy(req.time_ids).cuda())
     per_step = []
     with torch.cuda.stream(grp.main_stream):
         grp.prepare(**dev)
@@ -68,13 +72,14 @@ def run_engine(dtype):
     # conditioning scale into their zero convs, so the oracle takes the
     # unscaled ControlNets (same seeds) and applies the scales itself
     up = R.to_cpu_params(pipe.unet_p)
-    cps = [R.to_cpu_params(U.init_controlnet(cfg, "cuda", dtype, seed=1000 + i)) for i in range(2)]
+    cps = [R.to_cpu_params(U.init_controlnet(cfg, "cuda", dtype, seed=1000 + i)) for i in range(n_cn)]
     factors = [(lo.factors, LORA_SCALE) for lo in loras]
     return per_step, up, cps, factors, pipe.unet_p.matrices, req
 
 
-def oracle(up, cps, factors, matrices, req, bf16_acts):
-    return R.denoise(U.SDXL, up, cps, req, CN_SCALES, STEPS, GUIDANCE, adapters=factors, matrices=matrices,
+def oracle(up, cps, factors, matrices, req, bf16_acts, name="sdxl"):
+    cfg, scales, _ = ENGINES[name]
+    return R.denoise(cfg, up, cps, req, scales, STEPS, GUIDANCE, adapters=factors, matrices=matrices,
                      boundary=BOUNDARY, bf16_acts=bf16_acts)
 
 
@@ -87,34 +92,36 @@ def fp32_mode():
     torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = old
 
 
-def test_sdxl_engine_fp32_per_step(fp32_mode):
-    dev, up, cps, factors, matrices, req = run_engine(torch.float32)
+@pytest.mark.parametrize("name", ["sdxl", "sd15"])
+def test_engine_fp32_per_step(fp32_mode, name):
+    dev, up, cps, factors, matrices, req = run_engine(torch.float32, name)
     torch.cuda.empty_cache()
-    ref = oracle(up, cps, factors, matrices, req, False)
+    ref = oracle(up, cps, factors, matrices, req, False, name)
     errs = [rel(a, b) for a, b in zip(dev, ref)]
     # the same oracle in fp64: how far fp32 arithmetic itself (device or CPU)
     # sits from the exact result at SDXL depth
     up64 = {k: v.double() for k, v in up.items()}
     cps64 = [{k: v.double() for k, v in c.items()} for c in cps]
     del up, cps
-    truth = oracle(up64, cps64, factors, matrices, req, False)
+    truth = oracle(up64, cps64, factors, matrices, req, False, name)
     d_truth = [rel(a, b) for a, b in zip(dev, truth)]
     o_truth = [rel(a, b) for a, b in zip(ref, truth)]
-    print("SDXL config-3 engine fp32 per-step rel-L2: device-vs-oracle", ["%.2e" % e for e in errs],
+    print(f"{name} engine fp32 per-step rel-L2: device-vs-oracle", ["%.2e" % e for e in errs],
           "device-vs-fp64", ["%.2e" % e for e in d_truth], "oracle(fp32)-vs-fp64", ["%.2e" % e for e in o_truth])
     assert len(errs) == STEPS
     assert max(errs) <= 1e-5
 
 
-def test_sdxl_engine_bf16_per_step():
-    dev, up, cps, factors, matrices, req = run_engine(torch.bfloat16)
+@pytest.mark.parametrize("name", ["sdxl", "sd15"])
+def test_engine_bf16_per_step(name):
+    dev, up, cps, factors, matrices, req = run_engine(torch.bfloat16, name)
     torch.cuda.empty_cache()
-    ref = oracle(up, cps, factors, matrices, req, False)
-    emu = oracle(up, cps, factors, matrices, req, True)
+    ref = oracle(up, cps, factors, matrices, req, False, name)
+    emu = oracle(up, cps, factors, matrices, req, True, name)
     d_ref = [rel(a, b) for a, b in zip(dev, ref)]
     d_emu = [rel(a, b) for a, b in zip(dev, emu)]
     floor = [rel(a, b) for a, b in zip(emu, ref)]
-    print("SDXL config-3 engine bf16 per-step rel-L2: device-vs-fp32", ["%.2e" % e for e in d_ref],
+    print(f"{name} engine bf16 per-step rel-L2: device-vs-fp32", ["%.2e" % e for e in d_ref],
           "device-vs-bf16-emulator", ["%.2e" % e for e in d_emu], "emulator-vs-fp32", ["%.2e" % e for e in floor])
     for a, e, f in zip(d_ref, d_emu, floor):
         # two bf16 implementations with independent rounding sit ~sqrt(2) x
