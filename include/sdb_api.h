@@ -124,11 +124,12 @@ int sdb_lora_pack_bytes(int64_t h1, int64_t h2, int32_t rank, size_t* a_bytes, s
  * set of lora.py:147-160, down' = [d_i * f32(s_i)], up' = [u_i]; packed rank =
  * sum of the sources' ranks).  Scales stay exact: the scale carried by the
  * largest share of the rank (epi_scale) is applied by the patch epilogue in
- * fp32 and its sources are packed unscaled; each other source is packed as
- * x = d * (s_i / epi_scale) split into a bf16 high part and a bf16 low part
- * (an extra A K-block per affected B K-block, bit b of lo_mask), 2^-17
- * relative instead of a bf16 rounding of s_i * d.  Query the layout first
- * (sizes, epi_scale, lo_mask for the sdb_lora_tc_job), then pack. */
+ * fp32 and its sources are packed unscaled; each other source's up rows are
+ * packed as x = u * (s_i / epi_scale) split into a bf16 high part and a bf16
+ * low part (an extra B-panel K-block per affected K-block, bit b of
+ * lo_mask, multiplied by the same A K-block), 2^-17 relative instead of a
+ * bf16 rounding of s_i * d.  Query the layout first (sizes, epi_scale,
+ * lo_mask for the sdb_lora_tc_job), then pack. */
 typedef struct sdb_lora_src {
   const void* down; int64_t ldd;   /* h1 x rank   */
   const void* up;   int64_t ldu;   /* rank x h2   */

@@ -14,8 +14,9 @@
 //     shared memory -> TMA store.  The ring keeps S*16 KB of W in flight per SM.
 //   * Factors are pre-packed once per adapter set (sdb_lora_pack) into the
 //     UMMA canonical K-major SWIZZLE_128B layout, so they move with plain bulk
-//     copies: the B panel (256 output columns x R) stays resident while the
-//     CTA walks up to 8 row tiles of that panel; the A tile (128 rows x R) is
+//     copies: the B panel (256 output columns x R, plus the low-part blocks
+//     of scale-folded adapters, see the packing section) stays resident while
+//     the CTA walks up to 8 row tiles of that panel; the A tile (128 rows x R) is
 //     streamed per row tile in 64-deep K blocks through a 2-stage ring
 //     (L2-resident: its re-read costs R/256 of the W read).
 //   * tcgen05 path: one elected thread issues ceil(R/16) MMAs of
@@ -59,24 +60,24 @@ constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN
                             ((uint32_t)(kBM >> 4) << 24);   // f32 accum, bf16 A/B, K-major, 128x256
 
 struct TcJob {
-  const uint8_t* a;   // packed A: [m_tiles][akb][128 rows][128 B]
-  const uint8_t* b;   // packed B: [n_tiles][kb][256 rows][128 B]
+  const uint8_t* a;   // packed A: [m_tiles][kb][128 rows][128 B]
+  const uint8_t* b;   // packed B: [n_tiles][bkb][256 rows][128 B]
   int64_t h1, h2;
-  int32_t kb, rank;
+  int32_t kb, rank;       // A K-blocks (= high-part B K-blocks), stacked rank
   float scale;
   int32_t map_in, map_out;
   int32_t map_a, map_b;   // tensor maps over the packed factors (CTA-pair kernel)
   int32_t mt;             // row tiles of W
-  int32_t akb;            // A K-blocks per row tile: kb high parts + the low parts (see lo_b)
-  uint32_t lo_b;          // byte i: the B K-block that A K-block kb + i (a low part) multiplies
+  int32_t bkb;            // B-panel K-blocks: kb high parts + the low parts (see lo_of)
+  uint32_t lo_of;         // byte a: 0, or 1 + the B-panel block holding the low part A block a also multiplies
   int32_t pad;
 };
 
-// A K-block a of a tile multiplies B K-block b_of(J, a): the first kb blocks
-// are the (unscaled or high-part) stacked factors, the rest the low parts of
-// the scale-folded sources (hi/lo split, see the packing section)
-__device__ __forceinline__ int b_of(const TcJob& J, int a) {
-  return a < J.kb ? a : (int)((J.lo_b >> (8 * (a - J.kb))) & 0xFF);
+// The B panel's first kb blocks are the (unscaled or high-part) stacked
+// factors; A K-block a also multiplies low-part block lo_block(J, a) when the
+// scale-folded sources touch it (hi/lo split, see the packing section)
+__device__ __forceinline__ int lo_block(const TcJob& J, int a) {
+  return (int)((J.lo_of >> (8 * a)) & 0xFF) - 1;
 }
 struct TcUnit {
   int32_t job, n_tile, m_begin, m_end;
@@ -169,23 +170,23 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
         const TcUnit un = units[u];
         const TcJob& J = jobs[un.job];
         if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
-        mbar_expect_tx(bar(B_FULL), J.kb * kPanelBlock);
+        mbar_expect_tx(bar(B_FULL), J.bkb * kPanelBlock);
         if (BN == kBN) {
-          bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.kb * kBBlockBytes, J.kb * kBBlockBytes, bar(B_FULL),
+          bulk_g2s(smem_u32(sB), J.b + (size_t)un.n_tile * J.bkb * kBBlockBytes, J.bkb * kBBlockBytes, bar(B_FULL),
                    keep);
         } else {  // a BN-wide half of a packed 256-wide panel: one copy per K block
           const int p256 = un.n_tile / (kBN / BN), hh = un.n_tile % (kBN / BN);
-          for (int kb = 0; kb < J.kb; ++kb)
+          for (int kb = 0; kb < J.bkb; ++kb)
             bulk_g2s(smem_u32(sB + kb * kPanelBlock),
-                     J.b + (((size_t)p256 * J.kb + kb) * kBN + (size_t)hh * BN) * 128, kPanelBlock, bar(B_FULL),
+                     J.b + (((size_t)p256 * J.bkb + kb) * kBN + (size_t)hh * BN) * 128, kPanelBlock, bar(B_FULL),
                      keep);
         }
         ++b_cnt;
         for (int m = un.m_begin; m < un.m_end; ++m) {
-          for (int kb = 0; kb < J.akb; ++kb) {
+          for (int kb = 0; kb < J.kb; ++kb) {
             if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
             mbar_expect_tx(bar(A_FULL + a_st), kABlockBytes);
-            bulk_g2s(smem_u32(sA + a_st * kABlockBytes), J.a + ((size_t)m * J.akb + kb) * kABlockBytes, kABlockBytes,
+            bulk_g2s(smem_u32(sA + a_st * kABlockBytes), J.a + ((size_t)m * J.kb + kb) * kABlockBytes, kABlockBytes,
                      bar(A_FULL + a_st), keep);
             if (++a_st == kAStages) { a_st = 0; ++a_round; }
           }
@@ -230,16 +231,16 @@ lora_patch_tma_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __restr
           const int buf = tile & 1;
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           const uint32_t d = tmem_base + buf * BN;
-          for (int kb = 0; kb < J.akb; ++kb, ++a_cnt) {
+          for (int kb = 0; kb < J.kb; ++kb, ++a_cnt) {
             const int st = a_cnt & (kAStages - 1);
             mbar_wait(bar(A_FULL + st), (a_cnt / kAStages) & 1);
             tc_fence_after();
-            const int bb = b_of(J, kb);
-            const int ks_end = std::min(4, nks - bb * 4);
+            const int ks_end = std::min(4, nks - kb * 4);
+            const int lb = lo_block(J, kb);
             for (int ks = 0; ks < ks_end; ++ks) {
               const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
-              const uint64_t bd = sw128_desc(smem_u32(sB + bb * kPanelBlock + ks * 32));
-              tc_mma(d, ad, bd, kIdescBN, (kb | ks) ? 1u : 0u);
+              tc_mma(d, ad, sw128_desc(smem_u32(sB + kb * kPanelBlock + ks * 32)), kIdescBN, (kb | ks) ? 1u : 0u);
+              if (lb >= 0) tc_mma(d, ad, sw128_desc(smem_u32(sB + lb * kPanelBlock + ks * 32)), kIdescBN, 1u);
             }
             tc_commit(bar(A_EMPTY + st));       // stage free once these MMAs completed
           }
@@ -445,18 +446,18 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
         const CUtensorMap* ma = maps + J.map_a;
         const CUtensorMap* mb = maps + J.map_b;
         if (b_cnt > 0) mbar_wait(bar(B_EMPTY), (b_cnt - 1) & 1);
-        if (leader) mbar_expect_tx(bar(B_FULL), 2 * J.kb * kHalfBlock);
-        for (int kb = 0; kb < J.kb; ++kb)
-          tma_load_2d_pair(smem_u32(sB + kb * kHalfBlock), mb, 0, (un.n_tile * J.kb + kb) * kBN + (int)cta * 128,
+        if (leader) mbar_expect_tx(bar(B_FULL), 2 * J.bkb * kHalfBlock);
+        for (int kb = 0; kb < J.bkb; ++kb)
+          tma_load_2d_pair(smem_u32(sB + kb * kHalfBlock), mb, 0, (un.n_tile * J.bkb + kb) * kBN + (int)cta * 128,
                            mapa_shared(bar(B_FULL), 0), keep);
         ++b_cnt;
         for (int m0 = un.m_begin; m0 < un.m_end; m0 += 2) {
           // past the last row tile the follower multiplies a valid (ignored) A tile
           const int mload = std::min(m0 + (int)cta, J.mt - 1);
-          for (int kb = 0; kb < J.akb; ++kb) {
+          for (int kb = 0; kb < J.kb; ++kb) {
             if (a_round > 0) mbar_wait(bar(A_EMPTY + a_st), (a_round - 1) & 1);
             if (leader) mbar_expect_tx(bar(A_FULL + a_st), 2 * kABlockBytes);
-            tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.akb + kb) * kBM,
+            tma_load_2d_pair(smem_u32(sA + a_st * kABlockBytes), ma, 0, (mload * J.kb + kb) * kBM,
                              mapa_shared(bar(A_FULL + a_st), 0), keep);
             if (++a_st == na) { a_st = 0; ++a_round; }
           }
@@ -507,17 +508,17 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
           if (tile >= 2) mbar_wait(bar(T_EMPTY + buf), ((tile >> 1) - 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem_base + buf * kBN;
-          for (int kb = 0; kb < J.akb; ++kb) {
+          for (int kb = 0; kb < J.kb; ++kb) {
             const int st = a_st;
             mbar_wait(bar(A_FULL + st), a_round & 1);
             if (++a_st == na) { a_st = 0; ++a_round; }
             tc_fence_after();
-            const int bb = b_of(J, kb);
-            const int ks_end = std::min(4, nks - bb * 4);
+            const int ks_end = std::min(4, nks - kb * 4);
+            const int lb = lo_block(J, kb);
             for (int ks = 0; ks < ks_end; ++ks) {
               const uint64_t ad = sw128_desc(smem_u32(sA + st * kABlockBytes + ks * 32));
-              const uint64_t bd = sw128_desc(smem_u32(sB + bb * kHalfBlock + ks * 32));
-              tc_mma2(d, ad, bd, kIdesc2, (kb | ks) ? 1u : 0u);
+              tc_mma2(d, ad, sw128_desc(smem_u32(sB + kb * kHalfBlock + ks * 32)), kIdesc2, (kb | ks) ? 1u : 0u);
+              if (lb >= 0) tc_mma2(d, ad, sw128_desc(smem_u32(sB + lb * kHalfBlock + ks * 32)), kIdesc2, 1u);
             }
             tc_commit2(bar(A_EMPTY + st));
           }
@@ -606,12 +607,15 @@ lora_patch_pair_kernel(const CUtensorMap* __restrict__ maps, const TcJob* __rest
 // time (2^-9 relative per factor element) — where W + delta nearly cancels
 // that is many bf16 ulps of the result.  Instead the scale carried by the
 // largest share of the stacked rank (s_e) is applied in the fp32 epilogue and
-// its sources are packed unscaled (exact); every other source is packed as
-// x = f32(d) * f32(s_k / s_e) split into hi = bf16(x) (in the stacked K-blocks)
-// and lo = bf16(x - hi) (in an extra A K-block that multiplies the SAME B
-// K-block, see b_of): hi + lo carries x to 2^-17 relative.  Only B K-blocks
-// that hold a folded source get a low block, so equal scales (the serving
-// case: every adapter at one strength) cost nothing extra.
+// its sources are packed unscaled (exact); for every other source the ratio
+// goes into its `up` rows — the B panel, which stays resident in shared
+// memory while the CTA walks its row tiles — as x = f32(u) * f32(s_k / s_e)
+// split into hi = bf16(x) (in the stacked K-blocks) and lo = bf16(x - hi) (in
+// an extra B K-block that the SAME A K-block also multiplies, see lo_block):
+// hi + lo carries x to 2^-17 relative, A (down, re-read per column panel) is
+// packed once, unscaled.  Only K-blocks that hold a folded source get a low
+// block, so equal scales (the serving case: every adapter at one strength)
+// cost nothing extra.
 constexpr int kMaxSrc = 8;
 struct PackSrcs {
   const __nv_bfloat16* down[kMaxSrc];
@@ -621,7 +625,7 @@ struct PackSrcs {
   float fold[kMaxSrc];     // s_k / s_e (exactly 1 for the epilogue-scaled sources)
   int n;
   int kb;                  // stacked K-blocks (high parts)
-  uint32_t lo_b;           // byte i: the K-block whose low part is A K-block kb + i
+  uint32_t lo_b;           // byte i: the K-block whose low part is B-panel block kb + i
 };
 
 struct MultiLayout {
@@ -672,58 +676,58 @@ __device__ __forceinline__ int src_of(const PackSrcs& s, int k) {
   return i;
 }
 
-__global__ void pack_a_multi_kernel(PackSrcs s, int64_t h1, int akb, int64_t mt, uint4* __restrict__ out) {
+__global__ void pack_a_multi_kernel(PackSrcs s, int64_t h1, int kbt, int64_t mt, uint4* __restrict__ out) {
   const int rank = s.koff[s.n];
-  const int64_t total = mt * akb * kBM * 8;
+  const int64_t total = mt * kbt * kBM * 8;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i & 7);
-    const int64_t rowi = i >> 3;                // (m*akb + a)*128 + r
+    const int64_t rowi = i >> 3;                // (m*kbt + kb)*128 + r
     const int r = (int)(rowi % kBM);
     const int64_t mk = rowi / kBM;
-    const int a = (int)(mk % akb);
-    const int64_t m = mk / akb;
+    const int kb = (int)(mk % kbt);
+    const int64_t m = mk / kbt;
     const int64_t row = m * kBM + r;
-    const bool low = a >= s.kb;
-    const int kb = low ? (int)((s.lo_b >> (8 * (a - s.kb))) & 0xFF) : a;
+    const int k0 = kb * kKB + c * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = k0 + e;
+      v[e] = __float2bfloat16_rn(0.f);
+      if (row < h1 && k < rank) {
+        const int si = src_of(s, k);
+        v[e] = s.down[si][row * s.ldd[si] + (k - s.koff[si])];   // unscaled: the scales live in B / the epilogue
+      }
+    }
+    out[rowi * 8 + (c ^ (r & 7))] = *reinterpret_cast<uint4*>(v);
+  }
+}
+
+// B: [nt][bkb][256][8 chunks x 16 B]; blocks kb.. hold the low parts
+__global__ void pack_b_multi_kernel(PackSrcs s, int64_t h2, int bkb, int64_t nt, uint4* __restrict__ out) {
+  const int rank = s.koff[s.n];
+  const int64_t total = nt * bkb * 8 * kBN;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int n = (int)(i % kBN);               // fastest: coalesced reads of up rows
+    const int64_t q = i / kBN;
+    const int c = (int)(q & 7);
+    const int64_t nk = q >> 3;                  // nt*bkb + b
+    const int b = (int)(nk % bkb);
+    const int64_t ntile = nk / bkb;
+    const int64_t col = ntile * kBN + n;
+    const bool low = b >= s.kb;
+    const int kb = low ? (int)((s.lo_b >> (8 * (b - s.kb))) & 0xFF) : b;
     const int k0 = kb * kKB + c * 8;
     __align__(16) __nv_bfloat16 v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int k = k0 + e;
       float x = 0.f;
-      if (row < h1 && k < rank) {
+      if (col < h2 && k < rank) {
         const int si = src_of(s, k);
-        x = __bfloat162float(s.down[si][row * s.ldd[si] + (k - s.koff[si])]) * s.fold[si];
+        x = __bfloat162float(s.up[si][(int64_t)(k - s.koff[si]) * s.ldu[si] + col]) * s.fold[si];
         if (low) x -= __bfloat162float(__float2bfloat16_rn(x));   // exactly 0 for fold == 1
       }
       v[e] = __float2bfloat16_rn(x);
-    }
-    out[rowi * 8 + (c ^ (r & 7))] = *reinterpret_cast<uint4*>(v);
-  }
-}
-
-__global__ void pack_b_multi_kernel(PackSrcs s, int64_t h2, int kbt, int64_t nt, uint4* __restrict__ out) {
-  const int rank = s.koff[s.n];
-  const int64_t total = nt * kbt * 8 * kBN;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int n = (int)(i % kBN);               // fastest: coalesced reads of up rows
-    const int64_t q = i / kBN;
-    const int c = (int)(q & 7);
-    const int64_t nk = q >> 3;                  // nt*kbt + kb
-    const int kb = (int)(nk % kbt);
-    const int64_t ntile = nk / kbt;
-    const int64_t col = ntile * kBN + n;
-    const int k0 = kb * kKB + c * 8;
-    __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int k = k0 + e;
-      __nv_bfloat16 x = __float2bfloat16_rn(0.f);
-      if (col < h2 && k < rank) {
-        const int si = src_of(s, k);
-        x = s.up[si][(int64_t)(k - s.koff[si]) * s.ldu[si] + col];
-      }
-      v[e] = x;
     }
     out[(nk * kBN + n) * 8 + (c ^ (n & 7))] = *reinterpret_cast<uint4*>(v);
   }
@@ -844,8 +848,8 @@ int tc_pack_multi_layout(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_
                          size_t* b_bytes, float* epi_scale, int32_t* lo_mask) {
   MultiLayout L;
   if (int rc = multi_layout(srcs, n_src, &L)) return rc;
-  if (a_bytes) *a_bytes = (size_t)((h1 + kBM - 1) / kBM) * (L.kb + L.nlo) * kABlockBytes;
-  if (b_bytes) *b_bytes = (size_t)((h2 + kBN - 1) / kBN) * L.kb * kBBlockBytes;
+  if (a_bytes) *a_bytes = (size_t)((h1 + kBM - 1) / kBM) * L.kb * kABlockBytes;
+  if (b_bytes) *b_bytes = (size_t)((h2 + kBN - 1) / kBN) * (L.kb + L.nlo) * kBBlockBytes;
   if (epi_scale) *epi_scale = L.epi_scale;
   if (lo_mask) *lo_mask = (int32_t)L.lo_mask;
   return SDB_OK;
@@ -873,14 +877,14 @@ int tc_pack_multi(const sdb_lora_src* srcs, int n_src, int64_t h1, int64_t h2, v
   }
   s.kb = L.kb;
   s.lo_b = L.lo_b;
-  const int akb = L.kb + L.nlo;
+  const int bkb = L.kb + L.nlo;
   const int64_t mt = (h1 + kBM - 1) / kBM, nt = (h2 + kBN - 1) / kBN;
-  const int64_t na = mt * akb * kBM * 8, nb = nt * L.kb * 8 * kBN;
+  const int64_t na = mt * L.kb * kBM * 8, nb = nt * bkb * 8 * kBN;
   pack_a_multi_kernel<<<(unsigned)std::min<int64_t>((na + 255) / 256, 65535), 256, 0, st>>>(
-      s, h1, akb, mt, static_cast<uint4*>(a_out));
+      s, h1, L.kb, mt, static_cast<uint4*>(a_out));
   if (int rc = check_launch("pack_a_multi_kernel")) return rc;
   pack_b_multi_kernel<<<(unsigned)std::min<int64_t>((nb + 255) / 256, 65535), 256, 0, st>>>(
-      s, h2, L.kb, nt, static_cast<uint4*>(b_out));
+      s, h2, bkb, nt, static_cast<uint4*>(b_out));
   return check_launch("pack_b_multi_kernel");
 }
 
@@ -909,14 +913,14 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
             int* kb_max_out) {
   if (n_jobs <= 0 || !jobs) return fail(SDB_EINVAL, "lora_tc_plan: no jobs");
   std::vector<TcUnit> units;
-  int kb_max = 1, akb_max = 1;
+  int kb_max = 1, bkb_max = 1;   // A K-blocks, B-panel K-blocks (incl. low parts)
   for (int j = 0; j < n_jobs; ++j) {
     const sdb_lora_tc_job& J = jobs[j];
     if (J.h1 <= 0 || J.h2 <= 0 || J.rank < 1 || J.rank > kMaxKB * kKB)
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": bad shape or rank (1..256)");
     if ((uint32_t)J.lo_mask >> tc_kb(J.rank))
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": lo_mask names a K block past the rank");
-    akb_max = std::max(akb_max, tc_kb(J.rank) + __builtin_popcount((uint32_t)J.lo_mask));
+    bkb_max = std::max(bkb_max, tc_kb(J.rank) + __builtin_popcount((uint32_t)J.lo_mask));
     if (J.ldw % 8 != 0 || ((uintptr_t)J.w_in & 15) || ((uintptr_t)J.w_out & 15))
       return fail(SDB_EINVAL, "lora_tc_plan: job " + std::to_string(j) + ": W rows must be 16-B aligned (ldw % 8 == 0)");
     if (((uintptr_t)J.a_packed | (uintptr_t)J.b_packed) & 1023)
@@ -975,7 +979,7 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
   const size_t need = maps_b + jobs_b + units_b;
   if (needed) *needed = need;
   if (n_units_out) *n_units_out = (int)units.size();
-  if (kb_max_out) *kb_max_out = kb_max | (mode << 8) | (akb_max << 12);
+  if (kb_max_out) *kb_max_out = bkb_max | (mode << 8) | (kb_max << 12);
   if (!blob) return SDB_OK;
   if (blob_bytes < need) return fail(SDB_EINVAL, "lora_tc_plan: blob too small");
   uint8_t* base = static_cast<uint8_t*>(blob);
@@ -985,15 +989,15 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
     const sdb_lora_tc_job& J = jobs[j];
     const int kb = tc_kb(J.rank);
     int nlo = 0;
-    uint32_t lo_b = 0;
+    uint32_t lo_of = 0;     // byte a: 1 + the B-panel block of A block a's low part
     for (int b = 0; b < kb; ++b)
-      if ((uint32_t)J.lo_mask >> b & 1u) lo_b |= (uint32_t)b << (8 * nlo++);
+      if ((uint32_t)J.lo_mask >> b & 1u) lo_of |= (uint32_t)(kb + nlo++ + 1) << (8 * b);
     const int64_t mt = (J.h1 + kBM - 1) / kBM, nt = (J.h2 + kBN - 1) / kBN;
     // loads move whole 128-row boxes; each epilogue warp stores its own 32 rows
     if (int rc = make_w_map(&maps[4 * j], J.w_in, J.h1, J.h2, J.ldw, kBM)) return rc;
     if (int rc = make_w_map(&maps[4 * j + 1], J.w_out, J.h1, J.h2, J.ldw, 32)) return rc;
-    if (int rc = make_f_map(&maps[4 * j + 2], J.a_packed, mt * (kb + nlo) * kBM)) return rc;
-    if (int rc = make_f_map(&maps[4 * j + 3], J.b_packed, nt * kb * kBN)) return rc;
+    if (int rc = make_f_map(&maps[4 * j + 2], J.a_packed, mt * kb * kBM)) return rc;
+    if (int rc = make_f_map(&maps[4 * j + 3], J.b_packed, nt * (kb + nlo) * kBN)) return rc;
     std::memset(&tj[j], 0, sizeof(TcJob));
     tj[j].a = static_cast<const uint8_t*>(J.a_packed);
     tj[j].b = static_cast<const uint8_t*>(J.b_packed);
@@ -1007,8 +1011,8 @@ int tc_plan(const sdb_lora_tc_job* jobs, int n_jobs, void* blob, size_t blob_byt
     tj[j].map_a = 4 * j + 2;
     tj[j].map_b = 4 * j + 3;
     tj[j].mt = (int32_t)mt;
-    tj[j].akb = kb + nlo;
-    tj[j].lo_b = lo_b;
+    tj[j].bkb = kb + nlo;
+    tj[j].lo_of = lo_of;
   }
   std::memcpy(base + maps_b + jobs_b, units.data(), units_b);
   return SDB_OK;
@@ -1023,10 +1027,11 @@ int tc_set_mode(int mode) {
 
 int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int simt_rank, float sign, int max_ctas,
              cudaStream_t st) {
-  const int kb_max = kb_word & 0xFF, mode = (kb_word >> 8) & 0xF, akb_max = std::max(kb_max, kb_word >> 12);
+  // kb_max: B-panel K-blocks (sizes the resident panel); akb_max: A K-blocks (the A ring)
+  const int kb_max = kb_word & 0xFF, mode = (kb_word >> 8) & 0xF, akb_max = std::max(1, kb_word >> 12);
   if (!blob_dev || n_units <= 0) return fail(SDB_EINVAL, "lora_tc_patch: empty plan");
   if (((uintptr_t)blob_dev) & 127) return fail(SDB_EINVAL, "lora_tc_patch: blob must be 128-B aligned");
-  if (kb_max < 1 || kb_max > kMaxKB) return fail(SDB_EINVAL, "lora_tc_patch: kb_max out of range");
+  if (kb_max < 1 || kb_max > 2 * kMaxKB) return fail(SDB_EINVAL, "lora_tc_patch: kb_max out of range");
   if (mode != 1 && mode != 2) return fail(SDB_EINVAL, "lora_tc_patch: kb_max word is not from sdb_lora_tc_plan");
   const size_t maps_b = (size_t)4 * n_jobs * sizeof(CUtensorMap);
   const uint8_t* base = static_cast<const uint8_t*>(blob_dev);
@@ -1040,7 +1045,10 @@ int tc_patch(const void* blob_dev, int n_jobs, int n_units, int kb_word, int sim
     // consume them in sequence, so at high rank a deeper A ring beats the
     // last W slots (round 1, R = 232: 4 stages + 6 slots 2.04 ms = 89% of the
     // copy peak vs 2 stages + 8 slots 2.42 ms; R <= 128: 2 stages best)
-    const int na = std::min(4, std::max(2, akb_max));
+    // with low-part B blocks the panel grows (R = 232, four scales: 6 blocks);
+    // 3 A stages leave 5 W slots — measured best (2 / 3 / 4 stages: 2.64 /
+    // 2.46 / 2.78 ms, all 794 SDXL matrices, scripts/k1_scales_probe.py)
+    const int na = kb_max > akb_max ? 3 : std::min(4, std::max(2, akb_max));
     const int fixed = 1024 + kb_max * kHalfBlock + na * kABlockBytes + 320;
     const int slots = std::min(kMaxSlots, (max_smem - fixed) / kBoxBytes);
     const int smem = fixed + slots * kBoxBytes;
