@@ -582,9 +582,15 @@ def lora_microbench(unet_p, shadow, hbm: float, cpu_full: bool = False, reps: in
            for i, (r, sc) in enumerate(zip(ranks, scales))]
     out_of_place = PatchSet(unet_p, ads, shadow=shadow)
     in_place = PatchSet(unet_p, ads, shadow=shadow, in_place_on_shadow=True)
-    names = [n for n, _ in unet_p.matrices]
+    from paper_2407_02031_b200.ops import BatchedCopy
+    names = [n for n, _ in unet_p.matrices if n not in unet_p.fused]
+    # fused storages (q|k|v, k|v) are restored as one block each
+    parents = list(unet_p.fused)
+    members = {m for ms in unet_p.fused.values() for m in ms}
+    names = [n for n in names if n not in members] + parents
     pristine = [unet_p.t[n + ".weight"] for n in names]
     dst = [shadow[n] for n in names]
+    restore = BatchedCopy(pristine, dst)
 
     def timed(fn):
         fn()
@@ -600,13 +606,13 @@ def lora_microbench(unet_p, shadow, hbm: float, cpu_full: bool = False, reps: in
         return statistics.median(ts)
 
     alg = out_of_place.alg_bytes
-    w_bytes = sum(t.numel() * t.element_size() for t in pristine)
+    w_bytes = restore.nbytes
     res = {}
     res["patch_out_of_place_ms"] = timed(lambda: out_of_place.launch())
-    torch._foreach_copy_(dst, pristine)
+    restore.launch()
     res["merge_in_place_ms"] = timed(lambda: in_place.launch(sign=1.0))
     res["unmerge_in_place_ms"] = timed(lambda: in_place.launch(sign=-1.0))
-    res["restore_from_pristine_ms"] = timed(lambda: torch._foreach_copy_(dst, pristine))
+    res["restore_from_pristine_ms"] = timed(lambda: restore.launch())     # sdb_batched_copy, one launch
     res["pointer_swap_ms"] = 0.0
     out = {"layers": len(names), "ranks": list(ranks), "scales": list(scales), "stacked_rank": sum(ranks),
            "kernel": out_of_place.plan.kernel, "alg_bytes_patch": alg, "alg_bytes_restore": 2 * w_bytes,

@@ -276,6 +276,15 @@ int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, v
  * (the UNet decoder's upsample before its 3x3 conv).  x [n, h, w, c], y
  * [n, 2h, 2w, c], c * elem_bytes a multiple of 16, 16-B aligned pointers.
  * No reference counterpart (addonsim has no UNet arithmetic). */
+/* Batched copy — restore-from-pristine unpatch of every patched matrix in
+ * ONE launch (the reference unmerges by subtracting, lora.py:107-114; a
+ * serving copy can restore W exactly).  Device arrays: per tensor its source,
+ * destination (16-B aligned), size in 16-B vectors, and the exclusive prefix
+ * of its chunk counts (n + 1 entries; a chunk is
+ * sdb_batched_copy_chunk_vectors() vectors). */
+int64_t sdb_batched_copy_chunk_vectors(void);
+int sdb_batched_copy(const void* const* src_dev, void* const* dst_dev, const int64_t* nvec_dev,
+                     const int64_t* chunk_prefix_dev, int n, int64_t total_chunks, void* stream);
 int sdb_upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t c, int elem_bytes,
                    void* stream);
 

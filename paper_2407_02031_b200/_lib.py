@@ -181,7 +181,7 @@ EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_mu
                        "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_add_layernorm",
                        "sdb_cross_attention", "sdb_stream_wait_value32", "sdb_stream_write_value32",
                        "sdb_memcpy_async", "sdb_cross_attention_set_mode", "sdb_self_attention",
-                       "sdb_upsample2x")
+                       "sdb_upsample2x", "sdb_batched_copy", "sdb_batched_copy_chunk_vectors")
 
 
 def _declare_tc(lib: ctypes.CDLL) -> None:
@@ -203,6 +203,10 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
     lib.sdb_lora_tc_patch.argtypes = [vp, i32, i32, i32, i32, f32, i32, vp]
     lib.sdb_lora_tc_set_mode.restype = i32
     lib.sdb_lora_tc_set_mode.argtypes = [i32]
+    lib.sdb_batched_copy.restype = i32
+    lib.sdb_batched_copy.argtypes = [vp, vp, vp, vp, i32, i64, vp]
+    lib.sdb_batched_copy_chunk_vectors.restype = i64
+    lib.sdb_batched_copy_chunk_vectors.argtypes = []
     lib.sdb_upsample2x.restype = i32
     lib.sdb_upsample2x.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
     lib.sdb_geglu.restype = i32

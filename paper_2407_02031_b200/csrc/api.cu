@@ -44,6 +44,9 @@ int residual_inject(void* out, const void* hidden, const void* skip, const void*
 // fused_ops.cu
 int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st);
 int upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t c, int elem_bytes, cudaStream_t st);
+int batched_copy(const void* const* src_dev, void* const* dst_dev, const int64_t* nvec_dev,
+                 const int64_t* chunk_prefix_dev, int n, int64_t total_chunks, cudaStream_t st);
+int64_t batched_copy_chunk_vectors();
 int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                   float eps, int dtype, cudaStream_t st);
 // cross_attn.cu
@@ -230,6 +233,15 @@ int sdb_residual_inject_bias(void* out, const void* hidden, const void* skip,
                              const float* skip_bias, int dtype, void* stream) {
   return residual_inject(out, hidden, skip, res_ptrs_host, scales_host, n_res, pixels, ch, cs, hidden_bias,
                          skip_bias, dtype, as_stream(stream));
+}
+
+int64_t sdb_batched_copy_chunk_vectors(void) { return batched_copy_chunk_vectors(); }
+
+int sdb_batched_copy(const void* const* src_dev, void* const* dst_dev, const int64_t* nvec_dev,
+                     const int64_t* chunk_prefix_dev, int n, int64_t total_chunks, void* stream) {
+  if (n < 0 || (n > 0 && (!src_dev || !dst_dev || !nvec_dev || !chunk_prefix_dev)))
+    return fail(SDB_EINVAL, "sdb_batched_copy: NULL table");
+  return batched_copy(src_dev, dst_dev, nvec_dev, chunk_prefix_dev, n, total_chunks, as_stream(stream));
 }
 
 int sdb_upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t c, int elem_bytes,

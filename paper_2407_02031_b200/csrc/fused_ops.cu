@@ -222,6 +222,48 @@ int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* b
   return check_launch("add_layernorm_kernel");
 }
 
+// ---- batched copy (unpatch by restoring the pristine weights) ---------------
+// Every tensor of a list copied by ONE launch: tensor t's 16-B vectors are cut
+// into kCopyChunk-vector chunks; chunk_prefix[t] is the first chunk of tensor
+// t (exclusive prefix, n + 1 entries), so a CTA finds its tensor with one
+// binary search per chunk and streams the chunk with 16-B loads / stores,
+// kCopyUnroll in flight per thread.  The reference's unmerge restores W by
+// subtracting (lora.py:107-114); a serving copy can restore it exactly.
+constexpr int kCopyThreads = 256, kCopyUnroll = 4;
+constexpr int64_t kCopyChunk = (int64_t)kCopyThreads * kCopyUnroll * 8;   // vectors per chunk (128 KB)
+
+struct CopyTable {
+  const uint4* const* src;
+  uint4* const* dst;
+  const int64_t* nvec;          // 16-B vectors per tensor
+  const int64_t* chunk_prefix;  // n + 1
+  int n;
+};
+
+__global__ void __launch_bounds__(kCopyThreads) batched_copy_kernel(CopyTable t) {
+  const int64_t chunks = t.chunk_prefix[t.n];
+  for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
+    int lo = 0, hi = t.n - 1;                   // last tensor whose first chunk <= ch
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (t.chunk_prefix[mid] <= ch) lo = mid; else hi = mid - 1;
+    }
+    const int64_t v0 = (ch - t.chunk_prefix[lo]) * kCopyChunk;
+    const int64_t v1 = min(t.nvec[lo], v0 + kCopyChunk);
+    const uint4* __restrict__ s = t.src[lo];
+    uint4* __restrict__ d = t.dst[lo];
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += (int64_t)kCopyThreads * kCopyUnroll) {
+      uint4 q[kCopyUnroll];
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u)
+        if (v + u * kCopyThreads < v1) q[u] = __ldcs(s + v + u * kCopyThreads);   // streamed once
+#pragma unroll
+      for (int u = 0; u < kCopyUnroll; ++u)
+        if (v + u * kCopyThreads < v1) __stcs(d + v + u * kCopyThreads, q[u]);
+    }
+  }
+}
+
 }  // namespace
 
 // K10 nearest 2x upsample, NHWC: y[n, 2i+a, 2j+b, :] = x[n, i, j, :].  One
@@ -283,5 +325,17 @@ int upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t 
                                                     (int)w, cv);
   return check_launch("upsample2x_kernel");
 }
+
+int batched_copy(const void* const* src_dev, void* const* dst_dev, const int64_t* nvec_dev,
+                 const int64_t* chunk_prefix_dev, int n, int64_t total_chunks, cudaStream_t st) {
+  if (n <= 0 || total_chunks <= 0) return SDB_OK;
+  CopyTable t{reinterpret_cast<const uint4* const*>(src_dev), reinterpret_cast<uint4* const*>(dst_dev), nvec_dev,
+              chunk_prefix_dev, n};
+  const int grid = (int)std::min<int64_t>(total_chunks, 8 * kNumSMs);
+  batched_copy_kernel<<<grid, kCopyThreads, 0, st>>>(t);
+  return check_launch("batched_copy_kernel");
+}
+
+int64_t batched_copy_chunk_vectors() { return kCopyChunk; }
 
 }  // namespace sdb

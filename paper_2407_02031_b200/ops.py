@@ -281,6 +281,47 @@ class LoraTmaPlan:
             int(max_ctas), _stream_ptr(stream)))
 
 
+class BatchedCopy:
+    """dst_i <- src_i for a fixed list of equally shaped device tensor pairs in
+    ONE launch (``sdb_batched_copy``): the restore-from-pristine unpatch of a
+    whole UNet.  Tensors must be contiguous in memory (any memory format), 16-B
+    aligned, with a size that is a multiple of 16 bytes."""
+
+    def __init__(self, srcs: Sequence[torch.Tensor], dsts: Sequence[torch.Tensor]):
+        if len(srcs) != len(dsts) or not srcs:
+            raise ValidationError("BatchedCopy needs matching, non-empty source / destination lists")
+        dev = srcs[0].device
+        nvec, ps, pd = [], [], []
+        for a, b in zip(srcs, dsts):
+            require_cuda(a, b)
+            nb = a.numel() * a.element_size()
+            if b.numel() * b.element_size() != nb or a.dtype != b.dtype:
+                raise ValidationError("BatchedCopy: source and destination differ in size or dtype")
+            if a.data_ptr() % 16 or b.data_ptr() % 16 or nb % 16:
+                raise ValidationError("BatchedCopy: 16-B aligned tensors of a multiple of 16 bytes only")
+            if not (a.is_contiguous() or a.is_contiguous(memory_format=torch.channels_last)) or \
+                    a.stride() != b.stride():
+                raise ValidationError("BatchedCopy: dense tensors with identical strides only")
+            nvec.append(nb // 16)
+            ps.append(a.data_ptr())
+            pd.append(b.data_ptr())
+        chunk = int(_lib.lib().sdb_batched_copy_chunk_vectors())
+        prefix = [0]
+        for v in nvec:
+            prefix.append(prefix[-1] + (v + chunk - 1) // chunk)
+        self.n, self.chunks = len(nvec), prefix[-1]
+        self.nbytes = 16 * sum(nvec)
+        tab = torch.tensor(ps + pd + nvec + prefix, dtype=torch.int64)
+        self._tab = tab.to(dev)
+        self._keep = (list(srcs), list(dsts))
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None) -> None:
+        n, base = self.n, self._tab.data_ptr()
+        _count(1)
+        _lib.check("sdb_batched_copy", _lib.lib().sdb_batched_copy(
+            base, base + 8 * n, base + 16 * n, base + 24 * n, n, self.chunks, _stream_ptr(stream)))
+
+
 # --------------------------------------------------------------------------
 # K2 — GroupNorm (+SiLU), NHWC
 # --------------------------------------------------------------------------

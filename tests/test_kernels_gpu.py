@@ -377,3 +377,21 @@ def test_hint_conv_out_cin_padding_256_to_320():
     assert y.shape == ref.shape
     err = (y.double() - ref).abs()
     assert (err <= ref.abs() * 2 ** -7 + 1e-2).all(), float(err.max())
+
+
+def test_batched_copy_restores_every_tensor_bitwise():
+    """sdb_batched_copy: one launch copies a list of tensors of ragged sizes
+    (incl. channels_last 4-d and ones smaller than a chunk) bitwise."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    shapes = [(1280, 1280), (320, 36 + 4), (8, 8), (10240, 1280), (320, 320, 3, 3), (77, 2048 + 8)]
+    src, dst = [], []
+    for sh in shapes:
+        a = torch.randn(sh, device="cuda", generator=g).to(torch.bfloat16)
+        if a.dim() == 4:
+            a = a.contiguous(memory_format=torch.channels_last)
+        src.append(a)
+        dst.append(torch.zeros_like(a))
+    cp = ops.BatchedCopy(src, dst)
+    cp.launch()
+    for a, b in zip(src, dst):
+        assert torch.equal(a, b)
