@@ -614,7 +614,8 @@ def lora_microbench(unet_p, shadow, hbm: float, cpu_full: bool = False, reps: in
     res["unmerge_in_place_ms"] = timed(lambda: in_place.launch(sign=-1.0))
     res["restore_from_pristine_ms"] = timed(lambda: restore.launch())     # sdb_batched_copy, one launch
     res["pointer_swap_ms"] = 0.0
-    out = {"layers": len(names), "ranks": list(ranks), "scales": list(scales), "stacked_rank": sum(ranks),
+    out = {"layers": len(unet_p.matrices), "restore_tensors": len(names), "ranks": list(ranks),
+           "scales": list(scales), "stacked_rank": sum(ranks),
            "kernel": out_of_place.plan.kernel, "alg_bytes_patch": alg, "alg_bytes_restore": 2 * w_bytes,
            "in_place_nbytes": w_bytes, "create_and_replace_nbytes": 2 * w_bytes + sum(
                a.nbytes for a, _ in ads), **{k: round(v, 4) for k, v in res.items()}}
@@ -626,8 +627,8 @@ def lora_microbench(unet_p, shadow, hbm: float, cpu_full: bool = False, reps: in
     out["peak_gbs"] = hbm
     del out_of_place, in_place, ads
     torch.cuda.empty_cache()
-    out["cpu_reference"] = cpu_merge_leg([(t.shape[0], t.numel() // t.shape[0]) for t in pristine],
-                                         sum(ranks), full=cpu_full)
+    mats = [unet_p.matrix_view(n) for n, _ in unet_p.matrices]
+    out["cpu_reference"] = cpu_merge_leg([tuple(m.shape) for m in mats], sum(ranks), full=cpu_full)
     return out
 
 

@@ -21,22 +21,24 @@
 //             16-B loads in flight and accumulates shifted sums (shift = the
 //             CTA's first pixel per group: no cancellation); rows folded in
 //             shared memory, one warp per group turns the CTA's sums into
-//             fp64 raw moments of x' = x + add and writes them to its slot.
-//             The LAST CTA of a sample (threadfence + arrival counter) sums
-//             the sample's slots in a fixed order — deterministic, no float
-//             atomics — and publishes (mean, var) per group.
+//             fp64 raw moments of x' = x + add and adds them to the site's
+//             bank as exact fixed-point integers (red.global.add of an int64
+//             integer part + an int64 2^-40 fraction): integer addition is
+//             associative, so the statistics are bit-for-bit the same
+//             whatever order the CTAs land in (round 1 added fp64 with
+//             atomics: order-dependent), and no CTA waits for a reduction.
 //   kernel 2  gn_apply_kernel: per CTA a table a_c = gamma_c rstd_g,
 //             b_c = beta_c + (add_c - mean_g) a_c for its sample in shared
 //             memory, then y = act(x a_c + b_c) streamed (same interleaved
 //             row blocks, ~4 CTAs per SM) with kApplyUnroll vectors in flight
 //             per thread; the map is an L2 hit after kernel 1.
 //
-// Workspace (per call site, zeroed once; every launch leaves the counters at
-// zero): [header: arrival counter per sample][stats: double2 (mean, var)
-// per (sample, group)][slots: double2 (sum x', sum x'^2) per (sample, chunk,
-// group)].  K3's fused form (inject_gn_kernel) publishes into the same
-// layout, so its consumer GN site runs kernel 2 alone.
-//
+// Workspace (per call site, zeroed once, 64 KB, any shape): a header (epoch,
+// current bank, high-water batch, arrival counter) and two banks of
+// [16 samples][64 groups] fixed-point (sum x', sum x'^2).  Producer launches
+// alternate banks (see producer_bank); K3's fused form (inject_gn_kernel)
+// is a producer too, so its consumer GN site runs kernel 2 alone.
+
 // Optional add_nc [N][C] (fp32) is added to x before normalisation (x' = x +
 // add): the ResNet block's time-embedding projection (h = conv1(x) +
 // temb_proj[n, c]) is fused here instead of costing its own read + write of
@@ -63,10 +65,18 @@ constexpr int kMaxN = 16;            // batch (x2 for CFG): serving batch 8 with
 constexpr int kMaxGroups = 64;
 constexpr int kStatsUnroll = 4;      // 16-B loads in flight per thread (stats; 8 measured slower, scripts/micro/gnstats_micro.cu)
 constexpr int kApplyUnroll = 4;      // vectors in flight per thread (apply)
-constexpr size_t kWsHeader = 256;    // arrival counter per sample (u32)
-constexpr size_t kStatsBytes = (size_t)kMaxN * kMaxGroups * 8;   // float2 (mean, var)
-
-__host__ __device__ __forceinline__ size_t ws_slots_offset() { return kWsHeader + kStatsBytes; }
+// Workspace: header | 2 banks of [kMaxN][kMaxGroups] x {sum x, sum x^2}, each
+// an exact fixed-point pair (int64 integer part, int64 2^-40 fraction).
+constexpr size_t kWsHeader = 256;
+constexpr int kBankWords = kMaxN * kMaxGroups * 4;
+constexpr size_t kWsBytes = kWsHeader + 2 * (size_t)kBankWords * sizeof(long long);
+constexpr double kFracScale = 1099511627776.0;        // 2^40
+struct WsHeader {
+  unsigned int epoch;      // bank of the next producer launch = epoch & 1
+  unsigned int cur;        // bank the last producer launch filled (what apply reads)
+  unsigned int hwm;        // rows (samples) any launch ever used: rows >= hwm of both banks are zero
+  unsigned int arrivals;   // CTAs of the running producer launch that finished
+};
 
 // Decomposition of one (n, hw, c) map for a kernel with ~ctas_per_sm CTAs of
 // <= max_threads threads per SM: a CTA is rpp pixel rows x cv lanes; a
@@ -91,14 +101,12 @@ GnShape gn_shape(int64_t n, int64_t hw, int64_t c, int64_t groups, int max_threa
   return s;
 }
 
-// slots for the most CTAs per sample any kernel of the family launches
-// (gn_shape caps chunks at ~2 per SM over the batch)
-int64_t max_chunks(int64_t n) { return std::max<int64_t>(1, (2 * kNumSMs + n - 1) / n); }
-
 size_t ws_bytes_for(int64_t n, int64_t hw, int64_t c, int64_t groups) {
+  (void)n;
   (void)hw;
   (void)c;
-  return ws_slots_offset() + (size_t)n * max_chunks(n) * groups * 16;
+  (void)groups;
+  return kWsBytes;   // fixed: one workspace serves any shape (batch <= 16, groups <= 64)
 }
 
 // Group of each of a thread's 8 channels without a division per channel: one
@@ -130,57 +138,58 @@ __device__ __forceinline__ void fold_rows(float* red1, float* red2, int c, int r
   }
 }
 
-// The chunk's per-group raw moments are in its slot: count the chunk in; the
-// last chunk of the sample reduces every slot in a fixed order and publishes
-// (mean, var).  Thread t takes group t % G and the chunks t / G + j * (T / G),
-// all its loads issued at once (the tail is one L2 round trip, not one per
-// slot); partial sums meet in shared memory and are added in thread order —
-// the same result whichever CTA arrives last.  The last CTA re-arms the counter.
-__device__ __forceinline__ void finish_chunk(uint8_t* ws, int n, int chunks, int groups, double count) {
-  __shared__ int s_last;
-  __shared__ double2 s_part[kMaxThreads];
-  __threadfence();
+// ---- the statistics exchange: exact fixed-point sums, no float atomics ------
+// Each producer CTA adds its per-group fp64 (sum x', sum x'^2) to the bank as
+// int64 integer part + int64 2^-40 fraction (red.global.add: integer sums are
+// order-independent, so the result is deterministic whichever CTA lands
+// first, and no CTA waits on them).  Banks alternate per producer launch:
+// launch L reads epoch e (the same for all its CTAs: e only advances after
+// every CTA of L arrived), accumulates into bank e & 1, zeroes bank (e + 1) & 1
+// for launch L + 1 and records cur = e & 1; its last CTA advances the epoch.
+// A consumer (the apply kernel, later on the same stream) reads bank `cur`.
+__device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// bank of this producer launch; zeroes the idle bank (a grid-strided slice per CTA)
+__device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch) {
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+  const unsigned int epoch = ld_relaxed(&hdr->epoch);
+  const int rows = max((int)ld_relaxed(&hdr->hwm), nbatch);
+  long long* banks = reinterpret_cast<long long*>(ws + kWsHeader);
+  long long* idle = banks + (size_t)((epoch + 1u) & 1u) * kBankWords;
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x, ctas = gridDim.x * gridDim.y;
+  for (int i = cta * blockDim.x + threadIdx.x; i < rows * kMaxGroups * 4; i += ctas * blockDim.x) idle[i] = 0;
+  if (cta == 0 && threadIdx.x == 0) {
+    hdr->cur = epoch & 1u;
+    hdr->hwm = (unsigned int)rows;
+  }
+  return banks + (size_t)(epoch & 1u) * kBankWords;
+}
+
+__device__ __forceinline__ void red_fixed(long long* w, double v) {
+  const double hi = floor(v);
+  atomicAdd(reinterpret_cast<unsigned long long*>(w), (unsigned long long)(long long)hi);
+  atomicAdd(reinterpret_cast<unsigned long long*>(w + 1), (unsigned long long)__double2ll_rn((v - hi) * kFracScale));
+}
+
+// this CTA is done with the bank: the last one advances the epoch
+__device__ __forceinline__ void producer_arrive(uint8_t* ws) {
   __syncthreads();
-  unsigned int* ctr = reinterpret_cast<unsigned int*>(ws) + n;
-  if (threadIdx.x == 0) s_last = atomicAdd(ctr, 1u) == (unsigned)(chunks - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const double2* slots = reinterpret_cast<const double2*>(ws + ws_slots_offset()) + (size_t)n * chunks * groups;
-  float2* stats = reinterpret_cast<float2*>(ws + kWsHeader) + (size_t)n * kMaxGroups;
-  const int per = blockDim.x / groups;            // threads per group (>= 1: blockDim >= groups)
-  const int g = threadIdx.x % groups, k0 = threadIdx.x / groups;
-  double m1 = 0.0, m2 = 0.0;
-  if (k0 < per) {
-    constexpr int kBatch = 8;
-    for (int k = k0; k < chunks; k += kBatch * per) {
-      double2 p[kBatch];
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
-        const int kk = k + j * per;
-        p[j] = kk < chunks ? __ldcg(slots + (size_t)kk * groups + g) : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
-        m1 += p[j].x;
-        m2 += p[j].y;
-      }
+  if (threadIdx.x == 0) {
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (atomicAdd(&hdr->arrivals, 1u) == total - 1) {
+      hdr->arrivals = 0u;
+      atomicAdd(&hdr->epoch, 1u);
     }
   }
-  s_part[threadIdx.x] = make_double2(m1, m2);
-  __syncthreads();
-  if (threadIdx.x < groups) {
-    double a = 0.0, b = 0.0;
-    for (int q = 0; q < per; ++q) {
-      const double2 v = s_part[q * groups + threadIdx.x];
-      a += v.x;
-      b += v.y;
-    }
-    const double mean = a / count;
-    const double var = b / count - mean * mean;      // fp64: exact enough at any |mean| / std of the UNet
-    stats[threadIdx.x] = make_float2((float)mean, (float)(var < 0.0 ? 0.0 : var));
-  }
-  if (threadIdx.x == 0) *ctr = 0u;
+}
+
+__device__ __forceinline__ double fixed_value(const long long* w) {
+  return (double)__ldg(w) + (double)__ldg(w + 1) / kFracScale;
 }
 
 // All index math is 32-bit within one sample (host checks n * hw * c < 2^31).
@@ -265,10 +274,11 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8
     }
     __syncthreads();
   }
-  // one warp per group: lanes over the group's channels, shuffle-reduce, the CTA's slot
-  double2* slot = reinterpret_cast<double2*>(ws + ws_slots_offset()) + ((size_t)n * chunks + blockIdx.x) * groups;
+  // one warp per group: lanes over the group's channels, shuffle-reduce, lane 0
+  // adds the CTA's fixed-point sums to the bank
+  long long* bank = producer_bank(ws, gridDim.y) + (size_t)n * kMaxGroups * 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int g = warp; g < groups; g += nwarps) {
+  for (int g = warp; warp < nwarps && g < groups; g += nwarps) {   // full warps only
     double m1 = 0.0, m2 = 0.0;
     for (int k = lane; k < cpg; k += 32) {
       m1 += red1[g * cpg + k];
@@ -279,9 +289,12 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8
       m1 += __shfl_xor_sync(0xffffffffu, m1, o);
       m2 += __shfl_xor_sync(0xffffffffu, m2, o);
     }
-    if (lane == 0) slot[g] = make_double2(m1, m2);
+    if (lane == 0) {
+      red_fixed(bank + g * 4, m1);
+      red_fixed(bank + g * 4 + 2, m2);
+    }
   }
-  finish_chunk(ws, n, chunks, groups, (double)hw * (double)cpg);
+  producer_arrive(ws);
 }
 
 constexpr int kApplyThreads = 512;
@@ -297,16 +310,27 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
   const int v = threadIdx.x % cv;
   const int r = threadIdx.x / cv;
   const int c0 = v * 8;
+  // the group statistics from the producer's bank (fixed point -> fp64 -> mean, var)
+  __shared__ float2 gstat[kMaxGroups];
+  {
+    const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws);
+    const unsigned int cur = __ldg(&hdr->cur);
+    const long long* bank = reinterpret_cast<const long long*>(ws + kWsHeader) + (size_t)cur * kBankWords +
+                            (size_t)n * kMaxGroups * 4;
+    const double count = (double)hw * (double)cpg;
+    for (int g = threadIdx.x; g < c / cpg; g += blockDim.x) {
+      const double mean = fixed_value(bank + g * 4) / count;
+      const double var = fixed_value(bank + g * 4 + 2) / count - mean * mean;
+      gstat[g] = make_float2((float)mean, (float)(var < 0.0 ? 0.0 : var));
+    }
+  }
+  __syncthreads();
   // this thread's 8 channels: a_c = gamma_c rstd_g, b_c = beta_c + (add_c - mean_g) a_c
-  // (every load of the prologue issued together: one round trip)
-  const float2* stats = reinterpret_cast<const float2*>(ws + kWsHeader) + (size_t)n * kMaxGroups;
   int g8[8];
   channel_groups(c0, cpg, g8);
   float2 st[8];
 #pragma unroll
-  // L1-cached loads: every CTA reads the same few lines (an L2-only __ldcg here
-  // made them a hot spot — ~35K requests on 4 lines serialised at one L2 slice)
-  for (int j = 0; j < 8; ++j) st[j] = __ldg(stats + g8[j]);
+  for (int j = 0; j < 8; ++j) st[j] = gstat[g8[j]];
   const float4 one = make_float4(1.f, 1.f, 1.f, 1.f), zero = make_float4(0.f, 0.f, 0.f, 0.f);
   const float4 ga0 = gamma ? *reinterpret_cast<const float4*>(gamma + c0) : one;
   const float4 ga1 = gamma ? *reinterpret_cast<const float4*>(gamma + c0 + 4) : one;
@@ -373,8 +397,8 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
 // block's residual add, the up-block concat, a folded conv bias).  This
 // kernel IS that K3 pass — out = [hidden (+hb) | skip (+sb) + sum s_i res_i] —
 // and publishes the GroupNorm statistics of the rounded output into the GN
-// site's workspace (per-chunk fp64 slots + last-CTA reduction, as
-// gn_stats_kernel), so that site runs gn_apply_kernel alone: one full read of
+// site's workspace (the fixed-point bank, as gn_stats_kernel), so that site
+// runs gn_apply_kernel alone: one full read of
 // the feature map and one launch less per site.  Per thread the sums are raw
 // fp32 over <= ~30 rows (relative error ~1e-6 of sum x^2, i.e. a variance
 // error ~1e-6 (1 + mean^2/var) — the UNet's post-residual activations sit at
@@ -464,10 +488,10 @@ inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T>
   *reinterpret_cast<float4*>(red2 + r * c + c0) = make_float4(s2[0].x, s2[0].y, s2[1].x, s2[1].y);
   *reinterpret_cast<float4*>(red2 + r * c + c0 + 4) = make_float4(s2[2].x, s2[2].y, s2[3].x, s2[3].y);
   fold_rows(red1, red2, c, rpp);
-  // one warp per group: lanes over its channels (fp64), shuffle-reduce, the chunk's slot
-  double2* slot = reinterpret_cast<double2*>(ws + ws_slots_offset()) + ((size_t)n * chunks + blockIdx.x) * groups;
+  // one warp per group: lanes over its channels (fp64), shuffle-reduce, fixed-point sums into the bank
+  long long* bank = producer_bank(ws, gridDim.y) + (size_t)n * kMaxGroups * 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int g = warp; g < groups; g += nwarps) {
+  for (int g = warp; warp < nwarps && g < groups; g += nwarps) {   // full warps only
     double m1 = 0.0, m2 = 0.0;
     for (int k = lane; k < cpg; k += 32) {
       m1 += (double)red1[g * cpg + k];
@@ -478,9 +502,12 @@ inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T>
       m1 += __shfl_xor_sync(0xffffffffu, m1, o);
       m2 += __shfl_xor_sync(0xffffffffu, m2, o);
     }
-    if (lane == 0) slot[g] = make_double2(m1, m2);
+    if (lane == 0) {
+      red_fixed(bank + g * 4, m1);
+      red_fixed(bank + g * 4 + 2, m2);
+    }
   }
-  finish_chunk(ws, n, chunks, groups, (double)hw * (double)cpg);
+  producer_arrive(ws);
 }
 
 template <typename K>
@@ -550,7 +577,6 @@ int run_inject_gn(void* out, const void* hidden, const void* skip, const void* c
   const GnShape s = gn_shape(n, hw, c, groups, 256, 2);
   const int rpp = s.rpp, threads = s.threads;
   if (threads > kInjThreads) return fail(SDB_EINVAL, "residual_inject_gn: channels > 4096 unsupported");
-  if (s.chunks > max_chunks(n)) return fail(SDB_EINVAL, "residual_inject_gn: internal decomposition error");
   const size_t smem = (size_t)2 * rpp * c * sizeof(float);
   dim3 grid((unsigned)s.chunks, (unsigned)n);
   T* o = static_cast<T*>(out);
