@@ -354,11 +354,13 @@ def run_caas(args, world, rank, local):
     barrier_sync(world)
     image(dev_in, timeline=tl)
     barrier_sync(world)
-    summ = tl.summary()
-    red = torch.tensor([summ.get("step_ms", 0.0) if role == "service" else 0.0,
+    mine_tl = tl.summary()
+    red = torch.tensor([mine_tl.get("step_ms", 0.0) if role == "service" else 0.0,
                         1.0 if role == "service" else 0.0], device=_red_device(), dtype=torch.float64)
     dist.all_reduce(red, op=dist.ReduceOp.SUM)
     svc_ms = float(red[0].item() / red[1].item()) if red[1].item() > 0 else 0.0
+    # the base's decoder wait, split with the services' measured step (compute + push)
+    summ = tl.summary(branch_ms=svc_ms) if role == "base" else mine_tl
     producers = len(layout.groups)
     images = args.steps * producers * B
     lat = torch.tensor([statistics.median(per_image) if (role == "base" or (role == "solo" and

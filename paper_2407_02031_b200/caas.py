@@ -721,10 +721,12 @@ class StepTimeline:
         self.steps.append(rec)
         return rec
 
-    def summary(self, comm_ms: float = 0.0) -> dict:
+    def summary(self, comm_ms: float = 0.0, branch_ms: Optional[float] = None) -> dict:
         """Mean per-step ms: encoder, each branch (ControlNet compute, from the
         step start), decoder, the decoder's wait and its comm / compute /
-        fetch / queue split (reference accounting)."""
+        fetch / queue split (reference accounting).  branch_ms: the critical
+        branch's per-step time measured elsewhere (multi-GPU: on the service
+        ranks, compute + push) when this timeline has no branch events."""
         n = len(self.steps)
         if n == 0:
             return {}
@@ -740,10 +742,11 @@ class StepTimeline:
             acc["step_ms"] += r["start"].elapsed_time(r["dec_end"])
             acc["decoder_wait_ms"] += gap
             branch = [a + b for a, b in zip(branch, br)] if branch is not None else br
-            if gap > 0 and br:
+            crit = max(br) if br else branch_ms
+            if gap > 0 and crit is not None:
                 comm = min(gap, comm_ms)
                 rest = gap - comm
-                compute = min(rest, max(br))          # the critical branch's compute
+                compute = min(rest, crit)             # the critical branch's compute
                 rest -= compute
                 acc["comm_ms"] += comm
                 acc["controlnet_wait_ms"] += compute

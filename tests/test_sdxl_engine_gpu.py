@@ -80,10 +80,10 @@ def run_engine(dtype, name="sdxl"):
     return per_step, up, cps, factors, pipe.unet_p.matrices, req
 
 
-def oracle(up, cps, factors, matrices, req, bf16_acts, name="sdxl"):
+def oracle(up, cps, factors, matrices, req, bf16_acts, name="sdxl", max_steps=None):
     cfg, scales, _ = ENGINES[name]
     return R.denoise(cfg, up, cps, req, scales, STEPS, GUIDANCE, adapters=factors, matrices=matrices,
-                     boundary=BOUNDARY, bf16_acts=bf16_acts)
+                     boundary=BOUNDARY, bf16_acts=bf16_acts, max_steps=max_steps)
 
 
 @pytest.fixture
@@ -101,12 +101,12 @@ def test_engine_fp32_per_step(fp32_mode, name):
     torch.cuda.empty_cache()
     ref = oracle(up, cps, factors, matrices, req, False, name)
     errs = [rel(a, b) for a, b in zip(dev, ref)]
-    # the same oracle in fp64: how far fp32 arithmetic itself (device or CPU)
-    # sits from the exact result at SDXL depth
+    # the same oracle in fp64 (step 1, before the patch lands): how far fp32
+    # arithmetic itself (device or CPU) sits from the exact result at SDXL depth
     up64 = {k: v.double() for k, v in up.items()}
     cps64 = [{k: v.double() for k, v in c.items()} for c in cps]
     del up, cps
-    truth = oracle(up64, cps64, factors, matrices, req, False, name)
+    truth = oracle(up64, cps64, None, matrices, req, False, name, max_steps=1)   # step 1: pristine weights
     d_truth = [rel(a, b) for a, b in zip(dev, truth)]
     o_truth = [rel(a, b) for a, b in zip(ref, truth)]
     print(f"{name} engine fp32 per-step rel-L2: device-vs-oracle", ["%.2e" % e for e in errs],
