@@ -168,14 +168,27 @@ int sdb_lora_tc_set_mode(int mode);
  * workspace must be ordered on one stream.  y may alias x.
  * ======================================================================== */
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
-/* K2 form selection: mode 0 (default) runs the single-pass cluster form
- * (the whole map of one (sample, channel slab) in the shared memory of a
- * thread-block cluster: one read, one write, one launch) wherever the shape
- * fits (bf16, C/G >= 8, slab rows <= 200 KB per CTA, <= 16 CTAs), else the
- * two-pass form; mode 1 forces the two-pass form.  sdb_groupnorm_launches
- * returns the kernel launches sdb_groupnorm_silu will make for a shape. */
+/* K2 form selection: mode 0 (default) runs a single-pass cluster form
+ * wherever the shape fits (bf16, C/G >= 8): one launch, one read, one write,
+ * a thread-block cluster per (sample, channel slab) holding that slab of the
+ * map in shared memory — round 1's form for maps <= 6 MB, the streamed form
+ * (TMA chunks overlapped with the statistics, each chunk stored as soon as it
+ * is normalised) for larger maps up to 64 MB — else the two-pass form.
+ * Mode 1 forces the two-pass form, 2 only round 1's cluster form, 3 only the
+ * streamed form.  sdb_groupnorm_launches returns the kernel launches
+ * sdb_groupnorm_silu will make for a shape; sdb_groupnorm_stream_plan fills
+ * out7 = {slab channels, cluster CTAs, rows per CTA, rows per chunk, chunks,
+ * clusters, co-resident clusters} of the streamed form (0 = not eligible). */
 void sdb_groupnorm_set_mode(int mode);
 int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
+int sdb_groupnorm_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7);
+
+/* Programmatic dependent launch (default on; SDB_PDL=0 in the environment
+ * turns it off at load): the streaming kernels (K2-K7, K9, K10) launch with
+ * the programmatic-stream-serialisation attribute and wait (griddepcontrol)
+ * before touching their predecessor's data, so their launch overlaps the tail
+ * of the previous kernel on the stream.  Returns the previous setting. */
+int sdb_set_pdl(int on);
 int sdb_groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta,
                        const float* add_nc, int64_t n, int64_t hw, int64_t c, int64_t groups, float eps,
                        int apply_silu, int dtype, void* workspace, void* stream);

@@ -42,6 +42,8 @@ EXPORTED = (
     "sdb_conv_out",
     "sdb_groupnorm_set_mode",
     "sdb_groupnorm_launches",
+    "sdb_groupnorm_stream_plan",
+    "sdb_set_pdl",
 )
 
 
@@ -113,6 +115,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.sdb_groupnorm_set_mode.argtypes = [i32]
     lib.sdb_groupnorm_launches.restype = i32
     lib.sdb_groupnorm_launches.argtypes = [i64, i64, i64, i64, i32]
+    lib.sdb_set_pdl.restype = i32
+    lib.sdb_set_pdl.argtypes = [i32]
+    lib.sdb_groupnorm_stream_plan.restype = i32
+    lib.sdb_groupnorm_stream_plan.argtypes = [i64, i64, i64, i64, ctypes.POINTER(ctypes.c_int)]
     lib.sdb_conv_out.restype = i32
     lib.sdb_conv_out.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, i32, vp]
 

@@ -1,6 +1,7 @@
 // api.cu — the extern "C" boundary declared in include/sdb_api.h.
 // Argument validation + dispatch only; the kernels live in the other units.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -10,6 +11,13 @@ namespace sdb {
 
 thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+// programmatic dependent launch for the streaming kernels (common.cuh); SDB_PDL=0 turns it off
+static int pdl_default() {
+  const char* e = getenv("SDB_PDL");
+  return e == nullptr || atoi(e) != 0;
+}
+int g_pdl = pdl_default();
 
 // lora_patch.cu
 int64_t simt_tiles(int64_t h1, int64_t h2);
@@ -63,6 +71,7 @@ int memcpy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // gn_cluster.cu
 extern int g_gn_cluster_mode;
 int gn_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
+int gn_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7);
 // conv_out.cu
 int conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h, int64_t w_,
              int64_t c, int64_t cout, int dtype, cudaStream_t st);
@@ -293,8 +302,18 @@ int sdb_cfg_ddim_step(const void* eps, int eps_dtype, const float* x, float* x_o
 
 void sdb_groupnorm_set_mode(int mode) { g_gn_cluster_mode = mode; }
 
+int sdb_set_pdl(int on) {
+  const int prev = g_pdl;
+  g_pdl = on != 0;
+  return prev;
+}
+
 int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype) {
   return gn_launches(n, hw, c, groups, dtype);
+}
+
+int sdb_groupnorm_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7) {
+  return gn_stream_plan(n, hw, c, groups, out7);
 }
 
 int sdb_conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h,

@@ -20,6 +20,7 @@ __global__ void __launch_bounds__(256)
 cfg_ddim_kernel(const TE* __restrict__ eps, const float* x, float* x_out,   // x_out may alias x (in place)
                 TI* __restrict__ unet_in, int64_t L, const float* __restrict__ coef,
                 int* __restrict__ step_dev) {
+  pdl_wait();
   const int step = *reinterpret_cast<volatile int*>(step_dev);
   const float a_t = coef[step * 4 + 0];
   const float a_prev = coef[step * 4 + 1];
@@ -60,7 +61,7 @@ int run_cfg(const void* eps, const float* x, float* x_out, void* unet_in, int64_
   int64_t grid = (L + 255) / 256;
   if (grid > kNumSMs * 4) grid = kNumSMs * 4;
   if (grid < 1) grid = 1;
-  cfg_ddim_kernel<TE, TI><<<(unsigned)grid, 256, 0, st>>>(static_cast<const TE*>(eps), x, x_out,
+  launch_k(cfg_ddim_kernel<TE, TI>, (unsigned)grid, 256, 0, st, static_cast<const TE*>(eps), x, x_out,
                                                           static_cast<TI*>(unet_in), L, coef, step_dev);
   return check_launch("cfg_ddim_kernel");
 }

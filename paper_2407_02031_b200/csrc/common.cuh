@@ -34,6 +34,37 @@ inline int check_launch(const char* what) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Every streaming kernel of this library is launched with the programmatic-
+// stream-serialisation attribute and begins with pdl_wait() (griddepcontrol.
+// wait) before it touches memory the previous kernel on its stream may read or
+// write: the launch and CTA rasterisation of kernel k+1 then overlap the tail
+// of kernel k (a cuBLAS / cuDNN kernel or one of ours) instead of following
+// its completion.  Inside CUDA graphs the attribute becomes a programmatic
+// edge.  Kernels never trigger early (no griddepcontrol.launch_dependents):
+// the dependent launches as the last CTA of its predecessor exits, so it can
+// never occupy SM slots its predecessor's later waves need, and a kernel that
+// starts early has only ever its immediate predecessor in flight.  Only state
+// that predecessor cannot touch (weights, gamma / beta, the per-request K/V
+// cache, shared memory, tensor maps) is read before the wait.
+extern int g_pdl;   // 1 = launch with PDL (default), 0 = plain launches (SDB_PDL=0 / sdb_set_pdl)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- scalar conversions -------------------------------------------------
 template <typename T> __device__ __forceinline__ float to_f32(T v);
 template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }

@@ -61,6 +61,7 @@ template <typename T, int STRIP, int MINB>
 __global__ void __launch_bounds__(kWarps * 32, MINB)
 conv_out_kernel(const T* __restrict__ x, const T* __restrict__ w, const float* __restrict__ bias,
                 float* __restrict__ out, int N, int H, int W, int C) {
+  pdl_wait();
   constexpr int kStrip = STRIP;
   using P = Pair<T>;
   using V = typename P::V;
@@ -188,6 +189,7 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS, 1)
 conv_out_mma_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
                     const float* __restrict__ bias, float* __restrict__ out, int N, int H, int W, int C) {
+  pdl_wait();
   extern __shared__ uint2 btab[];                 // [9][C/16][32]
   const int KC = C >> 4;
   const int chunks = C >> 5;
@@ -287,7 +289,7 @@ int launch_conv_out_mma(const void* x, const void* w, const float* bias, float* 
   const int want = 512 / THREADS > 0 ? 512 / THREADS : 1;
   const long cap = (long)kNumSMs * (per_sm > 0 ? (per_sm < want ? per_sm : want) : 1);
   if (grid > cap) grid = cap;
-  kern<<<(unsigned)grid, warps * 32, smem, st>>>(static_cast<const __nv_bfloat16*>(x),
+  launch_k(kern, (unsigned)grid, warps * 32, smem, st, static_cast<const __nv_bfloat16*>(x),
                                                  static_cast<const __nv_bfloat16*>(w), bias, out, N, H, W, C);
   return check_launch("conv_out_mma_kernel");
 }
@@ -308,7 +310,7 @@ int launch_conv_out(const void* x, const void* w, const float* bias, float* out,
   long grid = (strips + kWarps - 1) / kWarps;
   const long cap = (long)kNumSMs * (per_sm > 0 ? per_sm : 1);
   if (grid > cap) grid = cap;
-  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(static_cast<const T*>(x), static_cast<const T*>(w), bias, out,
+  launch_k(kern, (unsigned)grid, kWarps * 32, smem, st, static_cast<const T*>(x), static_cast<const T*>(w), bias, out,
                                                   N, H, W, C);
   return check_launch("conv_out_kernel");
 }

@@ -106,6 +106,7 @@ template <typename T, int DP, int NKP>
 __global__ void __launch_bounds__(kThreads)
 cross_attn_kernel(const T* __restrict__ q, int64_t ldq, const T* __restrict__ kv, int64_t ldkv, int64_t voff,
                   T* __restrict__ o, int64_t ldo, int lq, int lk, int d, float scale_log2, int tpw) {
+  pdl_wait();
   constexpr int LDS = DP + 8;                     // smem row pitch (elements): 16 B skew, no ldmatrix conflicts
   constexpr int NC = NKP / 8;                     // key chunks of 8 (S columns)
   constexpr int DC = DP / 8;                      // head-dim chunks of 8 (O columns)
@@ -281,6 +282,7 @@ template <int NKP>
 __global__ void __launch_bounds__(kTcThreads)
 xattn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap, int64_t voff,
                 __nv_bfloat16* __restrict__ o, int64_t ldo, int lq, int lk, float scale_log2) {
+  
   static_assert(NKP % 16 == 0 && NKP <= 128, "keys padded to 16, at most two 64-key atoms");
   constexpr int kKBytes = ((NKP * 128 + 1023) / 1024) * 1024;
   constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NKP >> 3) << 17) |
@@ -302,10 +304,13 @@ xattn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
     for (int i = 0; i < 3; ++i) mbar_init(smem_u32(bars + i), 1);
     mbar_fence_init();
     mbar_expect_tx(smem_u32(bars), kTcM * 128 + 2 * NKP * 128);
-    tma_load_2d(smem_u32(sQ), &qmap, h * 64, n * lq + q0, smem_u32(bars), policy_evict_first());
+    // K_h / V_h come from the per-request K/V cache (never the previous
+    // kernel's output): fetched before the programmatic wait
     tma_load_2d(smem_u32(sK), &kvmap, h * 64, n * lk, smem_u32(bars), policy_evict_last());
     tma_load_2d(smem_u32(sV), &kvmap, (int)voff + h * 64, n * lk, smem_u32(bars), policy_evict_last());
   }
+  pdl_wait();
+  if (tid == 0) tma_load_2d(smem_u32(sQ), &qmap, h * 64, n * lq + q0, smem_u32(bars), policy_evict_first());
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "r"(128));
@@ -446,7 +451,7 @@ int launch_tc(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t 
     attr = true;
   }
   dim3 grid((unsigned)((lq + kTcM - 1) / kTcM), (unsigned)heads, (unsigned)n);
-  xattn_tc_kernel<NKP><<<grid, kTcThreads, smem, st>>>(qm, km, voff, static_cast<__nv_bfloat16*>(o), ldo, lq, lk,
+  launch_k(xattn_tc_kernel<NKP>, grid, kTcThreads, smem, st, qm, km, voff, static_cast<__nv_bfloat16*>(o), ldo, lq, lk,
                                                        scale * 1.4426950408889634f);
   return check_launch("xattn_tc_kernel");
 }
@@ -466,7 +471,7 @@ int launch(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t vof
     cudaFuncSetAttribute(cross_attn_kernel<T, DP, NKP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  cross_attn_kernel<T, DP, NKP><<<grid, kThreads, smem, st>>>(
+  launch_k(cross_attn_kernel<T, DP, NKP>, grid, kThreads, smem, st, 
       static_cast<const T*>(q), ldq, static_cast<const T*>(kv), ldkv, voff, static_cast<T*>(o), ldo, lq, lk, d,
       scale * 1.4426950408889634f, tpw);
   return check_launch("cross_attn_kernel");

@@ -68,6 +68,7 @@ __device__ __forceinline__ float2 gelu2(float2 g) {
 template <typename T>
 __global__ void __launch_bounds__(128)
 geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int rows, int f) {
+  pdl_wait();
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c >= f) return;
   const T* src = proj + c;
@@ -115,6 +116,7 @@ template <typename T, int NV>
 __global__ void __launch_bounds__(128)
 add_layernorm_kernel(T* x, const T* __restrict__ d, T* __restrict__ y, const T* __restrict__ gamma,
                      const T* __restrict__ beta, int rows, int c, float eps) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
   for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows; row += warps_total) {
@@ -189,7 +191,7 @@ int run_geglu(const void* proj, void* out, int64_t rows, int64_t f, cudaStream_t
   // ~16 CTAs of 128 threads per SM in flight overall
   const int64_t want_y = std::max<int64_t>(1, (int64_t)kNumSMs * 16 / gx);
   const unsigned gy = (unsigned)std::min<int64_t>(std::min<int64_t>(want_y, (rows + kGegluVec - 1) / kGegluVec), 65535);
-  geglu_kernel<T><<<dim3(gx, std::max(gy, 1u)), 128, 0, st>>>(static_cast<const T*>(proj), static_cast<T*>(out),
+  launch_k(geglu_kernel<T>, dim3(gx, std::max(gy, 1u)), 128, 0, st, static_cast<const T*>(proj), static_cast<T*>(out),
                                                                (int)rows, (int)f);
   return check_launch("geglu_kernel");
 }
@@ -207,16 +209,16 @@ int run_add_ln(void* x, const void* d, void* y, const void* gamma, const void* b
   const T* bp = static_cast<const T*>(beta);
   const int nv = (int)((c / 8 + 31) / 32);
   switch (nv) {
-    case 1: add_layernorm_kernel<T, 1><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 2: add_layernorm_kernel<T, 2><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 3: add_layernorm_kernel<T, 3><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 4: add_layernorm_kernel<T, 4><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 5: add_layernorm_kernel<T, 5><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 6: add_layernorm_kernel<T, 6><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 7: add_layernorm_kernel<T, 7><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 8: add_layernorm_kernel<T, 8><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 9: add_layernorm_kernel<T, 9><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
-    case 10: add_layernorm_kernel<T, 10><<<grid, 128, 0, st>>>(xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 1: launch_k(add_layernorm_kernel<T, 1>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 2: launch_k(add_layernorm_kernel<T, 2>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 3: launch_k(add_layernorm_kernel<T, 3>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 4: launch_k(add_layernorm_kernel<T, 4>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 5: launch_k(add_layernorm_kernel<T, 5>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 6: launch_k(add_layernorm_kernel<T, 6>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 7: launch_k(add_layernorm_kernel<T, 7>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 8: launch_k(add_layernorm_kernel<T, 8>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 9: launch_k(add_layernorm_kernel<T, 9>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
+    case 10: launch_k(add_layernorm_kernel<T, 10>, grid, 128, 0, st, xp, dp, yp, gp, bp, rows, c, eps); break;
     default: return fail(SDB_EINVAL, "add_layernorm: channels must be <= 2560");
   }
   return check_launch("add_layernorm_kernel");
@@ -241,6 +243,7 @@ struct CopyTable {
 };
 
 __global__ void __launch_bounds__(kCopyThreads) batched_copy_kernel(CopyTable t) {
+  pdl_wait();
   const int64_t chunks = t.chunk_prefix[t.n];
   for (int64_t ch = blockIdx.x; ch < chunks; ch += gridDim.x) {
     int lo = 0, hi = t.n - 1;                   // last tensor whose first chunk <= ch
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(kCopyThreads) batched_copy_kernel(CopyTable t)
 // [2,640,64,64] (scripts/upsample_probe.py), i.e. ~5% of the HBM rate.
 __global__ void __launch_bounds__(256)
 upsample2x_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t total, int w, int cv) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % cv);
     const int64_t p = i / cv;                   // input pixel (n, i, j), row-major
@@ -321,7 +325,7 @@ int upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t 
   const int cv = (int)(c * elem_bytes / 16);
   const int64_t total = n * h * w * cv;
   const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)kNumSMs * 8);
-  upsample2x_kernel<<<(unsigned)grid, 256, 0, st>>>(static_cast<const uint4*>(x), static_cast<uint4*>(y), total,
+  launch_k(upsample2x_kernel, (unsigned)grid, 256, 0, st, static_cast<const uint4*>(x), static_cast<uint4*>(y), total,
                                                     (int)w, cv);
   return check_launch("upsample2x_kernel");
 }
@@ -332,7 +336,7 @@ int batched_copy(const void* const* src_dev, void* const* dst_dev, const int64_t
   CopyTable t{reinterpret_cast<const uint4* const*>(src_dev), reinterpret_cast<uint4* const*>(dst_dev), nvec_dev,
               chunk_prefix_dev, n};
   const int grid = (int)std::min<int64_t>(total_chunks, 8 * kNumSMs);
-  batched_copy_kernel<<<grid, kCopyThreads, 0, st>>>(t);
+  launch_k(batched_copy_kernel, grid, kCopyThreads, 0, st, t);
   return check_launch("batched_copy_kernel");
 }
 

@@ -197,6 +197,7 @@ template <typename T>
 __global__ void __launch_bounds__(kMaxThreads)
 gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8_t* __restrict__ ws, int hw, int c,
                 int groups, int cpg, int rpp, int chunks) {
+  pdl_wait();
   extern __shared__ __align__(16) double dred[];
   double* red1 = dred;             // [rpp][c] raw sums of x
   double* red2 = dred + rpp * c;   // [rpp][c] raw sums of x^2
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(kApplyThreads, 2)
 gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it is written, by its own thread
                 const float* __restrict__ add_nc, const uint8_t* __restrict__ ws, const float* __restrict__ gamma,
                 const float* __restrict__ beta, int hw, int c, int cpg, int rpp, int chunks, float eps) {
+  pdl_wait();
   const int n = blockIdx.y;
   const int cv = c >> 3;
   const int v = threadIdx.x % cv;
@@ -417,6 +419,7 @@ __global__ void __launch_bounds__(kInjThreads)
 inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T> ra, const float* __restrict__ hb,
                  const float* __restrict__ sb, uint8_t* __restrict__ ws, int hw, int ch, int cs, int groups, int cpg,
                  int rpp, int chunks) {
+  pdl_wait();
   extern __shared__ __align__(16) float red[];
   const int c = ch + cs;
   float* red1 = red;               // [rpp][c]
@@ -533,11 +536,11 @@ int run_apply(const T* x, T* y, const float* gamma, const float* beta, const flo
   const int ihw = (int)s.hw, ic = (int)s.c, icpg = (int)s.cpg, ich = (int)s.chunks;
   if (silu) {
     smem_attr(gn_apply_kernel<T, true>, smem);
-    gn_apply_kernel<T, true><<<grid, s.threads, smem, stream>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, icpg, s.rpp,
+    launch_k(gn_apply_kernel<T, true>, grid, s.threads, smem, stream, x, y, add_nc, ws, gamma, beta, ihw, ic, icpg, s.rpp,
                                                                 ich, eps);
   } else {
     smem_attr(gn_apply_kernel<T, false>, smem);
-    gn_apply_kernel<T, false><<<grid, s.threads, smem, stream>>>(x, y, add_nc, ws, gamma, beta, ihw, ic, icpg, s.rpp,
+    launch_k(gn_apply_kernel<T, false>, grid, s.threads, smem, stream, x, y, add_nc, ws, gamma, beta, ihw, ic, icpg, s.rpp,
                                                                  ich, eps);
   }
   return check_launch("gn_apply_kernel");
@@ -555,7 +558,7 @@ int run_gn(const void* xv, void* yv, const float* gamma, const float* beta, cons
     // (the statistics kernel's decomposition is fixed: the workspace is sized for it)
     const size_t smem = (size_t)s.rpp * c * 2 * sizeof(double);
     smem_attr(gn_stats_kernel<T>, smem);
-    gn_stats_kernel<T><<<grid, s.threads, smem, st>>>(x, add_nc, ws, (int)hw, (int)c, (int)groups, (int)s.cpg,
+    launch_k(gn_stats_kernel<T>, grid, s.threads, smem, st, x, add_nc, ws, (int)hw, (int)c, (int)groups, (int)s.cpg,
                                                       s.rpp, (int)s.chunks);
     if (int rc = check_launch("gn_stats_kernel")) return rc;
   }
@@ -589,7 +592,7 @@ int run_inject_gn(void* out, const void* hidden, const void* skip, const void* c
 #define SDB_INJ(NR)                                                                                            \
   case NR:                                                                                                     \
     smem_attr(inject_gn_kernel<T, NR>, smem);                                                                  \
-    inject_gn_kernel<T, NR><<<grid, threads, smem, st>>>(o, h, sk, ra, hb, sb, w, ihw, ich, ics, ig, icpg, rpp, \
+    launch_k(inject_gn_kernel<T, NR>, grid, threads, smem, st, o, h, sk, ra, hb, sb, w, ihw, ich, ics, ig, icpg, rpp, \
                                                          ichunks);                                           \
     break;
     SDB_INJ(0)

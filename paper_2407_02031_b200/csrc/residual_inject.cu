@@ -47,6 +47,7 @@ residual_inject_kernel(T* out, const T* __restrict__ hidden,
                        const T* skip, ResArgs<T> ra, int n_res,
                        int64_t pixels, int64_t ch, int64_t cs,
                        const float* __restrict__ hbias, const float* __restrict__ sbias) {
+  pdl_wait();
   const uint32_t vh = (uint32_t)(ch / 8), vs = (uint32_t)(cs / 8), vrow = vh + vs;
   const uint32_t total = (uint32_t)(pixels * vrow);
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
@@ -95,11 +96,11 @@ int run_inject(void* out, const void* hidden, const void* skip, const void* cons
   const T* h = static_cast<const T*>(hidden);
   const T* s = static_cast<const T*>(skip);
   switch (n_res) {
-    case 0: residual_inject_kernel<T, 0><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 0, pixels, ch, cs, hb, sb); break;
-    case 1: residual_inject_kernel<T, 1><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 1, pixels, ch, cs, hb, sb); break;
-    case 2: residual_inject_kernel<T, 2><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 2, pixels, ch, cs, hb, sb); break;
-    case 3: residual_inject_kernel<T, 3><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, 3, pixels, ch, cs, hb, sb); break;
-    default: residual_inject_kernel<T, -1><<<(unsigned)grid, 256, 0, st>>>(o, h, s, ra, n_res, pixels, ch, cs, hb, sb); break;
+    case 0: launch_k(residual_inject_kernel<T, 0>, (unsigned)grid, 256, 0, st, o, h, s, ra, 0, pixels, ch, cs, hb, sb); break;
+    case 1: launch_k(residual_inject_kernel<T, 1>, (unsigned)grid, 256, 0, st, o, h, s, ra, 1, pixels, ch, cs, hb, sb); break;
+    case 2: launch_k(residual_inject_kernel<T, 2>, (unsigned)grid, 256, 0, st, o, h, s, ra, 2, pixels, ch, cs, hb, sb); break;
+    case 3: launch_k(residual_inject_kernel<T, 3>, (unsigned)grid, 256, 0, st, o, h, s, ra, 3, pixels, ch, cs, hb, sb); break;
+    default: launch_k(residual_inject_kernel<T, -1>, (unsigned)grid, 256, 0, st, o, h, s, ra, n_res, pixels, ch, cs, hb, sb); break;
   }
   return check_launch("residual_inject_kernel");
 }

@@ -1,6 +1,7 @@
 """K2 (GroupNorm+SiLU), K3 (residual inject + concat), K4 (CFG + DDIM step)
 against plain PyTorch fp32 references of the same op."""
 
+import ctypes
 import math
 
 import pytest
@@ -322,10 +323,46 @@ def test_groupnorm_single_pass_cluster_form(c, h, w, n, with_add):
     assert (y.float() - yt.float()).abs().max().item() <= 2 ** -7 * (ref.abs().max().item() + 1)
 
 
+@pytest.mark.parametrize("n,c,h,w", [(2, 320, 128, 128), (2, 640, 64, 64), (2, 1280, 32, 32), (1, 960, 64, 64),
+                                     (2, 640, 128, 128), (4, 320, 64, 64), (2, 1920, 32, 32), (16, 320, 64, 64),
+                                     (2, 2560, 16, 16), (3, 384, 24, 40)])
+@pytest.mark.parametrize("with_add", [True, False])
+def test_groupnorm_streamed_cluster_form(n, c, h, w, with_add):
+    """K2 streamed cluster form (gn_cluster.cu gn_stream_kernel: TMA chunks
+    overlapped with the statistics, per-chunk stores) vs the fp32 torch GN and
+    the two-pass form; one launch; bitwise reproducible."""
+    lib = ops._lib.lib()
+    plan = (ctypes.c_int * 7)()
+    if not lib.sdb_groupnorm_stream_plan(n, h * w, c, 32, plan):
+        pytest.skip("no streamed plan for this shape")
+    g = torch.Generator(device="cuda").manual_seed(c + h + n + 7)
+    x = cl((torch.randn(n, c, h, w, device="cuda", generator=g) * 2 + 0.7).to(torch.bfloat16))
+    gamma = torch.rand(c, device="cuda", generator=g) + 0.5
+    beta = torch.randn(c, device="cuda", generator=g)
+    add = torch.randn(n, c, device="cuda", generator=g) if with_add else None
+    with ops.groupnorm_mode(3):
+        assert lib.sdb_groupnorm_launches(n, h * w, c, 32, ops.sdb_dtype(x)) == 1
+        y = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+        y2 = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+        yn = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=False, add_nc=add)
+    assert torch.equal(y, y2)
+    xin = x.float() + (add[:, :, None, None] if add is not None else 0)
+    ref = F.group_norm(xin, 32, gamma, beta, 1e-5)
+    err = (yn.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 2e-3).all(), float(err.max())
+    ref = F.silu(ref)
+    err = (y.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 2e-3).all(), float(err.max())
+    with ops.groupnorm_mode(1):
+        yt = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+    assert (y.float() - yt.float()).abs().max().item() <= 2 ** -7 * (ref.abs().max().item() + 1)
+
+
 def test_groupnorm_large_maps_take_the_two_pass_form():
     lib = ops._lib.lib()
     bf16 = ops.sdb_dtype(torch.empty(0, dtype=torch.bfloat16))
-    assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 2
+    assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 2     # streamed form would need 2 waves
+    assert lib.sdb_groupnorm_launches(2, 64 * 64, 640, 32, bf16) == 1       # streamed form, one wave
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, bf16) == 1
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, ops.sdb_dtype(torch.empty(0))) == 2   # fp32
 
