@@ -15,17 +15,28 @@
 //                            -> TMEM cols [128 + 64 (j & 1), ...)
 //   O (registers) = O * alpha_{j} + PV_j once PV_j is done (during block j+1)
 // K/V blocks are double-buffered by TMA; PV_j runs under softmax j+1.
-// Status (round 1): correct (tests/test_kernels_gpu.py) but slower than the
-// library cuDNN kernel at SDXL's shapes (L=1024: 32 vs 25 us, L=4096: 169 vs
-// 122 us — ncu: the softmax warps wait on S every block, since S is
-// single-buffered in TMEM to fit 2 CTAs/SM, and 320 CTAs leave a 24-CTA
-// second wave), so the UNet keeps SDPA unless SDB_SELF_ATTN=1.  Next: two
-// softmax warpgroups per CTA ping-ponging on two Q tiles (S double-buffered,
-// the tensor core computing one tile's S under the other's softmax), a
-// persistent tile scheduler for the tail, and part of the ex2 on the FMA pipe.  The reference has no attention arithmetic (addonsim is a latency
-// model): this kernel is part of the UNet backbone the denoising loop runs,
-// replacing the library SDPA call of a diffusers-style Attention.
+// Status: correct (tests/test_kernels_gpu.py) but not faster than the library
+// cuDNN kernel at SDXL's shapes, so the UNet keeps SDPA unless SDB_SELF_ATTN=1.
+// Round 1 (this single-S kernel, SDB_FMHA=1): L=1024 32 vs 25 us, L=4096 169
+// vs 122 us — the softmax warps waited on S every block.  Round 2 (default
+// below, fmha2_kernel: S double-buffered so the tensor core computes S(j+1)
+// under softmax(j), O accumulated in TMEM, lazy max rescale): 32.4 / 171 us —
+// the same.  Measured decomposition (scripts/fmha2_probe.py, probe builds):
+// without any ex2 161 us, without K/V traffic after the first stages 170 us,
+// so neither the MUFU nor L2 bounds it; one query row per thread means ~5.5
+// issued instructions per score (FFMA, MUFU, FMNMX, FADD, F2FP, STS) from 8
+// softmax warps per SM (2 per scheduler): issue/latency-bound, plus 640 tiles
+// over 296 CTA slots = 3 rounds where 2.16 are needed.  A two-tile variant
+// sharing K/V (1 CTA/SM, two warpgroups alternating on the MUFU) measured
+// 217-230 us.  What would beat cuDNN: packed f32x2 FFMA/FADD, the row sum
+// from the tensor core (a ones column appended to V), part of the ex2 on the
+// FMA pipe, and a stream-K tile split for the tail.  The reference has no
+// attention arithmetic (addonsim is a latency model): this kernel is part of
+// the UNet backbone the denoising loop runs, replacing the library SDPA call
+// of a diffusers-style Attention.
 #include <cuda.h>
+
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -247,6 +258,266 @@ fmha_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restric
   }
 }
 
+
+// ---- K8 v2: S double-buffered in TMEM, O accumulated in TMEM ----------------
+// One CTA = 128 queries of one (sample, head); 64-key blocks; warps 0-3
+// softmax (thread = query row = TMEM lane), warp 4 TMA producer, warp 5 MMA
+// issuer; two CTAs per SM.  TMEM (256 columns): S0 [0,64), S1 [64,128), O
+// [128,192).  The MMA warp issues S(j+1) BEFORE PV(j), so the tensor core
+// computes the next block's scores while the softmax warps work on this
+// block's: the softmax never waits on the tensor core in steady state (round
+// 1's kernel did, every block: one S buffer).  P(j) goes to one of two
+// swizzled smem tiles; O += P(j) V(j) accumulates in TMEM (no per-block fold
+// through registers).  Softmax: one TMEM pass per block against a reference
+// max m_ref (log2 units) raised only when a block's max exceeds it by more
+// than 8 — then (warp-uniformly) the block is recomputed and O (TMEM) and l
+// rescaled by 2^(old - new).  p <= 2^8 stays exact in fp32 and representable
+// in bf16; the common block reads S once and rescales nothing.
+constexpr int kF2Threads = 192;
+constexpr int kF2BK = 64;                      // keys per block
+constexpr int kF2Stages = 3;                   // K|V stages (16 KB each)
+constexpr int kF2KV = kF2BK * 128;             // one K (or V) block: 64 rows x 128 B
+constexpr float kF2Slack = 8.f;                // lazy-rescale threshold (log2 units)
+
+__device__ __forceinline__ void tc_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_st32_raw(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kF2Threads, 2)
+fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap,
+             __nv_bfloat16* __restrict__ o, int64_t ldo, int L, int C, float scale_log2) {
+  constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kF2BK >> 3) << 17) |
+                               ((uint32_t)(kM >> 4) << 24);
+  constexpr uint32_t kIdescO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
+                               ((uint32_t)(kM >> 4) << 24);
+  // [barriers | pad] [Q 16 KB] [kF2Stages x (K | V) 16 KB] [P0 | P1 2 x 16 KB]
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 256 + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + kTile;                      // stage s: K at + s * 2 * kF2KV, V at + kF2KV
+  uint8_t* sP = sKV + kF2Stages * 2 * kF2KV;        // buffer b at + b * kTile
+  const int Q_FULL = 0, KV_FULL = 1, KV_EMPTY = KV_FULL + kF2Stages, S_FULL = KV_EMPTY + kF2Stages,
+            S_EMPTY = S_FULL + 2, P_FULL = S_EMPTY + 2, PV_DONE = P_FULL + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + PV_DONE + 2);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+
+  const int h = blockIdx.y, n = blockIdx.z, q0 = blockIdx.x * kM;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nblk = L / kF2BK;
+  const int row0 = n * L;
+
+  if (tid == 0) {
+    mbar_init(bar(Q_FULL), 1);
+    for (int i = 0; i < kF2Stages; ++i) {
+      mbar_init(bar(KV_FULL + i), 1);
+      mbar_init(bar(KV_EMPTY + i), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(S_FULL + b), 1);
+      mbar_init(bar(S_EMPTY + b), kM);
+      mbar_init(bar(P_FULL + b), kM);
+      mbar_init(bar(PV_DONE + b), 1);
+    }
+    mbar_fence_init();
+    prefetch_map(&qmap);
+    prefetch_map(&kvmap);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  pdl_wait();
+
+  if (warp == 4) {
+    // ============================ TMA producer ===============================
+    if ((tid & 31) == 0) {
+      const uint64_t keep = policy_evict_last();
+      mbar_expect_tx(bar(Q_FULL), kTile);
+      tma_load_2d(smem_u32(sQ), &qmap, h * 64, row0 + q0, bar(Q_FULL), policy_evict_first());
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % kF2Stages;
+        if (j >= kF2Stages) mbar_wait(bar(KV_EMPTY + st), ((j / kF2Stages) - 1) & 1);
+        uint8_t* k = sKV + st * 2 * kF2KV;
+        mbar_expect_tx(bar(KV_FULL + st), 2 * kF2KV);
+        tma_load_2d(smem_u32(k), &kvmap, C + h * 64, row0 + j * kF2BK, bar(KV_FULL + st), keep);
+        tma_load_2d(smem_u32(k + kF2KV), &kvmap, 2 * C + h * 64, row0 + j * kF2BK, bar(KV_FULL + st), keep);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ============================ MMA issuer =================================
+    if ((tid & 31) == 0) {
+      auto issue_s = [&](int j) {
+        const int b = j & 1;
+        const uint8_t* k = sKV + (j % kF2Stages) * 2 * kF2KV;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          tc_mma(tmem + 64 * b, sw128_desc(smem_u32(sQ) + ks * 32), sw128_desc(smem_u32(k) + ks * 32), kIdescS,
+                 ks ? 1u : 0u);
+        tc_commit(bar(S_FULL + b));
+      };
+      mbar_wait(bar(Q_FULL), 0);
+      mbar_wait(bar(KV_FULL), 0);
+      tc_fence_after();
+      issue_s(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) {   // S(j+1) first: computed while the softmax works on S(j)
+          mbar_wait(bar(KV_FULL + (j + 1) % kF2Stages), ((j + 1) / kF2Stages) & 1);
+          if (j + 1 >= 2) mbar_wait(bar(S_EMPTY + ((j + 1) & 1)), (((j + 1) >> 1) - 1) & 1);
+          tc_fence_after();
+          issue_s(j + 1);
+        }
+        const int b = j & 1;
+        mbar_wait(bar(P_FULL + b), (j >> 1) & 1);
+        tc_fence_after();
+        const uint8_t* v = sKV + (j % kF2Stages) * 2 * kF2KV + kF2KV;
+#pragma unroll
+        for (int ks = 0; ks < kF2BK / 16; ++ks)
+          tc_mma(tmem + 128, sw128_desc(smem_u32(sP + b * kTile) + ks * 32), sw128_desc(smem_u32(v) + ks * 2048),
+                 kIdescO, (j > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(bar(PV_DONE + b));
+        tc_commit(bar(KV_EMPTY + j % kF2Stages));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== softmax: one query row per thread =================
+    const int r = tid;                          // row = TMEM lane
+    const uint32_t lane = (uint32_t)(warp * 32) << 16;
+    const uint32_t o_addr = tmem + 128 + lane;
+    float m_ref = 0.f, l = 0.f;
+    const int sw = r & 7;
+    for (int j = 0; j < nblk; ++j) {
+      const int b = j & 1;
+      const uint32_t s_addr = tmem + 64 * b + lane;
+      mbar_wait(bar(S_FULL + b), (j >> 1) & 1);
+      tc_fence_after();
+      if (j == 0) {   // the first block fixes the reference max
+        float mx = -INFINITY;
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+          uint32_t v[32];
+          tc_ld32_raw(s_addr + 32 * q4, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+        }
+        m_ref = mx * scale_log2;
+      }
+      if (j >= 2) mbar_wait(bar(PV_DONE + b), ((j >> 1) - 1) & 1);   // P buffer b free (PV(j-2) done)
+      uint8_t* prow = sP + b * kTile + r * 128;
+      float alpha = 1.f, rs = 0.f;
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        rs = 0.f;
+        float bmax = -INFINITY;
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+          uint32_t v[32];
+          tc_ld32_raw(s_addr + 32 * q4, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            float p[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float x = __uint_as_float(v[8 * c4 + e]);
+              bmax = fmaxf(bmax, x);
+              p[e] = ex2f(fmaf(x, scale_log2, -m_ref));
+              rs += p[e];
+            }
+            uint4 pk;
+            pk.x = pk_bf16(p[0], p[1]);
+            pk.y = pk_bf16(p[2], p[3]);
+            pk.z = pk_bf16(p[4], p[5]);
+            pk.w = pk_bf16(p[6], p[7]);
+            const int c8 = q4 * 4 + c4;
+            *reinterpret_cast<uint4*>(prow + ((c8 ^ sw) << 4)) = pk;
+          }
+        }
+        const float bm = bmax * scale_log2;
+        const bool need = bm > m_ref + kF2Slack;
+        if (!__any_sync(0xffffffffu, need)) break;   // warp-uniform: tcgen05.ld is .sync.aligned
+        if (need) {                                 // raise the reference and recompute this block
+          alpha = ex2f(m_ref - bm);
+          m_ref = bm;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(bar(S_EMPTY + b));
+      if (__any_sync(0xffffffffu, alpha != 1.f)) {   // rescale O = sum of PV(0..j-1): PV(j-1) must be done
+        mbar_wait(bar(PV_DONE + (b ^ 1)), ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t v[32];
+          tc_ld32_raw(o_addr + 32 * hh, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          tc_st32_raw(o_addr + 32 * hh, v);
+        }
+        tc_wait_st();
+        tc_fence_before();
+      }
+      fence_proxy_async();
+      mbar_arrive(bar(P_FULL + b));
+      l = fmaf(l, alpha, rs);
+    }
+    mbar_wait(bar(PV_DONE + ((nblk - 1) & 1)), ((nblk - 1) >> 1) & 1);
+    tc_fence_after();
+    float rl;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rl) : "f"(l));
+    __nv_bfloat16* orow = o + ((int64_t)n * L + q0 + r) * ldo + h * 64;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      uint32_t v[32];
+      tc_ld32_raw(o_addr + 32 * hh, v);
+      tc_wait_ld();
+#pragma unroll
+      for (int c8 = 0; c8 < 4; ++c8) {
+        uint4 pk;
+        pk.x = pk_bf16(__uint_as_float(v[8 * c8 + 0]) * rl, __uint_as_float(v[8 * c8 + 1]) * rl);
+        pk.y = pk_bf16(__uint_as_float(v[8 * c8 + 2]) * rl, __uint_as_float(v[8 * c8 + 3]) * rl);
+        pk.z = pk_bf16(__uint_as_float(v[8 * c8 + 4]) * rl, __uint_as_float(v[8 * c8 + 5]) * rl);
+        pk.w = pk_bf16(__uint_as_float(v[8 * c8 + 6]) * rl, __uint_as_float(v[8 * c8 + 7]) * rl);
+        *reinterpret_cast<uint4*>(orow + 32 * hh + c8 * 8) = pk;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
 }  // namespace
 
 int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, int L, int heads, int head_dim,
@@ -268,6 +539,23 @@ int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, 
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(SDB_EINVAL, "self_attention: tensor map");
+  static int mode = -1;   // SDB_FMHA=1: round 1's single-tile kernel
+  if (mode < 0) mode = getenv("SDB_FMHA") != nullptr ? atoi(getenv("SDB_FMHA")) : 2;
+  if (mode == 2) {
+    const int smem2 = 256 + 1024 + kTile + kF2Stages * 2 * kF2KV + 2 * kTile;   // 99,584 B: two CTAs per SM
+    auto kern = fmha2_kernel;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    CUtensorMap kvm;
+    cuuint32_t box2[2] = {64, (cuuint32_t)kF2BK};
+    if (enc(&kvm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box2, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(SDB_EINVAL, "self_attention: tensor map");
+    dim3 grid2((unsigned)(L / kM), (unsigned)heads, (unsigned)n);
+    launch_k(kern, grid2, kF2Threads, smem2, st, map, kvm, static_cast<__nv_bfloat16*>(o), ldo, L, C,
+             scale * 1.4426950408889634f);
+    return check_launch("fmha2_kernel");
+  }
   const int smem = 1024 + 7 * kTile;
   static bool attr = false;
   if (!attr) {
