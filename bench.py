@@ -472,6 +472,26 @@ def other_kernels_roofline(hbm: float) -> list:
     out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16, two-pass (stats + apply)", 2 * n_gn * 2,
                 timed(mk_gn, n_gn * 2)))
 
+    g6, b6 = torch.ones(640, device=dev), torch.zeros(640, device=dev)
+
+    def mk_gn64(mode):
+        def make():
+            x = torch.randn(2, 640, 64, 64, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+            add = torch.zeros(2, 640, device=dev)
+            ws = ops.groupnorm_workspace(x)
+            y = torch.empty_like(x)
+
+            def f():
+                with ops.groupnorm_mode(mode):
+                    ops.groupnorm_silu(x, g6, b6, out=y, add_nc=add, workspace=ws)
+            return f
+        return make
+    n_64 = 2 * 640 * 64 * 64
+    out.append(("K2 groupnorm+silu (+temb) [2,640,64,64] bf16, streamed cluster form (one launch, one read, "
+                "one write; the 9 two-pass sites at 64x64 per SDXL step)", 2 * n_64 * 2, timed(mk_gn64(0), n_64 * 2)))
+    out.append(("K2 groupnorm+silu (+temb) [2,640,64,64] bf16, two-pass form (round 1's choice at this site)",
+                2 * n_64 * 2, timed(mk_gn64(1), n_64 * 2)))
+
     def mk_gn_apply(c):
         def make():
             x = torch.randn(2, c, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
@@ -871,7 +891,8 @@ def run_ours(args):
         "clocks": clk,
         "detail": {"step_ms_calibrated": step_ms, "first_patched_step": pipe.last_first_patched_step,
                    "patch_path": pipe.patchset.plan.path, "per_image_s": [round(x, 4) for x in per_image],
-                   "patch_overhead": overhead},
+                   "patch_overhead": overhead,
+                   "programmatic_dependent_launch": os.environ.get("SDB_PDL", "1") != "0"},
     }
     if accounting is not None:
         line["caas_accounting"] = accounting
