@@ -274,9 +274,7 @@ fmha_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restric
 // rescaled by 2^(old - new).  p <= 2^8 stays exact in fp32 and representable
 // in bf16; the common block reads S once and rescales nothing.
 constexpr int kF2Threads = 192;
-constexpr int kF2BK = 64;                      // keys per block
-constexpr int kF2Stages = 3;                   // K|V stages (16 KB each)
-constexpr int kF2KV = kF2BK * 128;             // one K (or V) block: 64 rows x 128 B
+constexpr int kF2Stages = 3;                   // K|V stages
 constexpr float kF2Slack = 8.f;                // lazy-rescale threshold (log2 units)
 
 __device__ __forceinline__ void tc_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
@@ -302,9 +300,13 @@ __device__ __forceinline__ void tc_st32_raw(uint32_t taddr, const uint32_t (&r)[
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kF2Threads, 2)
+template <int BK>   // keys per block: 64 (2 CTAs/SM) or 32 (3 CTAs/SM)
+__global__ void __launch_bounds__(kF2Threads, BK == 32 ? 3 : 2)
 fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap,
              __nv_bfloat16* __restrict__ o, int64_t ldo, int L, int C, float scale_log2) {
+  constexpr int kF2BK = BK;
+  constexpr int kF2KV = BK * 128;               // one K (or V) block: BK rows x 128 B
+  constexpr uint32_t kTmemCols = BK == 32 ? 128 : 256;   // S0 | S1 | O (64)
   constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kF2BK >> 3) << 17) |
                                ((uint32_t)(kM >> 4) << 24);
   constexpr uint32_t kIdescO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
@@ -344,7 +346,7 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(256));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -377,7 +379,7 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
         const uint8_t* k = sKV + (j % kF2Stages) * 2 * kF2KV;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          tc_mma(tmem + 64 * b, sw128_desc(smem_u32(sQ) + ks * 32), sw128_desc(smem_u32(k) + ks * 32), kIdescS,
+          tc_mma(tmem + BK * b, sw128_desc(smem_u32(sQ) + ks * 32), sw128_desc(smem_u32(k) + ks * 32), kIdescS,
                  ks ? 1u : 0u);
         tc_commit(bar(S_FULL + b));
       };
@@ -398,7 +400,7 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
         const uint8_t* v = sKV + (j % kF2Stages) * 2 * kF2KV + kF2KV;
 #pragma unroll
         for (int ks = 0; ks < kF2BK / 16; ++ks)
-          tc_mma(tmem + 128, sw128_desc(smem_u32(sP + b * kTile) + ks * 32), sw128_desc(smem_u32(v) + ks * 2048),
+          tc_mma(tmem + 2 * BK, sw128_desc(smem_u32(sP + b * kTile) + ks * 32), sw128_desc(smem_u32(v) + ks * 2048),
                  kIdescO, (j > 0 || ks > 0) ? 1u : 0u);
         tc_commit(bar(PV_DONE + b));
         tc_commit(bar(KV_EMPTY + j % kF2Stages));
@@ -409,18 +411,18 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
     // ===================== softmax: one query row per thread =================
     const int r = tid;                          // row = TMEM lane
     const uint32_t lane = (uint32_t)(warp * 32) << 16;
-    const uint32_t o_addr = tmem + 128 + lane;
+    const uint32_t o_addr = tmem + 2 * BK + lane;
     float m_ref = 0.f, l = 0.f;
     const int sw = r & 7;
     for (int j = 0; j < nblk; ++j) {
       const int b = j & 1;
-      const uint32_t s_addr = tmem + 64 * b + lane;
+      const uint32_t s_addr = tmem + BK * b + lane;
       mbar_wait(bar(S_FULL + b), (j >> 1) & 1);
       tc_fence_after();
       if (j == 0) {   // the first block fixes the reference max
         float mx = -INFINITY;
 #pragma unroll
-        for (int q4 = 0; q4 < 2; ++q4) {
+        for (int q4 = 0; q4 < BK / 32; ++q4) {
           uint32_t v[32];
           tc_ld32_raw(s_addr + 32 * q4, v);
           tc_wait_ld();
@@ -437,7 +439,7 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
         rs = 0.f;
         float bmax = -INFINITY;
 #pragma unroll
-        for (int q4 = 0; q4 < 2; ++q4) {
+        for (int q4 = 0; q4 < BK / 32; ++q4) {
           uint32_t v[32];
           tc_ld32_raw(s_addr + 32 * q4, v);
           tc_wait_ld();
@@ -514,7 +516,7 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
@@ -542,11 +544,15 @@ int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, 
   static int mode = -1;   // SDB_FMHA=1: round 1's single-tile kernel
   if (mode < 0) mode = getenv("SDB_FMHA") != nullptr ? atoi(getenv("SDB_FMHA")) : 2;
   if (mode == 2) {
-    const int smem2 = 256 + 1024 + kTile + kF2Stages * 2 * kF2KV + 2 * kTile;   // 99,584 B: two CTAs per SM
-    auto kern = fmha2_kernel;
+    // 64-key blocks, 2 CTAs/SM; SDB_FMHA_BK=32: 32-key blocks, 3 CTAs/SM (444 resident tiles: one
+    // round at L = 1024) — measured 30.0 vs 32.4 us there, 172.9 vs 170.6 us at L = 4096
+    static int bk = -1;
+    if (bk < 0) bk = getenv("SDB_FMHA_BK") != nullptr ? atoi(getenv("SDB_FMHA_BK")) : 64;
+    const int smem2 = 256 + 1024 + kTile + kF2Stages * 2 * bk * 128 + 2 * kTile;   // 72,960 / 99,584 B
+    auto kern = bk == 64 ? fmha2_kernel<64> : fmha2_kernel<32>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     CUtensorMap kvm;
-    cuuint32_t box2[2] = {64, (cuuint32_t)kF2BK};
+    cuuint32_t box2[2] = {64, (cuuint32_t)bk};
     if (enc(&kvm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qkv), dims, strides, box2, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
