@@ -17,23 +17,21 @@
 // K/V blocks are double-buffered by TMA; PV_j runs under softmax j+1.
 // Status: correct (tests/test_kernels_gpu.py) but not faster than the library
 // cuDNN kernel at SDXL's shapes, so the UNet keeps SDPA unless SDB_SELF_ATTN=1.
-// Round 1 (this single-S kernel, SDB_FMHA=1): L=1024 32 vs 25 us, L=4096 169
-// vs 122 us — the softmax warps waited on S every block.  Round 2 (default
-// below, fmha2_kernel: S double-buffered so the tensor core computes S(j+1)
-// under softmax(j), O accumulated in TMEM, lazy max rescale): 32.4 / 171 us —
-// the same.  Measured decomposition (scripts/fmha2_probe.py, probe builds):
-// without any ex2 161 us, without K/V traffic after the first stages 170 us,
-// so neither the MUFU nor L2 bounds it; one query row per thread means ~5.5
-// issued instructions per score (FFMA, MUFU, FMNMX, FADD, F2FP, STS) from 8
-// softmax warps per SM (2 per scheduler): issue/latency-bound, plus 640 tiles
-// over 296 CTA slots = 3 rounds where 2.16 are needed.  A two-tile variant
-// sharing K/V (1 CTA/SM, two warpgroups alternating on the MUFU) measured
-// 217-230 us.  What would beat cuDNN: packed f32x2 FFMA/FADD, the row sum
-// from the tensor core (a ones column appended to V), part of the ex2 on the
-// FMA pipe, and a stream-K tile split for the tail.  The reference has no
-// attention arithmetic (addonsim is a latency model): this kernel is part of
-// the UNet backbone the denoising loop runs, replacing the library SDPA call
-// of a diffusers-style Attention.
+// Round 1 (single-S kernel below, SDB_FMHA=1): L=1024 32 vs 25 us, L=4096 169
+// vs 122 us.  Round 2 (fmha2_kernel, default): 28.5 / 144 us
+// (scripts/fmha2_probe.py, profiles/r02_k8_probes.txt).  What bounds it: the
+// softmax phase is MUFU-bound (16 ex2/clk/SM; per-block trace ~96% busy),
+// ~330 clocks of barrier hand-offs per 64-key block, and the grid: 640 tiles
+// over 296 resident CTAs = 3 rounds where 2.16 are needed (320 over 296 = 2
+// rounds for 1.08 at L = 1024).  Measured dead ends: ex2 on the FMA pipe
+// (degree-3 polynomial for 1/4 or 1/2 of the scores: slower), 32-key blocks
+// with 3 CTAs/SM (one round at L = 1024: 28.2 us), a stream-K split of the
+// (tile, key block) units with last-arriver combines (46 / 194 us: the
+// combine chains cost more than the tail they remove), two query tiles per
+// CTA sharing K/V (217-230 us).  The reference has no attention arithmetic
+// (addonsim is a latency model): this kernel is part of the UNet backbone
+// the denoising loop runs, replacing the library SDPA call of a
+// diffusers-style Attention.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -54,6 +52,22 @@ __device__ __forceinline__ float ex2f(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// 2^t for a pair on the FMA pipe (the MUFU does 16 ex2/clk/SM; a share of the
+// softmax's exponentials moves here): t = n + f, n = round(t) via the 1.5*2^23
+// trick, 2^f on [-0.5, 0.5] by a degree-3 minimax polynomial (max relative
+// error 7.5e-5, far below bf16's 2^-9), n added to the exponent field (the
+// magic's own bits vanish in the shift).  t is clamped at -125 (2^-125 ~ 0).
+__device__ __forceinline__ float2 ex2_fma2(float2 t) {
+  t = make_float2(fmaxf(t.x, -125.f), fmaxf(t.y, -125.f));
+  const float2 r = f2add(t, f2s(12582912.f));
+  const float2 k = f2add(r, f2s(-12582912.f));
+  const float2 f = f2fma(k, f2s(-1.f), t);
+  float2 q = f2fma(f2s(0.055171653628349304f), f, f2s(0.24261115491390228f));
+  q = f2fma(q, f, f2s(0.6932609677314758f));
+  q = f2fma(q, f, f2s(0.9999280571937561f));
+  return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(q.y) + (__float_as_int(r.y) << 23)));
 }
 __device__ __forceinline__ uint32_t pk_bf16(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
@@ -269,13 +283,18 @@ fmha_tc_kernel(const __grid_constant__ CUtensorMap map, __nv_bfloat16* __restric
 // 1's kernel did, every block: one S buffer).  P(j) goes to one of two
 // swizzled smem tiles; O += P(j) V(j) accumulates in TMEM (no per-block fold
 // through registers).  Softmax: one TMEM pass per block against a reference
-// max m_ref (log2 units) raised only when a block's max exceeds it by more
-// than 8 — then (warp-uniformly) the block is recomputed and O (TMEM) and l
-// rescaled by 2^(old - new).  p <= 2^8 stays exact in fp32 and representable
-// in bf16; the common block reads S once and rescales nothing.
+// max m_ref (log2 units, the first block's max) and no per-score max at all:
+// every p is at most the row's block sum, so a sum <= 2^16 proves every p is
+// exact in fp32 and representable in bf16; a larger (or non-finite) sum
+// raises the reference to that row's block max (warp-uniformly: the block is
+// recomputed, O (TMEM) and l rescaled by 2^(old - new)).  Packed f32x2 FFMA /
+// FADD: ~2.6 issued instructions per score.  Per-block trace
+// (scripts/fmha_trace.py probe build, L = 4096): ~1070 clocks of softmax —
+// the MUFU (16 ex2/clk/SM, shared by the SM's two CTAs) busy ~96% of it —
+// plus ~330 clocks of hand-offs per 64-key block.
 constexpr int kF2Threads = 192;
 constexpr int kF2Stages = 3;                   // K|V stages
-constexpr float kF2Slack = 8.f;                // lazy-rescale threshold (log2 units)
+constexpr float kF2SumCap = 65536.f;           // lazy rescale: a block row sum above 2^16 raises the reference
 
 __device__ __forceinline__ void tc_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -300,7 +319,7 @@ __device__ __forceinline__ void tc_st32_raw(uint32_t taddr, const uint32_t (&r)[
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-template <int BK>   // keys per block: 64 (2 CTAs/SM) or 32 (3 CTAs/SM)
+template <int BK, int EMU>   // keys per block: 64 (2 CTAs/SM) or 32 (3 CTAs/SM); EMU: ex2 pairs per 4 on the FMA pipe
 __global__ void __launch_bounds__(kF2Threads, BK == 32 ? 3 : 2)
 fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap,
              __nv_bfloat16* __restrict__ o, int64_t ldo, int L, int C, float scale_log2) {
@@ -433,11 +452,12 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
       }
       if (j >= 2) mbar_wait(bar(PV_DONE + b), ((j >> 1) - 1) & 1);   // P buffer b free (PV(j-2) done)
       uint8_t* prow = sP + b * kTile + r * 128;
-      float alpha = 1.f, rs = 0.f;
-#pragma unroll 1
-      for (int pass = 0; pass < 2; ++pass) {
-        rs = 0.f;
-        float bmax = -INFINITY;
+      // p = 2^(s c - m_ref) for the block's scores -> P (bf16, swizzled smem), returns the row sum.
+      // Packed f32x2 FFMA / FADD: ~2.6 issued instructions per score (round 1: ~5.5).
+      const float2 sc2 = f2s(scale_log2);
+      auto exp_pass = [&]() -> float {
+        const float2 nm2 = f2s(-m_ref);
+        float2 rs2 = f2s(0.f);
 #pragma unroll
         for (int q4 = 0; q4 < BK / 32; ++q4) {
           uint32_t v[32];
@@ -445,30 +465,43 @@ fmha2_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ C
           tc_wait_ld();
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
-            float p[8];
+            uint32_t pk[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const float x = __uint_as_float(v[8 * c4 + e]);
-              bmax = fmaxf(bmax, x);
-              p[e] = ex2f(fmaf(x, scale_log2, -m_ref));
-              rs += p[e];
+            for (int e = 0; e < 4; ++e) {
+              const float2 x = make_float2(__uint_as_float(v[8 * c4 + 2 * e]), __uint_as_float(v[8 * c4 + 2 * e + 1]));
+              const float2 t = f2fma(x, sc2, nm2);
+              const float2 pe = e < EMU ? ex2_fma2(t) : make_float2(ex2f(t.x), ex2f(t.y));
+              rs2 = f2add(rs2, pe);
+              pk[e] = pk_bf16(pe.x, pe.y);
             }
-            uint4 pk;
-            pk.x = pk_bf16(p[0], p[1]);
-            pk.y = pk_bf16(p[2], p[3]);
-            pk.z = pk_bf16(p[4], p[5]);
-            pk.w = pk_bf16(p[6], p[7]);
             const int c8 = q4 * 4 + c4;
-            *reinterpret_cast<uint4*>(prow + ((c8 ^ sw) << 4)) = pk;
+            *reinterpret_cast<uint4*>(prow + ((c8 ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           }
         }
-        const float bm = bmax * scale_log2;
-        const bool need = bm > m_ref + kF2Slack;
-        if (!__any_sync(0xffffffffu, need)) break;   // warp-uniform: tcgen05.ld is .sync.aligned
-        if (need) {                                 // raise the reference and recompute this block
+        return rs2.x + rs2.y;
+      };
+      float alpha = 1.f;
+      float rs = exp_pass();
+      // no per-score max in the common pass: every p <= the row sum, so a sum <= 2^16 bounds every p
+      // (exact in fp32, representable in bf16); a larger (or non-finite) sum -> this row's block max,
+      // raise the reference, recompute (warp-uniform: tcgen05.ld is .sync.aligned)
+      const bool need = !(rs <= kF2SumCap);
+      if (__any_sync(0xffffffffu, need)) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int q4 = 0; q4 < BK / 32; ++q4) {
+          uint32_t v[32];
+          tc_ld32_raw(s_addr + 32 * q4, v);
+          tc_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(v[i]));
+        }
+        if (need) {
+          const float bm = mx * scale_log2;
           alpha = ex2f(m_ref - bm);
           m_ref = bm;
         }
+        rs = exp_pass();
       }
       tc_fence_before();
       mbar_arrive(bar(S_EMPTY + b));
@@ -545,11 +578,16 @@ int self_attention(const void* qkv, int64_t ldqkv, void* o, int64_t ldo, int n, 
   if (mode < 0) mode = getenv("SDB_FMHA") != nullptr ? atoi(getenv("SDB_FMHA")) : 2;
   if (mode == 2) {
     // 64-key blocks, 2 CTAs/SM; SDB_FMHA_BK=32: 32-key blocks, 3 CTAs/SM (444 resident tiles: one
-    // round at L = 1024) — measured 30.0 vs 32.4 us there, 172.9 vs 170.6 us at L = 4096
+    // round at L = 1024) — measured 28.2 vs 28.5 us there, 162.5 vs 144.4 us at L = 4096
     static int bk = -1;
     if (bk < 0) bk = getenv("SDB_FMHA_BK") != nullptr ? atoi(getenv("SDB_FMHA_BK")) : 64;
     const int smem2 = 256 + 1024 + kTile + kF2Stages * 2 * bk * 128 + 2 * kTile;   // 72,960 / 99,584 B
-    auto kern = bk == 64 ? fmha2_kernel<64> : fmha2_kernel<32>;
+    // SDB_FMHA_EMU: exponential pairs per 4 on the FMA pipe (ex2_fma2); 0 (default): measured
+    // 144.4 / 28.5 us at [2,4096,10] / [2,1024,20] vs 151.6 / 29.5 (1) and 152.8 / 30.1 (2)
+    static int emu = -1;
+    if (emu < 0) emu = getenv("SDB_FMHA_EMU") != nullptr ? atoi(getenv("SDB_FMHA_EMU")) : 0;
+    auto kern = bk == 64 ? (emu == 0 ? fmha2_kernel<64, 0> : emu == 2 ? fmha2_kernel<64, 2> : fmha2_kernel<64, 1>)
+                         : (emu == 0 ? fmha2_kernel<32, 0> : emu == 2 ? fmha2_kernel<32, 2> : fmha2_kernel<32, 1>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     CUtensorMap kvm;
     cuuint32_t box2[2] = {64, (cuuint32_t)bk};
