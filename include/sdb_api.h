@@ -182,6 +182,12 @@ size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups)
 void sdb_groupnorm_set_mode(int mode);
 int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
 int sdb_groupnorm_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7);
+/* The resident form (one cooperative launch, one CTA per SM holding a run of
+ * pixels in shared memory, statistics exchanged through the workspace's
+ * fixed-point bank across one grid barrier): auto for bf16 maps > 6 MB that
+ * fit the SMs' shared memory; mode 4 forces it where eligible.  out4 = {rows
+ * per CTA, CTAs per sample, rows per copy chunk, CTAs}; 0 = not eligible. */
+int sdb_groupnorm_resident_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out4);
 
 /* Programmatic dependent launch (default on; SDB_PDL=0 in the environment
  * turns it off at load): the streaming kernels (K2-K7, K9, K10) launch with

@@ -43,6 +43,7 @@ EXPORTED = (
     "sdb_groupnorm_set_mode",
     "sdb_groupnorm_launches",
     "sdb_groupnorm_stream_plan",
+    "sdb_groupnorm_resident_plan",
     "sdb_set_pdl",
 )
 
@@ -119,6 +120,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.sdb_set_pdl.argtypes = [i32]
     lib.sdb_groupnorm_stream_plan.restype = i32
     lib.sdb_groupnorm_stream_plan.argtypes = [i64, i64, i64, i64, ctypes.POINTER(ctypes.c_int)]
+    lib.sdb_groupnorm_resident_plan.restype = i32
+    lib.sdb_groupnorm_resident_plan.argtypes = [i64, i64, i64, i64, ctypes.POINTER(ctypes.c_int)]
     lib.sdb_conv_out.restype = i32
     lib.sdb_conv_out.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64, i64, i32, vp]
 

@@ -72,6 +72,7 @@ int memcpy_async(void* dst, const void* src, size_t bytes, cudaStream_t st);
 extern int g_gn_cluster_mode;
 int gn_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
 int gn_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7);
+int gn_resident_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out4);
 // conv_out.cu
 int conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h, int64_t w_,
              int64_t c, int64_t cout, int dtype, cudaStream_t st);
@@ -314,6 +315,10 @@ int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int
 
 int sdb_groupnorm_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7) {
   return gn_stream_plan(n, hw, c, groups, out7);
+}
+
+int sdb_groupnorm_resident_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out4) {
+  return gn_resident_plan(n, hw, c, groups, out4);
 }
 
 int sdb_conv_out(const void* x, const void* w, const float* bias, float* out, int64_t n, int64_t h,

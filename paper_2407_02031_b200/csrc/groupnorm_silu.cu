@@ -52,14 +52,6 @@
 namespace sdb {
 namespace {
 
-// 1/d for d in [1, 2^127): bit-trick seed (rel. error <= 5.1%) and two
-// Newton steps on the FMA pipe (rel. error <= 6.7e-6, far below bf16's 2^-9)
-__device__ __forceinline__ float rcp_nr(float d) {
-  float x = __int_as_float(0x7EF311C3 - __float_as_int(d));
-  x = x * fmaf(-d, x, 2.f);
-  return x * fmaf(-d, x, 2.f);
-}
-
 constexpr int kMaxThreads = 512;
 constexpr int kMaxN = 16;            // batch (x2 for CFG): serving batch 8 with CFG
 constexpr int kMaxGroups = 64;
@@ -153,11 +145,21 @@ __device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
   return v;
 }
 
-// bank of this producer launch; zeroes the idle bank (a grid-strided slice per CTA)
-__device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch) {
+// bank of this producer launch; zeroes the idle bank (a grid-strided slice per
+// CTA).  Called by every thread of the CTA (uniform control flow): ONE thread
+// reads the header and shares it — every thread loading the same word would
+// queue thousands of requests on one L2 address ahead of the real traffic.
+__device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch, unsigned int* epoch_out = nullptr) {
+  __shared__ unsigned int snap[2];
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
-  const unsigned int epoch = ld_relaxed(&hdr->epoch);
-  const int rows = max((int)ld_relaxed(&hdr->hwm), nbatch);
+  if (threadIdx.x == 0) {
+    snap[0] = ld_relaxed(&hdr->epoch);
+    snap[1] = ld_relaxed(&hdr->hwm);
+  }
+  __syncthreads();
+  const unsigned int epoch = snap[0];
+  const int rows = max((int)snap[1], nbatch);
+  if (epoch_out != nullptr) *epoch_out = epoch;
   long long* banks = reinterpret_cast<long long*>(ws + kWsHeader);
   long long* idle = banks + (size_t)((epoch + 1u) & 1u) * kBankWords;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x, ctas = gridDim.x * gridDim.y;
@@ -316,11 +318,10 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
   __shared__ float2 gstat[kMaxGroups];
   {
     const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws);
-    const unsigned int cur = __ldg(&hdr->cur);
-    const long long* bank = reinterpret_cast<const long long*>(ws + kWsHeader) + (size_t)cur * kBankWords +
-                            (size_t)n * kMaxGroups * 4;
     const double count = (double)hw * (double)cpg;
     for (int g = threadIdx.x; g < c / cpg; g += blockDim.x) {
+      const long long* bank = reinterpret_cast<const long long*>(ws + kWsHeader) +
+                              (size_t)__ldg(&hdr->cur) * kBankWords + (size_t)n * kMaxGroups * 4;
       const double mean = fixed_value(bank + g * 4) / count;
       const double var = fixed_value(bank + g * 4 + 2) / count - mean * mean;
       gstat[g] = make_float2((float)mean, (float)(var < 0.0 ? 0.0 : var));
@@ -353,6 +354,10 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
       const float rstd = 1.f / sqrtf(st[j].y + eps);
       av[e] = ga[j] * rstd;
       bv[e] = be[j] + (ad[j] - st[j].x) * av[e];
+      if (SILU && sizeof(T) != 4) {   // the 16-bit SiLU path works on -w (silu2_neg)
+        av[e] = -av[e];
+        bv[e] = -bv[e];
+      }
     }
     A[i] = make_float2(av[0], av[1]);
     B[i] = make_float2(bv[0], bv[1]);
@@ -376,22 +381,304 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
         float2 w = f2fma(get_pair<T>(q[u], i), A[i], B[i]);
         if (SILU && sizeof(T) == 4) {   // fp32 parity mode: libdevice expf + IEEE division
           w = make_float2(w.x / (1.f + expf(-w.x)), w.y / (1.f + expf(-w.y)));
-        } else if (SILU) {   // SiLU(w) = w / (1 + 2^(-w log2 e)) -> 0 as w -> -inf
-          // ex2 on the MUFU; the reciprocal on the FMA pipe for 16-bit outputs
-          float2 t = f2mul(w, f2s(-1.4426950408889634f));
-          t.x = fminf(t.x, 126.f);
-          t.y = fminf(t.y, 126.f);
-          float2 e;
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(t.x));
-          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(t.y));
-          e = f2add(e, f2s(1.f));
-          w = f2mul(w, make_float2(rcp_nr(e.x), rcp_nr(e.y)));   // 2 Newton steps: 6.7e-6, far below a 16-bit ulp
+        } else if (SILU) {   // SiLU(w) = w / (1 + 2^(-w log2 e)) -> 0 as w -> -inf; here w holds -w
+          w = silu2_neg(w);
         }
         set_pair<T>(o, i, w);
       }
       store_raw<T>(y + base + (size_t)row * c, o);
     }
   }
+}
+
+// ---- resident form: the whole map in the SMs' shared memory, ONE launch ----
+// The two-pass form pays two launch ramps and a dependent round trip per map
+// (stats, then apply); at SDXL's two-pass sites those, not bytes, set its
+// time.  Here one CTA per SM (a co-resident grid: cooperative launch) owns a
+// contiguous run of P pixels of one sample — in NHWC one contiguous span, so
+// it arrives as a few 1-D bulk copies (TMA engine, one mbarrier each) while
+// the threads fold the chunks that have landed into shifted per-channel
+// sums.  The per-group CTA partials go to the site's fixed-point bank
+// (red.global.add of exact integers: deterministic in any arrival order),
+// one grid barrier (the bank's epoch word: the last CTA to arrive advances
+// it), then every CTA reads its sample's statistics and applies the affine
+// + SiLU to its resident tile and stores it: one read and one write of the
+// map, the minimum.  Eligible while the map fits 148 tiles of <= 176 KB
+// (SDXL's [2, 320, 128, 128] = 21 MB: 142 KB per CTA).
+constexpr int kRsThreads = 1024;
+constexpr int kRsMaxGroups = 32;
+constexpr int kRsMaxChunks = 12;
+constexpr int kRsTileMax = 176 * 1024;
+constexpr int kRsExtra = kRsThreads * 4 * 8 + 2 * kRsMaxGroups * 4 + kRsMaxChunks * 8 + 4 * 4 + 128;
+constexpr size_t kRsBarOffset = 128;     // the resident form's barrier word, in the header's second line
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// a bank entry written during THIS launch: read through L2, never the
+// non-coherent path
+__device__ __forceinline__ double fixed_value_cg(const long long* w) {
+  return (double)__ldcg(w) + (double)__ldcg(w + 1) / kFracScale;
+}
+
+#ifdef SDB_RS_TRACE   // probe build only: per-CTA phase timestamps (scripts/k2r_trace.py)
+__device__ unsigned long long g_rs_trace[1024][16];
+#define RS_T(k)                                                          \
+  if (threadIdx.x == 0) {                                                \
+    g_rs_trace[blockIdx.x][k] = global_ns();                             \
+    if (k == 0) {                                                        \
+      unsigned int sm;                                                   \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));                    \
+      g_rs_trace[blockIdx.x][15] = sm;                                    \
+    }                                                                    \
+  }
+#else
+#define RS_T(k)
+#endif
+
+template <bool SILU, int NT>
+__global__ void __launch_bounds__(NT, 1)
+gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                   const float* __restrict__ gamma, const float* __restrict__ beta, const float* __restrict__ add_nc,
+                   uint8_t* __restrict__ ws, int hw, int c, int cpg, int P, int per_sample, int cr, float eps) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  RS_T(0)
+  const int tid = threadIdx.x;
+  const int n = blockIdx.x / per_sample;
+  const int r0 = (blockIdx.x % per_sample) * P;
+  const int rows = min(P, hw - r0);
+  const int rowb = c * 2;
+  const int nch = (rows + cr - 1) / cr;
+  uint8_t* tile = smem;
+  double* part = reinterpret_cast<double*>(smem + (((size_t)P * rowb + 127) & ~(size_t)127));   // [threads][4]
+  float* stat = reinterpret_cast<float*>(part + NT * 4);                                  // mean | var
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stat + 2 * kRsMaxGroups);
+  unsigned int* snap = reinterpret_cast<unsigned int*>(mbar + kRsMaxChunks);                     // epoch, hwm, bar word
+  if (tid == 0) {
+    for (int k = 0; k < nch; ++k) mbar_init(smem_u32(mbar + k), 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_wait();
+  RS_T(1)
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+  unsigned int* barw = reinterpret_cast<unsigned int*>(ws + kRsBarOffset);
+  if (tid == 0) {
+    const __nv_bfloat16* xs = x + ((size_t)n * hw + r0) * c;
+    const uint64_t pol = policy_evict_first();       // x is dead after this op
+    for (int k = 0; k < nch; ++k) {
+      const uint32_t bytes = (uint32_t)(min(cr, rows - k * cr) * rowb);
+      const uint32_t bar = smem_u32(mbar + k);
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(smem_u32(tile + (size_t)k * cr * rowb), xs + (size_t)k * cr * c, bytes, bar, pol);
+    }
+  } else if (tid == 32) {   // the header, read once per CTA while the copies fly (nothing here can
+    snap[0] = ld_relaxed(&hdr->epoch);   // change before every CTA of this launch has arrived)
+    snap[1] = ld_relaxed(&hdr->hwm);
+    snap[2] = ld_relaxed(barw);
+  }
+
+  const int cv = c >> 3;
+  const int rstep = NT / cv;
+  const int j = tid % cv;
+  const int rstart = tid / cv;
+  const bool active = rstart < rstep;
+  const int ch0 = j * 8;
+  const int gA = ch0 / cpg;
+  const int nA = min(8, (gA + 1) * cpg - ch0);        // leading elements in group gA, the rest in gA + 1
+  const int gs = c / cpg;
+  // this thread's per-(n, c) add, loaded while the copies fly
+  const float* addp = add_nc != nullptr ? add_nc + (size_t)n * c + ch0 : nullptr;
+  float ad[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) ad[e] = addp != nullptr ? __ldg(addp + e) : 0.f;
+
+  // ---- statistics, chunk by chunk as the copies land ------------------------
+  // Shifted sums with ONE shift per group, K_g = x[first pixel of this CTA,
+  // first channel of g]: every thread of the CTA uses the same shift for a
+  // group, so the per-thread fp32 sums add up directly (no cancellation, no
+  // fp64 until one value per group — dependent fp64 chains are slow here).
+  mbar_wait(smem_u32(mbar), 0);
+  const int gB = min(gA + 1, gs - 1);
+  const float KA = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(tile)[gA * cpg]);
+  const float KB = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(tile)[gB * cpg]);
+  float Kp[8], s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    Kp[e] = (e < nA ? KA : KB) - ad[e];     // d = x + add - K_g
+    s1[e] = s2[e] = 0.f;
+  }
+  for (int k = 0; k < nch; ++k) {
+    mbar_wait(smem_u32(mbar + k), 0);
+    if (!active) continue;
+    const int rend = min(rows, (k + 1) * cr);
+    for (int r = k * cr + rstart; r < rend; r += rstep) {
+      const uint4 u = *reinterpret_cast<const uint4*>(tile + (size_t)r * rowb + ch0 * 2);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(h[q]);
+        const float d0 = f.x - Kp[2 * q], d1 = f.y - Kp[2 * q + 1];
+        s1[2 * q] += d0;
+        s1[2 * q + 1] += d1;
+        s2[2 * q] = fmaf(d0, d0, s2[2 * q]);
+        s2[2 * q + 1] = fmaf(d1, d1, s2[2 * q + 1]);
+      }
+    }
+  }
+  RS_T(2)
+  {  // this thread's shifted sums collapsed onto the (<= 2) groups of its column
+    float a1 = 0.f, a2 = 0.f, b1 = 0.f, b2 = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (e < nA) { a1 += s1[e]; a2 += s2[e]; }
+      else { b1 += s1[e]; b2 += s2[e]; }
+    }
+    reinterpret_cast<float4*>(part)[tid] = active ? make_float4(a1, a2, b1, b2) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  RS_T(6)
+  const unsigned int e0 = snap[0];
+  long long* banks = reinterpret_cast<long long*>(ws + kWsHeader);
+  long long* bank = banks + (size_t)(e0 & 1u) * kBankWords + (size_t)n * kMaxGroups * 4;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int g = warp; g < gs; g += NT / 32) {   // a warp per group: the columns touching it, their threads in a fixed order
+    float m1 = 0.f, m2 = 0.f;
+    const int jlo = (g * cpg) >> 3, jhi = min(cv - 1, ((g + 1) * cpg - 1) >> 3);
+    for (int jj = jlo; jj <= jhi; ++jj) {
+      const bool isA = (jj * 8) / cpg == g;           // this group is the column's A or B part
+      for (int q = lane; q < rstep; q += 32) {
+        const float4 p = reinterpret_cast<const float4*>(part)[jj + q * cv];
+        m1 += isA ? p.x : p.z;
+        m2 += isA ? p.y : p.w;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    }
+    if (lane == 0) {
+      // raw moments of x' over this CTA's rows x cpg channels of the group, in fp64
+      const double K = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(tile)[g * cpg]);
+      const double M = (double)rows * cpg, S1 = m1;
+      red_fixed(bank + g * 4, S1 + M * K);
+      red_fixed(bank + g * 4 + 2, (double)m2 + K * (2.0 * S1 + M * K));
+    }
+  }
+  {  // zero the idle bank for the next producer launch on this workspace (a slice per CTA)
+    const int brows = max((int)snap[1], (int)(gridDim.x / per_sample));
+    long long* idle = banks + (size_t)((e0 + 1u) & 1u) * kBankWords;
+    for (int i = blockIdx.x * NT + tid; i < brows * kMaxGroups * 4; i += gridDim.x * NT) idle[i] = 0;
+  }
+  float ga[8], be[8];   // the affine parameters, in flight across the barrier
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    ga[e] = gamma != nullptr ? __ldg(gamma + ch0 + e) : 1.f;
+    be[e] = beta != nullptr ? __ldg(beta + ch0 + e) : 0.f;
+  }
+  // ---- grid barrier: one release-add per CTA on the bar word, flip of its top bit --
+  // CTA 0 adds 2^31 - (ctas - 1), every other CTA 1: the word's top bit flips
+  // exactly when the last CTA arrives and its low bits return to their start
+  // value (zero), so it needs no reset and no second atomic.
+  __syncthreads();
+  RS_T(3)
+  if (tid == 0) {
+    const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(barw), "r"(inc) : "memory");
+    const unsigned int top = snap[2] & 0x80000000u;
+    // co-residency is guaranteed by the cooperative launch; the watchdog
+    // turns a broken guarantee into a loud fault instead of a hung GPU
+    const unsigned long long t0 = global_ns();
+    while ((ld_acquire(barw) & 0x80000000u) == top) {
+      if (global_ns() - t0 > 2000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+  RS_T(4)
+  if (tid < gs) {
+    const double count = (double)hw * cpg;
+    const double mean = fixed_value_cg(bank + tid * 4) / count;
+    double var = fixed_value_cg(bank + tid * 4 + 2) / count - mean * mean;
+    var = var < 0.0 ? 0.0 : var;
+    stat[tid] = (float)mean;
+    stat[kRsMaxGroups + tid] = (float)var;
+  }
+  if (blockIdx.x == 0 && tid == 32) {   // every CTA has read the epoch (it arrived): advance it
+    hdr->cur = e0 & 1u;
+    hdr->hwm = (unsigned int)max((int)snap[1], (int)(gridDim.x / per_sample));
+    hdr->epoch = e0 + 1u;
+  }
+  __syncthreads();
+  // ---- apply (+ SiLU) from shared memory, 16-B stores ------------------------
+  if (!active) return;
+  float2 A[4], B[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float av[2], bv[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int ee = 2 * i + e;
+      const int g = ee < nA ? gA : gA + 1;
+      const float rstd = 1.f / sqrtf(stat[kRsMaxGroups + g] + eps);
+      av[e] = ga[ee] * rstd;
+      bv[e] = be[ee] + (ad[ee] - stat[g]) * av[e];
+      if (SILU) {   // silu2_neg works on -w
+        av[e] = -av[e];
+        bv[e] = -bv[e];
+      }
+    }
+    A[i] = make_float2(av[0], av[1]);
+    B[i] = make_float2(bv[0], bv[1]);
+  }
+  __nv_bfloat16* ys = y + ((size_t)n * hw + r0) * c + ch0;
+  for (int r = rstart; r < rows; r += rstep) {
+    Raw8<__nv_bfloat16> q;
+    q.u = *reinterpret_cast<const uint4*>(tile + (size_t)r * rowb + ch0 * 2);
+    Raw8<__nv_bfloat16> o;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 w = f2fma(get_pair<__nv_bfloat16>(q, i), A[i], B[i]);
+      if (SILU) w = silu2_neg(w);   // as gn_apply_kernel (w holds -w here)
+      set_pair<__nv_bfloat16>(o, i, w);
+    }
+    store_raw<__nv_bfloat16>(ys + (size_t)r * c, o);
+  }
+  RS_T(5)
+}
+
+struct RsPlan {
+  int P = 0, per_sample = 0, cr = 0, ctas = 0;
+  size_t smem = 0;
+};
+
+bool rs_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, RsPlan& p) {
+  const int64_t cpg = c / groups;
+  if (groups > kRsMaxGroups || c % 8 != 0 || c / 8 > kRsThreads) return false;
+  if (cpg < 8) return false;                        // an 8-channel vector spans <= 2 groups
+  if (n > kNumSMs) return false;
+  const int64_t per = kNumSMs / n;                  // CTAs per sample, one per SM
+  int64_t P = (hw + per - 1) / per;
+  if (P * c * 2 > kRsTileMax) return false;
+  const int64_t per_sample = (hw + P - 1) / P;      // every CTA owns >= 1 row
+  const int64_t rstep = kRsThreads / (c / 8);
+  // chunks: a whole number of thread row-steps, ~8 of them per tile
+  int64_t cr = std::max<int64_t>(1, (P + 7) / 8);
+  cr = ((cr + rstep - 1) / rstep) * rstep;
+  if ((P + cr - 1) / cr > kRsMaxChunks) return false;
+  p.P = (int)P;
+  p.per_sample = (int)per_sample;
+  p.cr = (int)cr;
+  p.ctas = (int)(n * per_sample);
+  p.smem = (((size_t)P * c * 2 + 127) & ~(size_t)127) + kRsExtra;
+  return true;
 }
 
 // ---- K3 + GroupNorm statistics in one pass ---------------------------------
@@ -639,11 +926,115 @@ int gn_cluster_try(const void* x, void* y, const float* gamma, const float* beta
                    int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, cudaStream_t st,
                    bool* launched);
 
+extern int g_gn_cluster_mode;   // gn_cluster.cu: 0 auto, 1 two-pass, 2 / 3 cluster forms, 4 resident form
+bool gn_stream_one_wave(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu);   // gn_cluster.cu
+
+// Auto choice of the resident form (scripts/k2_resident.py, profiles/r02_k2_resident.txt):
+// wherever it is eligible except where the streamed cluster form runs in one
+// wave on a map <= 10.5 MB (there its clusters win: [2,640,64,64] 14.0 vs
+// 15.6 us); SDB_GN_RESIDENT=0 turns it off.
+bool gn_resident_auto(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu, int dtype) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SDB_GN_RESIDENT");
+    env = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  const int mode = g_gn_cluster_mode;
+  if (dtype != SDB_BF16 || (mode != 0 && mode != 4)) return false;
+  RsPlan p;
+  if (!rs_plan(n, hw, c, groups, p)) return false;
+  if (mode == 4) return true;
+  if (!env) return false;
+  return !(n * hw * c * 2 <= ((int64_t)21 << 19) && gn_stream_one_wave(n, hw, c, groups, silu));
+}
+
+// The resident form where the shape and the device allow it; *launched tells.
+static int gn_resident_try(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc,
+                           int64_t n, int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, void* ws,
+                           cudaStream_t st, bool* launched) {
+  *launched = false;
+  if (!gn_resident_auto(n, hw, c, groups, silu, dtype)) return SDB_OK;
+  RsPlan p;
+  if (!rs_plan(n, hw, c, groups, p)) return SDB_OK;
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 0;
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop) sms = 0;
+    cudaGetLastError();
+  }
+  if (p.ctas > sms) return SDB_OK;
+  static int nt = -1;      // SDB_GN_RS_THREADS: 512 / 768 / 1024 (probe knob; 512 measured best)
+  if (nt < 0) {
+    nt = 512;
+    if (const char* e = getenv("SDB_GN_RS_THREADS")) nt = atoi(e);
+    if (nt != 768 && nt != 1024) nt = 512;
+  }
+  if (c / 8 > nt) return SDB_OK;
+  auto kern = nt == 512   ? (silu ? gn_resident_kernel<true, 512> : gn_resident_kernel<false, 512>)
+              : nt == 768 ? (silu ? gn_resident_kernel<true, 768> : gn_resident_kernel<false, 768>)
+                          : (silu ? gn_resident_kernel<true, 1024> : gn_resident_kernel<false, 1024>);
+  static bool attr[6] = {false, false, false, false, false, false};
+  const int ai = (silu ? 1 : 0) + (nt == 512 ? 2 : nt == 768 ? 4 : 0);
+  if (!attr[ai]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((kRsTileMax + 127) / 128 * 128 + kRsExtra));
+    attr[ai] = true;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, p.smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return SDB_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p.ctas, 1, 1);
+  cfg.blockDim = dim3((unsigned)nt, 1, 1);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;      // the grid barrier needs every CTA resident
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), gamma, beta,
+                     add_nc, static_cast<uint8_t*>(ws), (int)hw, (int)c, (int)(c / groups), p.P, p.per_sample, p.cr,
+                     eps);
+  *launched = true;
+  return check_launch("gn_resident_kernel");
+}
+
+#ifdef SDB_RS_TRACE
+extern "C" __attribute__((visibility("default"))) int sdb_debug_rs_trace(unsigned long long* host, int ctas) {
+  return cudaMemcpyFromSymbol(host, g_rs_trace, (size_t)ctas * 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -2;
+}
+#endif
+
+// The resident form's plan for a shape (probes / tests): rows per CTA, CTAs
+// per sample, chunk rows, CTAs; returns 0 when not eligible.
+int gn_resident_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out4) {
+  RsPlan p;
+  if (!rs_plan(n, hw, c, groups, p)) return 0;
+  const int v[4] = {p.P, p.per_sample, p.cr, p.ctas};
+  for (int i = 0; i < 4; ++i) out4[i] = v[i];
+  return 1;
+}
+
 int groupnorm_silu(const void* x, void* y, const float* gamma, const float* beta, const float* add_nc, int64_t n,
                    int64_t hw, int64_t c, int64_t groups, float eps, int silu, int dtype, void* ws,
                    cudaStream_t st, int stats) {
   if (int rc = gn_checks(x, y, n, hw, c, groups, ws)) return rc;
   if (int rc = gn_param_checks(gamma, beta, add_nc)) return rc;
+  if (stats) {   // the resident single-launch form where the map fits the SMs' shared memory
+    bool launched = false;
+    if (int rc = gn_resident_try(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, dtype, ws, st, &launched))
+      return rc;
+    if (launched) return SDB_OK;
+  }
   if (stats) {   // single-pass cluster form where the map fits a cluster's shared memory (gn_cluster.cu)
     bool launched = false;
     if (int rc = gn_cluster_try(x, y, gamma, beta, add_nc, n, hw, c, groups, eps, silu, dtype, st, &launched))

@@ -381,10 +381,87 @@ def test_groupnorm_streamed_cluster_form(n, c, h, w, with_add):
     assert (y.float() - yt.float()).abs().max().item() <= 2 ** -7 * (ref.abs().max().item() + 1)
 
 
+@pytest.mark.parametrize("n,c,h,w", [(2, 320, 128, 128), (1, 320, 128, 128), (2, 640, 64, 64), (2, 960, 64, 64),
+                                     (2, 1280, 32, 32), (3, 384, 24, 40), (2, 2560, 16, 16), (16, 320, 32, 32),
+                                     (2, 256, 9, 7)])
+@pytest.mark.parametrize("with_add", [True, False])
+def test_groupnorm_resident_form(n, c, h, w, with_add):
+    """K2 resident form (groupnorm_silu.cu gn_resident_kernel: one cooperative
+    launch, tiles resident in shared memory, fixed-point statistics across one
+    grid barrier) vs the fp32 torch GN and the two-pass form; one launch;
+    bitwise reproducible; ragged last CTA (hw not a multiple of the run)."""
+    lib = ops._lib.lib()
+    plan = (ctypes.c_int * 4)()
+    if not lib.sdb_groupnorm_resident_plan(n, h * w, c, 32, plan):
+        pytest.skip("no resident plan for this shape")
+    p_rows, per_sample, _, ctas = list(plan)
+    assert ctas == n * per_sample <= 148 and (per_sample - 1) * p_rows < h * w <= per_sample * p_rows
+    g = torch.Generator(device="cuda").manual_seed(c + h + n + 11)
+    x = cl((torch.randn(n, c, h, w, device="cuda", generator=g) * 2 + 0.7).to(torch.bfloat16))
+    gamma = torch.rand(c, device="cuda", generator=g) + 0.5
+    beta = torch.randn(c, device="cuda", generator=g)
+    add = torch.randn(n, c, device="cuda", generator=g) if with_add else None
+    with ops.groupnorm_mode(4):
+        assert lib.sdb_groupnorm_launches(n, h * w, c, 32, ops.sdb_dtype(x)) == 1
+        y = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+        y2 = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+        yn = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=False, add_nc=add)
+    assert torch.equal(y, y2)
+    xin = x.float() + (add[:, :, None, None] if add is not None else 0)
+    ref = F.group_norm(xin, 32, gamma, beta, 1e-5)
+    err = (yn.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 2e-3).all(), float(err.max())
+    ref = F.silu(ref)
+    err = (y.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 2e-3).all(), float(err.max())
+    with ops.groupnorm_mode(1):
+        yt = ops.groupnorm_silu(x, gamma, beta, groups=32, eps=1e-5, silu=True, add_nc=add)
+    assert (y.float() - yt.float()).abs().max().item() <= 2 ** -7 * (ref.abs().max().item() + 1)
+
+
+def test_groupnorm_resident_form_concurrent_streams():
+    """Resident-form launches on three streams at once (the CaaS loopback
+    engine replays its encoder and ControlNet graphs concurrently), eagerly
+    and as parallel branches of one CUDA graph: every grid barrier completes
+    and each result is bitwise the sequential one."""
+    n, c, h, w = 2, 320, 128, 128
+    xs = [cl(torch.randn(n, c, h, w, device="cuda").to(torch.bfloat16)) for _ in range(3)]
+    wss = [ops.groupnorm_workspace(x) for x in xs]
+    gamma, beta = torch.rand(c, device="cuda") + 0.5, torch.randn(c, device="cuda")
+    with ops.groupnorm_mode(4):
+        seq = [ops.groupnorm_silu(x, gamma, beta, workspace=ws) for x, ws in zip(xs, wss)]
+        outs = [torch.empty_like(x) for x in xs]
+        streams = [torch.cuda.Stream() for _ in range(3)]
+        torch.cuda.synchronize()
+        for _ in range(20):
+            for x, ws, o, s in zip(xs, wss, outs, streams):
+                with torch.cuda.stream(s):
+                    ops.groupnorm_silu(x, gamma, beta, out=o, workspace=ws)
+        torch.cuda.synchronize()
+        assert all(torch.equal(a, b) for a, b in zip(seq, outs))
+        for o in outs:
+            o.zero_()
+        graph, cap = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+        with torch.cuda.graph(graph, stream=cap):
+            for _ in range(4):
+                for x, ws, o, s in zip(xs, wss, outs, streams):
+                    s.wait_stream(cap)
+                    with torch.cuda.stream(s):
+                        ops.groupnorm_silu(x, gamma, beta, out=o, workspace=ws)
+            for s in streams:
+                cap.wait_stream(s)
+        for _ in range(5):
+            graph.replay()
+        torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(seq, outs))
+
+
 def test_groupnorm_large_maps_take_the_two_pass_form():
     lib = ops._lib.lib()
     bf16 = ops.sdb_dtype(torch.empty(0, dtype=torch.bfloat16))
-    assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 2     # streamed form would need 2 waves
+    assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 1     # resident form (21 MB)
+    assert lib.sdb_groupnorm_launches(2, 128 * 128, 640, 32, bf16) == 2     # 42 MB: beyond the SMs' shared memory
+    assert lib.sdb_groupnorm_launches(16, 128 * 128, 320, 32, bf16) == 2
     assert lib.sdb_groupnorm_launches(2, 64 * 64, 640, 32, bf16) == 1       # streamed form, one wave
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, bf16) == 1
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, ops.sdb_dtype(torch.empty(0))) == 2   # fp32
