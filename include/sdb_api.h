@@ -255,8 +255,12 @@ int sdb_residual_inject_gn(void* out, const void* hidden, const void* skip,
 int sdb_cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o,
                         int64_t ldo, int n, int lq, int lk, int heads, int head_dim, float scale, int dtype,
                         void* stream);
-/* 1 (default): head_dim 64 runs the tcgen05 form (TMEM accumulators, one
- * query row per thread); 0: every head dim runs the mma.sync form.  Returns
+/* Head dim 64: 2 (default) runs the persistent tcgen05 form (one CTA per SM
+ * walking a run of 128-query tiles, Q by TMA two tiles ahead, S and O
+ * double-buffered in TMEM, one query row per thread) where each CTA's run
+ * spans <= 2 heads and the grid holds >= 2 waves of 128-query tiles (the
+ * serving batches), else as 1; 1: the per-tile tcgen05 form for one-wave
+ * grids, else mma.sync; 0: every head dim runs the mma.sync form.  Returns
  * the previous setting. */
 int sdb_cross_attention_set_mode(int tcgen05);
 

@@ -418,9 +418,221 @@ xattn_tc_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant_
   }
 }
 
+// ---- persistent tcgen05 form: two CTAs per SM, each walking a run of tiles --
+// The per-tile form above runs each tile's chain TMA -> S MMA -> softmax -> P V
+// -> store once per CTA with nothing overlapped inside the CTA.  Here each CTA
+// takes a contiguous run of the (sample, head, query-tile) sequence (<= 2
+// heads: both heads' K_h / V_h are fetched up front) and software-pipelines it:
+//   * Q tiles arrive by TMA two tiles ahead (2-slot ring: tile i + 2 reuses
+//     tile i's slot once S_i has completed);
+//   * S_{i+1} = Q_{i+1} K^T is issued as soon as every row of S_i has been
+//     read (one S slot), so it runs under P_i V and the epilogue;
+//   * O is double-buffered in TMEM and the epilogue (normalise, 128-B row
+//     stores) trails by one tile: tile i-1's rows drain while P_i V runs;
+// and two such CTAs share an SM (TMEM: S at column 0, O slots at 128 / 192,
+// 256 columns each), so one CTA's softmax overlaps the other's waits.  Keys
+// are padded to NKP = 16 * ceil(lk / 16): only the last 16-key chunk needs a
+// mask; exponent arguments and row sums run on packed fp32x2 FMA / ADD.
+constexpr int kXpQSlots = 2;
+#ifdef SDB_XA_TRACE   // probe build only: per-CTA phase timestamps (scripts/k7_trace.py)
+__device__ unsigned long long g_xa_trace[512][16];
+__device__ __forceinline__ unsigned long long xa_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define XA_T(k)                                                    \
+  if (threadIdx.x == 0 && (k) < 16) g_xa_trace[blockIdx.x][k] = xa_ns();
+#else
+#define XA_T(k)
+#endif
+
+template <int NKP>
+__global__ void __launch_bounds__(kTcThreads, 2)
+xattn_tc_persistent_kernel(const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kvmap,
+                           int64_t voff, __nv_bfloat16* __restrict__ o, int64_t ldo, int lq, int lk, int heads,
+                           int qtiles, int total, float scale_log2) {
+  static_assert(NKP % 16 == 0 && NKP <= 128, "keys padded to 16, S in columns 0..127");
+  constexpr int kKBytes = ((NKP * 128 + 1023) / 1024) * 1024;
+  constexpr int kPBytes = NKP > 64 ? 32768 : 16384;
+  constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NKP >> 3) << 17) |
+                               ((uint32_t)(kTcM >> 4) << 24);
+  constexpr uint32_t kIdescO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(64 >> 3) << 17) |
+                               ((uint32_t)(kTcM >> 4) << 24);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  XA_T(0)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                               // 2 x 16 KB query tiles
+  uint8_t* sP = sQ + kXpQSlots * 16384;             // P tile (keys 0..63 | 64..)
+  uint8_t* sKV = sP + kPBytes;                      // 2 heads x (K_h | V_h), kKBytes each
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 4 * kKBytes);   // kv[2] q[2] s o[2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 7);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int t0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int nt = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x) - t0;
+  const int hd0 = t0 / qtiles;                      // first (sample, head) index of the run
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  auto kv_slot = [&](int i) { return (t0 + i) / qtiles - hd0; };      // 0 or 1
+  auto load_q = [&](int i) {                        // tile i of the run -> ring slot i % 2
+    const int tt = t0 + i, hd = tt / qtiles, qt = tt - hd * qtiles;
+    const int n = hd / heads, h = hd - n * heads;
+    mbar_expect_tx(bar(2 + (i & 1)), kTcM * 128);
+    tma_load_2d(smem_u32(sQ + (i & 1) * 16384), &qmap, h * 64, n * lq + qt * kTcM, bar(2 + (i & 1)),
+                policy_evict_first());
+  };
+  auto issue_s = [&](int i) {                       // S_i = Q_i K_h^T into the S slot
+    const uint8_t* k = sKV + kv_slot(i) * 2 * kKBytes;
+    mbar_wait(bar(kv_slot(i)), 0);
+    mbar_wait(bar(2 + (i & 1)), (i >> 1) & 1);
+    tc_fence_after();
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+      tc_mma(*tmem_holder, sw128_desc(smem_u32(sQ + (i & 1) * 16384) + ks * 32), sw128_desc(smem_u32(k) + ks * 32),
+             kIdescS, ks ? 1u : 0u);
+    tc_commit(bar(4));
+  };
+
+  if (tid == 0) {
+    prefetch_map(&qmap);
+    prefetch_map(&kvmap);
+    for (int i = 0; i < 7; ++i) mbar_init(bar(i), 1);
+    mbar_fence_init();
+    // K_h / V_h of the run's (<= 2) heads: the per-request K/V cache, read before the programmatic wait
+    const int nkv = nt > 0 ? kv_slot(nt - 1) + 1 : 0;
+    for (int s = 0; s < nkv; ++s) {
+      const int hd = hd0 + s, n = hd / heads, h = hd - n * heads;
+      uint8_t* k = sKV + s * 2 * kKBytes;
+      mbar_expect_tx(bar(s), 2 * NKP * 128);
+      tma_load_2d(smem_u32(k), &kvmap, h * 64, n * lk, bar(s), policy_evict_last());
+      tma_load_2d(smem_u32(k + kKBytes), &kvmap, (int)voff + h * 64, n * lk, bar(s), policy_evict_last());
+    }
+  }
+  pdl_wait();
+  if (tid == 0) {
+    for (int i = 0; i < min(nt, 2); ++i) load_q(i);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  XA_T(1)
+  if (tid == 0 && nt > 0) issue_s(0);
+  XA_T(2)
+
+  auto epilogue = [&](int i, float rl) {            // O_i (TMEM slot i & 1) -> normalised bf16 row
+    mbar_wait(bar(5 + (i & 1)), (i >> 1) & 1);
+    tc_fence_after();
+    float a[32], b[32];
+    const uint32_t ob = tmem + lane_off + 128 + (uint32_t)((i & 1) * 64);
+    tc_ld32(ob, a);
+    tc_ld32(ob + 32, b);
+    const int tt = t0 + i, hd = tt / qtiles, qt = tt - hd * qtiles;
+    const int n = hd / heads, h = hd - n * heads, row = qt * kTcM + tid;
+    if (row < lq) {
+      __nv_bfloat16* orow = o + ((int64_t)n * lq + row) * ldo + h * 64;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float* src = c < 4 ? a + 8 * c : b + 8 * (c - 4);
+        uint4 pk;
+        pk.x = pack2<__nv_bfloat16>(src[0] * rl, src[1] * rl);
+        pk.y = pack2<__nv_bfloat16>(src[2] * rl, src[3] * rl);
+        pk.z = pack2<__nv_bfloat16>(src[4] * rl, src[5] * rl);
+        pk.w = pack2<__nv_bfloat16>(src[6] * rl, src[7] * rl);
+        *reinterpret_cast<uint4*>(orow + c * 8) = pk;
+      }
+    }
+  };
+
+  float rl_prev = 1.f;
+#pragma unroll 1
+  for (int i = 0; i < nt; ++i) {
+    // ---- this thread's row of S_i, exact softmax, P_i -> shared ---------------
+    mbar_wait(bar(4), i & 1);
+    tc_fence_after();
+    XA_T(3 + 4 * i)
+    if (tid == 0 && i + 2 < nt) load_q(i + 2);     // S_i completed: its Q slot is free
+    float sv[NKP];
+#pragma unroll
+    for (int c = 0; c < NKP; c += 16) {
+      uint32_t r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(tmem + lane_off + (uint32_t)c));
+#pragma unroll
+      for (int j = 0; j < 16; ++j) sv[c + j] = __uint_as_float(r[j]);
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = NKP - 16; j < NKP; ++j)            // lk > NKP - 16: only the last chunk holds padding
+      if (j >= lk) sv[j] = -INFINITY;
+    float mx[4] = {sv[0], sv[1], sv[2], sv[3]};
+#pragma unroll
+    for (int j = 4; j < NKP; ++j) mx[j & 3] = fmaxf(mx[j & 3], sv[j]);
+    const float nmb = -fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+    float2 ls[2] = {f2s(0.f), f2s(0.f)};
+#pragma unroll
+    for (int j = 0; j < NKP; j += 2) {
+      const float2 t = f2fma(make_float2(sv[j], sv[j + 1]), f2s(scale_log2), f2s(nmb));
+      sv[j] = fast_exp2(t.x);
+      sv[j + 1] = fast_exp2(t.y);
+      ls[(j >> 1) & 1] = f2add(ls[(j >> 1) & 1], make_float2(sv[j], sv[j + 1]));
+    }
+    const float2 l2 = f2add(ls[0], ls[1]);
+    const float rl = fast_rcp(l2.x + l2.y);
+    if (i > 0) {                                    // P's last reader, P_{i-1} V, must be done
+      mbar_wait(bar(5 + ((i - 1) & 1)), ((i - 1) >> 1) & 1);
+    }
+#pragma unroll
+    for (int c = 0; c < NKP / 8; ++c) {
+      uint4 pk;
+      pk.x = pack2<__nv_bfloat16>(sv[8 * c + 0], sv[8 * c + 1]);
+      pk.y = pack2<__nv_bfloat16>(sv[8 * c + 2], sv[8 * c + 3]);
+      pk.z = pack2<__nv_bfloat16>(sv[8 * c + 4], sv[8 * c + 5]);
+      pk.w = pack2<__nv_bfloat16>(sv[8 * c + 6], sv[8 * c + 7]);
+      *reinterpret_cast<uint4*>(sP + (c >> 3) * 16384 + tid * 128 + (((c & 7) ^ (tid & 7)) << 4)) = pk;
+    }
+    XA_T(4 + 4 * i)
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();                                 // P_i complete; every row of S_i read; epilogue i-2 done
+    tc_fence_after();
+    if (tid == 0) {
+      // O_i = P_i V_h into O slot i & 1 (its last reader, epilogue i-2, ran before the barrier)
+      const uint8_t* v = sKV + kv_slot(i) * 2 * kKBytes + kKBytes;
+      const uint32_t d = tmem + 128 + (uint32_t)((i & 1) * 64);
+#pragma unroll
+      for (int ks = 0; ks < NKP / 16; ++ks)
+        tc_mma(d, sw128_desc(smem_u32(sP) + (ks >> 2) * 16384 + (ks & 3) * 32), sw128_desc(smem_u32(v) + ks * 2048),
+               kIdescO, ks ? 1u : 0u);
+      tc_commit(bar(5 + (i & 1)));
+      if (i + 1 < nt) issue_s(i + 1);                // every row of S_i was read before the barrier
+    }
+    if (i > 0) epilogue(i - 1, rl_prev);
+    XA_T(5 + 4 * i)
+    rl_prev = rl;
+    tc_fence_before();
+  }
+  if (nt > 0) epilogue(nt - 1, rl_prev);
+  XA_T(15)
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
 template <int NKP>
 int launch_tc(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o, int64_t ldo, int n,
-              int lq, int lk, int heads, float scale, cudaStream_t st) {
+              int lq, int lk, int heads, float scale, cudaStream_t st, bool persistent) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled unavailable");
   CUtensorMap qm, km;
@@ -444,6 +656,20 @@ int launch_tc(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t 
       return fail(SDB_EINVAL, "cross_attention: kv tensor map");
   }
   constexpr int kKBytes = ((NKP * 128 + 1023) / 1024) * 1024;
+  if (persistent) {
+    const int qtiles = (lq + kTcM - 1) / kTcM;
+    const int total = qtiles * heads * n;
+    const int grid = std::min(total, 2 * kNumSMs);
+    const int psmem = 1024 + kXpQSlots * 16384 + (NKP > 64 ? 32768 : 16384) + 4 * kKBytes + 128;
+    static bool pattr = false;
+    if (!pattr) {
+      cudaFuncSetAttribute(xattn_tc_persistent_kernel<NKP>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem);
+      pattr = true;
+    }
+    launch_k(xattn_tc_persistent_kernel<NKP>, dim3((unsigned)grid), kTcThreads, psmem, st, qm, km, voff,
+             static_cast<__nv_bfloat16*>(o), ldo, lq, lk, heads, qtiles, total, scale * 1.4426950408889634f);
+    return check_launch("xattn_tc_persistent_kernel");
+  }
   const int smem = 1024 + 32768 + 2 * kKBytes + 64;
   static bool attr = false;
   if (!attr) {
@@ -497,11 +723,32 @@ int by_keys(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t vo
 
 }  // namespace
 
-static int g_xattn_tc = 1;   // 1: tcgen05 form for head dim 64 (sdb_cross_attention_set_mode)
+// head dim 64: 2 = the persistent tcgen05 form where each CTA's run spans
+// <= 2 heads (default), 1 = the per-tile tcgen05 form (one-wave grids) else
+// mma.sync, 0 = mma.sync only (sdb_cross_attention_set_mode)
+static int g_xattn_tc = 2;
 int cross_attention_set_mode(int tc) {
   const int prev = g_xattn_tc;
-  g_xattn_tc = tc ? 1 : 0;
+  g_xattn_tc = tc < 0 ? 0 : (tc > 2 ? 2 : tc);
   return prev;
+}
+
+#ifdef SDB_XA_TRACE
+extern "C" __attribute__((visibility("default"))) int sdb_debug_xa_trace(unsigned long long* host, int ctas) {
+  return cudaMemcpyFromSymbol(host, g_xa_trace, (size_t)ctas * 16 * sizeof(unsigned long long)) == cudaSuccess ? 0 : -2;
+}
+#endif
+
+// The persistent form where its CTA runs cover <= 2 (sample, head) pairs and
+// the grid is large enough for its pipeline to fill: >= 2 resident waves of
+// the per-tile form (measured, scripts/k7_forms.py: serving batch 16 [16,4096,
+// 640] 60.3 vs 69.4 us, [16,1024,1280] 30.7 vs 43.4 us; at batch 2 its runs are
+// ~2 tiles long and the per-tile / mma.sync forms win, 10.4 vs 13.4 us)
+static bool xattn_persistent_ok(int n, int lq, int heads) {
+  const int64_t qtiles = (lq + kTcM - 1) / kTcM, total = qtiles * heads * n;
+  if (total < 2 * 4 * (int64_t)kNumSMs) return false;
+  const int64_t grid = std::min<int64_t>(total, 2 * kNumSMs);
+  return (total + grid - 1) / grid - 1 <= qtiles;
 }
 
 int cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, int64_t voff, void* o, int64_t ldo,
@@ -526,9 +773,22 @@ int cross_attention(const void* q, int64_t ldq, const void* kv, int64_t ldkv, in
       // whose warps walk several tiles with the next tile's load in flight
       // (measured round 1: SDXL 32x32 level 7.4 vs 8.1 us, 64x64 level
       // 11.3 vs 10.4 us)
+      if (d == 64 && g_xattn_tc == 2 && xattn_persistent_ok(n, lq, heads)) {
+        // keys padded to the next 16 (the kernel masks only the last chunk)
+        switch ((lk + 15) / 16) {
+          case 1: return launch_tc<16>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          case 2: return launch_tc<32>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          case 3: return launch_tc<48>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          case 4: return launch_tc<64>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          case 5: return launch_tc<80>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          case 6: return launch_tc<96>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          case 7: return launch_tc<112>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+          default: return launch_tc<128>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, true);
+        }
+      }
       if (d == 64 && g_xattn_tc && (int64_t)((lq + kTcM - 1) / kTcM) * heads * n <= 4 * kNumSMs) {
-        if (lk <= 80) return launch_tc<80>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st);
-        return launch_tc<128>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st);
+        if (lk <= 80) return launch_tc<80>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, false);
+        return launch_tc<128>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, scale, st, false);
       }
       return by_keys<__nv_bfloat16>(q, ldq, kv, ldkv, voff, o, ldo, n, lq, lk, heads, d, scale, st);
     default: return fail(SDB_EUNSUP, "cross_attention: bf16 only");

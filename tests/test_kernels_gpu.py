@@ -173,16 +173,19 @@ def test_add_layernorm(c, with_delta):
 
 # K7 cross-attention: SDXL levels (d = 64), SD1.5 (8 heads: d = 40 / 80 / 160),
 # the toy config (d = 8, 8 tokens), ragged query counts, context 77 / 100 / 128
-XATTN = [(2, 4096, 640, 10, 77), (2, 1024, 1280, 20, 77), (2, 4096, 320, 8, 77), (2, 1024, 640, 8, 77),
+XATTN = [(2, 4096, 640, 10, 77), (2, 1024, 1280, 20, 77), (16, 1024, 1280, 20, 77), (8, 4096, 640, 10, 40),
+         (16, 4096, 640, 10, 77), (12, 2000, 640, 10, 128), (2, 4096, 320, 8, 77), (2, 1024, 640, 8, 77),
          (2, 256, 1280, 8, 77), (2, 4096, 32, 4, 8), (1, 1000, 640, 10, 100), (3, 77, 128, 2, 128),
          (2, 17, 64, 1, 1)]
 
 
-@pytest.mark.parametrize("tc", [1, 0])
+@pytest.mark.parametrize("tc", [2, 1, 0])
 @pytest.mark.parametrize("n,lq,c,heads,lk", XATTN)
 def test_cross_attention_vs_fp32(n, lq, c, heads, lk, tc):
-    """K7 vs fp32 SDPA; tc=1 runs head dim 64 through the tcgen05 form, tc=0
-    through the mma.sync form (other head dims always use the latter)."""
+    """K7 vs fp32 SDPA; head dim 64 runs the persistent tcgen05 form (tc=2,
+    the default: runs of 128-query tiles per CTA, S / O double-buffered in
+    TMEM), the per-tile tcgen05 form (tc=1) or the mma.sync form (tc=0);
+    other head dims always use the latter."""
     lib = ops._lib.lib()
     prev = lib.sdb_cross_attention_set_mode(tc)
     try:
