@@ -462,15 +462,24 @@ def other_kernels_roofline(hbm: float) -> list:
     out = []
     g, bta = torch.ones(320, device=dev), torch.zeros(320, device=dev)
 
-    def mk_gn():
-        x = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
-        add = torch.zeros(2, 320, device=dev)
-        ws = ops.groupnorm_workspace(x)
-        y = torch.empty_like(x)
-        return lambda: ops.groupnorm_silu(x, g, bta, out=y, add_nc=add, workspace=ws)
+    def mk_gn(mode):
+        def make():
+            x = torch.randn(2, 320, 128, 128, device=dev).to(torch.bfloat16).contiguous(memory_format=cl)
+            add = torch.zeros(2, 320, device=dev)
+            ws = ops.groupnorm_workspace(x)
+            y = torch.empty_like(x)
+
+            def f():
+                with ops.groupnorm_mode(mode):
+                    ops.groupnorm_silu(x, g, bta, out=y, add_nc=add, workspace=ws)
+            return f
+        return make
     n_gn = 2 * 320 * 128 * 128
-    out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16, two-pass (stats + apply)", 2 * n_gn * 2,
-                timed(mk_gn, n_gn * 2)))
+    out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16, resident form (the shipped choice: one cooperative "
+                "launch, tiles resident in shared memory, one grid barrier; the 9 two-pass sites at 128x128 per "
+                "SDXL step incl. ControlNets)", 2 * n_gn * 2, timed(mk_gn(0), n_gn * 2)))
+    out.append(("K2 groupnorm+silu (+temb) [2,320,128,128] bf16, two-pass form (stats + apply; round 1's choice)",
+                2 * n_gn * 2, timed(mk_gn(1), n_gn * 2)))
 
     g6, b6 = torch.ones(640, device=dev), torch.zeros(640, device=dev)
 
@@ -551,6 +560,15 @@ def other_kernels_roofline(hbm: float) -> list:
     nq = 2 * 1024 * 1280
     out.append(("K7 cross-attention [2,1024,1280] x 77 tokens, 20 heads bf16 (tcgen05 form)", 2 * nq * 2,
                 timed(mk_xattn_tc, nq * 2)))
+
+    def mk_xattn_srv():
+        q = torch.randn(16, 1024, 1280, device=dev).to(torch.bfloat16)
+        kv = torch.randn(16, 77, 2560, device=dev).to(torch.bfloat16)
+        o = torch.empty_like(q)
+        return lambda: ops.cross_attention(q, kv, 20, out=o)
+    nq = 16 * 1024 * 1280
+    out.append(("K7 cross-attention [16,1024,1280] x 77 tokens, 20 heads bf16 (config 5's CFG batch 16: persistent "
+                "tcgen05 form)", 2 * nq * 2 + 16 * 77 * 2560 * 2, timed(mk_xattn_srv, nq * 2)))
     return [{"kernel": k, "achieved": b / (m * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
              "frac": b / (m * 1e-3) / 1e9 / hbm, "alg_bytes": b, "launch_ms": m,
              "method": "CUDA-graph replay, inputs rotated over > 2x L2"} for k, b, m in out]
