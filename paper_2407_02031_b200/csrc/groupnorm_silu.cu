@@ -63,6 +63,7 @@ constexpr size_t kWsHeader = 256;
 constexpr int kBankWords = kMaxN * kMaxGroups * 4;
 constexpr size_t kWsBytes = kWsHeader + 2 * (size_t)kBankWords * sizeof(long long);
 constexpr double kFracScale = 1099511627776.0;        // 2^40
+constexpr size_t kRsCntOffset = 128;   // the resident form's per-sample arrival counts: header bytes [128, 256) = [2 banks][16 samples] u32
 struct WsHeader {
   unsigned int epoch;      // bank of the next producer launch = epoch & 1
   unsigned int cur;        // bank the last producer launch filled (what apply reads)
@@ -164,6 +165,8 @@ __device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch, uns
   long long* idle = banks + (size_t)((epoch + 1u) & 1u) * kBankWords;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x, ctas = gridDim.x * gridDim.y;
   for (int i = cta * blockDim.x + threadIdx.x; i < rows * kMaxGroups * 4; i += ctas * blockDim.x) idle[i] = 0;
+  if (cta == 0 && threadIdx.x < kMaxN)   // the resident form's counts of the next launch (any form may follow)
+    reinterpret_cast<unsigned int*>(ws + kRsCntOffset)[((epoch + 1u) & 1u) * kMaxN + threadIdx.x] = 0u;
   if (cta == 0 && threadIdx.x == 0) {
     hdr->cur = epoch & 1u;
     hdr->hwm = (unsigned int)rows;
@@ -410,7 +413,6 @@ constexpr int kRsMaxGroups = 32;
 constexpr int kRsMaxChunks = 12;
 constexpr int kRsTileMax = 176 * 1024;
 constexpr int kRsExtra = kRsThreads * 4 * 8 + 2 * kRsMaxGroups * 4 + kRsMaxChunks * 8 + 4 * 4 + 128;
-constexpr size_t kRsBarOffset = 128;     // the resident form's barrier word, in the header's second line
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int* p) {
   unsigned int v;
@@ -469,7 +471,7 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   pdl_wait();
   RS_T(1)
   WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
-  unsigned int* barw = reinterpret_cast<unsigned int*>(ws + kRsBarOffset);
+  unsigned int* cnts = reinterpret_cast<unsigned int*>(ws + kRsCntOffset);   // [2][kMaxN]
   if (tid == 0) {
     const __nv_bfloat16* xs = x + ((size_t)n * hw + r0) * c;
     const uint64_t pol = policy_evict_first();       // x is dead after this op
@@ -479,10 +481,19 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
       mbar_expect_tx(bar, bytes);
       bulk_g2s(smem_u32(tile + (size_t)k * cr * rowb), xs + (size_t)k * cr * c, bytes, bar, pol);
     }
-  } else if (tid == 32) {   // the header, read once per CTA while the copies fly (nothing here can
-    snap[0] = ld_relaxed(&hdr->epoch);   // change before every CTA of this launch has arrived)
-    snap[1] = ld_relaxed(&hdr->hwm);
-    snap[2] = ld_relaxed(barw);
+  } else if (tid == 32) {   // the header, read once per CTA while the copies fly
+    const unsigned int e = ld_relaxed(&hdr->epoch);
+    const unsigned int hwm = ld_relaxed(&hdr->hwm);
+    snap[0] = e;
+    snap[1] = hwm;
+    // the last CTA to have read the epoch advances it for the next launch on
+    // this workspace (every CTA of this one holds e by then); no CTA waits
+    if (atomicAdd(&hdr->arrivals, 1u) == gridDim.x - 1u) {
+      hdr->arrivals = 0u;
+      hdr->cur = e & 1u;
+      hdr->hwm = (unsigned int)max((int)hwm, (int)(gridDim.x / per_sample));
+      hdr->epoch = e + 1u;
+    }
   }
 
   const int cv = c >> 3;
@@ -548,35 +559,45 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   const unsigned int e0 = snap[0];
   long long* banks = reinterpret_cast<long long*>(ws + kWsHeader);
   long long* bank = banks + (size_t)(e0 & 1u) * kBankWords + (size_t)n * kMaxGroups * 4;
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int g = warp; g < gs; g += NT / 32) {   // a warp per group: the columns touching it, their threads in a fixed order
-    float m1 = 0.f, m2 = 0.f;
-    const int jlo = (g * cpg) >> 3, jhi = min(cv - 1, ((g + 1) * cpg - 1) >> 3);
-    for (int jj = jlo; jj <= jhi; ++jj) {
-      const bool isA = (jj * 8) / cpg == g;           // this group is the column's A or B part
-      for (int q = lane; q < rstep; q += 32) {
-        const float4 p = reinterpret_cast<const float4*>(part)[jj + q * cv];
-        m1 += isA ? p.x : p.z;
-        m2 += isA ? p.y : p.w;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
-      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
-    }
-    if (lane == 0) {
-      // raw moments of x' over this CTA's rows x cpg channels of the group, in fp64
-      const double K = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(tile)[g * cpg]);
-      const double M = (double)rows * cpg, S1 = m1;
-      red_fixed(bank + g * 4, S1 + M * K);
-      red_fixed(bank + g * 4 + 2, (double)m2 + K * (2.0 * S1 + M * K));
-    }
+  // two short, fixed-order stages (a warp per group walked its columns and
+  // shuffled serially: ~3 us of dependent latency at 4 warps per scheduler):
+  //   1. column sums: one thread per (column, component) over the rstep rows
+  //   2. group sums: one thread per (group, moment) over its <= 3 columns,
+  //      fp64 raw moments, one fixed-point red each
+  float4* part4 = reinterpret_cast<float4*>(part);
+  float* colsum = reinterpret_cast<float*>(part4 + NT);          // [cv][4]
+  for (int v = tid; v < cv * 4; v += NT) {
+    const int col = v >> 2, comp = v & 3;
+    const float* src = reinterpret_cast<const float*>(part4 + col) + comp;
+    float acc = 0.f;
+    for (int q = 0; q < rstep; ++q) acc += src[q * cv * 4];
+    colsum[v] = acc;
   }
-  {  // zero the idle bank for the next producer launch on this workspace (a slice per CTA)
+  __syncthreads();
+  for (int v = tid; v < gs * 2; v += NT) {
+    const int g = v >> 1, mom = v & 1;
+    const int jlo = (g * cpg) >> 3, jhi = min(cv - 1, ((g + 1) * cpg - 1) >> 3);
+    float m1 = 0.f, m2 = 0.f;
+    for (int jj = jlo; jj <= jhi; ++jj) {
+      const int off = jj * 8 >= g * cpg ? 0 : 2;        // the column's A part starts in it, else its B part
+      m1 += colsum[jj * 4 + off];
+      m2 += colsum[jj * 4 + off + 1];
+    }
+    // raw moments of x' over this CTA's rows x cpg channels of the group, in fp64
+    const double K = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(tile)[g * cpg]);
+    const double M = (double)rows * cpg, S1 = m1;
+    red_fixed(bank + g * 4 + 2 * mom, mom == 0 ? S1 + M * K : (double)m2 + K * (2.0 * S1 + M * K));
+  }
+  // ---- per-sample completion: one release-add per CTA on its sample's count
+  __syncthreads();                                   // every group's reds issued
+  RS_T(3)
+  unsigned int* cnt = cnts + (e0 & 1u) * kMaxN + n;
+  if (tid == 0) asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+  {  // zero the idle bank and counts for the next producer launch on this workspace (a slice per CTA)
     const int brows = max((int)snap[1], (int)(gridDim.x / per_sample));
     long long* idle = banks + (size_t)((e0 + 1u) & 1u) * kBankWords;
     for (int i = blockIdx.x * NT + tid; i < brows * kMaxGroups * 4; i += gridDim.x * NT) idle[i] = 0;
+    if (blockIdx.x == 0 && tid < kMaxN) cnts[((e0 + 1u) & 1u) * kMaxN + tid] = 0u;
   }
   float ga[8], be[8];   // the affine parameters, in flight across the barrier
 #pragma unroll
@@ -584,26 +605,14 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
     ga[e] = gamma != nullptr ? __ldg(gamma + ch0 + e) : 1.f;
     be[e] = beta != nullptr ? __ldg(beta + ch0 + e) : 0.f;
   }
-  // ---- grid barrier: one release-add per CTA on the bar word, flip of its top bit --
-  // CTA 0 adds 2^31 - (ctas - 1), every other CTA 1: the word's top bit flips
-  // exactly when the last CTA arrives and its low bits return to their start
-  // value (zero), so it needs no reset and no second atomic.
-  __syncthreads();
-  RS_T(3)
-  if (tid == 0) {
-    const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
-    asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(barw), "r"(inc) : "memory");
-    const unsigned int top = snap[2] & 0x80000000u;
-    // co-residency is guaranteed by the cooperative launch; the watchdog
+  if (tid < gs) {
+    // the sample's statistics are final once all its CTAs have counted in;
+    // co-residency is guaranteed by the cooperative launch, and the watchdog
     // turns a broken guarantee into a loud fault instead of a hung GPU
     const unsigned long long t0 = global_ns();
-    while ((ld_acquire(barw) & 0x80000000u) == top) {
+    while (ld_acquire(cnt) < (unsigned int)per_sample) {
       if (global_ns() - t0 > 2000000000ull) __trap();
     }
-  }
-  __syncthreads();
-  RS_T(4)
-  if (tid < gs) {
     const double count = (double)hw * cpg;
     const double mean = fixed_value_cg(bank + tid * 4) / count;
     double var = fixed_value_cg(bank + tid * 4 + 2) / count - mean * mean;
@@ -611,12 +620,8 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
     stat[tid] = (float)mean;
     stat[kRsMaxGroups + tid] = (float)var;
   }
-  if (blockIdx.x == 0 && tid == 32) {   // every CTA has read the epoch (it arrived): advance it
-    hdr->cur = e0 & 1u;
-    hdr->hwm = (unsigned int)max((int)snap[1], (int)(gridDim.x / per_sample));
-    hdr->epoch = e0 + 1u;
-  }
   __syncthreads();
+  RS_T(4)
   // ---- apply (+ SiLU) from shared memory, 16-B stores ------------------------
   if (!active) return;
   float2 A[4], B[4];

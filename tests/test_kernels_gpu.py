@@ -459,6 +459,27 @@ def test_groupnorm_resident_form_concurrent_streams():
     assert all(torch.equal(a, b) for a, b in zip(seq, outs))
 
 
+def test_groupnorm_forms_share_a_workspace():
+    """Resident, two-pass and K3-fed launches interleaved on ONE workspace
+    (each producer form re-arms the next launch's bank and counts): every
+    result equals the same form run on a fresh workspace, bitwise."""
+    n, c, h, w = 2, 320, 64, 64
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xs = [cl((torch.randn(n, c, h, w, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)) for _ in range(3)]
+    gamma, beta = torch.rand(c, device="cuda", generator=g) + 0.5, torch.randn(c, device="cuda", generator=g)
+    shared = ops.groupnorm_workspace(xs[0])
+    fresh = {}
+    for mode in (4, 1):
+        with ops.groupnorm_mode(mode):
+            fresh[mode] = [ops.groupnorm_silu(x, gamma, beta, workspace=ops.groupnorm_workspace(x)) for x in xs]
+    for rep in range(3):
+        for mode in (4, 1, 4, 4, 1, 1):
+            for i, x in enumerate(xs):
+                with ops.groupnorm_mode(mode):
+                    y = ops.groupnorm_silu(x, gamma, beta, workspace=shared)
+                assert torch.equal(y, fresh[mode][i]), (rep, mode, i)
+
+
 def test_groupnorm_large_maps_take_the_two_pass_form():
     lib = ops._lib.lib()
     bf16 = ops.sdb_dtype(torch.empty(0, dtype=torch.bfloat16))
