@@ -168,14 +168,15 @@ int sdb_lora_tc_set_mode(int mode);
  * workspace must be ordered on one stream.  y may alias x.
  * ======================================================================== */
 size_t sdb_groupnorm_workspace(int64_t n, int64_t hw, int64_t c, int64_t groups);
-/* K2 form selection: mode 0 (default) runs a single-pass cluster form
- * wherever the shape fits (bf16, C/G >= 8): one launch, one read, one write,
- * a thread-block cluster per (sample, channel slab) holding that slab of the
- * map in shared memory — round 1's form for maps <= 6 MB, the streamed form
- * (TMA chunks overlapped with the statistics, each chunk stored as soon as it
- * is normalised) for larger maps up to 64 MB — else the two-pass form.
+/* K2 form selection: mode 0 (default) runs the resident form wherever it
+ * fits (below), else a single-pass cluster form where the shape fits (bf16,
+ * C/G >= 8): one launch, one read, one write, a thread-block cluster per
+ * (sample, channel slab) holding that slab of the map in shared memory —
+ * round 1's form for maps <= 6 MB, the streamed form (TMA chunks overlapped
+ * with the statistics, each chunk stored as soon as it is normalised) for
+ * larger maps whose clusters fit one wave — else the two-pass form.
  * Mode 1 forces the two-pass form, 2 only round 1's cluster form, 3 only the
- * streamed form.  sdb_groupnorm_launches returns the kernel launches
+ * streamed form, 4 only the resident form.  sdb_groupnorm_launches returns the kernel launches
  * sdb_groupnorm_silu will make for a shape; sdb_groupnorm_stream_plan fills
  * out7 = {slab channels, cluster CTAs, rows per CTA, rows per chunk, chunks,
  * clusters, co-resident clusters} of the streamed form (0 = not eligible). */
@@ -183,10 +184,12 @@ void sdb_groupnorm_set_mode(int mode);
 int sdb_groupnorm_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype);
 int sdb_groupnorm_stream_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out7);
 /* The resident form (one cooperative launch, one CTA per SM holding a run of
- * pixels in shared memory, statistics exchanged through the workspace's
- * fixed-point bank across one grid barrier): auto for bf16 maps > 6 MB that
- * fit the SMs' shared memory; mode 4 forces it where eligible.  out4 = {rows
- * per CTA, CTAs per sample, rows per copy chunk, CTAs}; 0 = not eligible. */
+ * pixels of one sample in shared memory, statistics exchanged through the
+ * workspace's fixed-point bank, each CTA waiting only for its sample's
+ * CTAs): auto for bf16 maps with C/G >= 8, <= 32 groups and <= 148 CTAs of
+ * <= 176 KB tiles (SDB_GN_RESIDENT=0 in the environment turns it off).
+ * out4 = {rows per CTA, CTAs per sample, rows per copy chunk, CTAs}; 0 = not
+ * eligible. */
 int sdb_groupnorm_resident_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, int* out4);
 
 /* Programmatic dependent launch (default on; SDB_PDL=0 in the environment

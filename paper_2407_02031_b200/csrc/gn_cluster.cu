@@ -717,12 +717,6 @@ static int gn_form(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype, 
 // Kernel launches a full GroupNorm of this shape costs: 1 (a cluster form) or 2.
 bool gn_resident_auto(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu, int dtype);
 
-// The streamed form is eligible and its clusters run in one wave.
-bool gn_stream_one_wave(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu) {
-  GsPlan p;
-  return g_gn_cluster_mode != 1 && gs_plan(n, hw, c, groups, silu != 0, p) && p.clusters <= p.active;
-}
-
 int gn_launches(int64_t n, int64_t hw, int64_t c, int64_t groups, int dtype) {
   if (gn_resident_auto(n, hw, c, groups, 1, dtype)) return 1;
   return gn_form(n, hw, c, groups, dtype, 1, nullptr, nullptr) != 0 ? 1 : 2;

@@ -932,12 +932,11 @@ int gn_cluster_try(const void* x, void* y, const float* gamma, const float* beta
                    bool* launched);
 
 extern int g_gn_cluster_mode;   // gn_cluster.cu: 0 auto, 1 two-pass, 2 / 3 cluster forms, 4 resident form
-bool gn_stream_one_wave(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu);   // gn_cluster.cu
 
 // Auto choice of the resident form (scripts/k2_resident.py, profiles/r02_k2_resident.txt):
-// wherever it is eligible except where the streamed cluster form runs in one
-// wave on a map <= 10.5 MB (there its clusters win: [2,640,64,64] 14.0 vs
-// 15.6 us); SDB_GN_RESIDENT=0 turns it off.
+// wherever it is eligible — since the two-stage fold it beats the cluster
+// forms at every SDXL size too ([2,640,64,64] 12.4 vs 14.2 us, [2,1280,32,32]
+// 10.0 vs 12.3, [2,640,32,32] 8.3 vs 10.1); SDB_GN_RESIDENT=0 turns it off.
 bool gn_resident_auto(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu, int dtype) {
   static int env = -1;
   if (env < 0) {
@@ -949,8 +948,8 @@ bool gn_resident_auto(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu
   RsPlan p;
   if (!rs_plan(n, hw, c, groups, p)) return false;
   if (mode == 4) return true;
-  if (!env) return false;
-  return !(n * hw * c * 2 <= ((int64_t)21 << 19) && gn_stream_one_wave(n, hw, c, groups, silu));
+  (void)silu;
+  return env != 0;
 }
 
 // The resident form where the shape and the device allow it; *launched tells.

@@ -486,7 +486,7 @@ def test_groupnorm_large_maps_take_the_two_pass_form():
     assert lib.sdb_groupnorm_launches(2, 128 * 128, 320, 32, bf16) == 1     # resident form (21 MB)
     assert lib.sdb_groupnorm_launches(2, 128 * 128, 640, 32, bf16) == 2     # 42 MB: beyond the SMs' shared memory
     assert lib.sdb_groupnorm_launches(16, 128 * 128, 320, 32, bf16) == 2
-    assert lib.sdb_groupnorm_launches(2, 64 * 64, 640, 32, bf16) == 1       # streamed form, one wave
+    assert lib.sdb_groupnorm_launches(2, 64 * 64, 640, 32, bf16) == 1       # resident form
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, bf16) == 1
     assert lib.sdb_groupnorm_launches(2, 32 * 32, 1280, 32, ops.sdb_dtype(torch.empty(0))) == 2   # fp32
 
