@@ -664,16 +664,42 @@ struct RsPlan {
   size_t smem = 0;
 };
 
+// threads per CTA: SDB_GN_RS_THREADS = 512 (default, measured best) / 768 / 1024 (probe knob)
+int rs_threads() {
+  static int nt = -1;
+  if (nt < 0) {
+    nt = 512;
+    if (const char* e = getenv("SDB_GN_RS_THREADS")) nt = atoi(e);
+    if (nt != 768 && nt != 1024) nt = 512;
+  }
+  return nt;
+}
+
+// SMs a cooperative grid may span on the current device (0: no cooperative launch)
+int rs_coop_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0, coop = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    if (!coop) sms = 0;
+    cudaGetLastError();
+  }
+  return sms;
+}
+
 bool rs_plan(int64_t n, int64_t hw, int64_t c, int64_t groups, RsPlan& p) {
   const int64_t cpg = c / groups;
-  if (groups > kRsMaxGroups || c % 8 != 0 || c / 8 > kRsThreads) return false;
+  const int nt = rs_threads();
+  if (groups > kRsMaxGroups || c % 8 != 0 || c / 8 > nt) return false;
   if (cpg < 8) return false;                        // an 8-channel vector spans <= 2 groups
   if (n > kNumSMs) return false;
   const int64_t per = kNumSMs / n;                  // CTAs per sample, one per SM
   int64_t P = (hw + per - 1) / per;
   if (P * c * 2 > kRsTileMax) return false;
   const int64_t per_sample = (hw + P - 1) / P;      // every CTA owns >= 1 row
-  const int64_t rstep = kRsThreads / (c / 8);
+  const int64_t rstep = nt / (c / 8);
   // chunks: a whole number of thread row-steps, ~8 of them per tile
   int64_t cr = std::max<int64_t>(1, (P + 7) / 8);
   cr = ((cr + rstep - 1) / rstep) * rstep;
@@ -946,10 +972,9 @@ bool gn_resident_auto(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu
   const int mode = g_gn_cluster_mode;
   if (dtype != SDB_BF16 || (mode != 0 && mode != 4)) return false;
   RsPlan p;
-  if (!rs_plan(n, hw, c, groups, p)) return false;
-  if (mode == 4) return true;
+  if (!rs_plan(n, hw, c, groups, p) || p.ctas > rs_coop_sms()) return false;
   (void)silu;
-  return env != 0;
+  return mode == 4 || env != 0;
 }
 
 // The resident form where the shape and the device allow it; *launched tells.
@@ -960,24 +985,7 @@ static int gn_resident_try(const void* x, void* y, const float* gamma, const flo
   if (!gn_resident_auto(n, hw, c, groups, silu, dtype)) return SDB_OK;
   RsPlan p;
   if (!rs_plan(n, hw, c, groups, p)) return SDB_OK;
-  static int sms = -1;
-  if (sms < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 0;
-    int coop = 0;
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (!coop) sms = 0;
-    cudaGetLastError();
-  }
-  if (p.ctas > sms) return SDB_OK;
-  static int nt = -1;      // SDB_GN_RS_THREADS: 512 / 768 / 1024 (probe knob; 512 measured best)
-  if (nt < 0) {
-    nt = 512;
-    if (const char* e = getenv("SDB_GN_RS_THREADS")) nt = atoi(e);
-    if (nt != 768 && nt != 1024) nt = 512;
-  }
-  if (c / 8 > nt) return SDB_OK;
+  const int nt = rs_threads();
   auto kern = nt == 512   ? (silu ? gn_resident_kernel<true, 512> : gn_resident_kernel<false, 512>)
               : nt == 768 ? (silu ? gn_resident_kernel<true, 768> : gn_resident_kernel<false, 768>)
                           : (silu ? gn_resident_kernel<true, 1024> : gn_resident_kernel<false, 1024>);
