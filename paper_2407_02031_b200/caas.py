@@ -290,6 +290,66 @@ class CaaSPeerProtocol(CaaSProtocol):
         return []
 
 
+    _TEST = 0x5DB0_0001    # flag / marker value of the setup self-test (never a step number)
+
+    def self_test(self) -> bool:
+        """Exercise each peer operation the per-step protocol uses once, with
+        host-side checks only (no device-side wait that could hang): the base
+        raises every service's message flag and writes a marker into its
+        message; each service checks its flag, pulls the message over the
+        mapping and checks the marker, then raises the base's residual flag
+        and writes a marker into its slice of the base's receive buffer; the
+        base checks both.  Flags are reset to 0 afterwards.  Returns this
+        rank's verdict (``make_protocol`` takes the group's AND).  Run once at
+        setup, so a GPU pair whose NVLink mapping, stream memory operations or
+        peer copies misbehave falls back to the NCCL transport instead of
+        failing inside a captured step graph."""
+        ok = True
+        t = self._TEST
+        msg_i32 = self.msg.view(-1).view(torch.uint8)[:16].view(torch.int32)
+        try:
+            if self.role == "base":
+                msg_i32.fill_(t)
+                for f in self.peer_msg_flags:
+                    self._write(f, t)
+                torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.pg)
+            if self.role != "base":
+                ok &= int(self.msg_flag.item()) == t
+                pulled = torch.empty_like(self.msg)
+                self._copy(pulled, self.peer_msg)
+                torch.cuda.current_stream().synchronize()
+                ok &= bool((pulled.view(-1).view(torch.uint8)[:16].view(torch.int32) == t).all().item())
+                mark = torch.full((4,), self.rank + 1, dtype=torch.int32, device=self.msg.device)
+                _lib = self._lib()
+                _lib.check("sdb_memcpy_async", _lib.lib().sdb_memcpy_async(
+                    self.peer_flat.data_ptr(), mark.data_ptr(), 16, torch.cuda.current_stream().cuda_stream))
+                self._write(self.peer_res_flag, t)
+                torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.pg)
+            if self.role == "base":
+                ok &= bool((self.res_flags == t).all().item())
+                for i, s in enumerate(self.group.services):
+                    got = self.flats[i].view(-1).view(torch.uint8)[:16].view(torch.int32)
+                    ok &= bool((got == s + 1).all().item())
+        except Exception:   # noqa: BLE001 — any failure of the peer path selects the NCCL transport
+            ok = False
+        import os
+        if os.environ.get("SDB_CAAS_P2P_SELFTEST") == f"fail{self.rank}":   # fault injection (tests)
+            ok = False
+        # reset this rank's own flags (and the test markers) before any step runs
+        if self.role == "base":
+            self.res_flags.zero_()
+            msg_i32.zero_()
+            for f in self.flats:
+                f.view(-1).view(torch.uint8)[:16].zero_()
+        else:
+            self.msg_flag.zero_()
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.pg)
+        return ok
+
+
 class _FlagWait:
     """Base side: the current stream waits for service i's residuals of a step."""
 
@@ -315,7 +375,16 @@ def make_protocol(layout: CaaSLayout, rank: int, msg: torch.Tensor, flats: Seque
             a == b or torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs)
         transport = "p2p" if ok else "nccl"
     if transport == "p2p":
-        return CaaSPeerProtocol(layout, rank, msg, flats, pg)
+        try:
+            proto = CaaSPeerProtocol(layout, rank, msg, flats, pg)
+            ok = proto.self_test()
+        except Exception:   # noqa: BLE001 — e.g. an IPC mapping the driver refuses
+            proto, ok = None, False
+        verdicts = [None] * len(layout.group_of(rank).ranks)
+        dist.all_gather_object(verdicts, bool(ok), group=pg)
+        if all(verdicts):
+            return proto
+        transport = "nccl"      # every rank of the group falls back together
     if transport == "nccl":
         return CaaSProtocol(layout, rank, msg, flats, pg)
     raise ValueError(f"unknown CaaS transport {transport!r} (p2p | nccl | auto)")

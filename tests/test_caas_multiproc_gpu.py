@@ -32,7 +32,9 @@ def _worker(rank, world, port, out, transport):
     from paper_2407_02031_b200.caas import CaaSNode, caas_layout
     from paper_2407_02031_b200.patcher import synthetic_lora
     from paper_2407_02031_b200.pipeline import synthetic_request
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SDB_CAAS_TRANSPORT=transport)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SDB_CAAS_TRANSPORT=transport.split("-")[0])
+    if transport.endswith("-fail1"):       # rank 1's peer self-test fails: the group must fall back together
+        os.environ["SDB_CAAS_P2P_SELFTEST"] = "fail1"
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.allow_tf32 = False
     torch.cuda.set_device(0)
@@ -77,12 +79,14 @@ def single_gpu():
     return pipe.latent_nchw().cpu().clone()
 
 
-@pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (4, "p2p"), (3, "nccl")])
+@pytest.mark.parametrize("world,transport", [(2, "p2p"), (3, "p2p"), (4, "p2p"), (3, "nccl"), (3, "p2p-fail1")])
 def test_multiprocess_caas_matches_single_gpu(world, transport):
     """transport p2p: CaaSPeerProtocol (IPC mappings + GPU-side step flags; on
     one GPU the 'peer' copies are same-device copies); nccl: CaaSProtocol
     (here gloo, device buffers staged through the host).  world 4 adds a solo
-    rank (serves whole images alone, no transport)."""
+    rank (serves whole images alone, no transport); p2p-fail1: rank 1's setup
+    self-test of the peer path fails, so the whole group takes the NCCL
+    transport (caas.make_protocol)."""
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     out = mgr.dict()
@@ -94,7 +98,7 @@ def test_multiprocess_caas_matches_single_gpu(world, transport):
         p.join(600)
         assert p.exitcode == 0
     got = out["latent"]
-    assert out["transport"] == ("CaaSPeerProtocol" if transport == "p2p" else "CaaSProtocol")
+    assert out["transport"] == ("CaaSPeerProtocol" if transport == "p2p" else "CaaSProtocol")   # p2p-fail1: fallback
     ref = single_gpu()
     rel = float((got.double() - ref.double()).norm() / ref.double().norm())
     print(f"world {world}: multi-process CaaS vs single GPU rel-L2 {rel:.2e}")
