@@ -174,7 +174,7 @@ def test_add_layernorm(c, with_delta):
 # K7 cross-attention: SDXL levels (d = 64), SD1.5 (8 heads: d = 40 / 80 / 160),
 # the toy config (d = 8, 8 tokens), ragged query counts, context 77 / 100 / 128
 XATTN = [(2, 4096, 640, 10, 77), (2, 1024, 1280, 20, 77), (16, 1024, 1280, 20, 77), (8, 4096, 640, 10, 40),
-         (16, 4096, 640, 10, 77), (12, 2000, 640, 10, 128), (2, 4096, 320, 8, 77), (2, 1024, 640, 8, 77),
+         (16, 4096, 640, 10, 77), (12, 2000, 640, 10, 128), (16, 1024, 640, 10, 1), (16, 1000, 640, 10, 100), (2, 4096, 320, 8, 77), (2, 1024, 640, 8, 77),
          (2, 256, 1280, 8, 77), (2, 4096, 32, 4, 8), (1, 1000, 640, 10, 100), (3, 77, 128, 2, 128),
          (2, 17, 64, 1, 1)]
 
