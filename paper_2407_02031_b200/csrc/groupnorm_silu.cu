@@ -963,7 +963,10 @@ extern int g_gn_cluster_mode;   // gn_cluster.cu: 0 auto, 1 two-pass, 2 / 3 clus
 // wherever it is eligible — since the two-stage fold it beats the cluster
 // forms at every SDXL size too ([2,640,64,64] 12.4 vs 14.2 us, [2,1280,32,32]
 // 10.0 vs 12.3, [2,640,32,32] 8.3 vs 10.1); SDB_GN_RESIDENT=0 turns it off.
+static bool g_rs_refused = false;   // the context refused a cooperative launch once: never try again
+
 bool gn_resident_auto(int64_t n, int64_t hw, int64_t c, int64_t groups, int silu, int dtype) {
+  if (g_rs_refused) return false;
   static int env = -1;
   if (env < 0) {
     const char* e = getenv("SDB_GN_RESIDENT");
@@ -1013,9 +1016,17 @@ static int gn_resident_try(const void* x, void* y, const float* gamma, const flo
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 2 : 1;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), gamma, beta,
-                     add_nc, static_cast<uint8_t*>(ws), (int)hw, (int)c, (int)(c / groups), p.P, p.per_sample, p.cr,
-                     eps);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<const __nv_bfloat16*>(x),
+                                           static_cast<__nv_bfloat16*>(y), gamma, beta, add_nc,
+                                           static_cast<uint8_t*>(ws), (int)hw, (int)c, (int)(c / groups), p.P,
+                                           p.per_sample, p.cr, eps);
+  if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported || e == cudaErrorNotPermitted) {
+    // a context that refuses cooperative launches (e.g. shared through MPS):
+    // nothing was launched; this and every later call take the other forms
+    cudaGetLastError();
+    g_rs_refused = true;
+    return SDB_OK;
+  }
   *launched = true;
   return check_launch("gn_resident_kernel");
 }
