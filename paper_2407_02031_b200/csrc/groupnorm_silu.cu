@@ -33,7 +33,7 @@
 //             row blocks, ~4 CTAs per SM) with kApplyUnroll vectors in flight
 //             per thread; the map is an L2 hit after kernel 1.
 //
-// Workspace (per call site, zeroed once, 64 KB, any shape): a header (epoch,
+// Workspace (per call site, zeroed once, 256 KB, any shape): a header (epoch,
 // current bank, high-water batch, arrival counter) and two banks of
 // [16 samples][64 groups] fixed-point (sum x', sum x'^2).  Producer launches
 // alternate banks (see producer_bank); K3's fused form (inject_gn_kernel)
@@ -60,7 +60,13 @@ constexpr int kApplyUnroll = 4;      // vectors in flight per thread (apply)
 // Workspace: header | 2 banks of [kMaxN][kMaxGroups] x {sum x, sum x^2}, each
 // an exact fixed-point pair (int64 integer part, int64 2^-40 fraction).
 constexpr size_t kWsHeader = 256;
-constexpr int kBankWords = kMaxN * kMaxGroups * 4;
+// Each of a group's 4 words (sum hi, sum lo, sum-of-squares hi, lo) in its
+// own 32-B sector: the L2 serialises atomics per sector, and every producer
+// CTA adds to the same group words (scripts/k3_probe.py: with the words
+// packed in one sector the tail grew to ~16 us at 1184 CTAs).
+constexpr int kWordPad = 4;                       // longs between a group's words
+constexpr int kGroupStride = 4 * kWordPad;        // longs per (sample, group)
+constexpr int kBankWords = kMaxN * kMaxGroups * kGroupStride;
 constexpr size_t kWsBytes = kWsHeader + 2 * (size_t)kBankWords * sizeof(long long);
 constexpr double kFracScale = 1099511627776.0;        // 2^40
 constexpr size_t kRsCntOffset = 128;   // the resident form's per-sample arrival counts: header bytes [128, 256) = [2 banks][16 samples] u32
@@ -150,21 +156,29 @@ __device__ __forceinline__ unsigned int ld_relaxed(const unsigned int* p) {
 // CTA).  Called by every thread of the CTA (uniform control flow): ONE thread
 // reads the header and shares it — every thread loading the same word would
 // queue thousands of requests on one L2 address ahead of the real traffic.
-__device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch, unsigned int* epoch_out = nullptr) {
-  __shared__ unsigned int snap[2];
-  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+__shared__ unsigned int s_snap[2];   // the producer's header snapshot (epoch, hwm)
+
+// Producers call this right after their programmatic wait: the header read is
+// then in flight during the pass instead of on its tail (nothing changes it
+// before every CTA of this launch has arrived).
+__device__ __forceinline__ void producer_snap(const uint8_t* ws) {
   if (threadIdx.x == 0) {
-    snap[0] = ld_relaxed(&hdr->epoch);
-    snap[1] = ld_relaxed(&hdr->hwm);
+    const WsHeader* hdr = reinterpret_cast<const WsHeader*>(ws);
+    s_snap[0] = ld_relaxed(&hdr->epoch);
+    s_snap[1] = ld_relaxed(&hdr->hwm);
   }
-  __syncthreads();
-  const unsigned int epoch = snap[0];
-  const int rows = max((int)snap[1], nbatch);
+}
+
+__device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch, unsigned int* epoch_out = nullptr) {
+  WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+  __syncthreads();                 // s_snap (producer_snap) visible
+  const unsigned int epoch = s_snap[0];
+  const int rows = max((int)s_snap[1], nbatch);
   if (epoch_out != nullptr) *epoch_out = epoch;
   long long* banks = reinterpret_cast<long long*>(ws + kWsHeader);
   long long* idle = banks + (size_t)((epoch + 1u) & 1u) * kBankWords;
   const int cta = blockIdx.y * gridDim.x + blockIdx.x, ctas = gridDim.x * gridDim.y;
-  for (int i = cta * blockDim.x + threadIdx.x; i < rows * kMaxGroups * 4; i += ctas * blockDim.x) idle[i] = 0;
+  for (int i = cta * blockDim.x + threadIdx.x; i < rows * kMaxGroups * kGroupStride; i += ctas * blockDim.x) idle[i] = 0;
   if (cta == 0 && threadIdx.x < kMaxN)   // the resident form's counts of the next launch (any form may follow)
     reinterpret_cast<unsigned int*>(ws + kRsCntOffset)[((epoch + 1u) & 1u) * kMaxN + threadIdx.x] = 0u;
   if (cta == 0 && threadIdx.x == 0) {
@@ -177,7 +191,15 @@ __device__ __forceinline__ long long* producer_bank(uint8_t* ws, int nbatch, uns
 __device__ __forceinline__ void red_fixed(long long* w, double v) {
   const double hi = floor(v);
   atomicAdd(reinterpret_cast<unsigned long long*>(w), (unsigned long long)(long long)hi);
-  atomicAdd(reinterpret_cast<unsigned long long*>(w + 1), (unsigned long long)__double2ll_rn((v - hi) * kFracScale));
+  atomicAdd(reinterpret_cast<unsigned long long*>(w + kWordPad),
+            (unsigned long long)__double2ll_rn((v - hi) * kFracScale));
+}
+// word of moment m (0: sum, 1: sum of squares) of group g in a sample's bank
+__device__ __forceinline__ long long* moment_word(long long* bank_n, int g, int m) {
+  return bank_n + g * kGroupStride + 2 * m * kWordPad;
+}
+__device__ __forceinline__ const long long* moment_word(const long long* bank_n, int g, int m) {
+  return bank_n + g * kGroupStride + 2 * m * kWordPad;
 }
 
 // this CTA is done with the bank: the last one advances the epoch
@@ -194,7 +216,7 @@ __device__ __forceinline__ void producer_arrive(uint8_t* ws) {
 }
 
 __device__ __forceinline__ double fixed_value(const long long* w) {
-  return (double)__ldg(w) + (double)__ldg(w + 1) / kFracScale;
+  return (double)__ldg(w) + (double)__ldg(w + kWordPad) / kFracScale;
 }
 
 // All index math is 32-bit within one sample (host checks n * hw * c < 2^31).
@@ -203,6 +225,7 @@ __global__ void __launch_bounds__(kMaxThreads)
 gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8_t* __restrict__ ws, int hw, int c,
                 int groups, int cpg, int rpp, int chunks) {
   pdl_wait();
+  producer_snap(ws);
   extern __shared__ __align__(16) double dred[];
   double* red1 = dred;             // [rpp][c] raw sums of x
   double* red2 = dred + rpp * c;   // [rpp][c] raw sums of x^2
@@ -280,25 +303,15 @@ gn_stats_kernel(const T* __restrict__ x, const float* __restrict__ add_nc, uint8
     }
     __syncthreads();
   }
-  // one warp per group: lanes over the group's channels, shuffle-reduce, lane 0
-  // adds the CTA's fixed-point sums to the bank
-  long long* bank = producer_bank(ws, gridDim.y) + (size_t)n * kMaxGroups * 4;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int g = warp; warp < nwarps && g < groups; g += nwarps) {   // full warps only
-    double m1 = 0.0, m2 = 0.0;
-    for (int k = lane; k < cpg; k += 32) {
-      m1 += red1[g * cpg + k];
-      m2 += red2[g * cpg + k];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
-      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
-    }
-    if (lane == 0) {
-      red_fixed(bank + g * 4, m1);
-      red_fixed(bank + g * 4 + 2, m2);
-    }
+  // one thread per (group, moment): the group's channels in a fixed order, one
+  // fixed-point red of the CTA's sum each (short independent chains; see inject_gn_kernel)
+  long long* bank = producer_bank(ws, gridDim.y) + (size_t)n * kMaxGroups * kGroupStride;
+  for (int v = threadIdx.x; v < 2 * groups; v += blockDim.x) {
+    const double* src = (v & 1) ? red2 : red1;
+    const int g = v >> 1;
+    double m = 0.0;
+    for (int k = 0; k < cpg; ++k) m += src[g * cpg + k];
+    red_fixed(moment_word(bank, g, v & 1), m);
   }
   producer_arrive(ws);
 }
@@ -324,9 +337,9 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
     const double count = (double)hw * (double)cpg;
     for (int g = threadIdx.x; g < c / cpg; g += blockDim.x) {
       const long long* bank = reinterpret_cast<const long long*>(ws + kWsHeader) +
-                              (size_t)__ldg(&hdr->cur) * kBankWords + (size_t)n * kMaxGroups * 4;
-      const double mean = fixed_value(bank + g * 4) / count;
-      const double var = fixed_value(bank + g * 4 + 2) / count - mean * mean;
+                              (size_t)__ldg(&hdr->cur) * kBankWords + (size_t)n * kMaxGroups * kGroupStride;
+      const double mean = fixed_value(moment_word(bank, g, 0)) / count;
+      const double var = fixed_value(moment_word(bank, g, 1)) / count - mean * mean;
       gstat[g] = make_float2((float)mean, (float)(var < 0.0 ? 0.0 : var));
     }
   }
@@ -427,7 +440,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // a bank entry written during THIS launch: read through L2, never the
 // non-coherent path
 __device__ __forceinline__ double fixed_value_cg(const long long* w) {
-  return (double)__ldcg(w) + (double)__ldcg(w + 1) / kFracScale;
+  return (double)__ldcg(w) + (double)__ldcg(w + kWordPad) / kFracScale;
 }
 
 #ifdef SDB_RS_TRACE   // probe build only: per-CTA phase timestamps (scripts/k2r_trace.py)
@@ -558,7 +571,7 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   RS_T(6)
   const unsigned int e0 = snap[0];
   long long* banks = reinterpret_cast<long long*>(ws + kWsHeader);
-  long long* bank = banks + (size_t)(e0 & 1u) * kBankWords + (size_t)n * kMaxGroups * 4;
+  long long* bank = banks + (size_t)(e0 & 1u) * kBankWords + (size_t)n * kMaxGroups * kGroupStride;
   // two short, fixed-order stages (a warp per group walked its columns and
   // shuffled serially: ~3 us of dependent latency at 4 warps per scheduler):
   //   1. column sums: one thread per (column, component) over the rstep rows
@@ -586,7 +599,7 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
     // raw moments of x' over this CTA's rows x cpg channels of the group, in fp64
     const double K = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(tile)[g * cpg]);
     const double M = (double)rows * cpg, S1 = m1;
-    red_fixed(bank + g * 4 + 2 * mom, mom == 0 ? S1 + M * K : (double)m2 + K * (2.0 * S1 + M * K));
+    red_fixed(moment_word(bank, g, mom), mom == 0 ? S1 + M * K : (double)m2 + K * (2.0 * S1 + M * K));
   }
   // ---- per-sample completion: one release-add per CTA on its sample's count
   __syncthreads();                                   // every group's reds issued
@@ -596,7 +609,7 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
   {  // zero the idle bank and counts for the next producer launch on this workspace (a slice per CTA)
     const int brows = max((int)snap[1], (int)(gridDim.x / per_sample));
     long long* idle = banks + (size_t)((e0 + 1u) & 1u) * kBankWords;
-    for (int i = blockIdx.x * NT + tid; i < brows * kMaxGroups * 4; i += gridDim.x * NT) idle[i] = 0;
+    for (int i = blockIdx.x * NT + tid; i < brows * kMaxGroups * kGroupStride; i += gridDim.x * NT) idle[i] = 0;
     if (blockIdx.x == 0 && tid < kMaxN) cnts[((e0 + 1u) & 1u) * kMaxN + tid] = 0u;
   }
   float ga[8], be[8];   // the affine parameters, in flight across the barrier
@@ -614,8 +627,8 @@ gn_resident_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restric
       if (global_ns() - t0 > 2000000000ull) __trap();
     }
     const double count = (double)hw * cpg;
-    const double mean = fixed_value_cg(bank + tid * 4) / count;
-    double var = fixed_value_cg(bank + tid * 4 + 2) / count - mean * mean;
+    const double mean = fixed_value_cg(moment_word(bank, tid, 0)) / count;
+    double var = fixed_value_cg(moment_word(bank, tid, 1)) / count - mean * mean;
     var = var < 0.0 ? 0.0 : var;
     stat[tid] = (float)mean;
     stat[kRsMaxGroups + tid] = (float)var;
@@ -732,12 +745,13 @@ struct InjArgs {
   float scale[kInjMaxRes];
 };
 
-template <typename T, int NR>
+template <typename T, int NR, int KB>
 __global__ void __launch_bounds__(kInjThreads)
 inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T> ra, const float* __restrict__ hb,
                  const float* __restrict__ sb, uint8_t* __restrict__ ws, int hw, int ch, int cs, int groups, int cpg,
                  int rpp, int chunks) {
   pdl_wait();
+  producer_snap(ws);
   extern __shared__ __align__(16) float red[];
   const int c = ch + cs;
   float* red1 = red;               // [rpp][c]
@@ -750,7 +764,7 @@ inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T>
   const int p0 = n * hw;                           // first pixel of the sample (global pixel index)
   const int step = chunks * rpp;
 
-  constexpr int kB = 4;
+  constexpr int kB = KB;
   const bool hid_lane = v < vh;
   const T* src0 = hid_lane ? hidden + c0 : skip + (c0 - ch);
   const int ld0 = hid_lane ? ch : cs;
@@ -809,24 +823,18 @@ inject_gn_kernel(T* out, const T* __restrict__ hidden, const T* skip, InjArgs<T>
   *reinterpret_cast<float4*>(red2 + r * c + c0) = make_float4(s2[0].x, s2[0].y, s2[1].x, s2[1].y);
   *reinterpret_cast<float4*>(red2 + r * c + c0 + 4) = make_float4(s2[2].x, s2[2].y, s2[3].x, s2[3].y);
   fold_rows(red1, red2, c, rpp);
-  // one warp per group: lanes over its channels (fp64), shuffle-reduce, fixed-point sums into the bank
-  long long* bank = producer_bank(ws, gridDim.y) + (size_t)n * kMaxGroups * 4;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int g = warp; warp < nwarps && g < groups; g += nwarps) {   // full warps only
-    double m1 = 0.0, m2 = 0.0;
-    for (int k = lane; k < cpg; k += 32) {
-      m1 += (double)red1[g * cpg + k];
-      m2 += (double)red2[g * cpg + k];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
-      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
-    }
-    if (lane == 0) {
-      red_fixed(bank + g * 4, m1);
-      red_fixed(bank + g * 4 + 2, m2);
-    }
+  // one thread per (group, moment): its channels in a fixed order (fp64), one
+  // fixed-point red each.  (A warp per group walking its channels and then
+  // shuffling — 32 groups over the CTA's ~7 warps — chained ~5 dependent fp64
+  // reductions per warp: ~10 us of tail, more than the pass itself,
+  // scripts/k3_probe.py.)
+  long long* bank = producer_bank(ws, gridDim.y) + (size_t)n * kMaxGroups * kGroupStride;
+  for (int v = threadIdx.x; v < 2 * groups; v += blockDim.x) {
+    const float* src = (v & 1) ? red2 : red1;
+    const int g = v >> 1;
+    double m = 0.0;
+    for (int k = 0; k < cpg; ++k) m += (double)src[g * cpg + k];
+    red_fixed(moment_word(bank, g, v & 1), m);
   }
   producer_arrive(ws);
 }
@@ -893,9 +901,20 @@ int run_inject_gn(void* out, const void* hidden, const void* skip, const void* c
     ra.res[i] = i < n_res ? static_cast<const T*>(res[i]) : nullptr;
     ra.scale[i] = i < n_res ? scales[i] : 0.f;
   }
-  // ~2 CTAs of ~256 threads per SM (its row batches keep 4 x (1 + n_res)
-  // vectors per thread in flight, ~100 registers); chunks <= max_chunks(n)
-  const GnShape s = gn_shape(n, hw, c, groups, 256, 2);
+  // KB row batches of (1 + n_res) vectors in flight per thread, ~CPS CTAs of
+  // ~THR threads per SM.  Measured (scripts/k3_probe.py, [2,320,128,128] + 1
+  // residual): 4 / 2 / 256 (round 1) 19.8 us, 1 / 2 / 512 14.8 us; without a
+  // residual 2 / 2 / 512 (11.2 us) wins.  SDB_K3GN="kb,cps,threads" overrides.
+  static int env_kb = -1, env_cps = 2, env_thr = 512;
+  if (env_kb < 0) {
+    env_kb = 0;
+    if (const char* e = getenv("SDB_K3GN")) sscanf(e, "%d,%d,%d", &env_kb, &env_cps, &env_thr);
+  }
+  int kb = env_kb > 0 ? env_kb : (n_res == 0 ? 2 : 1);
+  if (kb != 1 && kb != 2) kb = 4;
+  const int cps = std::max(1, std::min(env_cps, 8));
+  const int thr = env_thr == 256 ? 256 : 512;
+  const GnShape s = gn_shape(n, hw, c, groups, thr, cps);
   const int rpp = s.rpp, threads = s.threads;
   if (threads > kInjThreads) return fail(SDB_EINVAL, "residual_inject_gn: channels > 4096 unsupported");
   const size_t smem = (size_t)2 * rpp * c * sizeof(float);
@@ -907,11 +926,13 @@ int run_inject_gn(void* out, const void* hidden, const void* skip, const void* c
   const int ihw = (int)hw, ich = (int)ch, ics = (int)cs, ig = (int)groups, icpg = (int)(c / groups);
   const int ichunks = (int)s.chunks;
   switch (n_res) {
+#define SDB_INJ_KB(NR, KB)                                                                                      \
+  smem_attr(inject_gn_kernel<T, NR, KB>, smem);                                                                 \
+  launch_k(inject_gn_kernel<T, NR, KB>, grid, threads, smem, st, o, h, sk, ra, hb, sb, w, ihw, ich, ics, ig, icpg, \
+           rpp, ichunks);
 #define SDB_INJ(NR)                                                                                            \
   case NR:                                                                                                     \
-    smem_attr(inject_gn_kernel<T, NR>, smem);                                                                  \
-    launch_k(inject_gn_kernel<T, NR>, grid, threads, smem, st, o, h, sk, ra, hb, sb, w, ihw, ich, ics, ig, icpg, rpp, \
-                                                         ichunks);                                           \
+    if (kb == 1) { SDB_INJ_KB(NR, 1) } else if (kb == 2) { SDB_INJ_KB(NR, 2) } else { SDB_INJ_KB(NR, 4) }      \
     break;
     SDB_INJ(0)
     SDB_INJ(1)
@@ -919,6 +940,7 @@ int run_inject_gn(void* out, const void* hidden, const void* skip, const void* c
     SDB_INJ(3)
     SDB_INJ(4)
 #undef SDB_INJ
+#undef SDB_INJ_KB
     default: return fail(SDB_EINVAL, "residual_inject_gn: at most 4 residuals");
   }
   return check_launch("inject_gn_kernel");
