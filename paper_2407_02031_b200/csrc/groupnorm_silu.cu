@@ -413,15 +413,15 @@ gn_apply_kernel(const T* x, T* y,  // may alias: every element is read before it
 // time.  Here one CTA per SM (a co-resident grid: cooperative launch) owns a
 // contiguous run of P pixels of one sample — in NHWC one contiguous span, so
 // it arrives as a few 1-D bulk copies (TMA engine, one mbarrier each) while
-// the threads fold the chunks that have landed into shifted per-channel
-// sums.  The per-group CTA partials go to the site's fixed-point bank
-// (red.global.add of exact integers: deterministic in any arrival order),
-// one grid barrier (the bank's epoch word: the last CTA to arrive advances
-// it), then every CTA reads its sample's statistics and applies the affine
-// + SiLU to its resident tile and stores it: one read and one write of the
+// the threads fold the chunks that have landed into shifted sums (one shift
+// per group).  The per-group CTA partials go to the site's fixed-point bank
+// (red.global.add of exact integers: deterministic in any arrival order);
+// each CTA then release-adds its sample's arrival count and waits for its
+// sample's CTAs only, reads the sample's statistics, applies the affine +
+// SiLU to its resident tile and stores it: one read and one write of the
 // map, the minimum.  Eligible while the map fits 148 tiles of <= 176 KB
 // (SDXL's [2, 320, 128, 128] = 21 MB: 142 KB per CTA).
-constexpr int kRsThreads = 1024;
+constexpr int kRsThreads = 1024;   // the largest thread count (smem / plan bounds); rs_threads() picks the launch's
 constexpr int kRsMaxGroups = 32;
 constexpr int kRsMaxChunks = 12;
 constexpr int kRsTileMax = 176 * 1024;
