@@ -25,6 +25,7 @@ N(0, 0.02) so residual parity is not vacuous, SURVEY §7 hard part 9).
 
 from __future__ import annotations
 
+import contextlib
 import math
 from dataclasses import dataclass
 from typing import Optional, Sequence
@@ -39,6 +40,22 @@ from . import ops
 
 # A/B switch for measurements: SDB_K3_GN_STATS=0 keeps the two-pass GroupNorm everywhere
 _NO_K3_STATS = os.environ.get("SDB_K3_GN_STATS", "1") == "0"
+# cuDNN's per-shape algorithm autotuning (torch.backends.cudnn.benchmark) for
+# the 16-bit convolutions: the heuristic picks cost the SDXL step ~2% (945 vs
+# 925 ms/image, bench.py A/B on one B200).  Each shape is tuned on its first
+# (eager) call — the engines run every shape eagerly before capturing their
+# CUDA graphs, and a capture then replays the tuned algorithm.  fp32 (the
+# parity mode) keeps the heuristics.  SDB_CUDNN_BENCHMARK=0 turns it off.
+_CUDNN_TUNE = os.environ.get("SDB_CUDNN_BENCHMARK", "1") != "0"
+
+
+def _conv_tuning(x):
+    if not _CUDNN_TUNE or x.dtype == torch.float32 or not x.is_cuda:
+        return contextlib.nullcontext()
+    cd = torch.backends.cudnn
+    return cd.flags(enabled=cd.enabled, benchmark=True, deterministic=cd.deterministic, allow_tf32=cd.allow_tf32)
+
+
 # K8 (tcgen05 flash-style self-attention) is opt-in: SDB_SELF_ATTN=1 (round 1: slower than
 # the library SDPA at SDXL's shapes, see csrc/self_attn.cu)
 _SELF_ATTN = os.environ.get("SDB_SELF_ATTN", "0") == "1"
@@ -371,7 +388,13 @@ class Net:
         return F.linear(x, self.t[name + ".weight"], self.t.get(name + ".bias"))
 
     def conv(self, name, x, stride=1, bias=True):
-        """bias=False: the caller folds ``self.fb[name]`` into the next kernel."""
+        """bias=False: the caller folds ``self.fb[name]`` into the next kernel.
+        16-bit convolutions run with cuDNN's algorithm autotuning on (see
+        _conv2d)."""
+        with _conv_tuning(x):
+            return self._conv(name, x, stride, bias)
+
+    def _conv(self, name, x, stride=1, bias=True):
         w = self.t[name + ".weight"]
         pad = w.shape[-1] // 2
         if w.shape[1] % 8 != 0 and x.dtype != torch.float32:
