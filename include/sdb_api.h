@@ -322,6 +322,15 @@ int sdb_upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int6
 int sdb_add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta,
                       int64_t rows, int64_t c, float eps, int dtype, void* stream);
 
+/* K5' — the transformer FF projection with GEGLU fused into its epilogue (one
+ * tcgen05 GEMM; the paper's fused GEGLU):
+ *   out[m, j] = (x w_v^T + b_v)[m, j] * gelu((x w_g^T + b_g)[m, j])
+ * x: [m, k] bf16 rows, w: [2f, k] bf16 (value rows, then gate rows: the GEGLU
+ * proj weight as stored), bias: [2f] fp32 or NULL, out: [m, f] bf16.
+ * k % 64 == 0, f % 128 == 0, 16-B aligned pointers. */
+int sdb_ff_geglu(const void* x, const void* w, const float* bias, void* out, int64_t m, int64_t k, int64_t f,
+                 void* stream);
+
 /* ========================================================================
  * K4 — classifier-free guidance + DDIM (eta = 0) step, fused.
  *   eps     = eps_u + g * (eps_c - eps_u)           (eps = [eps_u ; eps_c])

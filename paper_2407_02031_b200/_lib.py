@@ -187,7 +187,7 @@ class LoraSrc(ctypes.Structure):
 
 EXPORTED = EXPORTED + ("sdb_lora_pack_bytes", "sdb_lora_pack", "sdb_lora_pack_multi", "sdb_lora_pack_multi_layout",
                        "sdb_lora_tc_plan",
-                       "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_add_layernorm",
+                       "sdb_lora_tc_patch", "sdb_lora_tc_set_mode", "sdb_geglu", "sdb_ff_geglu", "sdb_add_layernorm",
                        "sdb_cross_attention", "sdb_stream_wait_value32", "sdb_stream_write_value32",
                        "sdb_memcpy_async", "sdb_cross_attention_set_mode", "sdb_self_attention",
                        "sdb_upsample2x", "sdb_batched_copy", "sdb_batched_copy_chunk_vectors")
@@ -232,5 +232,7 @@ def _declare_tc(lib: ctypes.CDLL) -> None:
     lib.sdb_memcpy_async.argtypes = [vp, vp, ctypes.c_size_t, vp]
     lib.sdb_cross_attention.restype = i32
     lib.sdb_cross_attention.argtypes = [vp, i64, vp, i64, i64, vp, i64, i32, i32, i32, i32, i32, f32, i32, vp]
+    lib.sdb_ff_geglu.restype = i32
+    lib.sdb_ff_geglu.argtypes = [vp, vp, vp, vp, i64, i64, i64, vp]
     lib.sdb_add_layernorm.restype = i32
     lib.sdb_add_layernorm.argtypes = [vp, vp, vp, vp, vp, i64, i64, f32, i32, vp]

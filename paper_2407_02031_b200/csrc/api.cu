@@ -55,6 +55,8 @@ int upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int64_t 
 int batched_copy(const void* const* src_dev, void* const* dst_dev, const int64_t* nvec_dev,
                  const int64_t* chunk_prefix_dev, int n, int64_t total_chunks, cudaStream_t st);
 int64_t batched_copy_chunk_vectors();
+int ff_geglu(const void* x, const void* w, const float* bias, void* out, int64_t m, int64_t k, int64_t f,
+             cudaStream_t st);
 int add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows, int64_t c,
                   float eps, int dtype, cudaStream_t st);
 // cross_attn.cu
@@ -261,6 +263,11 @@ int sdb_upsample2x(const void* x, void* y, int64_t n, int64_t h, int64_t w, int6
 
 int sdb_geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, void* stream) {
   return geglu(proj, out, rows, f, dtype, as_stream(stream));
+}
+
+int sdb_ff_geglu(const void* x, const void* w, const float* bias, void* out, int64_t m, int64_t k, int64_t f,
+                 void* stream) {
+  return ff_geglu(x, w, bias, out, m, k, f, as_stream(stream));
 }
 
 int sdb_add_layernorm(void* x, const void* d, void* y, const void* gamma, const void* beta, int64_t rows,

@@ -14,6 +14,8 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "ptx.cuh"
+#include "tcgen05.cuh"
 
 namespace sdb {
 namespace {
@@ -104,6 +106,149 @@ geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int rows, int f) {
         store_raw<T>(dst + (unsigned)m * (unsigned)f, o);
       }
     }
+  }
+}
+
+// ---- K5' the FF projection GEMM with GEGLU in its epilogue (tcgen05) -------
+// out[m, j] = (x W_v^T + b_v)[m, j] * gelu((x W_g^T + b_g)[m, j]),
+// W = [W_v; W_g] (2F x K, the diffusers GEGLU proj weight as stored).  The
+// library path writes the 2F-wide projection and K5 reads it back (a 64²-level
+// call: 84 MB out + 84 MB in + 42 MB out); here each 128 x 256 accumulator
+// tile holds 128 value columns AND the matching 128 gate columns (two TMA
+// boxes of W per K step: rows [128 n, 128 n + 128) and [F + 128 n, ...)), so
+// the epilogue gates in registers and only the F-wide result is written.
+// Persistent, warp-specialised: warp 0 TMA producer (4-stage ring of A 128 x
+// 64 + B 256 x 64 bf16, 128-B swizzled), warp 1 the tcgen05 issuer
+// (M128 N256 K16, fp32 in TMEM, two 256-column accumulators), warps 2-5 the
+// epilogue (TMEM lane quadrant = warp % 4; one row per thread).
+constexpr int kFgBM = 128, kFgBN = 256, kFgBK = 64, kFgStages = 4;
+constexpr int kFgThreads = 192;
+constexpr int kFgStageBytes = kFgBM * 128 + kFgBN * 128;          // 48 KB
+constexpr int kFgSmem = 1024 + kFgStages * kFgStageBytes + 256;
+
+__global__ void __launch_bounds__(kFgThreads, 1)
+ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, int M, int K, int F, int tiles_n,
+                int total) {
+  extern __shared__ __align__(1024) uint8_t fg_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fg_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFgStages * kFgStageBytes);   // full[S] empty[S] tfull[2] tempty[2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kFgStages + 4);
+  constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFgBN >> 3) << 17) |
+                              ((uint32_t)(kFgBM >> 4) << 24);       // f32 accum, bf16 A/B, K-major, 128 x 256
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto full = [&](int s) { return smem_u32(bars + s); };
+  auto empty = [&](int s) { return smem_u32(bars + kFgStages + s); };
+  auto tfull = [&](int b) { return smem_u32(bars + 2 * kFgStages + b); };
+  auto tempty = [&](int b) { return smem_u32(bars + 2 * kFgStages + 2 + b); };
+  if (tid == 0) {
+    prefetch_map(&amap);
+    prefetch_map(&bmap);
+    for (int s = 0; s < kFgStages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 4);                                      // the 4 epilogue warps
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  pdl_wait();
+  const int nk = K / kFgBK;
+  if (warp == 0) {
+    if (lane == 0) {                                                // ---- TMA producer
+      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      int s = 0, round = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int tm = t / tiles_n, tn = t - tm * tiles_n;
+        for (int k = 0; k < nk; ++k) {
+          if (round > 0) mbar_wait(empty(s), (round - 1) & 1);
+          uint8_t* st = smem + s * kFgStageBytes;
+          mbar_expect_tx(full(s), kFgStageBytes);
+          tma_load_2d(smem_u32(st), &amap, k * kFgBK, tm * kFgBM, full(s), pol_a);
+          tma_load_2d(smem_u32(st + kFgBM * 128), &bmap, k * kFgBK, tn * 128, full(s), pol_b);
+          tma_load_2d(smem_u32(st + kFgBM * 128 + 128 * 128), &bmap, k * kFgBK, F + tn * 128, full(s), pol_b);
+          if (++s == kFgStages) { s = 0; ++round; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {                                                // ---- tcgen05 issuer
+      int s = 0, round = 0, tl = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
+        const int buf = tl & 1, use = tl >> 1;
+        if (use > 0) mbar_wait(tempty(buf), (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(buf * kFgBN);
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(full(s), round & 1);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + s * kFgStageBytes), b = a + kFgBM * 128;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc_mma(d, sw128_desc(a + ks * 32), sw128_desc(b + ks * 32), kIdesc, (k | ks) ? 1u : 0u);
+          tc_commit(empty(s));                                      // the stage is free once these MMAs are done
+          if (++s == kFgStages) { s = 0; ++round; }
+        }
+        tc_commit(tfull(buf));
+      }
+    }
+  } else {                                                          // ---- epilogue: warps 2..5
+    const int q = warp & 3;                                         // TMEM lane quadrant this warp may read
+    const int r = q * 32 + lane;
+    int tl = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
+      const int buf = tl & 1, use = tl >> 1;
+      const int tm = t / tiles_n, tn = t - tm * tiles_n;
+      mbar_wait(tfull(buf), use & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kFgBN);
+      const int row = tm * kFgBM + r;
+      const int col0 = tn * 128;
+      __nv_bfloat16* orow = out + (size_t)row * F + col0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 128; c0 += 32) {
+        float v[32], g[32];
+        tc_ld32(base + c0, v);
+        tc_ld32(base + 128 + c0, g);
+        if (row < M) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float2 hv = make_float2(v[j], v[j + 1]), gv = make_float2(g[j], g[j + 1]);
+            if (bias != nullptr) {
+              hv = f2add(hv, *reinterpret_cast<const float2*>(bias + col0 + c0 + j));
+              gv = f2add(gv, *reinterpret_cast<const float2*>(bias + F + col0 + c0 + j));
+            }
+            const float2 o = f2mul(hv, gelu2(gv));
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(o.x, o.y);
+            pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(orow + c0 + 8 * i) = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(buf));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -288,6 +433,50 @@ upsample2x_kernel(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t to
     y[o + 2 * w * cv] = v;
     y[o + 2 * w * cv + cv] = v;
   }
+}
+
+// K5': out[M, F] = GEGLU(x[M, K] W[2F, K]^T + bias[2F]) in one tcgen05 GEMM.
+// bf16 only; K % 64 == 0, F % 128 == 0, row strides dense (x: K, W: K, out: F).
+int ff_geglu(const void* x, const void* w, const float* bias, void* out, int64_t m, int64_t k, int64_t f,
+             cudaStream_t st) {
+  if (m <= 0 || k <= 0 || f <= 0) return fail(SDB_EINVAL, "ff_geglu: empty shape");
+  if (k % kFgBK != 0 || f % 128 != 0) return fail(SDB_EUNSUP, "ff_geglu: K % 64 and F % 128 must be 0");
+  if (m * f >= ((int64_t)1 << 31) || m >= ((int64_t)1 << 31)) return fail(SDB_EINVAL, "ff_geglu: too large");
+  if (((uintptr_t)x | (uintptr_t)w | (uintptr_t)out | (uintptr_t)bias) & 15)
+    return fail(SDB_EINVAL, "ff_geglu: pointers must be 16-byte aligned");
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap am, bm;
+  const cuuint32_t es[2] = {1, 1};
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)m};
+    const cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kFgBK, (cuuint32_t)kFgBM};
+    if (enc(&am, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(SDB_EINVAL, "ff_geglu: x tensor map");
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)k, (cuuint64_t)(2 * f)};
+    const cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)kFgBK, 128u};
+    if (enc(&bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(SDB_EINVAL, "ff_geglu: weight tensor map");
+  }
+  const int tiles_m = (int)((m + kFgBM - 1) / kFgBM), tiles_n = (int)(f / 128);
+  const int total = tiles_m * tiles_n;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ff_geglu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFgSmem);
+    attr = true;
+  }
+  const int grid = std::min(total, kNumSMs);
+  launch_k(ff_geglu_kernel, dim3((unsigned)grid), kFgThreads, kFgSmem, st, am, bm, bias,
+           static_cast<__nv_bfloat16*>(out), (int)m, (int)k, (int)f, tiles_n, total);
+  return check_launch("ff_geglu_kernel");
 }
 
 int geglu(const void* proj, void* out, int64_t rows, int64_t f, int dtype, cudaStream_t st) {

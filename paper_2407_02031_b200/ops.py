@@ -497,6 +497,33 @@ def residual_inject(skip: torch.Tensor, residuals: Sequence[torch.Tensor], scale
 # --------------------------------------------------------------------------
 # K5 / K6 — GEGLU and residual-add + LayerNorm of the transformer blocks
 # --------------------------------------------------------------------------
+def ff_geglu_supported(x: torch.Tensor, w: torch.Tensor) -> bool:
+    return (x.dtype == torch.bfloat16 and w.dtype == torch.bfloat16 and x.shape[-1] % 64 == 0
+            and w.dim() == 2 and w.shape[0] % 256 == 0 and w.shape[1] == x.shape[-1])
+
+
+def ff_geglu(x: torch.Tensor, w: torch.Tensor, bias: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """GEGLU(x W^T + bias) in one tcgen05 GEMM (K5'): W = [W_value; W_gate]
+    ([2F, K] bf16, the GEGLU proj weight as stored), bias fp32 [2F] or None;
+    returns [..., F]."""
+    require_cuda(x, w, bias)
+    k = x.shape[-1]
+    if not ff_geglu_supported(x, w):
+        raise ValidationError("ff_geglu: bf16, K % 64 == 0, W [2F, K] with F % 128 == 0")
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != w.shape[0] or not bias.is_contiguous()):
+        raise ValidationError("ff_geglu: bias must be a contiguous fp32 vector of 2F values")
+    x2 = x.reshape(-1, k)
+    if not x2.is_contiguous() or not w.is_contiguous():
+        raise ValidationError("ff_geglu: x rows and W must be contiguous")
+    f = w.shape[0] // 2
+    out = torch.empty((*x.shape[:-1], f), dtype=x.dtype, device=x.device)
+    _count(1)
+    _lib.check("sdb_ff_geglu", _lib.lib().sdb_ff_geglu(
+        x2.data_ptr(), w.data_ptr(), bias.data_ptr() if bias is not None else None, out.data_ptr(),
+        x2.shape[0], k, f, _stream_ptr(None)))
+    return out
+
+
 def geglu(proj: torch.Tensor) -> torch.Tensor:
     """proj [..., 2F] contiguous -> [..., F] = proj[..., :F] * gelu(proj[..., F:])."""
     require_cuda(proj)

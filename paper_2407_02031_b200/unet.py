@@ -56,6 +56,10 @@ def _conv_tuning(x):
     return cd.flags(enabled=cd.enabled, benchmark=True, deterministic=cd.deterministic, allow_tf32=cd.allow_tf32)
 
 
+# K5' (the FF projection GEMM with GEGLU in its epilogue, tcgen05) replaces cuBLAS + K5
+# for bf16 (scripts/ffg_probe.py: [8192,640]x5120 54.7 vs 66.9 us, [2048,1280]x10240 44.9
+# vs 47.8 us); SDB_FF_FUSED=0 keeps the library GEMM + K5
+_FF_FUSED = os.environ.get("SDB_FF_FUSED", "1") != "0"
 # K8 (tcgen05 flash-style self-attention) is opt-in: SDB_SELF_ATTN=1 (round 1: slower than
 # the library SDPA at SDXL's shapes, see csrc/self_attn.cu)
 _SELF_ATTN = os.environ.get("SDB_SELF_ATTN", "0") == "1"
@@ -381,11 +385,22 @@ class Net:
                 c2, sc = fb.get(pre + ".conv2"), fb.get(pre + ".conv_shortcut")
                 if c2 is not None or sc is not None:
                     fb[pre + ".out_bias"] = ((c2 if c2 is not None else 0) + (sc if sc is not None else 0)).contiguous()
+        for k, v in t.items():   # fp32 biases of the GEGLU projections (K5' adds them in its epilogue)
+            if k.endswith(".ff.proj.bias"):
+                fb[k[: -len(".bias")] + ".bias_f32"] = v.float().contiguous()
         self.fb = fb
 
     # -- primitives -------------------------------------------------------
     def lin(self, name, x):
         return F.linear(x, self.t[name + ".weight"], self.t.get(name + ".bias"))
+
+    def ff_proj_geglu(self, name, x):
+        """GEGLU(x W^T + b) of a transformer FF: K5' (one tcgen05 GEMM with the
+        gating in its epilogue) for bf16, else the library GEMM then K5."""
+        w = self.t[name + ".weight"]
+        if _FF_FUSED and x.is_cuda and ops.ff_geglu_supported(x, w):
+            return ops.ff_geglu(x, w, self.fb.get(name + ".bias_f32"))
+        return ops.geglu(self.lin(name, x))   # K5
 
     def conv(self, name, x, stride=1, bias=True):
         """bias=False: the caller folds ``self.fb[name]`` into the next kernel.
@@ -566,7 +581,7 @@ class Net:
             y = ln("norm1", delta)
             y = ln("norm2", self.attention(b + ".attn1", y, None, heads))
             y = ln("norm3", self.attention(b + ".attn2", y, ctx, heads))
-            delta = self.lin(b + ".ff.out", ops.geglu(self.lin(b + ".ff.proj", y)))   # K5
+            delta = self.lin(b + ".ff.out", self.ff_proj_geglu(b + ".ff.proj", y))
         tok = ops.residual_inject(tok, [delta], [1.0])
         tok = self.lin(pre + ".proj_out", tok)
         out = tok.view(n, h, w, c).permute(0, 3, 1, 2)            # channels_last view

@@ -171,6 +171,26 @@ def test_add_layernorm(c, with_delta):
     assert ((y.float() - ref).abs() <= ref.abs() * 2 ** -7 + 2e-2).all()
 
 
+@pytest.mark.parametrize("m,k,f", [(8192, 640, 2560), (2048, 1280, 5120), (300, 128, 256), (77, 64, 128),
+                                   (1000, 320, 1280)])
+@pytest.mark.parametrize("with_bias", [True, False])
+def test_ff_geglu_vs_fp32(m, k, f, with_bias):
+    """K5': the GEGLU projection GEMM with the gating in its tcgen05 epilogue
+    vs an fp32 reference of x W^T + b then value * gelu(gate): one bf16
+    rounding of the output (the library path rounds the 2F projection too),
+    ragged M (partial last tile), deterministic."""
+    g = torch.Generator(device="cuda").manual_seed(m + k + f)
+    x = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(2 * f, k, device="cuda", generator=g) * k ** -0.5).to(torch.bfloat16)
+    b = torch.randn(2 * f, device="cuda", generator=g) if with_bias else None
+    y = ops.ff_geglu(x, w, b)
+    p = x.float() @ w.float().t() + (b if with_bias else 0)
+    ref = p[:, :f] * F.gelu(p[:, f:])
+    err = (y.float() - ref).abs()
+    assert (err <= ref.abs() * 2 ** -8 + 1e-2).all(), float(err.max())
+    assert torch.equal(y, ops.ff_geglu(x, w, b))
+
+
 # K7 cross-attention: SDXL levels (d = 64), SD1.5 (8 heads: d = 40 / 80 / 160),
 # the toy config (d = 8, 8 tokens), ragged query counts, context 77 / 100 / 128
 XATTN = [(2, 4096, 640, 10, 77), (2, 1024, 1280, 20, 77), (16, 1024, 1280, 20, 77), (8, 4096, 640, 10, 40),
