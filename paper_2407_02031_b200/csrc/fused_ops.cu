@@ -12,6 +12,7 @@
 // One warp per row (C up to 2560 for LN); fp32 statistics, two-pass over the
 // row held in registers.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -119,12 +120,15 @@ geglu_kernel(const T* __restrict__ proj, T* __restrict__ out, int rows, int f) {
 // the epilogue gates in registers and only the F-wide result is written.
 // Persistent, warp-specialised: warp 0 TMA producer (4-stage ring of A 128 x
 // 64 + B 256 x 64 bf16, 128-B swizzled), warp 1 the tcgen05 issuer
-// (M128 N256 K16, fp32 in TMEM, two 256-column accumulators), warps 2-5 the
-// epilogue (TMEM lane quadrant = warp % 4; one row per thread).
+// (M128 N256 K16, fp32 in TMEM, two 256-column accumulators), warps 2-9 the
+// epilogue (TMEM lane quadrant = warp % 4, two warps per quadrant splitting
+// the 128 output columns; one row per thread; the tile's biases staged in
+// shared memory).
 constexpr int kFgBM = 128, kFgBN = 256, kFgBK = 64, kFgStages = 4;
-constexpr int kFgThreads = 192;
+constexpr int kFgEpiWarps = 8;                                   // two per TMEM lane quadrant
+constexpr int kFgThreads = 64 + 32 * kFgEpiWarps;
 constexpr int kFgStageBytes = kFgBM * 128 + kFgBN * 128;          // 48 KB
-constexpr int kFgSmem = 1024 + kFgStages * kFgStageBytes + 256;
+constexpr int kFgSmem = 1024 + kFgStages * kFgStageBytes + 256 + 2 * 256 * 4;
 
 __global__ void __launch_bounds__(kFgThreads, 1)
 ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
@@ -134,6 +138,7 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fg_smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFgStages * kFgStageBytes);   // full[S] empty[S] tfull[2] tempty[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kFgStages + 4);
+  float* sbias = reinterpret_cast<float*>(smem + kFgStages * kFgStageBytes + 256);   // [2][256]: the tile's bias
   constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFgBN >> 3) << 17) |
                               ((uint32_t)(kFgBM >> 4) << 24);       // f32 accum, bf16 A/B, K-major, 128 x 256
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -150,7 +155,7 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), 4);                                      // the 4 epilogue warps
+      mbar_init(tempty(b), kFgEpiWarps);
     }
     mbar_fence_init();
   }
@@ -203,13 +208,19 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
         tc_commit(tfull(buf));
       }
     }
-  } else {                                                          // ---- epilogue: warps 2..5
+  } else {                                                          // ---- epilogue: warps 2..9
     const int q = warp & 3;                                         // TMEM lane quadrant this warp may read
+    const int half = (warp - 2) >> 2;                               // which 64 of the 128 output columns
     const int r = q * 32 + lane;
     int tl = 0;
+    const int et = tid - 64;                                        // 0..255 over the epilogue warps
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++tl) {
       const int buf = tl & 1, use = tl >> 1;
       const int tm = t / tiles_n, tn = t - tm * tiles_n;
+      // the tile's 128 value + 128 gate biases into shared memory while its MMAs run
+      float* tb = sbias + buf * 256;
+      if (bias != nullptr) tb[et] = __ldg(bias + (et < 128 ? tn * 128 + et : F + tn * 128 + et - 128));
+      named_bar(1, 32 * kFgEpiWarps);
       mbar_wait(tfull(buf), use & 1);
       tc_fence_after();
       const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kFgBN);
@@ -217,7 +228,7 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
       const int col0 = tn * 128;
       __nv_bfloat16* orow = out + (size_t)row * F + col0;
 #pragma unroll 1
-      for (int c0 = 0; c0 < 128; c0 += 32) {
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
         float v[32], g[32];
         tc_ld32(base + c0, v);
         tc_ld32(base + 128 + c0, g);
@@ -227,8 +238,8 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
           for (int j = 0; j < 32; j += 2) {
             float2 hv = make_float2(v[j], v[j + 1]), gv = make_float2(g[j], g[j + 1]);
             if (bias != nullptr) {
-              hv = f2add(hv, *reinterpret_cast<const float2*>(bias + col0 + c0 + j));
-              gv = f2add(gv, *reinterpret_cast<const float2*>(bias + F + col0 + c0 + j));
+              hv = f2add(hv, *reinterpret_cast<const float2*>(tb + c0 + j));
+              gv = f2add(gv, *reinterpret_cast<const float2*>(tb + 128 + c0 + j));
             }
             const float2 o = f2mul(hv, gelu2(gv));
             __nv_bfloat162 h2 = __floats2bfloat162_rn(o.x, o.y);
@@ -249,6 +260,163 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// CTA-pair form (cta_group::2): one 256-row x 256-column accumulator tile per
+// pair — each CTA TMA-loads its own 128 rows of x and ONE of the two W boxes
+// (the leader the value rows, the follower the gate rows: the MMA's N = 256 is
+// the leader's 128 B rows then the follower's), so a K step moves 32 KB per
+// CTA instead of 48 and six stages fit; the leader issues M256 MMAs, every
+// CTA's TMEM receives its 128 rows x [value | gate] and runs the same
+// epilogue.  Loads of both CTAs complete on the leader's barriers; commits
+// multicast to both.
+constexpr int kFpStages = 6;
+constexpr int kFpStageBytes = 128 * 128 + 128 * 128;              // A half + B half: 32 KB
+constexpr int kFpSmem = 1024 + kFpStages * kFpStageBytes + 512 + 2 * 256 * 4;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kFgThreads, 1)
+ff_geglu_pair_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                     const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, int M, int K, int F,
+                     int tiles_n, int total) {
+  extern __shared__ __align__(1024) uint8_t fp_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fp_smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFpStages * kFpStageBytes);   // full[S] empty[S] tfull[2] tempty[2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kFpStages + 4);
+  float* sbias = reinterpret_cast<float*>(smem + kFpStages * kFpStageBytes + 512);
+  constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);       // f32 accum, bf16, K-major, M256 x N256
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int cid = (int)cluster_idx(), ncl = (int)cluster_count();
+  auto full = [&](int s) { return smem_u32(bars + s); };
+  auto empty = [&](int s) { return smem_u32(bars + kFpStages + s); };
+  auto tfull = [&](int b) { return smem_u32(bars + 2 * kFpStages + b); };
+  auto tempty = [&](int b) { return smem_u32(bars + 2 * kFpStages + 2 + b); };
+  if (tid == 0) {
+    prefetch_map(&amap);
+    prefetch_map(&bmap);
+    for (int s = 0; s < kFpStages; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 2 * kFgEpiWarps);                        // both CTAs' epilogue warps
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  pdl_wait();
+  const int nk = K / kFgBK;
+  if (warp == 0) {
+    if (lane == 0) {                                                // ---- TMA producer (both CTAs)
+      const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+      int s = 0, round = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const int tm = t / tiles_n, tn = t - tm * tiles_n;
+        for (int k = 0; k < nk; ++k) {
+          if (round > 0) mbar_wait(empty(s), (round - 1) & 1);
+          uint8_t* st = smem + s * kFpStageBytes;
+          if (leader) mbar_expect_tx(full(s), 2 * kFpStageBytes);
+          const uint32_t lb = mapa_shared(full(s), 0);
+          tma_load_2d_pair(smem_u32(st), &amap, k * kFgBK, tm * 256 + (int)cta * 128, lb, pol_a);
+          tma_load_2d_pair(smem_u32(st + 128 * 128), &bmap, k * kFgBK, (int)cta * F + tn * 128, lb, pol_b);
+          if (++s == kFpStages) { s = 0; ++round; }
+        }
+      }
+      // drain: the leader's last multicast commits must land before this CTA exits
+      for (int i = 0; i < kFpStages; ++i) {
+        const int uses = round + (i < s ? 1 : 0);
+        if (uses > 0) mbar_wait(empty(i), (uses - 1) & 1);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (leader && lane == 0) {                                      // ---- tcgen05 issuer (leader)
+      int s = 0, round = 0, tl = 0;
+      for (int t = cid; t < total; t += ncl, ++tl) {
+        const int buf = tl & 1, use = tl >> 1;
+        if (use > 0) mbar_wait(tempty(buf), (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(buf * kFgBN);
+        for (int k = 0; k < nk; ++k) {
+          mbar_wait(full(s), round & 1);
+          tc_fence_after();
+          const uint32_t a = smem_u32(smem + s * kFpStageBytes), b = a + 128 * 128;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc_mma2(d, sw128_desc(a + ks * 32), sw128_desc(b + ks * 32), kIdesc2, (k | ks) ? 1u : 0u);
+          tc_commit2(empty(s));
+          if (++s == kFpStages) { s = 0; ++round; }
+        }
+        tc_commit2(tfull(buf));
+      }
+    }
+    __syncwarp();
+  } else {                                                          // ---- epilogue: warps 2..9 (each CTA)
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = q * 32 + lane;
+    const int et = tid - 64;
+    int tl = 0;
+    for (int t = cid; t < total; t += ncl, ++tl) {
+      const int buf = tl & 1, use = tl >> 1;
+      const int tm = t / tiles_n, tn = t - tm * tiles_n;
+      float* tb = sbias + buf * 256;
+      if (bias != nullptr) tb[et] = __ldg(bias + (et < 128 ? tn * 128 + et : F + tn * 128 + et - 128));
+      named_bar(1, 32 * kFgEpiWarps);
+      mbar_wait(tfull(buf), use & 1);
+      tc_fence_after();
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * kFgBN);
+      const int row = tm * 256 + (int)cta * 128 + r;
+      const int col0 = tn * 128;
+      __nv_bfloat16* orow = out + (size_t)row * F + col0;
+#pragma unroll 1
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 32) {
+        float v[32], g[32];
+        tc_ld32(base + c0, v);
+        tc_ld32(base + 128 + c0, g);
+        if (row < M) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float2 hv = make_float2(v[j], v[j + 1]), gv = make_float2(g[j], g[j + 1]);
+            if (bias != nullptr) {
+              hv = f2add(hv, *reinterpret_cast<const float2*>(tb + c0 + j));
+              gv = f2add(gv, *reinterpret_cast<const float2*>(tb + 128 + c0 + j));
+            }
+            const float2 o = f2mul(hv, gelu2(gv));
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(o.x, o.y);
+            pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(orow + c0 + 8 * i) = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader) mbar_arrive(tempty(buf));
+        else mbar_arrive_remote(mapa_shared(tempty(buf), 0));
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -466,7 +634,26 @@ int ff_geglu(const void* x, const void* w, const float* bias, void* out, int64_t
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return fail(SDB_EINVAL, "ff_geglu: weight tensor map");
   }
-  const int tiles_m = (int)((m + kFgBM - 1) / kFgBM), tiles_n = (int)(f / 128);
+  const int tiles_n = (int)(f / 128);
+  static int pair = -1;   // SDB_FF_PAIR=0: the single-CTA form (probe knob)
+  if (pair < 0) {
+    const char* e = getenv("SDB_FF_PAIR");
+    pair = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  if (pair) {
+    const int tiles_m = (int)((m + 255) / 256);
+    const int total = tiles_m * tiles_n;
+    static bool pattr = false;
+    if (!pattr) {
+      cudaFuncSetAttribute(ff_geglu_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFpSmem);
+      pattr = true;
+    }
+    const int clusters = std::min(total, kNumSMs / 2);
+    launch_k(ff_geglu_pair_kernel, dim3((unsigned)(2 * clusters)), kFgThreads, kFpSmem, st, am, bm, bias,
+             static_cast<__nv_bfloat16*>(out), (int)m, (int)k, (int)f, tiles_n, total);
+    return check_launch("ff_geglu_pair_kernel");
+  }
+  const int tiles_m = (int)((m + kFgBM - 1) / kFgBM);
   const int total = tiles_m * tiles_n;
   static bool attr = false;
   if (!attr) {
