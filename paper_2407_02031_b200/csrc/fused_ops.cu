@@ -138,7 +138,7 @@ ff_geglu_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant_
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fg_smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFgStages * kFgStageBytes);   // full[S] empty[S] tfull[2] tempty[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kFgStages + 4);
-  float* sbias = reinterpret_cast<float*>(smem + kFgStages * kFgStageBytes + 256);   // [2][256]: the tile's bias
+  __shared__ float sbias[2 * 256];   // the tile's value | gate biases, per accumulator (static: plain LDS)
   constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kFgBN >> 3) << 17) |
                               ((uint32_t)(kFgBM >> 4) << 24);       // f32 accum, bf16 A/B, K-major, 128 x 256
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -283,7 +283,7 @@ ff_geglu_pair_kernel(const __grid_constant__ CUtensorMap amap, const __grid_cons
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(fp_smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFpStages * kFpStageBytes);   // full[S] empty[S] tfull[2] tempty[2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kFpStages + 4);
-  float* sbias = reinterpret_cast<float*>(smem + kFpStages * kFpStageBytes + 512);
+  __shared__ float sbias[2 * 256];   // the tile's value | gate biases, per accumulator (static: plain LDS)
   constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
                                ((uint32_t)(256 >> 4) << 24);       // f32 accum, bf16, K-major, M256 x N256
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
