@@ -1013,6 +1013,11 @@ def run_lora(args):
 
 
 def main():
+    # a run that outlives ~6 minutes (a normal default run takes ~100 s) dumps
+    # every thread's Python stack to stderr, every 6 minutes: a hang leaves a
+    # trace of where it sits instead of an empty log
+    import faulthandler
+    faulthandler.dump_traceback_later(360, repeat=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
