@@ -2,7 +2,9 @@
 reference's own outputs (golden fixtures) and the pinned oracle.  Mirrors
 /root/reference/pkg/tests/test_lora.py and test_acceptance.py:341-391."""
 
+import concurrent.futures
 import json
+import os
 import tracemalloc
 from pathlib import Path
 
@@ -376,14 +378,8 @@ def _stacked_inventory_parity(ranks, scales, seed):
     ps.launch()
     torch.cuda.synchronize()
     R = sum(ranks)
-    worst, n_el, n_over = 0.0, 0, 0
-    for name, _ in params.matrices:
-        w = params.t[name + ".weight"]
-        cout = w.shape[0]
-        wl = w.float().cpu().reshape(cout, -1).numpy()
-        got = shadow[name].float().cpu().reshape(cout, -1).numpy()
-        trip = [(lo.factors[name][0].float().cpu().numpy(), lo.factors[name][1].float().cpu().numpy(), s)
-                for lo, s in zip(los, scales)]
+
+    def check(name, wl, got, trip):
         down, up = lora_ref.stack(trip)
         exp = lora_ref.accumulate_bf16(wl, down, up, 1.0, 1.0)
         ulp = lora_ref.bf16_ulp(exp)
@@ -392,10 +388,30 @@ def _stacked_inventory_parity(ranks, scales, seed):
         # hi/lo bf16 split of a scale-folded source, lora_patch_tc.cu)
         tol = ulp + (R * 2.0 ** -24 + 2.0 ** -16) * terms
         err = np.abs(got - exp)
-        worst = max(worst, float((err / ulp).max()))
-        n_over += int((err > ulp).sum())
-        n_el += err.size
-        assert not (err > tol).any(), (name, int((err > tol).sum()), float((err / ulp).max()))
+        return name, float((err / ulp).max()), int((err > ulp).sum()), err.size, int((err > tol).sum())
+
+    # the host-side check is mostly single-threaded numpy elementwise work:
+    # a few matrices at a time on a thread pool (device->host copies stay on
+    # this thread; at most 2x workers matrices are held on the host)
+    workers = max(1, min(8, (os.cpu_count() or 2) // 2))
+    results, pending = [], []
+    with concurrent.futures.ThreadPoolExecutor(workers) as pool:
+        for name, _ in params.matrices:
+            w = params.t[name + ".weight"]
+            cout = w.shape[0]
+            wl = w.float().cpu().reshape(cout, -1).numpy()
+            got = shadow[name].float().cpu().reshape(cout, -1).numpy()
+            trip = [(lo.factors[name][0].float().cpu().numpy(), lo.factors[name][1].float().cpu().numpy(), s)
+                    for lo, s in zip(los, scales)]
+            pending.append(pool.submit(check, name, wl, got, trip))
+            if len(pending) >= 2 * workers:
+                results.append(pending.pop(0).result())
+        results += [f.result() for f in pending]
+    worst = max(r[1] for r in results)
+    n_over = sum(r[2] for r in results)
+    n_el = sum(r[3] for r in results)
+    bad = [(r[0], r[4], r[1]) for r in results if r[4]]
+    assert not bad, bad[:5]
     print(f"stacked K1 ranks={ranks} scales={scales}: {n_el} elements, max {worst:.2f} ulp, "
           f"{n_over} over 1 ulp")
     # over 1 ulp only where the result nearly cancels (|W + delta| << its
